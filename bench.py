@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""bench.py — the ScratchPipe hot path on B200 (BASELINE.json metric).
+
+One "step" = one pass of the whole hot path over one synthetic mini-batch:
+sp_plan (index ingest + dedup + Hit-Map probe + hit/miss + window-safe victim
+selection + bookkeeping), the fused zero-copy Collect/Exchange/Insert
+transfer, sp_forward (EmbeddingBag gather-reduce), the MLP stand-in
+(surrogate gradient kernel) and sp_train (coalescing segmented reduce + fused
+SGD).  Workload at N=1: BASELINE configs[1], Criteo-Kaggle-shaped (the config
+the metric is quoted on that fits one GPU), in steady state: `preroll`
+untimed batches first fill the scratchpad (cold start is not the paper's
+regime), then W warm-up steps, then K timed steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config kaggle]
+
+Prints ONE JSON line on rank 0.  `value` times device-resident int32 indices
+(inputs in HBM); `e2e` times the same steps through sp_plan with indices in
+pinned host memory (H2D inside the timed region) plus a D2H read of every
+step's Plan counters.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "embedding training iters/s at 1/2/4/8 B200; Train-stage HBM GB/s vs peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="kaggle")
+    ap.add_argument("--preroll", type=int, default=-1, help="untimed steady-state fill batches (-1: config)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="cpu_baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=200)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + clock-event reasons during a timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": [n for bit, n in self.REASONS.items() if self.reasons & bit]}
+
+
+# --------------------------------------------------------------------------- helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle (plain CPU program, as it stands) on this box's host cores:
+    each step = one oracle iteration (reference policy Plan + uncached
+    EmbeddingBag SGD) over one batch of the same workload."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+    from oracle import Policy, UncachedTrainer
+    from workload import CONFIGS, sample_trace
+    cfg = CONFIGS[args.config]
+    g, d, e = cfg.surrogate()
+    nb = args.warmup + args.steps
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    tr = sample_trace(cfg.rows, cfg.batch, cfg.pooling, cfg.alpha, nb, cfg.trace_seed,
+                      device=dev, dtype=torch.int64).cpu().numpy()
+    pol = Policy(cfg.rows, cfg.slots, cfg.window, max(cfg.window - 1, 0))
+    orc = UncachedTrainer(cfg.rows, cfg.dim, cfg.batch, cfg.pooling, cfg.init_seed)
+
+    def step(b):
+        pol.plan(tr, b)
+        orc.step(tr[b], g, d, e)
+
+    for b in range(args.warmup):
+        step(b)
+    t0 = time.perf_counter()
+    for b in range(args.warmup, nb):
+        step(b)
+    el = time.perf_counter() - t0
+    v = args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.description, "note": "oracle from a cold scratchpad"},
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} consecutive batches after {args.warmup} warm-up, "
+                                       "reference policy + uncached EmbeddingBag SGD, single thread"},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def cpu_baseline(cfg, trace_dev, seconds):
+    """Oracle on a bounded sample of the same trace (cold start), 1 thread."""
+    import torch
+    from oracle import Policy, UncachedTrainer
+    g, d, e = cfg.surrogate()
+    pol = Policy(cfg.rows, cfg.slots, cfg.window, max(cfg.window - 1, 0))
+    orc = UncachedTrainer(cfg.rows, cfg.dim, cfg.batch, cfg.pooling, cfg.init_seed)
+    chunk = 16
+    tr = trace_dev[:chunk].to(torch.int64).cpu().numpy()
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        if n >= tr.shape[0]:
+            break
+        pol.plan(tr, n)
+        orc.step(tr[n], g, d, e)
+        n += 1
+        if time.perf_counter() - t0 > seconds and n >= 3:
+            break
+    el = time.perf_counter() - t0
+    return {"value": n / el, "unit": "iters/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {n} batches of the bench trace from a cold scratchpad: reference policy "
+                      f"(Part B) + uncached EmbeddingBag SGD (Part A), single thread, {el:.1f} s"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2205_04702_b200 import ScratchPipe
+    from paper_2205_04702_b200.sharding import (exchange_backward, exchange_forward, lpt_assign,
+                                                table_weights, tables_of)
+    from workload import CONFIGS, init_table, sample_trace
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    T, D, N, L = cfg.num_tables, cfg.dim, cfg.batch, cfg.pooling
+    slots_all = cfg.slots
+    owner = lpt_assign(table_weights(cfg.rows, slots_all, N * L, D), world)
+    mine = tables_of(owner, rank)
+    rows = [cfg.rows[t] for t in mine]
+    slots = [slots_all[t] for t in mine]
+    g_, d_, e_ = cfg.surrogate()
+    W, K = max(3, args.warmup), args.steps
+    KP = min(K, args.profile_steps)
+    pre = cfg.preroll if args.preroll < 0 else args.preroll
+    P, F = cfg.window, max(cfg.window - 1, 0)
+    ahead = P + F + 1
+    nb_dev = pre + W + K + KP          # device-index phase (incl. the `ahead` pushed first)
+    nb_host = W + K                    # host-index (e2e) phase
+    nb = nb_dev + ahead + nb_host
+
+    # ---- inputs: host tables (pinned), trace (device int32; host int32 part pinned)
+    tables = []
+    for t in mine:
+        h = torch.empty((cfg.rows[t], D), dtype=torch.float32).pin_memory()
+        init_table(cfg.init_seed, t, cfg.rows[t], D, device=dev, out=h)
+        tables.append(h)
+    trace = torch.empty((nb, len(mine), N, L), dtype=torch.int32, device=dev)
+    CH = 512
+    for b0 in range(0, nb, CH):
+        b1 = min(nb, b0 + CH)
+        full = sample_trace(cfg.rows, N, L, cfg.alpha, b1 - b0, cfg.trace_seed, first_batch=b0,
+                            device=dev, dtype=torch.int32)
+        trace[b0:b1] = full[:, mine]
+        del full
+    host_trace = trace[nb_dev + ahead:].cpu().pin_memory()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    sp = ScratchPipe(rows, tables, D, slots, N, L, window=cfg.window, device=local, stream=stream,
+                     index_dtype="int32", index_on_device=False)
+    pooled = torch.empty((len(mine), N, D), dtype=torch.float32, device=dev)
+    grad = torch.empty_like(pooled)
+    stats_host = torch.zeros((K + W + 8, len(mine), 4), dtype=torch.int32).pin_memory()
+    state = {"pushed": 0, "trained": 0}
+
+    def push_dev():
+        j = state["pushed"]
+        sp.plan_device(trace[j])
+        state["pushed"] = j + 1
+
+    def push_host():
+        j = state["pushed"]
+        sp.plan(host_trace[j - nb_dev - ahead])
+        state["pushed"] = j + 1
+
+    def train_step(push, read_stats_slot=None):
+        push()
+        sp.forward(pooled)
+        if world > 1:
+            pb = exchange_forward(pooled, owner, rank, world)
+            gb = sp.surrogate(pb, g_, d_)
+            gl = exchange_backward(gb, owner, rank, world, N)
+            sp.train(gl, e_)
+        else:
+            sp.surrogate(pooled, g_, d_, out=grad)
+            sp.train(grad, e_)
+        if read_stats_slot is not None:
+            sp.copy_batch_stats(state["trained"], stats_host[read_stats_slot])
+        state["trained"] += 1
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, n, sampler_index=None):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(sampler_index) if sampler_index is not None else None
+        if sampler:
+            sampler.__enter__()
+        s.record(stream)
+        for k in range(n):
+            fn(k)
+        e.record(stream)
+        barrier()
+        if sampler:
+            sampler.__exit__()
+        ms = torch.tensor([s.elapsed_time(e)], device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item()), sampler
+
+    # ---- preroll + warm-up (device indices)
+    for _ in range(ahead):
+        push_dev()
+    t_pre = time.perf_counter()
+    for _ in range(pre):
+        train_step(push_dev)
+    for _ in range(W):
+        train_step(push_dev)
+    torch.cuda.synchronize()
+    t_pre = time.perf_counter() - t_pre
+    st0 = sp.stats()
+    # ---- timed: value (inputs resident in HBM)
+    ms, sampler = timed(lambda k: train_step(push_dev), K, sampler_index=local)
+    st1 = sp.stats()
+    value = K / (ms / 1e3)   # iterations of the global batch per second (max over ranks)
+    ms_per_step = ms / K
+    launches = {k: st1["kernel_launches"][k] - st0["kernel_launches"][k] for k in st1["kernel_launches"]}
+    gpu_launches = sum(launches.values())
+    # ---- profiling pass: per-kernel CUDA-event durations (separate from the timed region)
+    sp.set_profiling(True)
+    for _ in range(KP):
+        train_step(push_dev)
+    sp.set_profiling(False)
+    st2 = sp.stats()
+    # ---- e2e: host indices through the public API, D2H of every step's Plan counters
+    assert state["pushed"] == nb_dev + ahead
+    for k in range(W):
+        train_step(push_host, read_stats_slot=k)
+    hits_seen = []
+
+    def e2e_step(k):
+        train_step(push_host, read_stats_slot=W + k)
+        if k >= 1:  # read the previous step's result (lag 1 keeps the pipeline full)
+            hits_seen.append(int(stats_host[W + k - 1, :, 1].sum()))
+    ms_e2e, _ = timed(e2e_step, K)
+    hits_seen.append(int(stats_host[W + K - 1, :, 1].sum()))
+    e2e_value = K / (ms_e2e / 1e3)
+    st3 = sp.stats()
+    idx_bytes = len(mine) * N * L * 4
+    stats_bytes = len(mine) * 4 * 4
+
+    # ---- per-kernel accounting (profiling window)
+    def delta(key):
+        return st2[key] - st1[key]
+    steps_p = KP
+    U = delta("uniques") / steps_p
+    m = delta("misses") / steps_p
+    ev = delta("evictions") / steps_p
+    Tg = len(mine)
+    n = N * L
+    kms = {k: st2["kernel_ms"][k] - st1["kernel_ms"][k] for k in st2["kernel_ms"]}
+    kcount = {k: st2["kernel_timed"][k] - st1["kernel_timed"][k] for k in st2["kernel_timed"]}
+    avg_ms = {k: (kms[k] / kcount[k] if kcount[k] else 0.0) for k in kms}
+    alg_bytes = {
+        # slot map + gathered rows + pooled out (nominal TBE bytes)
+        "forward": 4 * Tg * n + 4 * D * Tg * n + 4 * D * Tg * N,
+        # pooled grad in + occurrence list + per-unique segment/slot words + SGD read+write
+        "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 8 * D * U,
+        "surrogate": 8 * D * Tg * N,
+        "transfer": 4 * D * (m + ev),
+        "plan": 4 * Tg * n,
+    }
+    peak, peak_kind = peaks()
+    traffic = load_traffic()
+    total_ms = sum(kms.values()) or 1.0
+    kernels = {}
+    for k in ["plan", "transfer", "forward", "backward", "surrogate"]:
+        gbs = alg_bytes[k] / (avg_ms[k] * 1e-3) / 1e9 if avg_ms[k] else None
+        kernels[k] = {"avg_us": round(avg_ms[k] * 1e3, 3), "share": round(kms[k] / total_ms, 4),
+                      "alg_bytes_per_launch": int(alg_bytes[k]), "alg_GBs": None if gbs is None else round(gbs, 1)}
+    # dominant HBM-bound kernel (the Train stage: forward or backward)
+    dom = max(["forward", "backward"], key=lambda k: kms[k])
+    ach = kernels[dom]["alg_GBs"] or 0.0
+    tr_bytes = traffic.get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "traffic": tr_bytes,
+                "bytes_per_launch": int(alg_bytes[dom]),
+                "bytes_formula": ("4*T*n + 4*D*T*n + 4*D*T*N" if dom == "forward"
+                                  else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
+    train_ms = avg_ms["forward"] + avg_ms["backward"]
+    train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
+    link_GBs = alg_bytes["transfer"] / (avg_ms["transfer"] * 1e-3) / 1e9 if avg_ms["transfer"] else None
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.description, "config_key": args.config, "tables": T, "dim": D,
+                   "batch": N, "pooling": L, "zipf_alpha": cfg.alpha, "slots_total": sum(slots_all),
+                   "window": cfg.window, "preroll_batches": pre, "index_input": "device int32 (value)",
+                   "l2": "no flush: inputs larger than L2 (Storage %.2f GB, Hit-Map %.0f MB, host tables "
+                         "%.1f GB); every step reads a fresh batch" % (
+                             sum(slots_all) * D * 4 / 1e9, sum(cfg.rows) * 4 / 1e6, sum(cfg.rows) * D * 4 / 1e9),
+                   "parallelism": f"table-wise x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline,
+        "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
+                        "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
+        "host_link": {"kernel": "transfer", "alg_bytes_per_launch": int(alg_bytes["transfer"]),
+                      "alg_GBs": None if link_GBs is None else round(link_GBs, 2),
+                      "peak_h2d_GBs": 55.6, "peak_d2h_GBs": 57.0,
+                      "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)"},
+        "kernels": kernels,
+        "per_step": {"uniques": round(U, 1), "misses": round(m, 1), "evictions": round(ev, 1)},
+        "gpu_launches": int(gpu_launches),
+        "launches_per_step": {k: v / K for k, v in launches.items()},
+        "clocks": sampler.summary() if sampler else None,
+        "e2e": {"value": round(e2e_value, 2), "unit": "iters/s", "h2d_bytes_per_step": idx_bytes,
+                "d2h_bytes_per_step": stats_bytes, "ms_per_step": round(ms_e2e / K, 5),
+                "path": "sp_plan(host int32 indices, pinned) -> H2D on the plan stream; "
+                        "sp_copy_batch_stats D2H each step, read one step later"},
+        "preroll_s": round(t_pre, 2),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, trace, args.cpu_seconds)
+    sp.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

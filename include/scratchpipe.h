@@ -1,0 +1,215 @@
+/* scratchpipe.h — C ABI of the B200-native ScratchPipe hot path.
+ *
+ * ScratchPipe (Kwon & Rhu, ISCA'22, arXiv 2205.04702; PAPER.md = the LaTeX
+ * source, cited as P:<line>) keeps the full embedding tables in host memory
+ * and, because the sparse IDs of upcoming mini-batches are known ahead of
+ * time, plans a GPU scratchpad so that the Train stage always hits
+ * (P:159-163).  This library is that scratchpad on one B200:
+ *
+ *   sp_plan     [Plan]  (Alg. 1): index ingest, dedup,
+ *               Hit-Map probe, hit/miss, window-safe LRU victim selection
+ *               (past window P:840-861, future window P:864-884, superset
+ *               P:887-896), Hit-Map/Storage bookkeeping.
+ *               [Collect]+[Exchange]+[Insert] run fused as one
+ *               zero-copy transfer kernel: write back each victim row to the
+ *               host table, then pull the missed row into the freed slot.
+ *   sp_forward  [Training] part 1: EmbeddingBag gather-reduce.
+ *   sp_train    [Training] part 2: gradient duplication + coalescing
+ *                and the SGD update in place in the scratchpad
+ *               (P:713-715).
+ *   sp_flush    end-of-run write-back of every (dirty) resident row.
+ *
+ * Everything on the path runs in this library's sm_100a kernels; the
+ * caller supplies device memory for pooled outputs / gradients and a stream.
+ *
+ * Conventions
+ * - All calls return sp_status; no exceptions, no exit(), no host aborts.
+ * - Batch indices are laid out [T][N][L] (table, sample, lookup position),
+ *   int64 by default (SP_FLAG_INDEX_I32 for int32), host memory by default
+ *   (SP_FLAG_INDEX_DEVICE for a device pointer).
+ * - pooled / pooled_grad are DEVICE pointers, fp32, layout [T][N][D],
+ *   ordered on desc.stream like any CUDA library argument.
+ * - Host tables: caller-owned, row-major fp32 [rows[t]][dim], pinned
+ *   (cudaHostAlloc) or, with SP_FLAG_REGISTER_HOST, registered by the
+ *   library for the context's lifetime.  They are NOT coherent between
+ *   sp_create and sp_flush: resident rows are newer in HBM.
+ * - Errors found on the device (SP_ERR_INDEX_RANGE, SP_ERR_CAPACITY) are
+ *   latched in device memory and returned by the next call that observes
+ *   them (at the latest sp_flush); sp_last_error_batch() then gives the
+ *   (batch, table) where it happened.  After CAPACITY, INDEX_RANGE, CUDA
+ *   errors the context is poisoned: only sp_error_string, sp_last_error_batch,
+ *   sp_get_stats and sp_destroy remain valid.
+ * - One context per GPU; a context is not thread-safe.
+ */
+#ifndef SCRATCHPIPE_H
+#define SCRATCHPIPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+typedef struct sp_ctx sp_ctx;
+
+typedef enum {
+    SP_OK = 0,
+    SP_ERR_INVALID_ARG = 1,  /* bad descriptor / pointer / size                 */
+    SP_ERR_CAPACITY = 2,     /* no evictable slot: the window working set does  */
+                             /* not fit in Storage                */
+    SP_ERR_INDEX_RANGE = 3,  /* a sparse ID < 0 or >= rows[t]                   */
+    SP_ERR_STATE = 4,        /* call-order violation (see sp_forward/sp_train)  */
+    SP_ERR_CUDA = 5,         /* CUDA runtime error                              */
+    SP_ERR_NCCL = 6,         /* reserved                                        */
+    SP_ERR_OOM = 7           /* device or pinned allocation failed              */
+} sp_status;
+
+/* desc.flags */
+#define SP_FLAG_REGISTER_HOST (1u << 0) /* cudaHostRegister the host tables      */
+#define SP_FLAG_INDEX_I32     (1u << 1) /* batch indices are int32              */
+#define SP_FLAG_INDEX_DEVICE  (1u << 2) /* batch indices are a device pointer   */
+#define SP_FLAG_PROFILE       (1u << 3) /* CUDA events around every kernel ->   */
+                                        /* per-kernel times in sp_get_stats     */
+
+/* sp_create(tables, dim, slots, window) of the problem statement. */
+typedef struct {
+    int32_t num_tables;          /* T tables on THIS device (>= 1)                 */
+    const int64_t *rows;         /* [T] rows per table, 1 <= rows[t] < 2^32 - 1    */
+    float *const *host_tables;   /* [T] host pointers, rows[t] x dim fp32 each      */
+    int32_t dim;                 /* D, multiple of 4, 4 <= D <= 1024                */
+    const int64_t *slots;        /* [T] scratchpad rows per table (per-table        */
+                                 /* pools: one cache manager per table)     */
+    int32_t window;              /* w: past hold P = w, future hold F = w - 1;      */
+                                 /* w = 3 is the paper's 3 past + current + 2       */
+                                 /* future = six batches     */
+    int32_t past, future;        /* >= 0 overrides P / F (requires F <= P + 1);     */
+                                 /* -1 = derive from window                         */
+    int32_t batch_size, pooling; /* N bags per table, L lookups per bag (fixed)     */
+    int32_t device;              /* CUDA device ordinal                             */
+    void *stream;                /* cudaStream_t for sp_forward / sp_train /        */
+                                 /* sp_surrogate_grad (NULL = legacy default)       */
+    uint32_t flags;              /* SP_FLAG_*                                       */
+    int32_t log_factor;          /* LRU-log ring capacity per table =               */
+                                 /* log_factor * slots[t] + 4*N*L (0 -> 8)          */
+} sp_desc;
+
+typedef enum {
+    SP_K_PLAN = 0,      /* dedup + future probe + Plan (one launch per sp_plan)  */
+    SP_K_TRANSFER = 1,  /* fused Collect/Exchange/Insert (zero-copy)              */
+    SP_K_FORWARD = 2,   /* EmbeddingBag gather-reduce                             */
+    SP_K_BACKWARD = 3,  /* duplicate-coalescing segmented reduce + fused SGD      */
+    SP_K_SURROGATE = 4, /* harness MLP stand-in g = fmaf(gamma, pooled, delta)    */
+    SP_K_FLUSH = 5,     /* write-back of all resident rows                        */
+    SP_K_COUNT = 6
+} sp_kernel_kind;
+
+typedef struct {
+    int64_t pushed, planned, transferred, forwarded, trained;
+    /* cumulative over planned batches, summed over tables (device counters,  */
+    /* read with a plan-stream synchronisation)                               */
+    int64_t uniques, hits, misses, evictions;
+    int64_t h2d_index_bytes;        /* batch indices uploaded                  */
+    int64_t h2d_row_bytes;          /* missed rows pulled from host tables     */
+    int64_t d2h_row_bytes;          /* victim rows written back                */
+    int64_t kernel_launches[SP_K_COUNT];
+    double kernel_ms[SP_K_COUNT];   /* SP_FLAG_PROFILE only: summed CUDA-event */
+                                    /* durations of completed launches         */
+    int64_t kernel_timed[SP_K_COUNT];
+} sp_stats;
+
+int32_t sp_abi_version(void);
+
+/* Create a context: validates the descriptor, allocates Storage
+ * (sum slots x dim fp32), the Hit-Map, per-slot metadata, the LRU log and a
+ * ring of per-batch buffers in HBM of desc.device; creates the plan and
+ * transfer streams.  *out is NULL on failure. */
+sp_status sp_create(const sp_desc *desc, sp_ctx **out);
+
+/* Push the next mini-batch B(j) into the look-forward window.
+ * batch_indices: [T][N][L] (int64 | int32; host | device per flags).  Host
+ * indices are copied before return.  Device indices must stay unmodified
+ * until sp_forward of that batch has returned; they are read on the plan
+ * stream after all work previously enqueued on desc.stream.
+ * Dedups B(j), probes it as the future window of Plan(j - F) and enqueues
+ * Plan(j - F) (when j >= F).  Asynchronous: never waits for the GPU except
+ * to recycle a pinned staging buffer.  Returns SP_ERR_STATE if the caller is
+ * more than 16 batches ahead of sp_train. */
+sp_status sp_plan(sp_ctx *c, const void *batch_indices);
+
+/* Same as sp_plan with SP_FLAG_INDEX_DEVICE for this one call: dev_indices
+ * is a device pointer ([T][N][L], index width per SP_FLAG_INDEX_I32), read
+ * on the plan stream after all work previously enqueued on desc.stream; it
+ * must stay unmodified until sp_forward of that batch has returned. */
+sp_status sp_plan_device(sp_ctx *c, const void *dev_indices);
+
+/* No more batches: the future window truncates at the last batch (reading
+ * R9); enqueues the Plans of the last F batches. */
+sp_status sp_end_of_data(sp_ctx *c);
+
+/* Forward of the oldest untrained batch b into pooled [T][N][D] (device).
+ * Requires B(b + F) to have been pushed, or sp_end_of_data.  sp_forward and
+ * sp_train strictly alternate. */
+sp_status sp_forward(sp_ctx *c, float *pooled);
+
+/* Backward + SGD of the batch last passed to sp_forward: pooled_grad is
+ * [T][N][D] on the device (one gradient per reduced embedding);
+ * w <- fmaf(-lr, g_row, w) for every unique row, in place in Storage. */
+sp_status sp_train(sp_ctx *c, const float *pooled_grad, float lr);
+
+/* Harness utility (the MLP stand-in, not part of the method):
+ * grad[i] = fmaf(gamma, pooled[i], delta) for i < count (count = 0 means
+ * T*N*D; count must be a multiple of 4; device pointers, 16-byte aligned),
+ * on desc.stream. */
+sp_status sp_surrogate_grad(sp_ctx *c, const float *pooled, float *grad, int64_t count,
+                            float gamma, float delta);
+
+/* Enqueue (on desc.stream, after the work already enqueued there) an
+ * asynchronous copy of batch b's Plan counters into host_out[T][4]
+ * (U, hits, misses, evictions per table; host_out should be pinned).  Valid
+ * while batch b's ring entry is live (until batch b + 16 is pushed). */
+sp_status sp_copy_batch_stats(sp_ctx *c, int64_t b, uint32_t *host_out);
+
+/* Turn per-kernel CUDA-event timing (SP_FLAG_PROFILE) on or off. */
+sp_status sp_set_profiling(sp_ctx *c, int32_t on);
+
+/* Drain and write every resident row back to its host table; on return the
+ * host tables are coherent.  Requires every pushed batch to be trained (call
+ * sp_end_of_data first).  Synchronises the device. */
+sp_status sp_flush(sp_ctx *c);
+
+/* Free everything (unregisters host tables registered by the library). */
+sp_status sp_destroy(sp_ctx *c);
+
+/* Human-readable description of the last error (never NULL). */
+const char *sp_error_string(const sp_ctx *c);
+/* Batch / table of the latched device error (-1 if none or not device). */
+sp_status sp_last_error_batch(const sp_ctx *c, int64_t *batch, int32_t *table);
+
+/* Statistics (synchronises the plan stream to read device counters, and the
+ * streams whose profiled kernel events are pending). */
+sp_status sp_get_stats(sp_ctx *c, sp_stats *out);
+
+/* ---- introspection for parity tests (synchronise the plan stream) ---- */
+/* Plan record of batch b, table t, in the same format as the oracle's Part B:
+ * counts[4] = U, hits, misses, evictions; for k < U (arrays of capacity N*L):
+ * uniq[k] = k-th smallest unique ID, slot[k] = table-local Storage slot after
+ * the Plan, hit[k] = 1/0, evicted[k] = ID previously in the victim slot of a
+ * miss (-1 if vacant or a hit).  Valid while batch b's ring entry is live
+ * (until batch b + 16 is pushed). */
+sp_status sp_debug_plan(sp_ctx *c, int64_t b, int32_t t, int64_t *counts, int64_t *uniq,
+                        int64_t *slot, int64_t *hit, int64_t *evicted);
+/* Sorted resident IDs of table t as planned so far (Hit-Map view). */
+sp_status sp_debug_resident(sp_ctx *c, int32_t t, int64_t *ids, int64_t cap, int64_t *n);
+/* Per-slot view of table t: resident ID (-1 vacant), last_use (INT64_MIN if
+ * never used).  Arrays of slots[t] entries. */
+sp_status sp_debug_slots(sp_ctx *c, int32_t t, int64_t *resident, int64_t *last_use);
+/* Copy Storage rows [first, first+count) of table t to host (synchronises). */
+sp_status sp_debug_storage(sp_ctx *c, int32_t t, int64_t first, int64_t count, float *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCRATCHPIPE_H */

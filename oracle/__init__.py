@@ -73,6 +73,7 @@ def lib():
         L.orc_policy_resident.restype = ctypes.c_int64
         L.orc_policy_resident.argtypes = [P, ctypes.c_int32, i64p, ctypes.c_int64]
         L.orc_policy_slots.argtypes = [P, ctypes.c_int32, i64p, i64p]
+        L.orc_policy_set_full_sort.argtypes = [P, ctypes.c_int32]
         L.orc_fmaf_array.argtypes = [ctypes.c_int64, f32p, f32p, f32p, f32p]
         _lib = L
     return _lib
@@ -182,7 +183,8 @@ class PlanRecord:
 class Policy:
     """Part B: reference scratchpad policy (IDs only)."""
 
-    def __init__(self, rows: Sequence[int], slots: Sequence[int], past: int, future: int):
+    def __init__(self, rows: Sequence[int], slots: Sequence[int], past: int, future: int,
+                 full_sort: bool = False):
         self.rows = np.asarray(rows, dtype=np.int64)
         self.slots = np.asarray(slots, dtype=np.int64)
         self.T = len(rows)
@@ -191,6 +193,8 @@ class Policy:
                                           _p(self.slots, ctypes.c_int64), past, future)
         if not self._h:
             raise ValueError("bad policy config")
+        if full_sort:
+            lib().orc_policy_set_full_sort(self._h, 1)
 
     def close(self):
         if self._h:

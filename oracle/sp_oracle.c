@@ -241,6 +241,7 @@ typedef struct {
 
 struct orc_policy {
     int32_t T, P, F;
+    int32_t full_sort;     /* 1: always sort every candidate (cross-check mode) */
     pol_table *tab;
     int64_t *ids;          /* scratch for sorting a batch */
 };
@@ -286,6 +287,30 @@ static int cmp_cand(const void *a, const void *b) {
         if (x[i] != y[i]) return x[i] < y[i] ? -1 : 1;
     return 0;
 }
+
+/* move the k smallest triples of c[0..n) to c[0..k), ascending (bounded max-heap) */
+static void heap_sift(int64_t *h, int64_t k, int64_t i) {
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < k && cmp_cand(&h[3 * l], &h[3 * m]) > 0) m = l;
+        if (r < k && cmp_cand(&h[3 * r], &h[3 * m]) > 0) m = r;
+        if (m == i) return;
+        for (int j = 0; j < 3; j++) { int64_t x = h[3 * i + j]; h[3 * i + j] = h[3 * m + j]; h[3 * m + j] = x; }
+        i = m;
+    }
+}
+
+static void select_smallest(int64_t *c, int64_t n, int64_t k) {
+    for (int64_t i = k / 2 - 1; i >= 0; i--) heap_sift(c, k, i);
+    for (int64_t i = k; i < n; i++)
+        if (cmp_cand(&c[3 * i], &c[0]) < 0) {
+            for (int j = 0; j < 3; j++) c[j] = c[3 * i + j];
+            heap_sift(c, k, 0);
+        }
+    qsort(c, (size_t)k, 3 * sizeof(int64_t), cmp_cand);
+}
+
+void orc_policy_set_full_sort(orc_policy *p, int32_t on) { p->full_sort = on; }
 
 int32_t orc_policy_plan(orc_policy *p, const int64_t *trace, int64_t nb, int32_t N,
                         int32_t L, int64_t b, int64_t *counts, int64_t *uniq,
@@ -338,7 +363,10 @@ int32_t orc_policy_plan(orc_policy *p, const int64_t *trace, int64_t nb, int32_t
             nc++;
         }
         if (nc < nm) { if (err_table) *err_table = t; return ORC_ERR_CAPACITY; }
-        qsort(pt->cand, (size_t)nc, 3 * sizeof(int64_t), cmp_cand);
+        /* the first nm candidates in (last_use, resident, slot) order: the order is
+         * total, so selecting the nm smallest and sorting them equals sorting all */
+        if (!p->full_sort && nm > 0 && nm * 16 < nc) select_smallest(pt->cand, nc, nm);
+        else qsort(pt->cand, (size_t)nc, 3 * sizeof(int64_t), cmp_cand);
         /* 6. pair k-th miss with k-th victim */
         int64_t ne = 0, v = 0;
         for (int64_t k = 0; k < U; k++) {

@@ -68,6 +68,9 @@ int32_t orc_policy_plan(orc_policy *p, const int64_t *trace, int64_t nb, int32_t
                         int32_t L, int64_t b, int64_t *counts, int64_t *uniq,
                         int64_t *slot, int64_t *hit, int64_t *evicted,
                         int32_t *err_table);
+/* 1 = sort every candidate each Plan (cross-check of the default partial
+ * selection of the |misses| smallest, which yields the same victims) */
+void orc_policy_set_full_sort(orc_policy *p, int32_t on);
 /* sorted resident IDs of table t; returns count */
 int64_t orc_policy_resident(const orc_policy *p, int32_t t, int64_t *out, int64_t cap);
 /* slot-level view: resident id (-1 vacant) and last_use stamp per slot */

@@ -1,0 +1,275 @@
+"""Thin ctypes binding over libscratchpipe.so (include/scratchpipe.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+sm_100a kernels.  There is no CPU fallback: if the library is missing this
+module raises at import, and a context cannot be created without a CUDA
+device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libscratchpipe.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "scratchpipe.h")
+
+SP_OK, SP_ERR_INVALID_ARG, SP_ERR_CAPACITY, SP_ERR_INDEX_RANGE, SP_ERR_STATE, SP_ERR_CUDA, \
+    SP_ERR_NCCL, SP_ERR_OOM = range(8)
+STATUS_NAMES = {0: "SP_OK", 1: "SP_ERR_INVALID_ARG", 2: "SP_ERR_CAPACITY", 3: "SP_ERR_INDEX_RANGE",
+                4: "SP_ERR_STATE", 5: "SP_ERR_CUDA", 6: "SP_ERR_NCCL", 7: "SP_ERR_OOM"}
+SP_FLAG_REGISTER_HOST = 1 << 0
+SP_FLAG_INDEX_I32 = 1 << 1
+SP_FLAG_INDEX_DEVICE = 1 << 2
+SP_FLAG_PROFILE = 1 << 3
+KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush"]
+
+
+class SpDesc(ctypes.Structure):
+    _fields_ = [
+        ("num_tables", ctypes.c_int32),
+        ("rows", ctypes.POINTER(ctypes.c_int64)),
+        ("host_tables", ctypes.POINTER(ctypes.c_void_p)),
+        ("dim", ctypes.c_int32),
+        ("slots", ctypes.POINTER(ctypes.c_int64)),
+        ("window", ctypes.c_int32),
+        ("past", ctypes.c_int32),
+        ("future", ctypes.c_int32),
+        ("batch_size", ctypes.c_int32),
+        ("pooling", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+        ("flags", ctypes.c_uint32),
+        ("log_factor", ctypes.c_int32),
+    ]
+
+
+class SpStats(ctypes.Structure):
+    _fields_ = [
+        ("pushed", ctypes.c_int64), ("planned", ctypes.c_int64), ("transferred", ctypes.c_int64),
+        ("forwarded", ctypes.c_int64), ("trained", ctypes.c_int64),
+        ("uniques", ctypes.c_int64), ("hits", ctypes.c_int64), ("misses", ctypes.c_int64),
+        ("evictions", ctypes.c_int64),
+        ("h2d_index_bytes", ctypes.c_int64), ("h2d_row_bytes", ctypes.c_int64),
+        ("d2h_row_bytes", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64 * 6), ("kernel_ms", ctypes.c_double * 6),
+        ("kernel_timed", ctypes.c_int64 * 6),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    P = ctypes.c_void_p
+    S = ctypes.c_int
+    L.sp_abi_version.restype = ctypes.c_int32
+    L.sp_create.argtypes = [ctypes.POINTER(SpDesc), ctypes.POINTER(ctypes.c_void_p)]
+    L.sp_create.restype = S
+    for name, args in [("sp_plan", [P, P]), ("sp_plan_device", [P, P]),
+                       ("sp_copy_batch_stats", [P, ctypes.c_int64, P]),
+                       ("sp_set_profiling", [P, ctypes.c_int32]), ("sp_end_of_data", [P]), ("sp_forward", [P, P]),
+                       ("sp_train", [P, P, ctypes.c_float]),
+                       ("sp_surrogate_grad", [P, P, P, ctypes.c_int64, ctypes.c_float, ctypes.c_float]),
+                       ("sp_flush", [P]), ("sp_destroy", [P]),
+                       ("sp_last_error_batch", [P, i64p, ctypes.POINTER(ctypes.c_int32)]),
+                       ("sp_get_stats", [P, ctypes.POINTER(SpStats)]),
+                       ("sp_debug_plan", [P, ctypes.c_int64, ctypes.c_int32, i64p, i64p, i64p, i64p, i64p]),
+                       ("sp_debug_resident", [P, ctypes.c_int32, i64p, ctypes.c_int64, i64p]),
+                       ("sp_debug_slots", [P, ctypes.c_int32, i64p, i64p]),
+                       ("sp_debug_storage", [P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, P])]:
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = S
+    L.sp_error_string.argtypes = [P]
+    L.sp_error_string.restype = ctypes.c_char_p
+    return L
+
+
+lib = _load()
+
+
+def header_symbols() -> List[str]:
+    """Every function the public header declares."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sp_[a-z_]+)\s*\(", src)))
+
+
+class SpError(RuntimeError):
+    def __init__(self, status: int, msg: str, batch: int = -1, table: int = -1):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status, self.batch, self.table = status, batch, table
+
+
+def _i64(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+class ScratchPipe:
+    """One scratchpad context (the embedding tables of one GPU).
+
+    host_tables: list of pinned CPU float32 torch tensors [rows_t, dim] (or any
+    objects exposing data_ptr()).  With register_host=True ordinary host memory
+    is registered by the library instead.
+    """
+
+    def __init__(self, rows: Sequence[int], host_tables, dim: int, slots: Sequence[int],
+                 batch_size: int, pooling: int, window: int = 3, past: int = -1, future: int = -1,
+                 device: int = 0, stream=None, index_dtype: str = "int64", index_on_device: bool = False,
+                 register_host: bool = False, profile: bool = False, log_factor: int = 0):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("ScratchPipe needs a CUDA device (no CPU fallback)")
+        self.T, self.D, self.N, self.L = len(rows), dim, batch_size, pooling
+        self.device = device
+        self._rows = np.ascontiguousarray(rows, dtype=np.int64)
+        self._slots = np.ascontiguousarray(slots, dtype=np.int64)
+        self._tables = list(host_tables)  # keep alive
+        self._hp = (ctypes.c_void_p * self.T)(*[t.data_ptr() for t in self._tables])
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        flags = 0
+        if register_host:
+            flags |= SP_FLAG_REGISTER_HOST
+        if index_dtype == "int32":
+            flags |= SP_FLAG_INDEX_I32
+        if index_on_device:
+            flags |= SP_FLAG_INDEX_DEVICE
+        if profile:
+            flags |= SP_FLAG_PROFILE
+        self.index_dtype, self.index_on_device = index_dtype, index_on_device
+        d = SpDesc(self.T, _i64(self._rows), self._hp, dim, _i64(self._slots), window, past, future,
+                   batch_size, pooling, device, ctypes.c_void_p(stream.cuda_stream), flags, log_factor)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            st = lib.sp_create(ctypes.byref(d), ctypes.byref(h))
+        if st != SP_OK:
+            raise SpError(st, "sp_create failed")
+        self._h = h
+        if past < 0 or future < 0:
+            past, future = window, max(window - 1, 0)
+        self.P, self.F = past, future
+        self._pooled = None
+
+    # ------------------------------------------------------------------ core
+    def _check(self, st: int):
+        if st != SP_OK:
+            b = ctypes.c_int64(-1)
+            t = ctypes.c_int32(-1)
+            lib.sp_last_error_batch(self._h, ctypes.byref(b), ctypes.byref(t))
+            raise SpError(st, lib.sp_error_string(self._h).decode(), b.value, t.value)
+
+    def plan(self, idx):
+        """Push the next batch [T][N][L] (torch tensor or numpy array)."""
+        import torch
+        if isinstance(idx, np.ndarray):
+            idx = torch.from_numpy(idx)
+        want = torch.int32 if self.index_dtype == "int32" else torch.int64
+        if idx.dtype != want:
+            raise TypeError(f"indices must be {want}")
+        if idx.numel() != self.T * self.N * self.L:
+            raise ValueError("indices must have T*N*L elements")
+        if self.index_on_device != idx.is_cuda:
+            raise ValueError("index device does not match index_on_device")
+        idx = idx.contiguous()
+        self._last_idx = idx  # keep alive (device indices are read asynchronously)
+        self._check(lib.sp_plan(self._h, ctypes.c_void_p(idx.data_ptr())))
+
+    def plan_device(self, idx):
+        """Push a device-resident batch (any context): read on the plan stream."""
+        want = "int32" if self.index_dtype == "int32" else "int64"
+        if not idx.is_cuda or str(idx.dtype) != f"torch.{want}" or not idx.is_contiguous():
+            raise TypeError(f"device indices must be contiguous cuda {want}")
+        self._last_idx = idx
+        self._check(lib.sp_plan_device(self._h, ctypes.c_void_p(idx.data_ptr())))
+
+    def copy_batch_stats(self, b: int, host_out):
+        """Async D2H of batch b's per-table (U, hits, misses, evictions) into a
+        pinned int32 tensor [T][4], ordered on the context's stream."""
+        self._check(lib.sp_copy_batch_stats(self._h, b, ctypes.c_void_p(host_out.data_ptr())))
+
+    def set_profiling(self, on: bool):
+        self._check(lib.sp_set_profiling(self._h, 1 if on else 0))
+
+    def end_of_data(self):
+        self._check(lib.sp_end_of_data(self._h))
+
+    def forward(self, out=None):
+        import torch
+        if out is None:
+            out = torch.empty((self.T, self.N, self.D), dtype=torch.float32, device=f"cuda:{self.device}")
+        self._check(lib.sp_forward(self._h, ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def train(self, grad, lr: float):
+        self._check(lib.sp_train(self._h, ctypes.c_void_p(grad.data_ptr()), float(lr)))
+
+    def surrogate(self, pooled, gamma: float, delta: float, out=None):
+        import torch
+        if out is None:
+            out = torch.empty_like(pooled)
+        if not (pooled.is_contiguous() and out.is_contiguous() and out.numel() == pooled.numel()):
+            raise ValueError("surrogate: contiguous tensors of equal size required")
+        self._check(lib.sp_surrogate_grad(self._h, ctypes.c_void_p(pooled.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr()), pooled.numel(),
+                                          float(gamma), float(delta)))
+        return out
+
+    def flush(self):
+        self._check(lib.sp_flush(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.sp_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def stats(self) -> dict:
+        s = SpStats()
+        st = lib.sp_get_stats(self._h, ctypes.byref(s))
+        out = {k: getattr(s, k) for k, _ in SpStats._fields_[:12]}
+        out["kernel_launches"] = dict(zip(KERNEL_KINDS, list(s.kernel_launches)))
+        out["kernel_ms"] = dict(zip(KERNEL_KINDS, list(s.kernel_ms)))
+        out["kernel_timed"] = dict(zip(KERNEL_KINDS, list(s.kernel_timed)))
+        out["status"] = st
+        return out
+
+    # --------------------------------------------------------- introspection
+    def debug_plan(self, b: int, t: int) -> dict:
+        n = self.N * self.L
+        counts = np.zeros(4, np.int64)
+        uniq, slot, hit, ev = (np.empty(n, np.int64) for _ in range(4))
+        self._check(lib.sp_debug_plan(self._h, b, t, _i64(counts), _i64(uniq), _i64(slot), _i64(hit), _i64(ev)))
+        U = int(counts[0])
+        return {"U": U, "hits": int(counts[1]), "misses": int(counts[2]), "evictions": int(counts[3]),
+                "uniq": uniq[:U].copy(), "slot": slot[:U].copy(), "hit": hit[:U].astype(bool),
+                "evicted": ev[:U].copy()}
+
+    def debug_resident(self, t: int) -> np.ndarray:
+        n = ctypes.c_int64(0)
+        self._check(lib.sp_debug_resident(self._h, t, None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, np.int64)
+        self._check(lib.sp_debug_resident(self._h, t, _i64(out), n.value, ctypes.byref(n)))
+        return out
+
+    def debug_slots(self, t: int):
+        S = int(self._slots[t])
+        res, lu = np.empty(S, np.int64), np.empty(S, np.int64)
+        self._check(lib.sp_debug_slots(self._h, t, _i64(res), _i64(lu)))
+        return res, lu
+
+    def debug_storage(self, t: int, first: int = 0, count: Optional[int] = None) -> np.ndarray:
+        if count is None:
+            count = int(self._slots[t]) - first
+        out = np.empty((count, self.D), np.float32)
+        self._check(lib.sp_debug_storage(self._h, t, first, count, out.ctypes.data_as(ctypes.c_void_p)))
+        return out

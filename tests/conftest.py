@@ -25,3 +25,15 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionstart(session):
+    # build the in-tree libraries if a fresh checkout lacks them (no JIT at import)
+    import oracle
+    oracle.build()
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_sp_build", os.path.join(ROOT, "paper_2205_04702_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()

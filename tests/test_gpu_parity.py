@@ -1,0 +1,176 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle.
+
+Bar (BASELINE.json north_star): unique / hit / miss / victim / evicted /
+resident sets and slot stamps bit-exact; pooled outputs bit-exact (same fp32
+left fold); final host tables within max relative error 1e-5 (bit-exact
+expected: the coalesced gradient is an fp64 sum on both sides, rounded once).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import Policy
+from paper_2205_04702_b200 import SP_ERR_CAPACITY, SP_ERR_INDEX_RANGE, ScratchPipe, SpError
+from paper_2205_04702_b200.harness import run_loop
+from workload import CONFIGS, sample_trace
+from tests.gpu_helpers import max_window_union, pinned_tables, run_parity
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def _assert_tables(rep, exact=True):
+    t = rep["tables"]
+    assert t["max_rel"] <= TOL, t
+    if exact:
+        assert t["mismatch"] == 0, t
+
+
+def test_tiny_config_parity():
+    c = CONFIGS["tiny"]
+    rep = run_parity(c.rows, c.slots, c.dim, c.batch, c.pooling, c.num_batches, 3, 2,
+                     alpha=c.alpha, trace_seed=c.trace_seed, init_seed=c.init_seed,
+                     gde=(c.gamma, c.delta, c.eta))
+    assert rep["plans"] == c.num_batches and rep["pooled"] == c.num_batches
+    assert rep["evictions"] > 0
+    _assert_tables(rep)
+
+
+@pytest.mark.parametrize("P,F", [(3, 2), (2, 1), (1, 1), (0, 0), (4, 3), (3, 0), (1, 2)])
+def test_window_variants_policy_and_values(P, F):
+    rows, D, N, L, nb = [300, 64, 1000], 8, 16, 3, 40
+    tr = sample_trace(rows, N, L, 0.9, nb, 31 + P * 7 + F)
+    slots = [max_window_union(tr.numpy(), t, P, F) + 2 for t in range(3)]
+    slots = [min(s, R) for s, R in zip(slots, rows)]
+    rep = run_parity(rows, slots, D, N, L, nb, P, F, trace=tr, gde=(0.5, 0.01, 0.02))
+    assert rep["evictions"] > 0
+    _assert_tables(rep)
+
+
+def test_log_compaction_and_heavy_eviction():
+    # log_factor=1: the LRU log ring is S_t + 4n entries and must compact often
+    rows, D, N, L, nb = [500, 200], 16, 24, 2, 80
+    tr = sample_trace(rows, N, L, 0.7, nb, 77)
+    slots = [max_window_union(tr.numpy(), t, 3, 2) + 1 for t in range(2)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr, log_factor=1)
+    assert rep["evictions"] > 500
+    _assert_tables(rep)
+
+
+@pytest.mark.parametrize("D", [4, 12, 32, 64, 128, 256])
+def test_dims(D):
+    rows, N, L, nb = [400, 90], 8, 5, 16
+    tr = sample_trace(rows, N, L, 1.0, nb, D)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 3) for t, R in enumerate(rows)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr, gde=(0.5, 0.01, 0.05))
+    _assert_tables(rep)
+
+
+def test_hot_segments_multichunk_backward():
+    # 3-row table: every row occurs hundreds of times per batch -> multi-chunk
+    rows, D, N, L, nb = [3, 7, 5000], 16, 256, 4, 10
+    tr = sample_trace(rows, N, L, 1.05, nb, 5)
+    slots = [3, 7, min(5000, max_window_union(tr.numpy(), 2, 3, 2) + 5)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr,
+                     gde=(float(np.float32(0.5 / N)), float(np.float32(0.01 / N)), 0.5))
+    _assert_tables(rep, exact=False)
+
+
+def test_large_batch_radix_sort_path():
+    # N*L = 16800 > 16384: the global-memory radix-sort dedup path
+    rows, D, N, L, nb = [60000, 300], 8, 4200, 4, 9
+    tr = sample_trace(rows, N, L, 0.9, nb, 9)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 10) for t, R in enumerate(rows)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr, check_slots=False,
+                     gde=(float(np.float32(0.5 / N)), float(np.float32(0.01 / N)), 1.0))
+    _assert_tables(rep, exact=False)
+
+
+@pytest.mark.parametrize("index_dtype,on_device", [("int32", False), ("int64", True), ("int32", True)])
+def test_index_formats(index_dtype, on_device):
+    c = CONFIGS["tiny"]
+    rep = run_parity(c.rows, c.slots, c.dim, c.batch, c.pooling, c.num_batches, 3, 2,
+                     alpha=c.alpha, index_dtype=index_dtype, index_on_device=on_device)
+    _assert_tables(rep)
+
+
+def test_register_host_flag():
+    c = CONFIGS["tiny"]
+    rep = run_parity(c.rows, c.slots, c.dim, c.batch, c.pooling, 8, 3, 2, alpha=c.alpha,
+                     register_host=True, profile=True)
+    st = rep["stats"]
+    assert st["kernel_timed"]["forward"] == 8 and st["kernel_ms"]["backward"] > 0
+    _assert_tables(rep)
+
+
+def test_capacity_error_at_oracle_batch_and_table():
+    rows, D, N, L, nb = [400, 400], 8, 8, 2, 40
+    tr = sample_trace(rows, N, L, 0.5, nb, 3)
+    slots = [200, 30]   # table 1 too small for its window working set
+    pol = Policy(rows, slots, 3, 2)
+    from oracle import OracleError
+    want = None
+    try:
+        for b in range(nb):
+            pol.plan(tr.numpy(), b)
+    except OracleError as e:
+        want = (e.batch, e.table)
+    assert want is not None
+    tables = pinned_tables(rows, D, 1)
+    sp = ScratchPipe(rows, tables, D, slots, N, L)
+    with pytest.raises(SpError) as ei:
+        run_loop(sp, tr, 0.5, 0.01, 0.01)
+    assert ei.value.status == SP_ERR_CAPACITY
+    assert (ei.value.batch, ei.value.table) == want
+    sp.close()
+
+
+def test_index_range_error():
+    rows, D, N, L, nb = [100, 50], 8, 4, 2, 12
+    tr = sample_trace(rows, N, L, 1.0, nb, 4)
+    tr[6, 1, 2, 1] = 50  # out of range for table 1
+    tables = pinned_tables(rows, D, 1)
+    sp = ScratchPipe(rows, tables, D, [60, 40], N, L)
+    with pytest.raises(SpError) as ei:
+        run_loop(sp, tr, 0.5, 0.01, 0.01)
+    assert ei.value.status == SP_ERR_INDEX_RANGE
+    assert (ei.value.batch, ei.value.table) == (6, 1)
+    sp.close()
+
+
+def test_call_order_errors():
+    rows, D, N, L = [50], 4, 2, 1
+    tables = pinned_tables(rows, D, 1)
+    sp = ScratchPipe(rows, tables, D, [20], N, L)
+    pooled = torch.empty((1, N, D), device="cuda")
+    with pytest.raises(SpError):
+        sp.forward(pooled)                  # nothing planned
+    sp.plan(torch.zeros((1, N, L), dtype=torch.int64))
+    with pytest.raises(SpError):
+        sp.train(pooled, 0.1)               # train before forward
+    sp.end_of_data()
+    sp.forward(pooled)
+    with pytest.raises(SpError):
+        sp.forward(pooled)                  # forward twice
+    sp.train(pooled, 0.0)
+    sp.flush()
+    sp.close()
+
+
+def test_kaggle_full_size_parity_sampled():
+    """BASELINE configs[1] at full size (26 Criteo-Kaggle tables, D=64,
+    N=2048), int32 device indices as bench.py runs them, 1% slots so that
+    evictions start within the checked batches; every plan record bit-exact,
+    every pooled output bit-exact, sampled final rows within 1e-5."""
+    c = CONFIGS["kaggle"]
+    nb = 16
+    tr = sample_trace(c.rows, c.batch, c.pooling, c.alpha, nb, c.trace_seed)
+    # tightest safe Storage per table: evictions start within the checked batches
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 64) for t, R in enumerate(c.rows)]
+    g, d, e = c.surrogate()
+    rep = run_parity(c.rows, slots, c.dim, c.batch, c.pooling, nb, 3, 2, trace=tr,
+                     init_seed=c.init_seed, gde=(g, d, e),
+                     index_dtype="int32", index_on_device=True, check_slots=False,
+                     sample_rows=4000)
+    assert rep["plans"] == nb and rep["evictions"] > 1000
+    _assert_tables(rep, exact=False)

@@ -220,3 +220,16 @@ def test_worst_case_storage_formula():
     from paper_2205_04702_b200.sizing import worst_case_storage_bytes
     assert worst_case_storage_bytes(tables=8, pooling=20, batch=2048, dim=128, window=3) == 1006632960
     assert 1006632960 == 960 * 2 ** 20
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_partial_selection_equals_full_sort(seed):
+    """The oracle's default picks the |misses| smallest candidates with a
+    bounded heap; sorting every candidate must give identical plans."""
+    rows, slots, N, L, nb = [2000, 500], [900, 300], 8, 2, 60
+    tr = sample_trace(rows, N, L, 0.9, nb, 50 + seed).numpy()
+    a, b = Policy(rows, slots, 3, 2), Policy(rows, slots, 3, 2, full_sort=True)
+    for bb in range(nb):
+        ra, rb = a.plan(tr, bb), b.plan(tr, bb)
+        for x, y in zip(ra, rb):
+            assert np.array_equal(x.slot, y.slot) and np.array_equal(x.evicted, y.evicted)
