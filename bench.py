@@ -176,7 +176,7 @@ def cpu_baseline(cfg, trace_dev, seconds):
     g, d, e = cfg.surrogate()
     pol = Policy(cfg.rows, cfg.slots, cfg.window, max(cfg.window - 1, 0))
     orc = UncachedTrainer(cfg.rows, cfg.dim, cfg.batch, cfg.pooling, cfg.init_seed)
-    chunk = 16
+    chunk = 1024
     tr = trace_dev[:chunk].to(torch.int64).cpu().numpy()
     n = 0
     t0 = time.perf_counter()

@@ -728,7 +728,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->h2d_index_bytes = c->h2d_index_bytes;
     o->h2d_row_bytes = (int64_t)cum[2] * c->D * 4;
     o->d2h_row_bytes = (int64_t)cum[3] * c->D * 4;
-    if (c->flags & SP_FLAG_PROFILE) {
+    if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);
         cudaStreamSynchronize(c->compute);
         harvest_profile(c, true);
