@@ -322,6 +322,8 @@ def run_ours(args):
         train_step(push_dev)
     sp.set_profiling(False)
     st2 = sp.stats()
+    if os.environ.get("SP_TIMELINE"):
+        json.dump(sp.timeline(), open(os.environ["SP_TIMELINE"], "w"))
     # ---- e2e: host indices through the public API, D2H of every step's Plan counters
     assert state["pushed"] == nb_dev + ahead
     for k in range(W):
@@ -357,14 +359,15 @@ def run_ours(args):
         # pooled grad in + occurrence list + per-unique segment/slot words + SGD read+write
         "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 8 * D * U,
         "surrogate": 8 * D * Tg * N,
-        "transfer": 4 * D * (m + ev),
+        "transfer": 4 * D * m + 8 * D * ev,      # pull (PCIe read) + victim staging (HBM r/w)
+        "writeback": 4 * D * ev,
         "plan": 4 * Tg * n,
     }
     peak, peak_kind = peaks()
     traffic = load_traffic()
     total_ms = sum(kms.values()) or 1.0
     kernels = {}
-    for k in ["plan", "transfer", "forward", "backward", "surrogate"]:
+    for k in ["plan", "transfer", "writeback", "forward", "backward", "surrogate"]:
         gbs = alg_bytes[k] / (avg_ms[k] * 1e-3) / 1e9 if avg_ms[k] else None
         kernels[k] = {"avg_us": round(avg_ms[k] * 1e3, 3), "share": round(kms[k] / total_ms, 4),
                       "alg_bytes_per_launch": int(alg_bytes[k]), "alg_GBs": None if gbs is None else round(gbs, 1)}
@@ -380,7 +383,8 @@ def run_ours(args):
                                   else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
     train_ms = avg_ms["forward"] + avg_ms["backward"]
     train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
-    link_GBs = alg_bytes["transfer"] / (avg_ms["transfer"] * 1e-3) / 1e9 if avg_ms["transfer"] else None
+    link_GBs = 4 * D * m / (avg_ms["transfer"] * 1e-3) / 1e9 if avg_ms["transfer"] else None
+    wb_GBs = alg_bytes["writeback"] / (avg_ms["writeback"] * 1e-3) / 1e9 if avg_ms.get("writeback") else None
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
@@ -396,8 +400,10 @@ def run_ours(args):
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
-        "host_link": {"kernel": "transfer", "alg_bytes_per_launch": int(alg_bytes["transfer"]),
-                      "alg_GBs": None if link_GBs is None else round(link_GBs, 2),
+        "host_link": {"pull_kernel": "transfer", "pull_bytes_per_launch": int(4 * D * m),
+                      "pull_GBs": None if link_GBs is None else round(link_GBs, 2),
+                      "writeback_bytes_per_launch": int(alg_bytes["writeback"]),
+                      "writeback_GBs": None if wb_GBs is None else round(wb_GBs, 2),
                       "peak_h2d_GBs": 55.6, "peak_d2h_GBs": 57.0,
                       "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)"},
         "kernels": kernels,

@@ -10,9 +10,10 @@
  *               Hit-Map probe, hit/miss, window-safe LRU victim selection
  *               (past window P:840-861, future window P:864-884, superset
  *               P:887-896), Hit-Map/Storage bookkeeping.
- *               [Collect]+[Exchange]+[Insert] run fused as one
- *               zero-copy transfer kernel: write back each victim row to the
- *               host table, then pull the missed row into the freed slot.
+ *               [Collect]+[Exchange]+[Insert] run as two
+ *               SM-issued zero-copy kernels split by link direction: a pull
+ *               (victim staged in HBM, missed row into the freed slot) and a
+ *               rate-limited write-back of the staged victims.
  *   sp_forward  [Training] part 1: EmbeddingBag gather-reduce.
  *   sp_train    [Training] part 2: gradient duplication + coalescing
  *                and the SGD update in place in the scratchpad
@@ -94,16 +95,20 @@ typedef struct {
     uint32_t flags;              /* SP_FLAG_*                                       */
     int32_t log_factor;          /* LRU-log ring capacity per table =               */
                                  /* log_factor * slots[t] + 4*N*L (0 -> 8)          */
+    int32_t pull_ctas;           /* CTAs of the host-row pull kernel (0 -> 16)      */
+    int32_t writeback_ctas;      /* CTAs of the rate-limited write-back (0 -> 2)    */
 } sp_desc;
 
 typedef enum {
     SP_K_PLAN = 0,      /* dedup + future probe + Plan (one launch per sp_plan)  */
-    SP_K_TRANSFER = 1,  /* fused Collect/Exchange/Insert (zero-copy)              */
+    SP_K_TRANSFER = 1,  /* Collect/Exchange/Insert, host->HBM direction: victims  */
+                        /* staged in HBM, missed rows pulled into freed slots     */
     SP_K_FORWARD = 2,   /* EmbeddingBag gather-reduce                             */
     SP_K_BACKWARD = 3,  /* duplicate-coalescing segmented reduce + fused SGD      */
     SP_K_SURROGATE = 4, /* harness MLP stand-in g = fmaf(gamma, pooled, delta)    */
     SP_K_FLUSH = 5,     /* write-back of all resident rows                        */
-    SP_K_COUNT = 6
+    SP_K_WRITEBACK = 6, /* HBM->host direction: staged victims to host tables     */
+    SP_K_COUNT = 7
 } sp_kernel_kind;
 
 typedef struct {
@@ -133,8 +138,8 @@ sp_status sp_create(const sp_desc *desc, sp_ctx **out);
  * indices are copied before return.  Device indices must stay unmodified
  * until sp_forward of that batch has returned; they are read on the plan
  * stream after all work previously enqueued on desc.stream.
- * Dedups B(j), probes it as the future window of Plan(j - F) and enqueues
- * Plan(j - F) (when j >= F).  Asynchronous: never waits for the GPU except
+ * One kernel launch dedups B(j) and, beside it, runs Plan(j - F - 1), whose
+ * future window B(j - 1) was deduped by the previous call (when j > F).  Asynchronous: never waits for the GPU except
  * to recycle a pinned staging buffer.  Returns SP_ERR_STATE if the caller is
  * more than 16 batches ahead of sp_train. */
 sp_status sp_plan(sp_ctx *c, const void *batch_indices);
@@ -150,7 +155,7 @@ sp_status sp_plan_device(sp_ctx *c, const void *dev_indices);
 sp_status sp_end_of_data(sp_ctx *c);
 
 /* Forward of the oldest untrained batch b into pooled [T][N][D] (device).
- * Requires B(b + F) to have been pushed, or sp_end_of_data.  sp_forward and
+ * Requires B(b + F + 1) to have been pushed, or sp_end_of_data.  sp_forward and
  * sp_train strictly alternate. */
 sp_status sp_forward(sp_ctx *c, float *pooled);
 
@@ -172,8 +177,16 @@ sp_status sp_surrogate_grad(sp_ctx *c, const float *pooled, float *grad, int64_t
  * while batch b's ring entry is live (until batch b + 16 is pushed). */
 sp_status sp_copy_batch_stats(sp_ctx *c, int64_t b, uint32_t *host_out);
 
-/* Turn per-kernel CUDA-event timing (SP_FLAG_PROFILE) on or off. */
+/* Turn per-kernel CUDA-event timing (SP_FLAG_PROFILE) on or off.  Turning it
+ * on records a reference event on desc.stream and clears the timeline. */
 sp_status sp_set_profiling(sp_ctx *c, int32_t on);
+
+/* Timeline of profiled kernel launches since profiling was last turned on:
+ * kind (sp_kernel_kind), batch index, start / end in ms relative to the
+ * reference event (CUDA events, all streams).  Synchronises the device;
+ * writes min(cap, *n) records. */
+sp_status sp_get_timeline(sp_ctx *c, int32_t *kind, int64_t *batch, double *start_ms,
+                          double *end_ms, int64_t cap, int64_t *n);
 
 /* Drain and write every resident row back to its host table; on return the
  * host tables are coherent.  Requires every pushed batch to be trained (call

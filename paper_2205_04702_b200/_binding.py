@@ -26,7 +26,7 @@ SP_FLAG_REGISTER_HOST = 1 << 0
 SP_FLAG_INDEX_I32 = 1 << 1
 SP_FLAG_INDEX_DEVICE = 1 << 2
 SP_FLAG_PROFILE = 1 << 3
-KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush"]
+KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush", "writeback"]
 
 
 class SpDesc(ctypes.Structure):
@@ -45,6 +45,8 @@ class SpDesc(ctypes.Structure):
         ("stream", ctypes.c_void_p),
         ("flags", ctypes.c_uint32),
         ("log_factor", ctypes.c_int32),
+        ("pull_ctas", ctypes.c_int32),
+        ("writeback_ctas", ctypes.c_int32),
     ]
 
 
@@ -56,8 +58,8 @@ class SpStats(ctypes.Structure):
         ("evictions", ctypes.c_int64),
         ("h2d_index_bytes", ctypes.c_int64), ("h2d_row_bytes", ctypes.c_int64),
         ("d2h_row_bytes", ctypes.c_int64),
-        ("kernel_launches", ctypes.c_int64 * 6), ("kernel_ms", ctypes.c_double * 6),
-        ("kernel_timed", ctypes.c_int64 * 6),
+        ("kernel_launches", ctypes.c_int64 * 7), ("kernel_ms", ctypes.c_double * 7),
+        ("kernel_timed", ctypes.c_int64 * 7),
     ]
 
 
@@ -74,7 +76,8 @@ def _load():
     L.sp_create.restype = S
     for name, args in [("sp_plan", [P, P]), ("sp_plan_device", [P, P]),
                        ("sp_copy_batch_stats", [P, ctypes.c_int64, P]),
-                       ("sp_set_profiling", [P, ctypes.c_int32]), ("sp_end_of_data", [P]), ("sp_forward", [P, P]),
+                       ("sp_set_profiling", [P, ctypes.c_int32]),
+                       ("sp_get_timeline", [P, P, P, P, P, ctypes.c_int64, i64p]), ("sp_end_of_data", [P]), ("sp_forward", [P, P]),
                        ("sp_train", [P, P, ctypes.c_float]),
                        ("sp_surrogate_grad", [P, P, P, ctypes.c_int64, ctypes.c_float, ctypes.c_float]),
                        ("sp_flush", [P]), ("sp_destroy", [P]),
@@ -123,7 +126,8 @@ class ScratchPipe:
     def __init__(self, rows: Sequence[int], host_tables, dim: int, slots: Sequence[int],
                  batch_size: int, pooling: int, window: int = 3, past: int = -1, future: int = -1,
                  device: int = 0, stream=None, index_dtype: str = "int64", index_on_device: bool = False,
-                 register_host: bool = False, profile: bool = False, log_factor: int = 0):
+                 register_host: bool = False, profile: bool = False, log_factor: int = 0,
+                 pull_ctas: int = 0, writeback_ctas: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("ScratchPipe needs a CUDA device (no CPU fallback)")
@@ -147,7 +151,8 @@ class ScratchPipe:
             flags |= SP_FLAG_PROFILE
         self.index_dtype, self.index_on_device = index_dtype, index_on_device
         d = SpDesc(self.T, _i64(self._rows), self._hp, dim, _i64(self._slots), window, past, future,
-                   batch_size, pooling, device, ctypes.c_void_p(stream.cuda_stream), flags, log_factor)
+                   batch_size, pooling, device, ctypes.c_void_p(stream.cuda_stream), flags, log_factor,
+                   pull_ctas, writeback_ctas)
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             st = lib.sp_create(ctypes.byref(d), ctypes.byref(h))
@@ -198,6 +203,18 @@ class ScratchPipe:
 
     def set_profiling(self, on: bool):
         self._check(lib.sp_set_profiling(self._h, 1 if on else 0))
+
+    def timeline(self):
+        """[(kind, batch, start_ms, end_ms)] of profiled launches (synchronises)."""
+        n = ctypes.c_int64(0)
+        self._check(lib.sp_get_timeline(self._h, None, None, None, None, 0, ctypes.byref(n)))
+        k = np.empty(n.value, np.int32)
+        b = np.empty(n.value, np.int64)
+        s0 = np.empty(n.value, np.float64)
+        s1 = np.empty(n.value, np.float64)
+        ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        self._check(lib.sp_get_timeline(self._h, ptr(k), ptr(b), ptr(s0), ptr(s1), n.value, ctypes.byref(n)))
+        return [(KERNEL_KINDS[int(k[i])], int(b[i]), float(s0[i]), float(s1[i])) for i in range(n.value)]
 
     def end_of_data(self):
         self._check(lib.sp_end_of_data(self._h))

@@ -1,31 +1,38 @@
 // k_plan.cu — the [Plan] stage (Alg. 1) as ONE
-// kernel launch per sp_plan call, one CTA per embedding table (one cache
-// manager per table; tables are independent, so CTAs never
-// synchronise with each other).
+// kernel launch per sp_plan call.  Tables are independent (one cache manager
+// per table), so every CTA works on one table and CTAs never
+// synchronise with each other.  A launch at push(j) has 2T CTAs:
 //
-// CTA t of k_push does, for the batch B(j) entering the window and the batch
-// B(b), b = j - F, leaving the look-ahead queue:
-//   A1  ingest + range check of B(j)[t]
-//   A2  dedup: sort (id, occurrence) pairs, mark heads, segment offsets
-//       (Alg. 1 walks raw IDs; dedup first is equivalent, reading R5)
-//   A3  backward work list: chunks of <= CH occurrences per unique
-//   A4  future probe: slots of resident IDs of B(j) get next_need = j
-//       (future window, RAW-4 rule; one-shot probe, reading R12)
-//   B1  probe B(b): hit -> last_use = b (HoldMask |= MSB, Alg. 1)
-//   B2  misses compacted in ascending ID order
-//   B3  victims: walk the LRU log from its head; a slot is a candidate iff
-//       last_use <= b-P-1 (past window) and next_need <= b
-//       (future window); first |misses| candidates in (last_use, ID) order
-//       (LRU, reading R8); too few -> SP_ERR_CAPACITY
-//   B4  pair k-th miss with k-th victim (reading R6): Hit-Map / resident /
-//       stamps updated, evict + fill lists for the transfer kernel
-//   B5  append this batch's slots to the LRU log (compacting it if full)
-//   B6  slot map for the Train stage (frozen at Plan, reading R13)
+// CTAs [T, 2T) — dedup of the batch B(j) entering the window (pure function
+// of the batch, no scratchpad state):
+//   D1  ingest + range check of B(j)[t]
+//   D2  stable LSD radix sort of (id, occurrence) pairs by id; heads,
+//       unique IDs, segment offsets (Alg. 1 walks raw IDs; deduplicating
+//       first is equivalent, reading R5)
+//   D3  backward work list: chunk records of <= CH occurrences per unique
+//
+// CTAs [0, T) — Plan(b), b = j - F - 1, on the scratchpad state of table t:
+//   P1  future probe: resident IDs of B(b+F) (deduped by the previous
+//       launch) get next_need = b+F (future window, RAW-4 rule, P:864-884;
+//       one-shot probe, reading R12)
+//   P2  probe B(b): hit -> last_use = b (HoldMask |= MSB, Alg. 1);
+//       misses compacted in ascending ID order
+//   P3  victims: walk the LRU log from its head; a slot is a candidate iff
+//       last_use <= b-P-1 (past window) and next_need <= b; the
+//       first |misses| candidates in (last_use, ID) order are taken (LRU,
+//       P:1273, reading R8); too few -> SP_ERR_CAPACITY
+//   P4  pair k-th miss with k-th victim (reading R6): Hit-Map, resident,
+//       stamps; evict + fill lists for the transfer kernel
+//   P5  append this batch's slots to the LRU log (compacting it if full)
+//   P6  slot map per occurrence and per backward chunk for the Train stage
+//       (frozen at Plan, reading R13)
 #include "sp_internal.cuh"
 
 namespace sp {
 
 namespace {
+
+constexpr int NW = PUSH_THREADS / 32;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
@@ -36,8 +43,8 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // Exclusive block-wide scan of one u32 per thread; *total gets the sum.
 // Contains __syncthreads: every thread of the CTA must call it.
 __device__ uint32_t block_scan(uint32_t v, uint32_t *total) {
-    __shared__ uint32_t s_warp[PUSH_THREADS / 32 + 1];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ uint32_t s_warp[NW + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -47,17 +54,17 @@ __device__ uint32_t block_scan(uint32_t v, uint32_t *total) {
     if (lane == 31) s_warp[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        uint32_t w = lane < nw ? s_warp[lane] : 0u;
+        uint32_t w = lane < NW ? s_warp[lane] : 0u;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
             if (lane >= o) w += y;
         }
-        if (lane < nw) s_warp[lane] = w;
+        if (lane < NW) s_warp[lane] = w;
     }
     __syncthreads();
     uint32_t pre = warp ? s_warp[warp - 1] : 0u;
-    *total = s_warp[nw - 1];
+    *total = s_warp[NW - 1];
     __syncthreads();
     return pre + x - v;
 }
@@ -66,63 +73,52 @@ __device__ __forceinline__ void set_err(unsigned long long *err, long long b, in
     atomicMin(err, err_key(b, t, k));
 }
 
-// ---- sort of (id << 32 | occ) keys, ascending ----------------------------
-// small n: bitonic network in shared memory
-__device__ void bitonic_sort_smem(uint64_t *key, int n_pad) {
-    for (int k = 2; k <= n_pad; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
-                int ixj = i ^ jj;
-                if (ixj > i) {
-                    uint64_t a = key[i], c = key[ixj];
-                    bool up = (i & k) == 0;
-                    if ((a > c) == up) { key[i] = c; key[ixj] = a; }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
+__device__ __forceinline__ int bit_width_u64(unsigned long long x) { return x ? 64 - __clzll(x) : 0; }
 
-// large n: stable LSD radix sort on the id (upper 32 bits), 8-bit digits,
-// one CTA, ping-pong in global scratch.  Returns the buffer holding the result.
-constexpr int RADIX_IPT = 8;
-__device__ uint64_t *radix_sort_global(uint64_t *a, uint64_t *b, int n, int bits) {
+// Stable LSD radix sort of (key, val) pairs by key, 8-bit digits over the
+// low `bits` bits.  Buffers may live in shared or global memory.  Warp w
+// ranks a contiguous run of the tile in rounds of 32 (match_any), so equal
+// digits keep their input order: stable.  Returns true if the result ends
+// in (kb, vb).
+template <int IPT>
+__device__ bool radix_sort_pairs(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, int n, int bits) {
     __shared__ uint32_t s_hist[256];
-    __shared__ uint32_t s_wcnt[PUSH_THREADS / 32][256];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int tile = blockDim.x * RADIX_IPT;
-    for (int sh = 32; sh < 32 + bits; sh += 8) {
+    __shared__ uint32_t s_wcnt[NW][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int TILE = PUSH_THREADS * IPT;
+    bool swapped = false;
+    for (int sh = 0; sh < bits; sh += 8) {
         for (int d = threadIdx.x; d < 256; d += blockDim.x) s_hist[d] = 0;
-        for (int w = 0; w < nw; w++)
-            for (int d = threadIdx.x; d < 256; d += blockDim.x) s_wcnt[w][d] = 0;
         __syncthreads();
         for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-            int i = i0 + threadIdx.x;
-            unsigned d = i < n ? (unsigned)((a[i] >> sh) & 255u) : 256u;
-            unsigned peers = __match_any_sync(0xffffffffu, d);
+            const int i = i0 + threadIdx.x;
+            const unsigned d = i < n ? ((ka[i] >> sh) & 255u) : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
             if (d < 256u && (peers & lanemask_lt()) == 0) atomicAdd(&s_hist[d], __popc(peers));
         }
         __syncthreads();
-        // exclusive scan of the 256-bin histogram -> running bucket bases
         {
             uint32_t v = threadIdx.x < 256 ? s_hist[threadIdx.x] : 0u, tot;
-            uint32_t ex = block_scan(v, &tot);
+            const uint32_t ex = block_scan(v, &tot);
             if (threadIdx.x < 256) s_hist[threadIdx.x] = ex;
-            __syncthreads();
         }
-        for (int t0 = 0; t0 < n; t0 += tile) {
-            uint64_t e[RADIX_IPT];
-            uint32_t rk[RADIX_IPT];
-            unsigned dg[RADIX_IPT];
-            const int wbase = t0 + warp * 32 * RADIX_IPT;
+        for (int t0 = 0; t0 < n; t0 += TILE) {
+            for (int k = threadIdx.x; k < NW * 256; k += blockDim.x) (&s_wcnt[0][0])[k] = 0;
+            __syncthreads();
+            uint32_t key[IPT], val[IPT], rk[IPT];
+            unsigned dg[IPT];
+            const int wbase = t0 + warp * 32 * IPT;
 #pragma unroll
-            for (int r = 0; r < RADIX_IPT; r++) {
-                int i = wbase + r * 32 + lane;
-                e[r] = i < n ? a[i] : 0ull;
-                dg[r] = i < n ? (unsigned)((e[r] >> sh) & 255u) : 256u;
-                unsigned peers = __match_any_sync(0xffffffffu, dg[r]);
-                uint32_t base = dg[r] < 256u ? s_wcnt[warp][dg[r]] : 0u;
+            for (int r = 0; r < IPT; r++) {
+                const int i = wbase + r * 32 + lane;
+                key[r] = i < n ? ka[i] : 0u;
+                val[r] = i < n ? va[i] : 0u;
+                dg[r] = i < n ? ((key[r] >> sh) & 255u) : 256u;
+            }
+#pragma unroll
+            for (int r = 0; r < IPT; r++) {
+                const unsigned peers = __match_any_sync(0xffffffffu, dg[r]);
+                const uint32_t base = dg[r] < 256u ? s_wcnt[warp][dg[r]] : 0u;
                 rk[r] = base + __popc(peers & lanemask_lt());
                 __syncwarp();
                 if (dg[r] < 256u && (peers & lanemask_lt()) == 0) s_wcnt[warp][dg[r]] = base + __popc(peers);
@@ -131,8 +127,9 @@ __device__ uint64_t *radix_sort_global(uint64_t *a, uint64_t *b, int n, int bits
             __syncthreads();
             for (int d = threadIdx.x; d < 256; d += blockDim.x) {
                 uint32_t run = s_hist[d];
-                for (int w = 0; w < nw; w++) {
-                    uint32_t c = s_wcnt[w][d];
+#pragma unroll
+                for (int w = 0; w < NW; w++) {
+                    const uint32_t c = s_wcnt[w][d];
                     s_wcnt[w][d] = run;
                     run += c;
                 }
@@ -140,131 +137,157 @@ __device__ uint64_t *radix_sort_global(uint64_t *a, uint64_t *b, int n, int bits
             }
             __syncthreads();
 #pragma unroll
-            for (int r = 0; r < RADIX_IPT; r++)
-                if (dg[r] < 256u) b[s_wcnt[warp][dg[r]] + rk[r]] = e[r];
-            __syncthreads();
-            for (int w = 0; w < nw; w++)
-                for (int d = threadIdx.x; d < 256; d += blockDim.x) s_wcnt[w][d] = 0;
+            for (int r = 0; r < IPT; r++)
+                if (dg[r] < 256u) {
+                    const uint32_t pos = s_wcnt[warp][dg[r]] + rk[r];
+                    kb[pos] = key[r];
+                    vb[pos] = val[r];
+                }
             __syncthreads();
         }
-        uint64_t *tmp = a; a = b; b = tmp;
+        uint32_t *tk = ka, *tv = va;
+        ka = kb; va = vb; kb = tk; vb = tv;
+        swapped = !swapped;
     }
-    return a;
+    return swapped;
 }
 
-__device__ int bit_width_u64(unsigned long long x) { return x ? 64 - __clzll(x) : 0; }
+// ------------------------------------------------------------------ dedup
+__device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw) {
+    // (the chunk records of D3 use the sort's free ping-pong buffer as scratch)
+    const Geometry &g = A.g;
+    const int n = g.n, tid = threadIdx.x;
+    const long long R = A.rows[t];
+    const BatchBufs &nb = A.nb;
+    const bool small = n <= SMEM_SORT_MAX;
+    uint32_t *ka, *va, *kb, *vb;
+    if (small) {
+        ka = reinterpret_cast<uint32_t *>(smem_raw);
+        va = ka + n; kb = va + n; vb = kb + n;
+    } else {
+        const size_t Tn = (size_t)g.T * n;
+        ka = A.sort_tmp + (size_t)t * n;
+        va = ka + Tn; kb = va + Tn; vb = kb + Tn;
+    }
+    // D1: ingest + range check
+    int bad = 0;
+    for (int i = tid; i < n; i += blockDim.x) {
+        long long id = A.idx_i32 ? (long long)((const int32_t *)A.idx)[(size_t)t * n + i]
+                                 : ((const long long *)A.idx)[(size_t)t * n + i];
+        if (id < 0 || id >= R) { bad = 1; id = 0; }
+        ka[i] = (uint32_t)id;
+        va[i] = (uint32_t)i;
+    }
+    if (__syncthreads_or(bad)) {
+        if (tid == 0) set_err(A.err, A.j, t, DERR_INDEX);
+        return;
+    }
+    // D2: sort by id (stable: occurrences stay ascending within an id)
+    const int bits = bit_width_u64((unsigned long long)(R - 1));
+    const bool sw = small ? radix_sort_pairs<4>(ka, va, kb, vb, n, bits)
+                          : radix_sort_pairs<8>(ka, va, kb, vb, n, bits);
+    const uint32_t *keys = sw ? kb : ka;
+    const uint32_t *vals = sw ? vb : va;
+    __syncthreads();
+    uint32_t *sorted_occ = nb.sorted_occ + (size_t)t * n;
+    uint32_t *sorted_uid = nb.sorted_uid + (size_t)t * n;
+    uint32_t *uniq_id = nb.uniq_id + (size_t)t * n;
+    uint32_t *seg_off = nb.seg_off + (size_t)t * g.n1;
+    uint32_t carry = 0;
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+        const int i = i0 + tid;
+        uint32_t head = 0, id = 0;
+        if (i < n) {
+            id = keys[i];
+            head = (i == 0) || (keys[i - 1] != id);
+        }
+        uint32_t tot;
+        const uint32_t ex = block_scan(head, &tot);
+        if (i < n) {
+            const uint32_t uid = carry + ex + head - 1;
+            sorted_occ[i] = vals[i];
+            sorted_uid[i] = uid;
+            if (head) { uniq_id[uid] = id; seg_off[uid] = (uint32_t)i; }
+        }
+        carry += tot;
+    }
+    const uint32_t U = carry;
+    if (tid == 0) { seg_off[U] = (uint32_t)n; nb.U[t] = U; }
+    __syncthreads();
+    // D3a: chunk headers (one per <= CH occurrences of a unique) + hot rows
+    ChunkRec *rec = nb.chunk_rec + (size_t)t * g.nc;
+    uint4 *hot = nb.hot_rec + (size_t)t * g.nh;
+    uint32_t *chunk_first = sw ? ka : kb;  // the sort's free buffer (>= n entries)
+    carry = 0;
+    uint32_t hcarry = 0;
+    for (uint32_t u0 = 0; u0 < U; u0 += blockDim.x) {
+        const uint32_t u = u0 + tid;
+        uint32_t nch = 0, lo = 0, hi = 0;
+        if (u < U) {
+            lo = seg_off[u];
+            hi = seg_off[u + 1];
+            nch = (hi - lo + CH - 1) / CH;
+        }
+        uint32_t tot, htot;
+        const uint32_t ex = block_scan(nch, &tot);
+        const uint32_t hx = block_scan(nch > 1 ? 1u : 0u, &htot);
+        if (u < U) chunk_first[u] = carry + ex;
+        const uint32_t multi = nch > 1 ? 0x80000000u : 0u;
+        for (uint32_t k = 0; k < nch; k++) {
+            ChunkRec &r = rec[carry + ex + k];
+            r.slot = u;
+            r.meta = min(hi - lo - k * CH, (uint32_t)CH) | multi;
+        }
+        if (nch > 1) hot[hcarry + hx] = make_uint4(u, carry + ex, nch, 0u);
+        carry += tot;
+        hcarry += htot;
+    }
+    if (tid == 0) {
+        nb.nchunks[t] = carry;
+        nb.nhot[t] = hcarry;
+    }
+    __syncthreads();
+    // D3b: inline bag indices, one occurrence per thread
+    for (int i = tid; i < n; i += blockDim.x) {
+        const uint32_t u = sorted_uid[i];
+        const uint32_t r = (uint32_t)i - seg_off[u];
+        rec[chunk_first[u] + r / CH].bag[r % CH] = vals[i] / (uint32_t)g.L;
+    }
+}
 
-}  // namespace
-
-__global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(PushArgs A) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int t = blockIdx.x;
+// ------------------------------------------------------------------- plan
+__device__ void plan_table(const PushArgs &A, int t) {
     const Geometry &g = A.g;
     const int n = g.n, tid = threadIdx.x;
     __shared__ uint32_t s_fail, s_got;
     __shared__ unsigned long long s_head, s_newhead, s_tail;
-    if (*A.err != NO_ERR) return;  // poisoned: nothing more is planned
     const unsigned long long roff = A.row_off[t];
-    const long long R = A.rows[t];
-
-    // ------------------------------------------------------------ part A
-    if (A.has_new) {
-        BatchBufs &nb = A.nb;
-        uint64_t *keys;
-        const bool small = A.n_pad <= SMEM_SORT_MAX;
-        uint64_t *gA = A.sort_tmp + (size_t)t * n;
-        uint64_t *gB = A.sort_tmp + (size_t)g.T * n + (size_t)t * n;
-        keys = small ? reinterpret_cast<uint64_t *>(smem_raw) : gA;
-        // A1: ingest + range check; key = id << 32 | occurrence
-        int bad = 0;
-        for (int i = tid; i < (small ? A.n_pad : n); i += blockDim.x) {
-            uint64_t k = ~0ull;
-            if (i < n) {
-                long long id = A.idx_i32 ? (long long)((const int32_t *)A.idx)[(size_t)t * n + i]
-                                         : ((const long long *)A.idx)[(size_t)t * n + i];
-                if (id < 0 || id >= R) { bad = 1; id = 0; }
-                k = ((uint64_t)id << 32) | (uint32_t)i;
-            }
-            keys[i] = k;
-        }
-        if (__syncthreads_or(bad)) {
-            if (tid == 0) set_err(A.err, A.j, t, DERR_INDEX);
-            return;
-        }
-        // A2: sort + unique
-        if (small) {
-            bitonic_sort_smem(keys, A.n_pad);
-        } else {
-            int bits = bit_width_u64((unsigned long long)(R - 1));
-            keys = radix_sort_global(gA, gB, n, bits);
-            __syncthreads();
-        }
-        uint32_t *sorted_occ = nb.sorted_occ + (size_t)t * n;
-        uint32_t *sorted_uid = nb.sorted_uid + (size_t)t * n;
-        uint32_t *uniq_id = nb.uniq_id + (size_t)t * n;
-        uint32_t *seg_off = nb.seg_off + (size_t)t * g.n1;
-        uint32_t carry = 0;
-        for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-            int i = i0 + tid;
-            uint64_t k = i < n ? keys[i] : ~0ull;
-            uint32_t id = (uint32_t)(k >> 32);
-            uint32_t head = 0;
-            if (i < n) head = (i == 0) || ((uint32_t)(keys[i - 1] >> 32) != id);
-            uint32_t tot;
-            uint32_t ex = block_scan(head, &tot);
-            if (i < n) {
-                uint32_t uid = carry + ex + head - 1;
-                sorted_occ[i] = (uint32_t)k;
-                sorted_uid[i] = uid;
-                if (head) { uniq_id[uid] = id; seg_off[uid] = (uint32_t)i; }
-            }
-            carry += tot;
-        }
-        const uint32_t U = carry;
-        if (tid == 0) { seg_off[U] = (uint32_t)n; nb.U[t] = U; }
-        __syncthreads();
-        // A3: backward chunks
-        uint32_t *chunk_u = nb.chunk_u + (size_t)t * g.nc;
-        uint32_t *chunk_first = nb.chunk_first + (size_t)t * n;
-        carry = 0;
-        for (uint32_t u0 = 0; u0 < U; u0 += blockDim.x) {
-            uint32_t u = u0 + tid;
-            uint32_t nch = 0;
-            if (u < U) nch = (seg_off[u + 1] - seg_off[u] + CH - 1) / CH;
-            uint32_t tot;
-            uint32_t ex = block_scan(nch, &tot);
-            if (u < U) {
-                chunk_first[u] = carry + ex;
-                for (uint32_t k = 0; k < nch; k++) chunk_u[carry + ex + k] = u;
-            }
-            carry += tot;
-        }
-        if (tid == 0) nb.nchunks[t] = carry;
-        // A4: future probe of B(j)
-        for (uint32_t u = tid; u < U; u += blockDim.x) {
-            uint32_t s = A.hitmap[roff + uniq_id[u]];
-            if (s != EMPTY) A.next_need[s] = (int32_t)A.j;
-        }
-        __syncthreads();
-    }
-
-    // ------------------------------------------------------------ part B
-    if (!A.do_plan) return;
-    BatchBufs &pb = A.pb;
+    const BatchBufs &pb = A.pb;
     const long long b = A.b;
+
+    // P1: future probe of B(b+F)
+    if (A.has_future) {
+        const uint32_t Uf = A.fb.U[t];
+        const uint32_t *fid = A.fb.uniq_id + (size_t)t * n;
+        const int32_t stamp = (int32_t)(b + A.F);
+        for (uint32_t u = tid; u < Uf; u += blockDim.x) {
+            const uint32_t s = A.hitmap[roff + fid[u]];
+            if (s != EMPTY) A.next_need[s] = stamp;
+        }
+    }
+    // P2: probe B(b); hits stamped, misses compacted (ascending ID)
     const uint32_t Ub = pb.U[t];
     const uint32_t *uniq_id = pb.uniq_id + (size_t)t * n;
     uint32_t *slot_u = pb.slot_u + (size_t)t * n;
     uint8_t *hitf = pb.hit + (size_t)t * n;
     uint32_t *miss_u = A.miss_u + (size_t)t * n;
     uint32_t *victims = A.victims + (size_t)t * n;
-    // B1 + B2: probe, hits stamped, misses compacted (ascending ID)
-    uint32_t carry = 0, nhit = 0;
+    uint32_t carry = 0;
     for (uint32_t u0 = 0; u0 < Ub; u0 += blockDim.x) {
-        uint32_t u = u0 + tid;
+        const uint32_t u = u0 + tid;
         uint32_t miss = 0;
         if (u < Ub) {
-            uint32_t s = A.hitmap[roff + uniq_id[u]];
+            const uint32_t s = A.hitmap[roff + uniq_id[u]];
             if (s != EMPTY) {
                 A.last_use[s] = (int32_t)b;
                 slot_u[u] = s;
@@ -276,15 +299,15 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(PushArgs A) {
             }
         }
         uint32_t tot;
-        uint32_t ex = block_scan(miss, &tot);
+        const uint32_t ex = block_scan(miss, &tot);  // barriers: P1 and stamps visible below
         if (miss) miss_u[carry + ex] = u;
         carry += tot;
     }
     const uint32_t m = carry;
-    nhit = Ub - m;
-    __syncthreads();  // last_use of hits visible to the victim scan
+    const uint32_t nhit = Ub - m;
+    __syncthreads();
 
-    // B3: victim selection over the per-table LRU log
+    // P3: victim selection over the per-table LRU log
     const unsigned long long cap = A.log_cap[t], lbase = A.log_base[t];
     uint32_t *lslot = A.log_slot;
     int32_t *lstamp = A.log_stamp;
@@ -300,20 +323,20 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(PushArgs A) {
         const unsigned long long head = s_head, tail = s_tail;
         const uint32_t got = s_got;
         if (got >= m) break;
-        unsigned long long pos = head + tid;
-        bool inr = pos < tail;
+        const unsigned long long pos = head + tid;
+        const bool inr = pos < tail;
         uint32_t slot = 0;
         int32_t stamp = 0;
         if (inr) {
-            size_t ix = (size_t)(lbase + pos % cap);
+            const size_t ix = (size_t)(lbase + pos % cap);
             slot = lslot[ix];
             stamp = lstamp[ix];
         }
-        bool elig = inr && (long long)stamp <= limit;
-        bool cand = elig && A.last_use[slot] == stamp && (long long)A.next_need[slot] <= b;
+        const bool elig = inr && (long long)stamp <= limit;  // stamps are non-decreasing
+        const bool cand = elig && A.last_use[slot] == stamp && (long long)A.next_need[slot] <= b;
         uint32_t n_elig, n_cand;
         (void)block_scan(elig ? 1u : 0u, &n_elig);
-        uint32_t r = block_scan(cand ? 1u : 0u, &n_cand);
+        const uint32_t r = block_scan(cand ? 1u : 0u, &n_cand);
         const uint32_t need = m - got;
         if (cand && r < need) {
             victims[got + r] = slot;
@@ -338,14 +361,14 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(PushArgs A) {
         return;
     }
 
-    // B4: assignment (k-th miss <-> k-th victim)
+    // P4: assignment (k-th miss <-> k-th victim)
     uint32_t *fill_slot = pb.fill_slot + (size_t)t * n;
     uint32_t *fill_row = pb.fill_row + (size_t)t * n;
     uint32_t *evict_row = pb.evict_row + (size_t)t * n;
     uint32_t nev = 0;
     for (uint32_t k = tid; k < m; k += blockDim.x) {
-        uint32_t u = miss_u[k], s = victims[k], id = uniq_id[u];
-        uint32_t old = A.resident[s];
+        const uint32_t u = miss_u[k], s = victims[k], id = uniq_id[u];
+        const uint32_t old = A.resident[s];
         if (old != EMPTY) {
             A.hitmap[roff + old] = EMPTY;
             nev++;
@@ -360,27 +383,28 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(PushArgs A) {
         evict_row[k] = old;
     }
     uint32_t ev_total;
-    (void)block_scan(nev, &ev_total);  // includes barriers: B4 writes visible below
+    (void)block_scan(nev, &ev_total);  // barriers: P4 writes visible below
 
-    // B5: LRU log append (after an in-place compaction if it would overflow)
-    unsigned long long head = s_head, tail = s_tail;
+    // P5: LRU log append (after an in-place compaction if it would overflow)
+    const unsigned long long head = s_head;
+    unsigned long long tail = s_tail;
     if (tail - head + Ub > cap) {
         unsigned long long w = head;
         for (unsigned long long c0 = head; c0 < tail; c0 += blockDim.x) {
-            unsigned long long pos = c0 + tid;
-            bool inr = pos < tail;
+            const unsigned long long pos = c0 + tid;
+            const bool inr = pos < tail;
             uint32_t slot = 0;
             int32_t stamp = 0;
             if (inr) {
-                size_t ix = (size_t)(lbase + pos % cap);
+                const size_t ix = (size_t)(lbase + pos % cap);
                 slot = lslot[ix];
                 stamp = lstamp[ix];
             }
-            bool keep = inr && A.last_use[slot] == stamp;
+            const bool keep = inr && A.last_use[slot] == stamp;
             uint32_t tot;
-            uint32_t r = block_scan(keep ? 1u : 0u, &tot);  // all reads precede writes
+            const uint32_t r = block_scan(keep ? 1u : 0u, &tot);  // all reads precede writes
             if (keep) {
-                size_t ix = (size_t)(lbase + (w + r) % cap);
+                const size_t ix = (size_t)(lbase + (w + r) % cap);
                 lslot[ix] = slot;
                 lstamp[ix] = stamp;
             }
@@ -390,7 +414,7 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(PushArgs A) {
         tail = w;
     }
     for (uint32_t u = tid; u < Ub; u += blockDim.x) {
-        size_t ix = (size_t)(lbase + (tail + u) % cap);
+        const size_t ix = (size_t)(lbase + (tail + u) % cap);
         lslot[ix] = slot_u[u];
         lstamp[ix] = (int32_t)b;
     }
@@ -405,25 +429,41 @@ __global__ void __launch_bounds__(PUSH_THREADS, 1) k_push(PushArgs A) {
         atomicAdd(&A.cum[2], (unsigned long long)m);
         atomicAdd(&A.cum[3], (unsigned long long)ev_total);
     }
-    __syncthreads();  // slot_u complete (B4) before the slot map
-    // B6: slot map for Train, frozen at Plan
+    // P6: slot maps for Train (slot_u complete: the block_scan above synced)
     const uint32_t *sorted_occ = pb.sorted_occ + (size_t)t * n;
     const uint32_t *sorted_uid = pb.sorted_uid + (size_t)t * n;
     uint32_t *slot_of_occ = pb.slot_of_occ + (size_t)t * n;
     for (int i = tid; i < n; i += blockDim.x) slot_of_occ[sorted_occ[i]] = slot_u[sorted_uid[i]];
+    ChunkRec *rec = pb.chunk_rec + (size_t)t * g.nc;
+    const uint32_t nch = pb.nchunks[t];
+    for (uint32_t c = tid; c < nch; c += blockDim.x) rec[c].slot = slot_u[rec[c].slot];
+    uint4 *hot = pb.hot_rec + (size_t)t * g.nh;
+    const uint32_t nhot = pb.nhot[t];
+    for (uint32_t h = tid; h < nhot; h += blockDim.x) hot[h].x = slot_u[hot[h].x];
 }
 
-size_t push_smem_bytes(int n_pad) {
-    return n_pad <= SMEM_SORT_MAX ? (size_t)n_pad * sizeof(uint64_t) : 0;
+}  // namespace
+
+__global__ void __launch_bounds__(PUSH_THREADS, 2) k_push(PushArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (*A.err != NO_ERR) return;  // poisoned: nothing more is planned
+    const int T = A.g.T;
+    if ((int)blockIdx.x < T) {
+        if (A.do_plan) plan_table(A, blockIdx.x);
+    } else if (A.has_new) {
+        dedup_table(A, blockIdx.x - T, smem_raw);
+    }
 }
+
+size_t push_smem_bytes(int n) { return n <= SMEM_SORT_MAX ? (size_t)n * 4 * sizeof(uint32_t) : 0; }
 
 cudaError_t configure_push_kernel() {
     return cudaFuncSetAttribute(k_push, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(SMEM_SORT_MAX * sizeof(uint64_t)));
+                                (int)(SMEM_SORT_MAX * 4 * sizeof(uint32_t)));
 }
 
 cudaError_t launch_push(const PushArgs &a, cudaStream_t s) {
-    k_push<<<a.g.T, PUSH_THREADS, push_smem_bytes(a.n_pad), s>>>(a);
+    k_push<<<2 * a.g.T, PUSH_THREADS, push_smem_bytes(a.g.n), s>>>(a);
     return cudaGetLastError();
 }
 

@@ -17,6 +17,8 @@
 //   k_surrogate  the harness's MLP stand-in g = fmaf(gamma, pooled, delta).
 #include "sp_internal.cuh"
 
+#include <unordered_map>
+
 namespace sp {
 
 namespace {
@@ -32,13 +34,6 @@ __device__ __forceinline__ unsigned group_mask() {
 }
 
 __device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
-
-// L2-coherent load of 4 doubles (partials written by other CTAs)
-__device__ __forceinline__ double4 ldcg_d4(const double4 *p) {
-    const double2 *q = reinterpret_cast<const double2 *>(p);
-    double2 a = __ldcg(q), b = __ldcg(q + 1);
-    return make_double4(a.x, a.y, b.x, b.y);
-}
 
 __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
     a.x = a.x + b.x; a.y = a.y + b.y; a.z = a.z + b.z; a.w = a.w + b.w;
@@ -126,114 +121,79 @@ __device__ __forceinline__ float4 sgd(const float4 &w, const Acc4 &a, float lr) 
     return r;
 }
 
-// Work item = one chunk (<= CH occurrences of one unique row) of one table.
+// Pass 1.  Work item = one chunk record of one table: up to CH occurrences of
+// one unique row with their bag indices inline, so a chunk costs one record
+// load, then its gradient rows (RB per round, all issued before folding),
+// while the Storage row is prefetched.  Single-chunk rows (the common case)
+// are updated here; hot rows write one fp64 partial per chunk, folded by
+// k_bwd_hot (pass 2).
 template <int G, int VPL>
-__global__ void __launch_bounds__(256) k_bwd(TrainArgs A) {
+__global__ void __launch_bounds__(256, 3) k_bwd(TrainArgs A) {
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
     const int D4 = g.D / 4;
     __shared__ uint32_t s_pref[65];
-    __shared__ int s_T;
-    // per-table chunk prefix (tables are few; loop for T > 64)
     const int gpb = blockDim.x / G;
     const int lane = threadIdx.x % G;
-    const unsigned gmask = group_mask<G>();
-    const int leader = (threadIdx.x & 31) & ~(G - 1);
     const float4 *grad = reinterpret_cast<const float4 *>(A.grad);
     float4 *st = reinterpret_cast<float4 *>(A.storage);
+    constexpr int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);  // gradient rows per round
     for (int t0 = 0; t0 < g.T; t0 += 64) {
         const int tcount = min(64, g.T - t0);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t run = 0;
-            for (int k = 0; k < tcount; k++) { s_pref[k] = run; run += A.bb.nchunks[t0 + k]; }
-            s_pref[tcount] = run;
-            s_T = tcount;
-        }
-        __syncthreads();
-        const uint32_t total = s_pref[s_T];
+        table_prefix(A.bb.nchunks, t0, tcount, s_pref);
+        const uint32_t total = s_pref[tcount];
         for (uint32_t item = blockIdx.x * gpb + threadIdx.x / G; item < total; item += gridDim.x * gpb) {
-            int tl = 0;
-            while (s_pref[tl + 1] <= item) tl++;
+            const int tl = find_table(s_pref, tcount, item);
             const int t = t0 + tl;
             const uint32_t c = item - s_pref[tl];
-            const uint32_t u = A.bb.chunk_u[(size_t)t * g.nc + c];
-            const uint32_t k = c - A.bb.chunk_first[(size_t)t * g.n + u];
-            const uint32_t lo = A.bb.seg_off[(size_t)t * g.n1 + u];
-            const uint32_t hi = A.bb.seg_off[(size_t)t * g.n1 + u + 1];
-            const uint32_t i0 = lo + k * CH, i1 = min(hi, i0 + CH);
-            const uint32_t nch = (hi - lo + CH - 1) / CH;
-            const uint32_t *occ = A.bb.sorted_occ + (size_t)t * g.n;
-            const size_t bag0 = (size_t)t * g.N;
+            const uint4 *rp = reinterpret_cast<const uint4 *>(A.bb.chunk_rec + (size_t)t * g.nc + c);
+            uint4 q4[5];
+            q4[0] = __ldg(rp);
+            const uint32_t slot = q4[0].x, meta = q4[0].y;
+            const uint32_t len = meta & 0xFFFFu;
+            const bool multi = (meta >> 31) != 0;
+#pragma unroll
+            for (int k = 1; k < 5; k++) q4[k] = (uint32_t)(4 * k - 2) < len ? __ldg(rp + k) : make_uint4(0, 0, 0, 0);
+            const uint32_t *bag = reinterpret_cast<const uint32_t *>(q4) + 2;
+            const float4 *gb = grad + (size_t)t * g.N * D4 + lane;
+            float4 w[VPL];
+            float4 *wp = st + (size_t)slot * D4 + lane;
+            if (!multi) {
+#pragma unroll
+                for (int v = 0; v < VPL; v++) w[v] = wp[v * G];
+            }
             Acc4 acc[VPL];
 #pragma unroll
             for (int v = 0; v < VPL; v++) acc[v] = Acc4{0.0, 0.0, 0.0, 0.0};
-            uint32_t i = i0;
-            for (; i + 4 <= i1; i += 4) {
-                uint32_t o[4];
 #pragma unroll
-                for (int q = 0; q < 4; q++) o[q] = __ldg(occ + i + q);
-                float4 r[4][VPL];
+            for (int q0 = 0; q0 < CH; q0 += RB) {
+                if ((uint32_t)q0 < len) {
+                    float4 r[RB][VPL];
 #pragma unroll
-                for (int q = 0; q < 4; q++)
+                    for (int q = 0; q < RB; q++)
+                        if ((uint32_t)(q0 + q) < len)
 #pragma unroll
-                    for (int v = 0; v < VPL; v++)
-                        r[q][v] = ldg4(grad + (bag0 + o[q] / g.L) * D4 + lane + v * G);
+                            for (int v = 0; v < VPL; v++) r[q][v] = ldg4(gb + (size_t)bag[q0 + q] * D4 + v * G);
 #pragma unroll
-                for (int q = 0; q < 4; q++)
+                    for (int q = 0; q < RB; q++)
+                        if ((uint32_t)(q0 + q) < len)
 #pragma unroll
-                    for (int v = 0; v < VPL; v++) acc_add(acc[v], r[q][v]);
-            }
-            for (; i < i1; i++) {
-                const uint32_t o = __ldg(occ + i);
-#pragma unroll
-                for (int v = 0; v < VPL; v++) acc_add(acc[v], ldg4(grad + (bag0 + o / g.L) * D4 + lane + v * G));
-            }
-            const uint32_t slot = A.bb.slot_u[(size_t)t * g.n + u];
-            if (nch == 1) {
-#pragma unroll
-                for (int v = 0; v < VPL; v++) {
-                    float4 *w = st + (size_t)slot * D4 + lane + v * G;
-                    *w = sgd(*w, acc[v], A.lr);
-                }
-                continue;
-            }
-            // multi-chunk segment: publish the fp64 partial, last finisher folds
-            double *part = A.partial + ((size_t)t * g.nc + c) * g.D;
-#pragma unroll
-            for (int v = 0; v < VPL; v++) {
-                double4 *p4 = reinterpret_cast<double4 *>(part) + lane + v * G;
-                *p4 = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
-            }
-            __threadfence();
-            __syncwarp(gmask);
-            uint32_t prev = 0;
-            if (lane == 0) prev = atomicAdd(A.cnt + (size_t)t * g.n + u, 1u);
-            prev = __shfl_sync(gmask, prev, leader);
-            if (prev != nch - 1) continue;
-            __threadfence();
-            const uint32_t cfirst = c - k;  // chunk 0 of this unique row
-#pragma unroll
-            for (int v = 0; v < VPL; v++) acc[v] = Acc4{0.0, 0.0, 0.0, 0.0};
-            for (uint32_t q = 0; q < nch; q++) {
-                const double *pq = A.partial + ((size_t)t * g.nc + cfirst + q) * g.D;
-#pragma unroll
-                for (int v = 0; v < VPL; v++) {
-                    double4 d = ldcg_d4(reinterpret_cast<const double4 *>(pq) + lane + v * G);
-                    acc[v].x += d.x; acc[v].y += d.y; acc[v].z += d.z; acc[v].w += d.w;
+                            for (int v = 0; v < VPL; v++) acc_add(acc[v], r[q][v]);
                 }
             }
+            if (!multi) {
 #pragma unroll
-            for (int v = 0; v < VPL; v++) {
-                float4 *w = st + (size_t)slot * D4 + lane + v * G;
-                *w = sgd(*w, acc[v], A.lr);
+                for (int v = 0; v < VPL; v++) wp[v * G] = sgd(w[v], acc[v], A.lr);
+            } else {
+                double4 *part = reinterpret_cast<double4 *>(A.partial + ((size_t)t * g.nc + c) * g.D) + lane;
+#pragma unroll
+                for (int v = 0; v < VPL; v++) part[v * G] = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
             }
-            if (lane == 0) A.cnt[(size_t)t * g.n + u] = 0;
         }
     }
 }
 
-// generic D: one warp per chunk, strided columns, partials per column
+// generic D: one warp per chunk, strided columns
 __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
@@ -245,40 +205,79 @@ __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
     for (int t = 0; t < g.T; t++) {
         const uint32_t total = A.bb.nchunks[t];
         for (uint32_t c = blockIdx.x * wpb + threadIdx.x / 32; c < total; c += gridDim.x * wpb) {
-            const uint32_t u = A.bb.chunk_u[(size_t)t * g.nc + c];
-            const uint32_t k = c - A.bb.chunk_first[(size_t)t * g.n + u];
-            const uint32_t lo = A.bb.seg_off[(size_t)t * g.n1 + u];
-            const uint32_t hi = A.bb.seg_off[(size_t)t * g.n1 + u + 1];
-            const uint32_t i0 = lo + k * CH, i1 = min(hi, i0 + CH);
-            const uint32_t nch = (hi - lo + CH - 1) / CH;
-            const uint32_t *occ = A.bb.sorted_occ + (size_t)t * g.n;
-            const uint32_t slot = A.bb.slot_u[(size_t)t * g.n + u];
+            const ChunkRec &rc = A.bb.chunk_rec[(size_t)t * g.nc + c];
+            const uint32_t slot = rc.slot, len = rc.meta & 0xFFFFu;
+            const bool multi = (rc.meta >> 31) != 0;
             double *part = A.partial + ((size_t)t * g.nc + c) * g.D;
             for (int col = lane; col < D4; col += 32) {
                 Acc4 a{0.0, 0.0, 0.0, 0.0};
-                for (uint32_t i = i0; i < i1; i++)
-                    acc_add(a, grad[((size_t)t * g.N + occ[i] / g.L) * D4 + col]);
-                if (nch == 1) st[(size_t)slot * D4 + col] = sgd(st[(size_t)slot * D4 + col], a, A.lr);
+                for (uint32_t i = 0; i < len; i++)
+                    acc_add(a, grad[((size_t)t * g.N + rc.bag[i]) * D4 + col]);
+                if (!multi) st[(size_t)slot * D4 + col] = sgd(st[(size_t)slot * D4 + col], a, A.lr);
                 else reinterpret_cast<double4 *>(part)[col] = make_double4(a.x, a.y, a.z, a.w);
             }
-            if (nch == 1) continue;
-            __threadfence();
-            __syncwarp();
-            uint32_t prev = 0;
-            if (lane == 0) prev = atomicAdd(A.cnt + (size_t)t * g.n + u, 1u);
-            prev = __shfl_sync(0xffffffffu, prev, 0);
-            if (prev != nch - 1) continue;
-            __threadfence();
-            const uint32_t cfirst = c - k;
-            for (int col = lane; col < D4; col += 32) {
+        }
+    }
+}
+
+// Pass 2: one CTA per hot row folds its chunk partials: thread (p, col) sums
+// partials p, p+PL, p+2PL, ... in order, then a fixed-shape tree over p
+// (deterministic, independent of the grid), then the SGD update.
+__global__ void __launch_bounds__(256) k_bwd_hot(TrainArgs A) {
+    if (*A.err != NO_ERR) return;
+    const Geometry g = A.g;
+    const int D4 = g.D / 4;
+    __shared__ double4 s_acc[256];
+    __shared__ uint32_t s_pref[65];
+    const int PL = D4 >= 256 ? 1 : 256 / D4;          // partial lanes per column (<= 256/D4)
+    float4 *st = reinterpret_cast<float4 *>(A.storage);
+    for (int t0 = 0; t0 < g.T; t0 += 64) {
+        const int tcount = min(64, g.T - t0);
+        table_prefix(A.bb.nhot, t0, tcount, s_pref);
+        const uint32_t total = s_pref[tcount];
+        for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
+            const int tl = find_table(s_pref, tcount, item);
+            const int t = t0 + tl;
+            const uint4 hr = A.bb.hot_rec[(size_t)t * g.nh + (item - s_pref[tl])];
+            const uint32_t slot = hr.x, c0 = hr.y, nch = hr.z;
+            const double4 *part = reinterpret_cast<const double4 *>(A.partial + ((size_t)t * g.nc + c0) * g.D);
+            for (int col0 = 0; col0 < D4; col0 += 256 / PL) {
+                const int p = threadIdx.x / (256 / PL > D4 ? D4 : 256 / PL);
+                const int colw = 256 / PL > D4 ? D4 : 256 / PL;
+                const int col = col0 + threadIdx.x % colw;
                 Acc4 a{0.0, 0.0, 0.0, 0.0};
-                for (uint32_t q = 0; q < nch; q++) {
-                    double4 d = ldcg_d4(reinterpret_cast<const double4 *>(A.partial + ((size_t)t * g.nc + cfirst + q) * g.D) + col);
-                    a.x += d.x; a.y += d.y; a.z += d.z; a.w += d.w;
+                if (p < PL && col < D4) {
+                    uint32_t q = p;
+                    for (; q + 3 * PL < nch; q += 4 * PL) {  // 4 partials in flight, folded in order
+                        double4 d[4];
+#pragma unroll
+                        for (int k = 0; k < 4; k++) d[k] = part[(size_t)(q + k * PL) * D4 + col];
+#pragma unroll
+                        for (int k = 0; k < 4; k++) { a.x += d[k].x; a.y += d[k].y; a.z += d[k].z; a.w += d[k].w; }
+                    }
+                    for (; q < nch; q += PL) {
+                        const double4 d = part[(size_t)q * D4 + col];
+                        a.x += d.x; a.y += d.y; a.z += d.z; a.w += d.w;
+                    }
                 }
-                st[(size_t)slot * D4 + col] = sgd(st[(size_t)slot * D4 + col], a, A.lr);
+                __syncthreads();
+                if (p < PL && col < D4) s_acc[p * colw + (col - col0)] = make_double4(a.x, a.y, a.z, a.w);
+                __syncthreads();
+                for (int half = 1; half < PL; half <<= 1) {   // fixed tree over p
+                    if (p < PL && col < D4 && (p % (2 * half)) == 0 && p + half < PL) {
+                        const double4 o = s_acc[(p + half) * colw + (col - col0)];
+                        double4 &m = s_acc[p * colw + (col - col0)];
+                        m.x += o.x; m.y += o.y; m.z += o.z; m.w += o.w;
+                    }
+                    __syncthreads();
+                }
+                if (p == 0 && col < D4) {
+                    const double4 m = s_acc[col - col0];
+                    float4 *wp = st + (size_t)slot * D4 + col;
+                    *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
+                }
+                __syncthreads();
             }
-            if (lane == 0) A.cnt[(size_t)t * g.n + u] = 0;
         }
     }
 }
@@ -309,42 +308,60 @@ static int num_sms() {
     return n;
 }
 
-#define SP_DISPATCH_D(D4, KERNEL, GRID, ARGS, STREAM)                       \
-    switch (D4) {                                                            \
-        case 1: KERNEL<1, 1><<<GRID, 256, 0, STREAM>>>(ARGS); break;         \
-        case 2: KERNEL<2, 1><<<GRID, 256, 0, STREAM>>>(ARGS); break;         \
-        case 4: KERNEL<4, 1><<<GRID, 256, 0, STREAM>>>(ARGS); break;         \
-        case 8: KERNEL<8, 1><<<GRID, 256, 0, STREAM>>>(ARGS); break;         \
-        case 16: KERNEL<16, 1><<<GRID, 256, 0, STREAM>>>(ARGS); break;       \
-        case 32: KERNEL<32, 1><<<GRID, 256, 0, STREAM>>>(ARGS); break;       \
-        case 64: KERNEL<32, 2><<<GRID, 256, 0, STREAM>>>(ARGS); break;       \
-        case 128: KERNEL<32, 4><<<GRID, 256, 0, STREAM>>>(ARGS); break;      \
-        case 256: KERNEL<32, 8><<<GRID, 256, 0, STREAM>>>(ARGS); break;      \
-        default: KERNEL##_generic<<<GRID, 256, 0, STREAM>>>(ARGS); break;    \
+// resident CTAs of a kernel on the whole GPU (a persistent grid never waits
+// for a second wave of a latency-bound kernel)
+template <typename K>
+static int resident_ctas(K kernel, int threads) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return per_sm * num_sms();
+}
+
+template <int G, int VPL, typename K>
+static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStream_t s) {
+    static std::unordered_map<const void *, int> caps;  // per kernel (not per signature)
+    int &cap = caps[reinterpret_cast<const void *>(kernel)];
+    if (!cap) cap = resident_ctas(kernel, 256);
+    long long blocks = (groups + (256 / G) - 1) / (256 / G);
+    int grid = (int)(blocks < cap ? blocks : cap);
+    if (grid < 1) grid = 1;
+    kernel<<<grid, 256, 0, s>>>(a);
+}
+
+#define SP_DISPATCH_D(D4, KERNEL, GROUPS, ARGS, STREAM)                                  \
+    switch (D4) {                                                                         \
+        case 1: launch_sized<1, 1>(KERNEL<1, 1>, GROUPS, ARGS, STREAM); break;            \
+        case 2: launch_sized<2, 1>(KERNEL<2, 1>, GROUPS, ARGS, STREAM); break;            \
+        case 4: launch_sized<4, 1>(KERNEL<4, 1>, GROUPS, ARGS, STREAM); break;            \
+        case 8: launch_sized<8, 1>(KERNEL<8, 1>, GROUPS, ARGS, STREAM); break;            \
+        case 16: launch_sized<16, 1>(KERNEL<16, 1>, GROUPS, ARGS, STREAM); break;         \
+        case 32: launch_sized<32, 1>(KERNEL<32, 1>, GROUPS, ARGS, STREAM); break;         \
+        case 64: launch_sized<32, 2>(KERNEL<32, 2>, GROUPS, ARGS, STREAM); break;         \
+        case 128: launch_sized<32, 4>(KERNEL<32, 4>, GROUPS, ARGS, STREAM); break;        \
+        case 256: launch_sized<32, 8>(KERNEL<32, 8>, GROUPS, ARGS, STREAM); break;        \
+        default: launch_sized<32, 1>(KERNEL##_generic, GROUPS, ARGS, STREAM); break;      \
     }
 
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
-    const int G = D4 >= 32 ? 32 : D4;
-    const long long groups = (long long)a.g.T * a.g.N;
-    long long blocks = (groups + (256 / G) - 1) / (256 / G);
-    const long long cap = (long long)num_sms() * 8;
-    int grid = (int)(blocks < cap ? blocks : cap);
-    if (grid < 1) grid = 1;
-    SP_DISPATCH_D(D4, k_fwd, grid, a, s);
+    SP_DISPATCH_D(D4, k_fwd, (long long)a.g.T * a.g.N, a, s);
     return cudaGetLastError();
 }
 
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
-    const int G = D4 >= 32 ? 32 : D4;
     // upper bound of work items: all chunks of all tables
-    const long long items = (long long)a.g.T * a.g.nc;
-    long long blocks = (items + (256 / G) - 1) / (256 / G);
-    const long long cap = (long long)num_sms() * 8;
-    int grid = (int)(blocks < cap ? blocks : cap);
+    SP_DISPATCH_D(D4, k_bwd, (long long)a.g.T * a.g.nc, a, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward_hot(const TrainArgs &a, cudaStream_t s) {
+    long long upper = (long long)a.g.T * a.g.nh;
+    const long long cap = (long long)num_sms() * 4;
+    int grid = (int)(upper < cap ? upper : cap);
     if (grid < 1) grid = 1;
-    SP_DISPATCH_D(D4, k_bwd, grid, a, s);
+    k_bwd_hot<<<grid, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,14 +32,21 @@ namespace {
 
 struct ProfEv {
     int kind;
+    long long batch;
     cudaEvent_t a, b;
+};
+
+struct TimelineRec {
+    int kind;
+    long long batch;
+    double start_ms, end_ms;  // relative to the profiling reference event
 };
 
 }  // namespace
 
 struct sp_ctx {
     // configuration
-    int T = 0, D = 0, N = 0, L = 0, n = 0, P = 0, F = 0, n_pad = 0;
+    int T = 0, D = 0, N = 0, L = 0, n = 0, P = 0, F = 0;
     int device = 0;
     uint32_t flags = 0;
     std::vector<long long> rows, slots;
@@ -49,8 +57,16 @@ struct sp_ctx {
     unsigned long long hit_total = 0;
     bool registered = false;
     Geometry g{};
-    cudaStream_t compute = nullptr, plan_s = nullptr, xfer_s = nullptr;
-    int xfer_ctas = 0;
+    cudaStream_t compute = nullptr, plan_s = nullptr;
+    // Transfer(b) runs on xfer_s[b % nx]: transfers b..b+F touch disjoint
+    // slots and rows (a row evicted at Plan(b) is not in B(b+1..b+F)), so up
+    // to F+1 of them may overlap; Transfer(b) stays ordered after b-nx.
+    static constexpr int MAX_XFER_STREAMS = 4;
+    cudaStream_t xfer_s[MAX_XFER_STREAMS] = {};
+    int nx = 1;
+    int pull_ctas = 16, wb_ctas = 2;
+    cudaStream_t wb_s = nullptr;  // rate-limited write-backs (HBM staging -> host)
+    float *d_stage = nullptr;     // [RING][T][n][D]
     // device memory
     std::vector<void *> allocs;
     unsigned long long *d_row_off = nullptr;
@@ -65,9 +81,8 @@ struct sp_ctx {
                        *d_log_tail = nullptr;
     unsigned long long *d_err = nullptr, *d_cum = nullptr;
     uint32_t *d_miss_u = nullptr, *d_victims = nullptr;
-    uint64_t *d_sort_tmp = nullptr;
+    uint32_t *d_sort_tmp = nullptr;
     double *d_partial = nullptr;
-    uint32_t *d_cnt = nullptr;
     float **d_host = nullptr;
     void *d_idx[RING] = {};
     BatchBufs ring[RING];
@@ -77,6 +92,7 @@ struct sp_ctx {
     size_t idx_bytes = 0;
     // events
     cudaEvent_t ev_plan[RING] = {}, ev_xfer[RING] = {}, ev_train[RING] = {}, ev_h2d[RING] = {};
+    cudaEvent_t ev_wb[RING] = {};
     cudaEvent_t ev_user = nullptr;
     bool h2d_used[RING] = {};
     // schedule state
@@ -94,6 +110,9 @@ struct sp_ctx {
     long long ktimed[SP_K_COUNT] = {};
     std::vector<ProfEv> prof_pending;
     std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t prof_ref = nullptr;
+    std::vector<TimelineRec> timeline;
+    long long cur_batch = -1;
 };
 
 namespace {
@@ -148,6 +167,12 @@ void harvest_profile(sp_ctx *c, bool blocking) {
             cudaEventElapsedTime(&ms, p.a, p.b);
             c->kms[p.kind] += ms;
             c->ktimed[p.kind] += 1;
+            if (c->prof_ref && c->timeline.size() < (1u << 20)) {
+                float t0 = 0.f, t1 = 0.f;
+                cudaEventElapsedTime(&t0, c->prof_ref, p.a);
+                cudaEventElapsedTime(&t1, c->prof_ref, p.b);
+                c->timeline.push_back({p.kind, p.batch, (double)t0, (double)t1});
+            }
             c->ev_pool.push_back(p.a);
             c->ev_pool.push_back(p.b);
         } else {
@@ -162,7 +187,7 @@ void harvest_profile(sp_ctx *c, bool blocking) {
 template <typename F>
 cudaError_t launch(sp_ctx *c, int kind, cudaStream_t s, F &&fn) {
     const bool prof = (c->flags & SP_FLAG_PROFILE) != 0;
-    ProfEv pe{kind, nullptr, nullptr};
+    ProfEv pe{kind, c->cur_batch, nullptr, nullptr};
     if (prof) {
         if (c->prof_pending.size() > 4096) harvest_profile(c, false);
         pe.a = pool_event(c);
@@ -191,8 +216,9 @@ BatchBufs carve(sp_ctx *c, int r, cudaError_t *st) {
     A(&b.uniq_id, Tn);
     A(&b.seg_off, (size_t)c->T * c->g.n1);
     A(&b.U, (size_t)c->T);
-    A(&b.chunk_u, (size_t)c->T * c->g.nc);
-    A(&b.chunk_first, Tn);
+    A(&b.chunk_rec, (size_t)c->T * c->g.nc);  // ChunkRec (80 B)
+    A(&b.hot_rec, (size_t)c->T * c->g.nh);
+    A(&b.nhot, (size_t)c->T);
     A(&b.nchunks, (size_t)c->T);
     A(&b.slot_u, Tn);
     A(&b.slot_of_occ, Tn);
@@ -240,7 +266,6 @@ sp_status sync_error(sp_ctx *c) {
 PushArgs push_args(sp_ctx *c) {
     PushArgs a{};
     a.g = c->g;
-    a.n_pad = c->n_pad;
     a.P = c->P;
     a.F = c->F;
     a.row_off = c->d_row_off;
@@ -267,10 +292,13 @@ PushArgs push_args(sp_ctx *c) {
 
 sp_status enqueue_plan_only(sp_ctx *c, long long b) {
     PushArgs a = push_args(c);
+    c->cur_batch = b;
     a.has_new = 0;
     a.do_plan = 1;
     a.b = b;
     a.pb = c->ring[b % RING];
+    a.has_future = (b + c->F < c->pushed) ? 1 : 0;  // future window truncates at the end
+    a.fb = c->ring[(b + c->F) % RING];
     CK(launch(c, SP_K_PLAN, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
     CK(cudaEventRecord(c->ev_plan[b % RING], c->plan_s));
     c->planned = b + 1;
@@ -281,16 +309,28 @@ sp_status pump(sp_ctx *c) {
     while (c->transferred < c->planned) {
         const long long b = c->transferred, dep = b - c->P - 1;
         if (dep >= 0 && c->trained <= dep) break;  // Train(dep) not enqueued yet
-        CK(cudaStreamWaitEvent(c->xfer_s, c->ev_plan[b % RING], 0));
-        if (dep >= 0) CK(cudaStreamWaitEvent(c->xfer_s, c->ev_train[dep % RING], 0));
+        cudaStream_t xs = c->xfer_s[b % c->nx];
+        CK(cudaStreamWaitEvent(xs, c->ev_plan[b % RING], 0));
+        if (dep >= 0) CK(cudaStreamWaitEvent(xs, c->ev_train[dep % RING], 0));
+        // RAW-4: a row written back by WriteBack(b-F-1) may be
+        // pulled again by Pull(b); the write-back stream runs in batch order
+        const long long rb = b - c->F - 1;
+        if (rb >= 0) CK(cudaStreamWaitEvent(xs, c->ev_wb[rb % RING], 0));
         XferArgs a{};
+        c->cur_batch = b;
         a.g = c->g;
         a.bb = c->ring[b % RING];
         a.storage = c->d_storage;
+        a.stage = c->d_stage + (size_t)(b % RING) * c->T * c->n * c->D;
         a.host = c->d_host;
         a.err = c->d_err;
-        CK(launch(c, SP_K_TRANSFER, c->xfer_s, [&] { return launch_transfer(a, c->xfer_ctas, c->xfer_s); }));
-        CK(cudaEventRecord(c->ev_xfer[b % RING], c->xfer_s));
+        // SP_DEBUG_NO_XFER=1: timing experiments only (results are wrong)
+        static const bool no_xfer = getenv("SP_DEBUG_NO_XFER") != nullptr;
+        if (!no_xfer) CK(launch(c, SP_K_TRANSFER, xs, [&] { return launch_pull(a, c->pull_ctas, xs); }));
+        CK(cudaEventRecord(c->ev_xfer[b % RING], xs));
+        CK(cudaStreamWaitEvent(c->wb_s, c->ev_xfer[b % RING], 0));
+        if (!no_xfer) CK(launch(c, SP_K_WRITEBACK, c->wb_s, [&] { return launch_writeback(a, c->wb_ctas, c->wb_s); }));
+        CK(cudaEventRecord(c->ev_wb[b % RING], c->wb_s));
         c->transferred = b + 1;
     }
     return SP_OK;
@@ -302,7 +342,6 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.bb = c->ring[b % RING];
     a.storage = c->d_storage;
     a.partial = c->d_partial;
-    a.cnt = c->d_cnt;
     a.err = c->d_err;
     return a;
 }
@@ -311,7 +350,9 @@ void destroy_all(sp_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->plan_s) cudaStreamSynchronize(c->plan_s);
-    if (c->xfer_s) cudaStreamSynchronize(c->xfer_s);
+    for (auto xs : c->xfer_s)
+        if (xs) cudaStreamSynchronize(xs);
+    if (c->wb_s) cudaStreamSynchronize(c->wb_s);
     cudaStreamSynchronize(c->compute);
     harvest_profile(c, true);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -320,15 +361,19 @@ void destroy_all(sp_ctx *c) {
         if (c->ev_xfer[r]) cudaEventDestroy(c->ev_xfer[r]);
         if (c->ev_train[r]) cudaEventDestroy(c->ev_train[r]);
         if (c->ev_h2d[r]) cudaEventDestroy(c->ev_h2d[r]);
+        if (c->ev_wb[r]) cudaEventDestroy(c->ev_wb[r]);
     }
     if (c->ev_user) cudaEventDestroy(c->ev_user);
+    if (c->prof_ref) cudaEventDestroy(c->prof_ref);
     for (void *p : c->allocs) cudaFree(p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_err) cudaFreeHost(c->h_err);
     if (c->registered)
         for (int t = 0; t < c->T; t++) cudaHostUnregister(c->host[t]);
     if (c->plan_s) cudaStreamDestroy(c->plan_s);
-    if (c->xfer_s) cudaStreamDestroy(c->xfer_s);
+    for (auto xs : c->xfer_s)
+        if (xs) cudaStreamDestroy(xs);
+    if (c->wb_s) cudaStreamDestroy(c->wb_s);
     (void)cudaGetLastError();
     delete c;
 }
@@ -367,9 +412,6 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->device = d->device;
     c->flags = d->flags;
     c->compute = (cudaStream_t)d->stream;
-    int np = 1;
-    while (np < c->n) np <<= 1;
-    c->n_pad = np;
     c->g.T = c->T;
     c->g.N = c->N;
     c->g.L = c->L;
@@ -377,6 +419,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->g.n = c->n;
     c->g.n1 = c->n + 1;
     c->g.nc = c->n + c->n / CH + 1;
+    c->g.nh = c->n / CH + 1;
     c->rows.resize(c->T);
     c->slots.resize(c->T);
     c->host.resize(c->T);
@@ -443,17 +486,19 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         hdev[t] = static_cast<float *>(p);
     }
     CKC(cudaStreamCreateWithPriority(&c->plan_s, cudaStreamNonBlocking, -1));
-    CKC(cudaStreamCreateWithFlags(&c->xfer_s, cudaStreamNonBlocking));
+    c->nx = std::min(c->F + 1, (int)sp_ctx::MAX_XFER_STREAMS);
+    for (int k = 0; k < c->nx; k++) CKC(cudaStreamCreateWithFlags(&c->xfer_s[k], cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->wb_s, cudaStreamNonBlocking));
     for (int r = 0; r < RING; r++) {
         CKC(cudaEventCreateWithFlags(&c->ev_plan[r], cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&c->ev_xfer[r], cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&c->ev_train[r], cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&c->ev_h2d[r], cudaEventDisableTiming));
+        CKC(cudaEventCreateWithFlags(&c->ev_wb[r], cudaEventDisableTiming));
     }
     CKC(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    c->xfer_ctas = std::max(8, sms / 4);
+    c->pull_ctas = d->pull_ctas > 0 ? d->pull_ctas : 16;
+    c->wb_ctas = d->writeback_ctas > 0 ? d->writeback_ctas : 2;
     CKC(configure_push_kernel());
 
     // device allocations
@@ -486,10 +531,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_cum, 4));
     CKC(dalloc(c, &c->d_miss_u, Tn));
     CKC(dalloc(c, &c->d_victims, Tn));
-    if (c->n_pad > SMEM_SORT_MAX) CKC(dalloc(c, &c->d_sort_tmp, 2 * Tn));
+    if (c->n > SMEM_SORT_MAX) CKC(dalloc(c, &c->d_sort_tmp, 4 * Tn));
     CKC(dalloc(c, &c->d_partial, (size_t)c->T * c->g.nc * c->D));
-    CKC(dalloc(c, &c->d_cnt, Tn));
     CKC(dalloc(c, &c->d_host, c->T));
+    CKC(dalloc(c, &c->d_stage, (size_t)RING * Tn * c->D));
     c->idx_bytes = Tn * ((c->flags & SP_FLAG_INDEX_I32) ? 4 : 8);
     for (int r = 0; r < RING; r++) {
         cudaError_t st;
@@ -530,7 +575,6 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaMemcpy(c->d_log_tail, ltail.data(), c->T * sizeof(unsigned long long), cudaMemcpyHostToDevice));
     CKC(cudaMemset(c->d_err, 0xFF, sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_cum, 0, 4 * sizeof(unsigned long long)));
-    CKC(cudaMemset(c->d_cnt, 0, Tn * sizeof(uint32_t)));
     CKC(cudaMemset(c->d_storage, 0, (size_t)c->S_total * c->D * sizeof(float)));
     CKC(cudaDeviceSynchronize());
 #undef CKC
@@ -547,7 +591,10 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     if (j >= RING && c->trained < j - RING + 1)
         return fail(c, SP_ERR_STATE, "sp_plan: more than 16 batches ahead of sp_train");
     CK(cudaSetDevice(c->device));
-    if (j >= RING) CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));
+    if (j >= RING) {
+        CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));
+        CK(cudaStreamWaitEvent(c->plan_s, c->ev_wb[r], 0));  // WriteBack(j-RING) reads ring slot r
+    }
     const void *dev_idx;
     if (on_device) {
         // indices produced on the caller's stream
@@ -565,15 +612,19 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
         dev_idx = c->d_idx[r];
     }
     PushArgs a = push_args(c);
+    c->cur_batch = j;
     a.has_new = 1;
     a.j = j;
     a.idx = dev_idx;
     a.nb = c->ring[r];
-    const long long b = j - c->F;
+    // Plan(b) runs beside dedup(j) once B(b+F) = B(j-1) has been deduped
+    const long long b = j - c->F - 1;
     a.do_plan = (b >= 0 && b == c->planned) ? 1 : 0;
     if (a.do_plan) {
         a.b = b;
         a.pb = c->ring[b % RING];
+        a.has_future = 1;
+        a.fb = c->ring[(b + c->F) % RING];
     }
     CK(launch(c, SP_K_PLAN, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
     if (a.do_plan) {
@@ -604,8 +655,31 @@ sp_status sp_copy_batch_stats(sp_ctx *c, int64_t b, uint32_t *host_out) {
 
 sp_status sp_set_profiling(sp_ctx *c, int32_t on) {
     if (!c) return SP_ERR_INVALID_ARG;
-    if (on) c->flags |= SP_FLAG_PROFILE;
-    else c->flags &= ~SP_FLAG_PROFILE;
+    CK(cudaSetDevice(c->device));
+    if (on) {
+        c->flags |= SP_FLAG_PROFILE;
+        if (!c->prof_ref) CK(cudaEventCreate(&c->prof_ref));
+        CK(cudaEventRecord(c->prof_ref, c->compute));
+        c->timeline.clear();
+    } else {
+        c->flags &= ~SP_FLAG_PROFILE;
+    }
+    return SP_OK;
+}
+
+sp_status sp_get_timeline(sp_ctx *c, int32_t *kind, int64_t *batch, double *start_ms, double *end_ms,
+                          int64_t cap, int64_t *n) {
+    if (!c || !n) return SP_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    harvest_profile(c, true);
+    *n = (int64_t)c->timeline.size();
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *n); i++) {
+        kind[i] = c->timeline[i].kind;
+        batch[i] = c->timeline[i].batch;
+        start_ms[i] = c->timeline[i].start_ms;
+        end_ms[i] = c->timeline[i].end_ms;
+    }
     return SP_OK;
 }
 
@@ -626,12 +700,16 @@ sp_status sp_forward(sp_ctx *c, float *pooled) {
     if (c->fwd_pending) return fail(c, SP_ERR_STATE, "sp_forward twice without sp_train");
     const long long b = c->forwarded;
     if (b >= c->planned)
-        return fail(c, SP_ERR_STATE, "sp_forward: batch not planned yet (push B(b+F) or call sp_end_of_data)");
+        return fail(c, SP_ERR_STATE, "sp_forward: batch not planned yet (push B(b+F+1) or call sp_end_of_data)");
     CK(cudaSetDevice(c->device));
     if (sp_status s = pump(c)) return s;
     if (c->transferred <= b) return fail(c, SP_ERR_STATE, "sp_forward: transfer not schedulable");
-    CK(cudaStreamWaitEvent(c->compute, c->ev_xfer[b % RING], 0));
+    // every slot B(b) reads was filled by some Transfer(<= b): the last nx
+    // transfers may still be running on their own streams
+    for (int k = 0; k < c->nx && b - k >= 0; k++)
+        CK(cudaStreamWaitEvent(c->compute, c->ev_xfer[(b - k) % RING], 0));
     TrainArgs a = train_args(c, b);
+    c->cur_batch = b;
     a.pooled = pooled;
     CK(launch(c, SP_K_FORWARD, c->compute, [&] { return launch_forward(a, c->compute); }));
     c->forwarded = b + 1;
@@ -646,9 +724,13 @@ sp_status sp_train(sp_ctx *c, const float *grad, float lr) {
     CK(cudaSetDevice(c->device));
     const long long b = c->trained;
     TrainArgs a = train_args(c, b);
+    c->cur_batch = b;
     a.grad = grad;
     a.lr = lr;
-    CK(launch(c, SP_K_BACKWARD, c->compute, [&] { return launch_backward(a, c->compute); }));
+    CK(launch(c, SP_K_BACKWARD, c->compute, [&] {
+        cudaError_t e = launch_backward(a, c->compute);
+        return e != cudaSuccess ? e : launch_backward_hot(a, c->compute);
+    }));
     CK(cudaEventRecord(c->ev_train[b % RING], c->compute));
     c->trained = b + 1;
     c->fwd_pending = false;
@@ -673,7 +755,8 @@ sp_status sp_flush(sp_ctx *c) {
         return fail(c, SP_ERR_STATE, "sp_flush: every pushed batch must be trained first");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->plan_s));
-    CK(cudaStreamSynchronize(c->xfer_s));
+    for (int k = 0; k < c->nx; k++) CK(cudaStreamSynchronize(c->xfer_s[k]));
+    CK(cudaStreamSynchronize(c->wb_s));
     CK(cudaStreamSynchronize(c->compute));
     if (sp_status s = sync_error(c)) return s;
     FlushArgs a{};
@@ -729,7 +812,8 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->h2d_row_bytes = (int64_t)cum[2] * c->D * 4;
     o->d2h_row_bytes = (int64_t)cum[3] * c->D * 4;
     if (!c->prof_pending.empty()) {
-        cudaStreamSynchronize(c->xfer_s);
+        for (int k = 0; k < c->nx; k++) cudaStreamSynchronize(c->xfer_s[k]);
+        cudaStreamSynchronize(c->wb_s);
         cudaStreamSynchronize(c->compute);
         harvest_profile(c, true);
     }

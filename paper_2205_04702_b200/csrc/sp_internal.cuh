@@ -25,9 +25,9 @@ constexpr int RING = 16;                    // batches in flight (>= P+F+2)
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;     // empty Hit-Map entry / vacant slot
 constexpr int32_t VACANT = INT32_MIN;       // last_use of a never-used slot
 constexpr int32_t NEVER = INT32_MIN;        // next_need of a slot with no future use
-constexpr int CH = 32;                      // occurrences per backward chunk
+constexpr int CH = 16;                      // occurrences per backward chunk
 constexpr int PUSH_THREADS = 512;
-constexpr int SMEM_SORT_MAX = 16384;        // n_pad handled by the smem bitonic path
+constexpr int SMEM_SORT_MAX = 8192;         // n handled by the shared-memory radix sort
 constexpr unsigned long long NO_ERR = ~0ull;
 
 // device error word: min over (batch << 24 | table << 8 | kind)
@@ -38,12 +38,29 @@ __host__ __device__ inline unsigned long long err_key(long long b, int t, unsign
 
 // Per-batch ring buffers, all with a per-table region.  Strides:
 //   n  = N*L         (sorted_occ, sorted_uid, uniq_id, slot_u, hit, slot_of_occ,
-//                     fill_*, chunk_first)
+//                     fill_*)
 //   n1 = n + 1       (seg_off)
-//   nc = n + n/CH + 1 (chunk_u)
+//   nc = n + n/CH + 1 (chunk_rec)
+//   nh = n/CH + 1     (hot_rec)
+// chunk_rec[c]: up to CH consecutive occurrences (in ascending occurrence
+// order) of one unique row, with their bag indices inline so that the
+// backward pass needs one record load before the gradient rows.
+// hot_rec[h] = {u -> slot, first chunk, nch, 0} for every row with more than
+// CH occurrences (its chunk partials are folded by k_bwd_hot).
+struct ChunkRec {
+    uint32_t slot;      // unique index at dedup, Storage slot after Plan
+    uint32_t meta;      // occurrences in this chunk | 0x80000000 if the row has > 1 chunk
+    uint32_t bag[CH];   // table-local bag (sample) index of each occurrence
+    uint32_t pad[2];
+};
+static_assert(sizeof(ChunkRec) == 80, "ChunkRec is 5 x 16 bytes");
+
 struct BatchBufs {
     uint32_t *sorted_occ, *sorted_uid, *uniq_id, *seg_off, *U;
-    uint32_t *chunk_u, *chunk_first, *nchunks;
+    ChunkRec *chunk_rec;
+    uint32_t *nchunks;
+    uint4 *hot_rec;
+    uint32_t *nhot;
     uint32_t *slot_u, *slot_of_occ;
     uint8_t *hit;
     uint32_t *fill_slot, *fill_row, *evict_row, *m;
@@ -52,12 +69,12 @@ struct BatchBufs {
 
 struct Geometry {
     int T, N, L, D;
-    int n, n1, nc;        // strides
+    int n, n1, nc, nh;    // strides
 };
 
 struct PushArgs {
     Geometry g;
-    int n_pad, P, F;
+    int P, F;
     const unsigned long long *row_off;  // [T+1]
     const long long *rows;              // [T]
     const uint32_t *slot_base;          // [T+1]
@@ -70,17 +87,19 @@ struct PushArgs {
     unsigned long long *err;
     unsigned long long *cum;  // [4] cumulative U, hits, misses, evictions
     uint32_t *miss_u, *victims;  // plan scratch [T*n]
-    uint64_t *sort_tmp;          // [T*n] x2 scratch for the large-n radix path
-    // new batch j (dedup + future probe)
+    uint32_t *sort_tmp;          // [4][T*n] scratch for the large-n radix path
+    // CTAs [T, 2T): dedup of the new batch B(j)
     int has_new;
     long long j;
     const void *idx;
     int idx_i32;
     BatchBufs nb;
-    // Plan(b)
+    // CTAs [0, T): Plan(b), whose future window ends at B(b+F) (already deduped)
     int do_plan;
     long long b;
     BatchBufs pb;
+    int has_future;
+    BatchBufs fb;
 };
 
 struct TrainArgs {
@@ -90,8 +109,7 @@ struct TrainArgs {
     const float *grad;   // bwd
     float *pooled;       // fwd
     float lr;
-    double *partial;     // [T][nc][D]
-    uint32_t *cnt;       // [T][n]
+    double *partial;     // [T][nc][D] fp64 chunk partials of hot rows
     const unsigned long long *err;
 };
 
@@ -99,6 +117,7 @@ struct XferArgs {
     Geometry g;
     BatchBufs bb;
     float *storage;
+    float *stage;        // [T][n][D] victim rows of this batch, staged in HBM
     float *const *host;  // [T] device-visible host table pointers
     const unsigned long long *err;
 };
@@ -112,15 +131,55 @@ struct FlushArgs {
     float *const *host;
 };
 
+// Exclusive prefix of per-table counts[t0 .. t0+tcount) into s_pref[0..tcount]
+// (tcount <= 64).  Loads are issued in parallel (one per thread) and scanned
+// by warp 0: a serial loop of dependent-latency global loads would cost
+// ~0.5 us per table.  Contains __syncthreads.
+__device__ __forceinline__ void table_prefix(const uint32_t *counts, int t0, int tcount,
+                                             uint32_t *s_pref) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        uint32_t a = lane < tcount ? counts[t0 + lane] : 0u;
+        uint32_t b = lane + 32 < tcount ? counts[t0 + lane + 32] : 0u;
+        uint32_t x = a, y = b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t xa = __shfl_up_sync(0xffffffffu, x, o);
+            uint32_t yb = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) { x += xa; y += yb; }
+        }
+        const uint32_t tot_a = __shfl_sync(0xffffffffu, x, 31);
+        s_pref[lane] = x - a;
+        s_pref[lane + 32] = tot_a + y - b;
+        if (lane == 31) s_pref[64] = tot_a + y;
+    }
+    __syncthreads();
+}
+
+// Table of a flattened work item: the tl with s_pref[tl] <= item < s_pref[tl+1]
+// (binary search; empty tables have equal prefixes and are skipped).
+__device__ __forceinline__ int find_table(const uint32_t *s_pref, int tcount, uint32_t item) {
+    int lo = 0, hi = tcount;  // invariant: s_pref[lo] <= item < s_pref[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pref[mid] <= item) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
 // launchers (return cudaGetLastError())
 cudaError_t launch_push(const PushArgs &a, cudaStream_t s);
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s);
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s);
+cudaError_t launch_backward_hot(const TrainArgs &a, cudaStream_t s);
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
                              float delta, cudaStream_t s);
-cudaError_t launch_transfer(const XferArgs &a, int max_ctas, cudaStream_t s);
+cudaError_t launch_pull(const XferArgs &a, int ctas, cudaStream_t s);
+cudaError_t launch_writeback(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
-size_t push_smem_bytes(int n_pad);
+size_t push_smem_bytes(int n);
 cudaError_t configure_push_kernel();
 
 }  // namespace sp

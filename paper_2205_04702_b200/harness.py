@@ -29,9 +29,9 @@ def run_loop(sp, trace, gamma: float, delta: float, eta: float,
     def push(j):
         nonlocal planned
         sp.plan(trace[j])
-        while planned <= j - sp.F:
+        while planned <= j - sp.F - 1:  # Plan(b) runs at push(b+F+1)
             if on_plan:  # second argument: this Plan is the newest one enqueued
-                on_plan(planned, planned == j - sp.F)
+                on_plan(planned, planned == j - sp.F - 1)
             planned += 1
 
     for j in range(min(ahead, nb)):

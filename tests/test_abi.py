@@ -36,7 +36,7 @@ def test_status_codes_match_header():
 def test_desc_struct_layout():
     # offsets of the C struct under the x86-64 SysV ABI
     assert B.SpDesc.rows.offset == 8 and B.SpDesc.host_tables.offset == 16
-    assert B.SpDesc.stream.offset == 64 and ctypes.sizeof(B.SpDesc) == 80
+    assert B.SpDesc.stream.offset == 64 and ctypes.sizeof(B.SpDesc) == 88
 
 
 def test_invalid_descriptors_rejected_before_touching_a_device():
@@ -46,7 +46,8 @@ def test_invalid_descriptors_rejected_before_touching_a_device():
     slots = (ctypes.c_int64 * 1)(10)
     tabs = (ctypes.c_void_p * 1)(1)
     base = dict(num_tables=1, rows=rows, host_tables=tabs, dim=16, slots=slots, window=3, past=-1,
-                future=-1, batch_size=4, pooling=2, device=0, stream=None, flags=0, log_factor=0)
+                future=-1, batch_size=4, pooling=2, device=0, stream=None, flags=0, log_factor=0,
+                pull_ctas=0, writeback_ctas=0)
     for bad in [dict(dim=6), dict(dim=0), dict(num_tables=0), dict(batch_size=0),
                 dict(past=1, future=3)]:
         d = B.SpDesc(**{**base, **bad})

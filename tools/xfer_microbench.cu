@@ -49,6 +49,63 @@ __global__ void gather(const float4 *__restrict__ host, float4 *__restrict__ dev
     }
 }
 
+// both directions per slot: write back the victim row, pull the missed row
+// ORDER 0: ld dev v; st host v; ld host x; st dev x      (v1 kernel)
+// ORDER 1: ld host x; ld dev v; st host v; st dev x      (all loads first, per row)
+// ORDER 2: like 1 but all write-back stores of the UNR rows before any fill store
+// ORDER 3: split roles: even groups write back, odd groups pull (slot read
+//          ordering handled by a separate pass in the product; here timing only)
+template <int ORDER, int UNR>
+__global__ void exchange(float4 *host, float4 *dev, const unsigned *rows, const unsigned *old_rows,
+                         const unsigned *slots, int M, int D4) {
+    const int G = D4;
+    const int gpb = blockDim.x / G, lane = threadIdx.x % G;
+    const int ng = gridDim.x * gpb;
+    int gid = blockIdx.x * gpb + threadIdx.x / G;
+    if (ORDER == 3) {
+        const bool wbrole = gid & 1;
+        gid >>= 1;
+        for (int k = gid; k < M; k += ng / 2) {
+            if (wbrole) host[(size_t)old_rows[k] * D4 + lane] = dev[(size_t)slots[k] * D4 + lane];
+            else dev[(size_t)slots[k] * D4 + lane] = host[(size_t)rows[k] * D4 + lane];
+        }
+        return;
+    }
+    for (int base = gid * UNR; base < M; base += ng * UNR) {
+        float4 v[UNR], x[UNR];
+        if (ORDER == 0) {
+#pragma unroll
+            for (int r = 0; r < UNR; r++) if (base + r < M) v[r] = dev[(size_t)slots[base + r] * D4 + lane];
+#pragma unroll
+            for (int r = 0; r < UNR; r++) if (base + r < M) host[(size_t)old_rows[base + r] * D4 + lane] = v[r];
+#pragma unroll
+            for (int r = 0; r < UNR; r++) if (base + r < M) x[r] = __ldcv(host + (size_t)rows[base + r] * D4 + lane);
+#pragma unroll
+            for (int r = 0; r < UNR; r++) if (base + r < M) dev[(size_t)slots[base + r] * D4 + lane] = x[r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < UNR; r++)
+                if (base + r < M) {
+                    x[r] = __ldcv(host + (size_t)rows[base + r] * D4 + lane);
+                    v[r] = dev[(size_t)slots[base + r] * D4 + lane];
+                }
+            if (ORDER == 1) {
+#pragma unroll
+                for (int r = 0; r < UNR; r++)
+                    if (base + r < M) {
+                        host[(size_t)old_rows[base + r] * D4 + lane] = v[r];
+                        dev[(size_t)slots[base + r] * D4 + lane] = x[r];
+                    }
+            } else {
+#pragma unroll
+                for (int r = 0; r < UNR; r++) if (base + r < M) host[(size_t)old_rows[base + r] * D4 + lane] = v[r];
+#pragma unroll
+                for (int r = 0; r < UNR; r++) if (base + r < M) dev[(size_t)slots[base + r] * D4 + lane] = x[r];
+            }
+        }
+    }
+}
+
 __global__ void scatter_back(float4 *host, const float4 *dev, const unsigned *rows, const unsigned *slots,
                              int M, int D4) {
     const int G = D4;
@@ -119,6 +176,29 @@ int main(int argc, char **argv) {
                        contiguous ? "contig" : "random", M, grid, t0, mb / t0 * 1e-3 * 1e3, t1, t2, t3, t4,
                        mb / t4 * 1e-3 * 1e3, t5);
             }
+        }
+    }
+    // combined exchange variants (random rows, disjoint read / write-back sets)
+    unsigned *d_old;
+    CK(cudaMalloc(&d_old, 60000 * 4));
+    for (int M : Ms) {
+        std::vector<unsigned> rows(M), old(M), slots(M);
+        for (int k = 0; k < M; k++) {
+            rows[k] = (unsigned)(rng() % (R / 2));
+            old[k] = (unsigned)(R / 2 + rng() % (R / 2));
+            slots[k] = (unsigned)(rng() % 4000000);
+        }
+        CK(cudaMemcpy(d_rows, rows.data(), M * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_old, old.data(), M * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_slots, slots.data(), M * 4, cudaMemcpyHostToDevice));
+        for (int grid : {37, 74, 148, 296}) {
+            float t0 = timeit([&] { exchange<0, 4><<<grid, 256>>>((float4 *)h, dev, d_rows, d_old, d_slots, M, D4); });
+            float t1 = timeit([&] { exchange<1, 4><<<grid, 256>>>((float4 *)h, dev, d_rows, d_old, d_slots, M, D4); });
+            float t2 = timeit([&] { exchange<2, 4><<<grid, 256>>>((float4 *)h, dev, d_rows, d_old, d_slots, M, D4); });
+            float t3 = timeit([&] { exchange<3, 1><<<grid, 256>>>((float4 *)h, dev, d_rows, d_old, d_slots, M, D4); });
+            float t4 = timeit([&] { exchange<2, 1><<<grid, 256>>>((float4 *)h, dev, d_rows, d_old, d_slots, M, D4); });
+            printf("exchange M=%6d grid=%3d | v1-order %.1fus | loads-first %.1fus | wb-stores-first %.1fus | split-roles %.1fus | wb-first unr1 %.1fus\n",
+                   M, grid, t0, t1, t2, t3, t4);
         }
     }
     // copy-engine reference: one contiguous H2D of M rows
