@@ -225,10 +225,11 @@ def run_ours(args):
     nb = nb_dev + ahead + nb_host
 
     # ---- inputs: host tables (pinned), trace (device int32; host int32 part pinned)
-    tables = []
+    from paper_2205_04702_b200 import HostTable
+    tables = []   # THP-backed, CUDA-registered host tables (sp_host_alloc)
     for t in mine:
-        h = torch.empty((cfg.rows[t], D), dtype=torch.float32).pin_memory()
-        init_table(cfg.init_seed, t, cfg.rows[t], D, device=dev, out=h)
+        h = HostTable(cfg.rows[t], D)
+        init_table(cfg.init_seed, t, cfg.rows[t], D, device=dev, out=h.tensor)
         tables.append(h)
     trace = torch.empty((nb, len(mine), N, L), dtype=torch.int32, device=dev)
     CH = 512
@@ -298,34 +299,60 @@ def run_ours(args):
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item()), sampler
 
-    # ---- preroll + warm-up (device indices)
-    for _ in range(ahead):
-        push_dev()
+    # ---- preroll + warm-up + timed value loop: device-resident indices, the
+    # library's C driver loop (sp_run_steps: plan / forward / surrogate / train)
+    dev_trace = trace[:nb_dev + ahead]
     t_pre = time.perf_counter()
-    for _ in range(pre):
-        train_step(push_dev)
-    for _ in range(W):
-        train_step(push_dev)
+    if world == 1:
+        sp.run_steps(dev_trace, pre + W, pooled, grad, g_, d_, e_)
+    else:
+        for _ in range(ahead):
+            push_dev()
+        for _ in range(pre + W):
+            train_step(push_dev)
     torch.cuda.synchronize()
     t_pre = time.perf_counter() - t_pre
     st0 = sp.stats()
+
+    def value_loop(n):
+        if world == 1:
+            sp.run_steps(dev_trace, n, pooled, grad, g_, d_, e_)
+        else:
+            for _ in range(n):
+                train_step(push_dev)
+
     # ---- timed: value (inputs resident in HBM)
-    ms, sampler = timed(lambda k: train_step(push_dev), K, sampler_index=local)
+    barrier()
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    sampler.__enter__()
+    t_host = time.perf_counter()
+    s_ev.record(stream)
+    value_loop(K)
+    e_ev.record(stream)
+    t_host_issue = time.perf_counter() - t_host
+    barrier()
+    sampler.__exit__()
+    ms_t = torch.tensor([s_ev.elapsed_time(e_ev)], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
     st1 = sp.stats()
     value = K / (ms / 1e3)   # iterations of the global batch per second (max over ranks)
     ms_per_step = ms / K
+    from paper_2205_04702_b200._binding import KERNEL_ONLY
     launches = {k: st1["kernel_launches"][k] - st0["kernel_launches"][k] for k in st1["kernel_launches"]}
-    gpu_launches = sum(launches.values())
+    gpu_launches = sum(v for k, v in launches.items() if k in KERNEL_ONLY)
     # ---- profiling pass: per-kernel CUDA-event durations (separate from the timed region)
     sp.set_profiling(True)
-    for _ in range(KP):
-        train_step(push_dev)
+    value_loop(KP)
     sp.set_profiling(False)
     st2 = sp.stats()
     if os.environ.get("SP_TIMELINE"):
         json.dump(sp.timeline(), open(os.environ["SP_TIMELINE"], "w"))
+    state["pushed"] = nb_dev + ahead
+    state["trained"] = nb_dev
     # ---- e2e: host indices through the public API, D2H of every step's Plan counters
-    assert state["pushed"] == nb_dev + ahead
     for k in range(W):
         train_step(push_host, read_stats_slot=k)
     hits_seen = []
@@ -359,15 +386,16 @@ def run_ours(args):
         # pooled grad in + occurrence list + per-unique segment/slot words + SGD read+write
         "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 8 * D * U,
         "surrogate": 8 * D * Tg * N,
-        "transfer": 4 * D * m + 8 * D * ev,      # pull (PCIe read) + victim staging (HBM r/w)
-        "writeback": 4 * D * ev,
+        "transfer": 8 * D * m + 8 * D * ev,      # k_fill: staged rows in + slot write, victims out
+        "h2d": 4 * D * m,                        # copy engine: gathered missed rows
+        "d2h": 4 * D * m,                        # copy engine: staged victims (one row per fill)
         "plan": 4 * Tg * n,
     }
     peak, peak_kind = peaks()
     traffic = load_traffic()
     total_ms = sum(kms.values()) or 1.0
     kernels = {}
-    for k in ["plan", "transfer", "writeback", "forward", "backward", "surrogate"]:
+    for k in ["plan", "transfer", "h2d", "d2h", "forward", "backward", "surrogate"]:
         gbs = alg_bytes[k] / (avg_ms[k] * 1e-3) / 1e9 if avg_ms[k] else None
         kernels[k] = {"avg_us": round(avg_ms[k] * 1e3, 3), "share": round(kms[k] / total_ms, 4),
                       "alg_bytes_per_launch": int(alg_bytes[k]), "alg_GBs": None if gbs is None else round(gbs, 1)}
@@ -383,8 +411,8 @@ def run_ours(args):
                                   else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
     train_ms = avg_ms["forward"] + avg_ms["backward"]
     train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
-    link_GBs = 4 * D * m / (avg_ms["transfer"] * 1e-3) / 1e9 if avg_ms["transfer"] else None
-    wb_GBs = alg_bytes["writeback"] / (avg_ms["writeback"] * 1e-3) / 1e9 if avg_ms.get("writeback") else None
+    link_GBs = alg_bytes["h2d"] / (avg_ms["h2d"] * 1e-3) / 1e9 if avg_ms.get("h2d") else None
+    wb_GBs = alg_bytes["d2h"] / (avg_ms["d2h"] * 1e-3) / 1e9 if avg_ms.get("d2h") else None
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
@@ -400,17 +428,25 @@ def run_ours(args):
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
-        "host_link": {"pull_kernel": "transfer", "pull_bytes_per_launch": int(4 * D * m),
-                      "pull_GBs": None if link_GBs is None else round(link_GBs, 2),
-                      "writeback_bytes_per_launch": int(alg_bytes["writeback"]),
-                      "writeback_GBs": None if wb_GBs is None else round(wb_GBs, 2),
+        "host_link": {"path": "CPU gather/scatter + copy-engine DMA (both directions)",
+                      "h2d_bytes_per_batch": int(alg_bytes["h2d"]),
+                      "h2d_GBs": None if link_GBs is None else round(link_GBs, 2),
+                      "d2h_bytes_per_batch": int(alg_bytes["d2h"]),
+                      "d2h_GBs": None if wb_GBs is None else round(wb_GBs, 2),
                       "peak_h2d_GBs": 55.6, "peak_d2h_GBs": 57.0,
                       "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)"},
         "kernels": kernels,
         "per_step": {"uniques": round(U, 1), "misses": round(m, 1), "evictions": round(ev, 1)},
+        "host_engine": {"gather_us_per_batch": round(1e3 * (st2["host_gather_ms"] - st1["host_gather_ms"]) / KP, 2),
+                        "scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1["host_scatter_ms"]) / KP, 2),
+                        "threads": "gather + scatter threads, 8 row-copy helpers"},
         "gpu_launches": int(gpu_launches),
         "launches_per_step": {k: v / K for k, v in launches.items()},
-        "clocks": sampler.summary() if sampler else None,
+        "clocks": sampler.summary(),
+        "host_issue_us_per_step": round(1e6 * t_host_issue / K, 2),
+        "host_waits_us_per_step": {"transfer": round(1e3 * (st1["wait_xfer_ms"] - st0["wait_xfer_ms"]) / K, 2),
+                                   "list_slot": round(1e3 * (st1["wait_list_ms"] - st0["wait_list_ms"]) / K, 2)},
+        "graph_steps": st1["graph_steps"] - st0["graph_steps"],
         "e2e": {"value": round(e2e_value, 2), "unit": "iters/s", "h2d_bytes_per_step": idx_bytes,
                 "d2h_bytes_per_step": stats_bytes, "ms_per_step": round(ms_e2e / K, 5),
                 "path": "sp_plan(host int32 indices, pinned) -> H2D on the plan stream; "

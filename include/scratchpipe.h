@@ -10,10 +10,11 @@
  *               Hit-Map probe, hit/miss, window-safe LRU victim selection
  *               (past window P:840-861, future window P:864-884, superset
  *               P:887-896), Hit-Map/Storage bookkeeping.
- *               [Collect]+[Exchange]+[Insert] run as two
- *               SM-issued zero-copy kernels split by link direction: a pull
- *               (victim staged in HBM, missed row into the freed slot) and a
- *               rate-limited write-back of the staged victims.
+ *               [Collect]+[Exchange]+[Insert] run in the
+ *               library's transfer engine: CPU threads gather missed rows /
+ *               scatter victims in host memory, the copy engines move both
+ *               directions over PCIe at once, one HBM kernel fills the
+ *               freed slots and stages the victims.
  *   sp_forward  [Training] part 1: EmbeddingBag gather-reduce.
  *   sp_train    [Training] part 2: gradient duplication + coalescing
  *                and the SGD update in place in the scratchpad
@@ -95,20 +96,23 @@ typedef struct {
     uint32_t flags;              /* SP_FLAG_*                                       */
     int32_t log_factor;          /* LRU-log ring capacity per table =               */
                                  /* log_factor * slots[t] + 4*N*L (0 -> 8)          */
-    int32_t pull_ctas;           /* CTAs of the host-row pull kernel (0 -> 16)      */
-    int32_t writeback_ctas;      /* CTAs of the rate-limited write-back (0 -> 2)    */
+    int32_t host_threads;        /* CPU helper threads of the transfer engine that  */
+                                 /* copy rows between host tables and pinned        */
+                                 /* staging (0 -> 8), split between the gather and  */
+                                 /* the scatter thread                              */
+    int32_t reserved;            /* must be 0                                       */
 } sp_desc;
 
 typedef enum {
     SP_K_PLAN = 0,      /* dedup + future probe + Plan (one launch per sp_plan)  */
-    SP_K_TRANSFER = 1,  /* Collect/Exchange/Insert, host->HBM direction: victims  */
-                        /* staged in HBM, missed rows pulled into freed slots     */
+    SP_K_TRANSFER = 1,  /* k_fill: victims staged, freed slots filled (HBM)       */
     SP_K_FORWARD = 2,   /* EmbeddingBag gather-reduce                             */
     SP_K_BACKWARD = 3,  /* duplicate-coalescing segmented reduce + fused SGD      */
     SP_K_SURROGATE = 4, /* harness MLP stand-in g = fmaf(gamma, pooled, delta)    */
     SP_K_FLUSH = 5,     /* write-back of all resident rows                        */
-    SP_K_WRITEBACK = 6, /* HBM->host direction: staged victims to host tables     */
-    SP_K_COUNT = 7
+    SP_K_H2D = 6,       /* copy-engine DMA of the gathered missed rows            */
+    SP_K_D2H = 7,       /* copy-engine DMA of the staged victims                  */
+    SP_K_COUNT = 8
 } sp_kernel_kind;
 
 typedef struct {
@@ -123,9 +127,23 @@ typedef struct {
     double kernel_ms[SP_K_COUNT];   /* SP_FLAG_PROFILE only: summed CUDA-event */
                                     /* durations of completed launches         */
     int64_t kernel_timed[SP_K_COUNT];
+    double host_gather_ms;          /* transfer engine: CPU time gathering missed */
+    double host_scatter_ms;         /* rows / scattering victims (wall, summed)   */
+    int64_t host_rows_gathered, host_rows_scattered;
+    double wait_xfer_ms;            /* caller thread waiting for the transfer     */
+    double wait_list_ms;            /* engine (forward / host-list ring reuse)    */
+    int64_t graph_steps;            /* sp_run_steps steps replayed as CUDA graphs */
 } sp_stats;
 
 int32_t sp_abi_version(void);
+
+/* Host-table allocator: `bytes` of anonymous host memory backed by 2 MB
+ * transparent huge pages where the OS allows (the CPU side of the transfer
+ * engine gathers / scatters random rows: 4 KB pages cost a TLB walk per row),
+ * registered with CUDA as mapped + portable.  Pass the pointer in
+ * desc.host_tables WITHOUT SP_FLAG_REGISTER_HOST.  Free with sp_host_free. */
+sp_status sp_host_alloc(size_t bytes, void **out);
+sp_status sp_host_free(void *ptr, size_t bytes);
 
 /* Create a context: validates the descriptor, allocates Storage
  * (sum slots x dim fp32), the Hit-Map, per-slot metadata, the LRU log and a
@@ -187,6 +205,23 @@ sp_status sp_set_profiling(sp_ctx *c, int32_t on);
  * writes min(cap, *n) records. */
 sp_status sp_get_timeline(sp_ctx *c, int32_t *kind, int64_t *batch, double *start_ms,
                           double *end_ms, int64_t cap, int64_t *n);
+
+/* Harness driver loop (benchmarks, tests): runs `steps` training iterations
+ * without returning to the caller, each exactly
+ *   sp_plan_device(indices + j*stride) while the look-ahead is short (sp_end_of_data
+ *   once the trace is exhausted and the next batch cannot be planned otherwise),
+ *   sp_forward(pooled), sp_surrogate_grad(pooled, grad, 0, gamma, delta),
+ *   sp_train(grad, lr)
+ * The first call pushes F+P+1 batches ahead.  `indices` is a DEVICE array of
+ * `num_batches` batches [T][N][L] (index width per SP_FLAG_INDEX_I32) with
+ * `stride` bytes between batches; batch j of the trace is pushed at most once
+ * (the loop continues from the context's counters).  pooled / grad: device
+ * [T][N][D].  When stats_out (pinned host, [steps][T][4]) is non-NULL, every
+ * step's Plan counters are copied back (sp_copy_batch_stats).  Returns the
+ * first error. */
+sp_status sp_run_steps(sp_ctx *c, const void *indices, int64_t num_batches, int64_t stride,
+                       int64_t steps, float *pooled, float *grad, float gamma, float delta,
+                       float lr, uint32_t *stats_out);
 
 /* Drain and write every resident row back to its host table; on return the
  * host tables are coherent.  Requires every pushed batch to be trained (call

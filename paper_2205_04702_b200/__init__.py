@@ -15,6 +15,7 @@ from ._binding import (  # noqa: F401
     SP_ERR_STATE,
     SP_OK,
     STATUS_NAMES,
+    HostTable,
     ScratchPipe,
     SpError,
     header_symbols,

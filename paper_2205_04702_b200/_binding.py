@@ -26,7 +26,8 @@ SP_FLAG_REGISTER_HOST = 1 << 0
 SP_FLAG_INDEX_I32 = 1 << 1
 SP_FLAG_INDEX_DEVICE = 1 << 2
 SP_FLAG_PROFILE = 1 << 3
-KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush", "writeback"]
+KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush", "h2d", "d2h"]
+KERNEL_ONLY = ["plan", "transfer", "forward", "backward", "surrogate", "flush"]
 
 
 class SpDesc(ctypes.Structure):
@@ -45,8 +46,8 @@ class SpDesc(ctypes.Structure):
         ("stream", ctypes.c_void_p),
         ("flags", ctypes.c_uint32),
         ("log_factor", ctypes.c_int32),
-        ("pull_ctas", ctypes.c_int32),
-        ("writeback_ctas", ctypes.c_int32),
+        ("host_threads", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -58,8 +59,12 @@ class SpStats(ctypes.Structure):
         ("evictions", ctypes.c_int64),
         ("h2d_index_bytes", ctypes.c_int64), ("h2d_row_bytes", ctypes.c_int64),
         ("d2h_row_bytes", ctypes.c_int64),
-        ("kernel_launches", ctypes.c_int64 * 7), ("kernel_ms", ctypes.c_double * 7),
-        ("kernel_timed", ctypes.c_int64 * 7),
+        ("kernel_launches", ctypes.c_int64 * 8), ("kernel_ms", ctypes.c_double * 8),
+        ("kernel_timed", ctypes.c_int64 * 8),
+        ("host_gather_ms", ctypes.c_double), ("host_scatter_ms", ctypes.c_double),
+        ("host_rows_gathered", ctypes.c_int64), ("host_rows_scattered", ctypes.c_int64),
+        ("wait_xfer_ms", ctypes.c_double), ("wait_list_ms", ctypes.c_double),
+        ("graph_steps", ctypes.c_int64),
     ]
 
 
@@ -77,6 +82,8 @@ def _load():
     for name, args in [("sp_plan", [P, P]), ("sp_plan_device", [P, P]),
                        ("sp_copy_batch_stats", [P, ctypes.c_int64, P]),
                        ("sp_set_profiling", [P, ctypes.c_int32]),
+                       ("sp_run_steps", [P, P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, P, P,
+                                         ctypes.c_float, ctypes.c_float, ctypes.c_float, P]),
                        ("sp_get_timeline", [P, P, P, P, P, ctypes.c_int64, i64p]), ("sp_end_of_data", [P]), ("sp_forward", [P, P]),
                        ("sp_train", [P, P, ctypes.c_float]),
                        ("sp_surrogate_grad", [P, P, P, ctypes.c_int64, ctypes.c_float, ctypes.c_float]),
@@ -90,6 +97,10 @@ def _load():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = S
+    L.sp_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+    L.sp_host_alloc.restype = S
+    L.sp_host_free.argtypes = [P, ctypes.c_size_t]
+    L.sp_host_free.restype = S
     L.sp_error_string.argtypes = [P]
     L.sp_error_string.restype = ctypes.c_char_p
     return L
@@ -103,6 +114,33 @@ def header_symbols() -> List[str]:
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(sp_[a-z_]+)\s*\(", src)))
+
+
+class HostTable:
+    """A host embedding table from sp_host_alloc (THP-backed, CUDA-registered);
+    `.tensor` is a float32 CPU torch view [rows][dim]."""
+
+    def __init__(self, rows: int, dim: int):
+        import torch
+        self.bytes = int(rows) * int(dim) * 4
+        p = ctypes.c_void_p()
+        st = lib.sp_host_alloc(self.bytes, ctypes.byref(p))
+        if st != SP_OK:
+            raise SpError(st, "sp_host_alloc failed")
+        self.ptr = p.value
+        buf = (ctypes.c_byte * self.bytes).from_address(self.ptr)
+        self.tensor = torch.frombuffer(buf, dtype=torch.float32).view(int(rows), int(dim))
+
+    def data_ptr(self):
+        return self.ptr
+
+    def free(self):
+        if self.ptr:
+            self.tensor = None
+            lib.sp_host_free(ctypes.c_void_p(self.ptr), self.bytes)
+            self.ptr = None
+
+    __del__ = free
 
 
 class SpError(RuntimeError):
@@ -127,7 +165,7 @@ class ScratchPipe:
                  batch_size: int, pooling: int, window: int = 3, past: int = -1, future: int = -1,
                  device: int = 0, stream=None, index_dtype: str = "int64", index_on_device: bool = False,
                  register_host: bool = False, profile: bool = False, log_factor: int = 0,
-                 pull_ctas: int = 0, writeback_ctas: int = 0):
+                 host_threads: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("ScratchPipe needs a CUDA device (no CPU fallback)")
@@ -152,7 +190,7 @@ class ScratchPipe:
         self.index_dtype, self.index_on_device = index_dtype, index_on_device
         d = SpDesc(self.T, _i64(self._rows), self._hp, dim, _i64(self._slots), window, past, future,
                    batch_size, pooling, device, ctypes.c_void_p(stream.cuda_stream), flags, log_factor,
-                   pull_ctas, writeback_ctas)
+                   host_threads, 0)
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             st = lib.sp_create(ctypes.byref(d), ctypes.byref(h))
@@ -200,6 +238,18 @@ class ScratchPipe:
         """Async D2H of batch b's per-table (U, hits, misses, evictions) into a
         pinned int32 tensor [T][4], ordered on the context's stream."""
         self._check(lib.sp_copy_batch_stats(self._h, b, ctypes.c_void_p(host_out.data_ptr())))
+
+    def run_steps(self, trace_dev, steps: int, pooled, grad, gamma: float, delta: float, lr: float,
+                  stats_out=None):
+        """C driver loop over a device-resident trace [nb][T][N][L] (see sp_run_steps)."""
+        if not trace_dev.is_cuda or not trace_dev.is_contiguous():
+            raise TypeError("trace must be a contiguous CUDA tensor")
+        self._last_idx = trace_dev
+        stride = trace_dev[0].numel() * trace_dev.element_size()
+        self._check(lib.sp_run_steps(self._h, ctypes.c_void_p(trace_dev.data_ptr()), trace_dev.shape[0],
+                                     stride, steps, ctypes.c_void_p(pooled.data_ptr()),
+                                     ctypes.c_void_p(grad.data_ptr()), float(gamma), float(delta), float(lr),
+                                     None if stats_out is None else ctypes.c_void_p(stats_out.data_ptr())))
 
     def set_profiling(self, on: bool):
         self._check(lib.sp_set_profiling(self._h, 1 if on else 0))
@@ -257,6 +307,9 @@ class ScratchPipe:
         out["kernel_launches"] = dict(zip(KERNEL_KINDS, list(s.kernel_launches)))
         out["kernel_ms"] = dict(zip(KERNEL_KINDS, list(s.kernel_ms)))
         out["kernel_timed"] = dict(zip(KERNEL_KINDS, list(s.kernel_timed)))
+        for k in ("host_gather_ms", "host_scatter_ms", "host_rows_gathered", "host_rows_scattered",
+                  "wait_xfer_ms", "wait_list_ms", "graph_steps"):
+            out[k] = getattr(s, k)
         out["status"] = st
         return out
 

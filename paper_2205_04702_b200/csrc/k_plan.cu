@@ -69,8 +69,12 @@ __device__ uint32_t block_scan(uint32_t v, uint32_t *total) {
     return pre + x - v;
 }
 
-__device__ __forceinline__ void set_err(unsigned long long *err, long long b, int t, unsigned k) {
-    atomicMin(err, err_key(b, t, k));
+// latch a device error: exact (min) key in device memory, plus a zero-copy
+// flag the host's transfer engine and API calls poll without a D2H copy
+__device__ __forceinline__ void set_err(const PushArgs &A, long long b, int t, unsigned k) {
+    atomicMin(A.err, err_key(b, t, k));
+    __threadfence_system();
+    *(volatile unsigned long long *)A.err_host = 1ull;
 }
 
 __device__ __forceinline__ int bit_width_u64(unsigned long long x) { return x ? 64 - __clzll(x) : 0; }
@@ -153,7 +157,7 @@ __device__ bool radix_sort_pairs(uint32_t *ka, uint32_t *va, uint32_t *kb, uint3
 }
 
 // ------------------------------------------------------------------ dedup
-__device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw) {
+__device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, long long j, const void *idx) {
     // (the chunk records of D3 use the sort's free ping-pong buffer as scratch)
     const Geometry &g = A.g;
     const int n = g.n, tid = threadIdx.x;
@@ -172,14 +176,14 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw) {
     // D1: ingest + range check
     int bad = 0;
     for (int i = tid; i < n; i += blockDim.x) {
-        long long id = A.idx_i32 ? (long long)((const int32_t *)A.idx)[(size_t)t * n + i]
-                                 : ((const long long *)A.idx)[(size_t)t * n + i];
+        long long id = A.idx_i32 ? (long long)((const int32_t *)idx)[(size_t)t * n + i]
+                                 : ((const long long *)idx)[(size_t)t * n + i];
         if (id < 0 || id >= R) { bad = 1; id = 0; }
         ka[i] = (uint32_t)id;
         va[i] = (uint32_t)i;
     }
     if (__syncthreads_or(bad)) {
-        if (tid == 0) set_err(A.err, A.j, t, DERR_INDEX);
+        if (tid == 0) set_err(A, j, t, DERR_INDEX);
         return;
     }
     // D2: sort by id (stable: occurrences stay ascending within an id)
@@ -256,14 +260,13 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw) {
 }
 
 // ------------------------------------------------------------------- plan
-__device__ void plan_table(const PushArgs &A, int t) {
+__device__ void plan_table(const PushArgs &A, int t, long long b) {
     const Geometry &g = A.g;
     const int n = g.n, tid = threadIdx.x;
     __shared__ uint32_t s_fail, s_got;
     __shared__ unsigned long long s_head, s_newhead, s_tail;
     const unsigned long long roff = A.row_off[t];
     const BatchBufs &pb = A.pb;
-    const long long b = A.b;
 
     // P1: future probe of B(b+F)
     if (A.has_future) {
@@ -357,7 +360,7 @@ __device__ void plan_table(const PushArgs &A, int t) {
         if (s_fail) break;
     }
     if (s_fail) {
-        if (tid == 0) set_err(A.err, b, t, DERR_CAPACITY);
+        if (tid == 0) set_err(A, b, t, DERR_CAPACITY);
         return;
     }
 
@@ -366,6 +369,7 @@ __device__ void plan_table(const PushArgs &A, int t) {
     uint32_t *fill_row = pb.fill_row + (size_t)t * n;
     uint32_t *evict_row = pb.evict_row + (size_t)t * n;
     uint32_t nev = 0;
+    uint2 *hent = A.hl.ent + (size_t)t * n;  // pinned host mirror (zero-copy, ~8 B per fill)
     for (uint32_t k = tid; k < m; k += blockDim.x) {
         const uint32_t u = miss_u[k], s = victims[k], id = uniq_id[u];
         const uint32_t old = A.resident[s];
@@ -381,9 +385,18 @@ __device__ void plan_table(const PushArgs &A, int t) {
         fill_slot[k] = s;
         fill_row[k] = id;
         evict_row[k] = old;
+        hent[k] = make_uint2(id, old);
     }
     uint32_t ev_total;
     (void)block_scan(nev, &ev_total);  // barriers: P4 writes visible below
+    if (tid == 0) {
+        pb.m[t] = m;  // device copy for k_fill, published before the ready flag
+        A.hl.m[t] = m;
+        // the CTA's host-list writes precede this fence through the barrier
+        // above (causality order), so one system-scope fence publishes them all
+        __threadfence_system();
+        *(volatile unsigned long long *)&A.hl.ready[t] = (unsigned long long)(b + 1);
+    }
 
     // P5: LRU log append (after an in-place compaction if it would overflow)
     const unsigned long long head = s_head;
@@ -421,7 +434,6 @@ __device__ void plan_table(const PushArgs &A, int t) {
     if (tid == 0) {
         A.log_head[t] = head;
         A.log_tail[t] = tail + Ub;
-        pb.m[t] = m;
         uint32_t *st = pb.stats + 4 * t;
         st[0] = Ub; st[1] = nhit; st[2] = m; st[3] = ev_total;
         atomicAdd(&A.cum[0], (unsigned long long)Ub);
@@ -448,10 +460,18 @@ __global__ void __launch_bounds__(PUSH_THREADS, 2) k_push(PushArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (*A.err != NO_ERR) return;  // poisoned: nothing more is planned
     const int T = A.g.T;
+    long long j = A.j, b = A.b;
+    const void *idx = A.idx;
+    if (A.ctl) {  // CUDA-graph replay: absolute batch indices from the device chain
+        j = A.ctl[A.ctl_r];
+        b = j - A.F - 1;
+        idx = static_cast<const char *>(A.idx) + j * A.idx_stride;
+        if (blockIdx.x == 0 && threadIdx.x == 0) A.ctl[(A.ctl_r + 1) % RING] = j + 1;
+    }
     if ((int)blockIdx.x < T) {
-        if (A.do_plan) plan_table(A, blockIdx.x);
+        if (A.do_plan) plan_table(A, blockIdx.x, b);
     } else if (A.has_new) {
-        dedup_table(A, blockIdx.x - T, smem_raw);
+        dedup_table(A, blockIdx.x - T, smem_raw, j, idx);
     }
 }
 

@@ -1,26 +1,39 @@
 // runtime.cu — host runtime behind include/scratchpipe.h.
 //
-// Pipeline schedule (Fig. 8 P:803-813 re-expressed with CUDA streams
-// and events instead of lock-step cycles):
-//   plan stream      push(j): H2D of B(j) -> k_push = dedup B(j) + future probe
-//                    + Plan(j-F)                      -> record ev_plan[j-F]
-//   transfer stream  Transfer(b) waits ev_plan[b] and ev_train[b-P-1]
-//                    (a victim's last reader/writer is Train(<= b-P-1), the
-//                    past-window rule P:840-861) -> record ev_xfer[b];
-//                    transfers run in batch order, so a row written back by
-//                    Transfer(b') is pulled again only by a later transfer
-//                    (RAW-4)
-//   compute stream   Train(b) = forward + caller's MLP + backward/SGD waits
-//                    ev_xfer[b]                      -> record ev_train[b]
-// Up to P transfers run ahead of Train; there is no host synchronisation in
-// the steady state (only pinned staging-buffer recycling, 16 batches back).
+// Pipeline schedule: PAPER.md Fig. 8 re-expressed with CUDA
+// streams, events and a native transfer-engine thread instead of lock-step
+// cycles:
+//
+//   plan stream     push(j): [H2D of B(j)] -> k_push: dedup B(j) beside
+//                   Plan(b = j-F-1) -> record ev_plan[b]; Plan(b) also
+//                   mirrors its fill lists into pinned host memory
+//   transfer stream Transfer(b) once Train(b-P-1) is enqueued (past window,
+//                   P:840-861): waits ev_plan[b], ev_train[b-P-1] and, on the
+//                   GPU, for the pinned counter "scattered >= b-F" (RAW-4,
+//                   the CPU write-back of batch b-F-1 has landed)
+//                   -> k_pullfill ([Collect] + [Insert] on the GPU side:
+//                   victims staged in HBM, missed rows pulled by zero-copy
+//                   reads into the freed slots) -> record ev_xfer[b]
+//   transfer engine (scatter thread + row-copy helpers): for b in order,
+//                   D2H DMA of the staged victims ([Exchange]) and CPU scatter
+//                   into the host tables ([Insert]), then scattered = b+1
+//   compute stream  forward(b) waits ev_xfer[b]; train(b) -> record ev_train[b]
+//
+// No host synchronisation on the caller's thread in the steady state.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <immintrin.h>
+#include <sys/mman.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/scratchpipe.h"
@@ -42,6 +55,91 @@ struct TimelineRec {
     double start_ms, end_ms;  // relative to the profiling reference event
 };
 
+// Fork-join pool of spinning threads copying rows between host tables and
+// pinned staging (the CPU side of Collect / Insert).
+struct RowPool {
+    std::vector<std::thread> th;
+    std::atomic<uint64_t> gen{0};
+    std::atomic<long> next{0};
+    std::atomic<int> done{0};
+    std::atomic<bool> stop{false};
+    const float *const *src = nullptr;
+    float *const *dst = nullptr;
+    long n = 0;
+    size_t bytes = 0;
+
+    static constexpr long CHUNK = 16;
+
+    void run_chunks() {
+        for (;;) {
+            const long i0 = next.fetch_add(CHUNK, std::memory_order_relaxed);
+            if (i0 >= n) break;
+            const long i1 = std::min(n, i0 + CHUNK);
+            // all source lines of the chunk in flight first (random host rows:
+            // memory-level parallelism, not bandwidth, bounds a core here)
+            for (long i = i0; i < i1; i++) {
+                const char *p = reinterpret_cast<const char *>(src[i]);
+                for (size_t o = 0; o < bytes; o += 64) __builtin_prefetch(p + o, 0, 2);
+            }
+            // non-temporal stores: a random destination row costs no
+            // read-for-ownership, and staging never pollutes the caches
+            for (long i = i0; i < i1; i++) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(src[i]) | reinterpret_cast<uintptr_t>(dst[i]);
+                if ((a & 15) == 0 && (bytes & 15) == 0) {
+                    const __m128i *sp = reinterpret_cast<const __m128i *>(src[i]);
+                    __m128i *dp = reinterpret_cast<__m128i *>(dst[i]);
+                    for (size_t q = 0; q < bytes / 16; q++) _mm_stream_si128(dp + q, _mm_load_si128(sp + q));
+                } else {
+                    std::memcpy(dst[i], src[i], bytes);
+                }
+            }
+            _mm_sfence();
+        }
+    }
+
+    void helper() {
+        uint64_t seen = 0;
+        int idle = 0;
+        while (!stop.load(std::memory_order_relaxed)) {
+            const uint64_t g = gen.load(std::memory_order_acquire);
+            if (g == seen) {
+                if (++idle > 4096) std::this_thread::yield();
+                else _mm_pause();
+                continue;
+            }
+            idle = 0;
+            seen = g;
+            run_chunks();
+            done.fetch_add(1, std::memory_order_acq_rel);
+        }
+    }
+
+    void start(int nthreads) {
+        for (int i = 0; i < nthreads; i++) th.emplace_back([this] { helper(); });
+    }
+
+    void copy(const float *const *s, float *const *d, long count, size_t row_bytes) {
+        if (count <= 0) return;
+        src = s;
+        dst = d;
+        n = count;
+        bytes = row_bytes;
+        next.store(0, std::memory_order_relaxed);
+        done.store(0, std::memory_order_relaxed);
+        gen.fetch_add(1, std::memory_order_acq_rel);
+        run_chunks();
+        while (done.load(std::memory_order_acquire) < (int)th.size()) _mm_pause();
+    }
+
+    void shutdown() {
+        stop = true;
+        for (auto &t : th) t.join();
+        th.clear();
+    }
+};
+
+enum : int { K_H2D = SP_K_H2D, K_D2H = SP_K_D2H };
+
 }  // namespace
 
 struct sp_ctx {
@@ -57,16 +155,8 @@ struct sp_ctx {
     unsigned long long hit_total = 0;
     bool registered = false;
     Geometry g{};
-    cudaStream_t compute = nullptr, plan_s = nullptr;
-    // Transfer(b) runs on xfer_s[b % nx]: transfers b..b+F touch disjoint
-    // slots and rows (a row evicted at Plan(b) is not in B(b+1..b+F)), so up
-    // to F+1 of them may overlap; Transfer(b) stays ordered after b-nx.
-    static constexpr int MAX_XFER_STREAMS = 4;
-    cudaStream_t xfer_s[MAX_XFER_STREAMS] = {};
-    int nx = 1;
-    int pull_ctas = 16, wb_ctas = 2;
-    cudaStream_t wb_s = nullptr;  // rate-limited write-backs (HBM staging -> host)
-    float *d_stage = nullptr;     // [RING][T][n][D]
+    cudaStream_t compute = nullptr, plan_s = nullptr, xfer_s = nullptr;
+    cudaStream_t d2h_s = nullptr;  // victims' D2H on its own stream (other copy engine)
     // device memory
     std::vector<void *> allocs;
     unsigned long long *d_row_off = nullptr;
@@ -86,24 +176,50 @@ struct sp_ctx {
     float **d_host = nullptr;
     void *d_idx[RING] = {};
     BatchBufs ring[RING];
-    // pinned host
+    // transfer staging of the victims: XSR slots of sum(m) rows (<= T*n)
+    int XSR = 4;
+    float *d_wb = nullptr;                     // device [XSR][T*n][D]
+    float *h_wb = nullptr;                     // pinned [XSR][T*n][D]
+    unsigned long long *h_scat = nullptr;      // pinned mapped: batches scattered
+    unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
+    int pull_ctas = 8;
+    long long xfer_enq = 0;                    // transfers enqueued (caller's thread)
+    // pinned host mirror of the fill lists, per ring slot
+    unsigned long long *hl_ready = nullptr;    // [RING][T]
+    uint32_t *hl_m = nullptr;                  // [RING][T]
+    uint2 *hl_ent = nullptr;                   // [RING][T][n]
+    HostList hl_dev[RING];                     // mapped device pointers of the same
+    // pinned index staging
     void *h_stage = nullptr;
-    unsigned long long *h_err = nullptr;
+    unsigned long long *h_err = nullptr;      // exact device error key (sync copies)
+    unsigned long long *h_errflag = nullptr;  // pinned mapped: kernels set it on error
+    unsigned long long *d_errflag = nullptr;  // device alias of h_errflag
     size_t idx_bytes = 0;
     // events
-    cudaEvent_t ev_plan[RING] = {}, ev_xfer[RING] = {}, ev_train[RING] = {}, ev_h2d[RING] = {};
-    cudaEvent_t ev_wb[RING] = {};
+    cudaEvent_t ev_plan[RING] = {}, ev_xfer[RING] = {}, ev_d2h[RING] = {}, ev_train[RING] = {},
+                ev_h2d[RING] = {};
     cudaEvent_t ev_user = nullptr;
     bool h2d_used[RING] = {};
-    // schedule state
-    long long pushed = 0, planned = 0, transferred = 0, forwarded = 0, trained = 0;
+    // schedule state (caller's thread)
+    long long pushed = 0, planned = 0, forwarded = 0, trained = 0;
     bool eod = false, fwd_pending = false;
+    // published to the transfer engine
+    std::atomic<long long> trained_pub{0};
+    std::atomic<long long> x_enqueued{0}, x_scattered{0};
+    std::atomic<int> x_error{0};
+    std::atomic<long long> x_gather_ns{0}, x_scatter_ns{0}, x_rows_g{0}, x_rows_s{0};
+    std::string x_errmsg;
+    std::thread scatter_worker;
+    std::atomic<bool> stop{false};
+    RowPool spool;  // scatter helpers
+    int host_threads = 6;
     // errors
     sp_status poisoned = SP_OK;
     std::string err = "no error";
     long long err_batch = -1;
     int err_table = -1;
-    // stats
+    // stats (guarded by prof_mu where shared with the worker)
+    std::mutex prof_mu;
     long long h2d_index_bytes = 0;
     long long launches[SP_K_COUNT] = {};
     double kms[SP_K_COUNT] = {};
@@ -112,7 +228,25 @@ struct sp_ctx {
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t prof_ref = nullptr;
     std::vector<TimelineRec> timeline;
-    long long cur_batch = -1;
+    std::atomic<bool> profiling{false};
+    // CUDA-graph replay of the steady-state step (sp_run_steps): per ring
+    // residue r, one plan-stream graph and one compute-stream graph
+    long long *d_ctl = nullptr;                 // [RING] device batch-index chain
+    cudaGraphExec_t gplan[RING] = {}, gcomp[RING] = {};
+    cudaStream_t cap_s = nullptr;
+    struct GraphKey {
+        const void *trace = nullptr;
+        long long stride = 0;
+        float *pooled = nullptr, *grad = nullptr;
+        float gamma = 0, delta = 0, lr = 0;
+        bool operator==(const GraphKey &o) const {
+            return trace == o.trace && stride == o.stride && pooled == o.pooled && grad == o.grad &&
+                   gamma == o.gamma && delta == o.delta && lr == o.lr;
+        }
+    } gkey;
+    long long g_next_j = -1;                    // j the device chain expects next
+    long long graph_steps = 0;
+    long long wait_xfer_ns = 0, wait_list_ns = 0;  // caller-thread waits on the engine
 };
 
 namespace {
@@ -158,6 +292,7 @@ cudaEvent_t pool_event(sp_ctx *c) {
     return e;
 }
 
+// caller holds prof_mu
 void harvest_profile(sp_ctx *c, bool blocking) {
     std::vector<ProfEv> keep;
     for (auto &p : c->prof_pending) {
@@ -183,18 +318,20 @@ void harvest_profile(sp_ctx *c, bool blocking) {
     c->prof_pending.swap(keep);
 }
 
-// wraps one kernel launch: counts it, optionally brackets it with events
-template <typename F>
-cudaError_t launch(sp_ctx *c, int kind, cudaStream_t s, F &&fn) {
-    const bool prof = (c->flags & SP_FLAG_PROFILE) != 0;
-    ProfEv pe{kind, c->cur_batch, nullptr, nullptr};
+// wraps one kernel launch / DMA: counts it, optionally brackets it with events
+template <typename Fn>
+cudaError_t launch(sp_ctx *c, int kind, long long batch, cudaStream_t s, Fn &&fn) {
+    const bool prof = c->profiling.load(std::memory_order_relaxed);
+    ProfEv pe{kind, batch, nullptr, nullptr};
     if (prof) {
+        std::lock_guard<std::mutex> lk(c->prof_mu);
         if (c->prof_pending.size() > 4096) harvest_profile(c, false);
         pe.a = pool_event(c);
         pe.b = pool_event(c);
         cudaEventRecord(pe.a, s);
     }
     cudaError_t e = fn();
+    std::lock_guard<std::mutex> lk(c->prof_mu);
     c->launches[kind] += 1;
     if (prof) {
         cudaEventRecord(pe.b, s);
@@ -203,8 +340,7 @@ cudaError_t launch(sp_ctx *c, int kind, cudaStream_t s, F &&fn) {
     return e;
 }
 
-BatchBufs carve(sp_ctx *c, int r, cudaError_t *st) {
-    (void)r;
+BatchBufs carve(sp_ctx *c, cudaError_t *st) {
     BatchBufs b{};
     const size_t Tn = (size_t)c->T * c->n;
     cudaError_t e = cudaSuccess;
@@ -217,9 +353,9 @@ BatchBufs carve(sp_ctx *c, int r, cudaError_t *st) {
     A(&b.seg_off, (size_t)c->T * c->g.n1);
     A(&b.U, (size_t)c->T);
     A(&b.chunk_rec, (size_t)c->T * c->g.nc);  // ChunkRec (80 B)
+    A(&b.nchunks, (size_t)c->T);
     A(&b.hot_rec, (size_t)c->T * c->g.nh);
     A(&b.nhot, (size_t)c->T);
-    A(&b.nchunks, (size_t)c->T);
     A(&b.slot_u, Tn);
     A(&b.slot_of_occ, Tn);
     A(&b.hit, Tn);
@@ -234,6 +370,11 @@ BatchBufs carve(sp_ctx *c, int r, cudaError_t *st) {
 
 sp_status check_async_error(sp_ctx *c) {
     if (c->poisoned != SP_OK) return c->poisoned;
+    if (*(volatile unsigned long long *)c->h_errflag && *(volatile unsigned long long *)c->h_err == NO_ERR) {
+        // a kernel latched an error: read the exact (earliest) key
+        cudaStreamSynchronize(c->plan_s);
+        cudaMemcpy(c->h_err, c->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    }
     unsigned long long e = *(volatile unsigned long long *)c->h_err;
     if (e != NO_ERR && e != 0ull) {
         unsigned kind = (unsigned)(e & 0xFF);
@@ -250,6 +391,11 @@ sp_status check_async_error(sp_ctx *c) {
         c->err = buf;
         return c->poisoned;
     }
+    if (c->x_error.load(std::memory_order_acquire)) {
+        c->poisoned = SP_ERR_CUDA;
+        c->err = "transfer engine: " + c->x_errmsg;
+        return c->poisoned;
+    }
     return SP_OK;
 }
 
@@ -261,6 +407,18 @@ sp_status sync_error(sp_ctx *c) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->plan_s);
     if (e != cudaSuccess) return cuda_fail(c, e, "sync_error");
     return check_async_error(c);
+}
+
+// spin until pred() (the transfer engine made progress) or an error shows up
+template <typename Pred>
+sp_status wait_engine(sp_ctx *c, Pred pred) {
+    int idle = 0;
+    while (!pred()) {
+        if (sp_status s = check_async_error(c)) return s;
+        if (++idle > 1024) std::this_thread::yield();
+        else _mm_pause();
+    }
+    return SP_OK;
 }
 
 PushArgs push_args(sp_ctx *c) {
@@ -282,6 +440,7 @@ PushArgs push_args(sp_ctx *c) {
     a.log_head = c->d_log_head;
     a.log_tail = c->d_log_tail;
     a.err = c->d_err;
+    a.err_host = c->d_errflag;
     a.cum = c->d_cum;
     a.miss_u = c->d_miss_u;
     a.victims = c->d_victims;
@@ -290,49 +449,27 @@ PushArgs push_args(sp_ctx *c) {
     return a;
 }
 
+// The host-list ring slot of Plan(b) is reused by Plan(b + RING): the transfer
+// engine must be done with batch b (gathered and scattered) first.
+sp_status wait_list_slot(sp_ctx *c, long long b) {
+    const long long prev = b - RING;
+    if (prev < 0) return SP_OK;
+    return wait_engine(c, [&] { return c->x_scattered.load(std::memory_order_acquire) > prev; });
+}
+
 sp_status enqueue_plan_only(sp_ctx *c, long long b) {
+    if (sp_status s = wait_list_slot(c, b)) return s;
     PushArgs a = push_args(c);
-    c->cur_batch = b;
     a.has_new = 0;
     a.do_plan = 1;
     a.b = b;
     a.pb = c->ring[b % RING];
+    a.hl = c->hl_dev[b % RING];
     a.has_future = (b + c->F < c->pushed) ? 1 : 0;  // future window truncates at the end
     a.fb = c->ring[(b + c->F) % RING];
-    CK(launch(c, SP_K_PLAN, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
+    CK(launch(c, SP_K_PLAN, b, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
     CK(cudaEventRecord(c->ev_plan[b % RING], c->plan_s));
     c->planned = b + 1;
-    return SP_OK;
-}
-
-sp_status pump(sp_ctx *c) {
-    while (c->transferred < c->planned) {
-        const long long b = c->transferred, dep = b - c->P - 1;
-        if (dep >= 0 && c->trained <= dep) break;  // Train(dep) not enqueued yet
-        cudaStream_t xs = c->xfer_s[b % c->nx];
-        CK(cudaStreamWaitEvent(xs, c->ev_plan[b % RING], 0));
-        if (dep >= 0) CK(cudaStreamWaitEvent(xs, c->ev_train[dep % RING], 0));
-        // RAW-4: a row written back by WriteBack(b-F-1) may be
-        // pulled again by Pull(b); the write-back stream runs in batch order
-        const long long rb = b - c->F - 1;
-        if (rb >= 0) CK(cudaStreamWaitEvent(xs, c->ev_wb[rb % RING], 0));
-        XferArgs a{};
-        c->cur_batch = b;
-        a.g = c->g;
-        a.bb = c->ring[b % RING];
-        a.storage = c->d_storage;
-        a.stage = c->d_stage + (size_t)(b % RING) * c->T * c->n * c->D;
-        a.host = c->d_host;
-        a.err = c->d_err;
-        // SP_DEBUG_NO_XFER=1: timing experiments only (results are wrong)
-        static const bool no_xfer = getenv("SP_DEBUG_NO_XFER") != nullptr;
-        if (!no_xfer) CK(launch(c, SP_K_TRANSFER, xs, [&] { return launch_pull(a, c->pull_ctas, xs); }));
-        CK(cudaEventRecord(c->ev_xfer[b % RING], xs));
-        CK(cudaStreamWaitEvent(c->wb_s, c->ev_xfer[b % RING], 0));
-        if (!no_xfer) CK(launch(c, SP_K_WRITEBACK, c->wb_s, [&] { return launch_writeback(a, c->wb_ctas, c->wb_s); }));
-        CK(cudaEventRecord(c->ev_wb[b % RING], c->wb_s));
-        c->transferred = b + 1;
-    }
     return SP_OK;
 }
 
@@ -346,34 +483,189 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     return a;
 }
 
+// --------------------------------------------------------------- transfer engine
+void engine_fail(sp_ctx *c, cudaError_t e, const char *where) {
+    c->x_errmsg = std::string(where) + ": " + cudaGetErrorString(e);
+    c->x_error.store(1, std::memory_order_release);
+}
+
+// [Insert] CPU scatter of batch s's victims into the host tables once its D2H
+// has landed, in batch order, on its own thread: it overlaps the gather of
+// later batches (rows evicted at s are not in B(s+1..s+F)).
+void scatter_main(sp_ctx *c) {
+    cudaSetDevice(c->device);
+    const size_t rowb = (size_t)c->D * sizeof(float);
+    const size_t slab = (size_t)c->T * c->n * c->D;
+    std::vector<const float *> src;
+    std::vector<float *> dst;
+    std::vector<uint32_t> pref(c->T + 1);
+    long long s = 0, d = 0;  // next batch to scatter / to issue the D2H for
+    int idle = 0;
+    auto ready = [&](long long b) {
+        const int r = (int)(b % RING);
+        for (int t = 0; t < c->T; t++)
+            if (((volatile unsigned long long *)c->hl_ready)[(size_t)r * c->T + t] != (unsigned long long)(b + 1))
+                return false;
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return true;
+    };
+    auto rows_of = [&](long long b) {
+        const int r = (int)(b % RING);
+        pref[0] = 0;
+        for (int t = 0; t < c->T; t++) pref[t + 1] = pref[t] + c->hl_m[(size_t)r * c->T + t];
+        return (size_t)pref[c->T];
+    };
+    while (!c->stop.load(std::memory_order_relaxed)) {
+        if (*(volatile unsigned long long *)c->h_errflag) break;
+        bool progressed = false;
+        // [Exchange] D2H of the staged victims of batch d once Transfer(d) is
+        // enqueued (ev_xfer exists) and its lists are known; the staging slot
+        // d % XSR is free because Transfer(d) waited for scatter(d-F-1)
+        if (d < s + c->XSR && d < c->x_enqueued.load(std::memory_order_acquire) && ready(d)) {
+            const int r = (int)(d % RING);
+            const size_t bytes = rows_of(d) * rowb;
+            cudaError_t e = cudaStreamWaitEvent(c->d2h_s, c->ev_xfer[r], 0);
+            if (e == cudaSuccess && bytes)
+                e = launch(c, K_D2H, d, c->d2h_s, [&] {
+                    return cudaMemcpyAsync(c->h_wb + (size_t)(d % c->XSR) * slab,
+                                           c->d_wb + (size_t)(d % c->XSR) * slab, bytes,
+                                           cudaMemcpyDeviceToHost, c->d2h_s);
+                });
+            if (e == cudaSuccess) e = cudaEventRecord(c->ev_d2h[r], c->d2h_s);
+            if (e != cudaSuccess) {
+                engine_fail(c, e, "D2H enqueue");
+                break;
+            }
+            d++;
+            progressed = true;
+        }
+        // [Insert] CPU scatter of batch s once its D2H has landed, in order
+        if (s < d) {
+            cudaError_t q = cudaEventQuery(c->ev_d2h[s % RING]);
+            if (q == cudaSuccess) {
+                const int r = (int)(s % RING);
+                rows_of(s);
+                src.clear();
+                dst.clear();
+                const float *wb = c->h_wb + (size_t)(s % c->XSR) * slab;
+                for (int t = 0; t < c->T; t++) {
+                    const uint2 *ent = c->hl_ent + ((size_t)r * c->T + t) * c->n;
+                    for (uint32_t k = 0; k < pref[t + 1] - pref[t]; k++)
+                        if (ent[k].y != EMPTY) {
+                            src.push_back(wb + (size_t)(pref[t] + k) * c->D);
+                            dst.push_back(c->host[t] + (size_t)ent[k].y * c->D);
+                        }
+                }
+                const auto t0 = std::chrono::steady_clock::now();
+                c->spool.copy(src.data(), dst.data(), (long)src.size(), rowb);
+                c->x_scatter_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                       std::chrono::steady_clock::now() - t0).count();
+                c->x_rows_s += (long long)src.size();
+                s++;
+                c->x_scattered.store(s, std::memory_order_release);
+                std::atomic_thread_fence(std::memory_order_seq_cst);
+                *(volatile unsigned long long *)c->h_scat = (unsigned long long)s;  // GPU wait-value
+                progressed = true;
+            } else if (q != cudaErrorNotReady) {
+                engine_fail(c, q, "ev_d2h");
+                break;
+            }
+        }
+        if (progressed) {
+            idle = 0;
+        } else if (++idle > 2048) {
+            std::this_thread::yield();
+        } else {
+            _mm_pause();
+        }
+    }
+}
+
+void stop_engine(sp_ctx *c) {
+    c->stop = true;
+    if (c->scatter_worker.joinable()) c->scatter_worker.join();
+    c->spool.shutdown();
+}
+
+// stream wait on a 64-bit pinned counter (cuStreamWaitValue64 through the
+// runtime's driver entry point: no link-time dependency on libcuda)
+typedef CUresult (*wait_value64_fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+wait_value64_fn wait_value64() {
+    static wait_value64_fn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<wait_value64_fn>(p);
+    }
+    return fn;
+}
+
+// Enqueue every Transfer(b) whose preconditions exist: Plan(b) enqueued and
+// Train(b-P-1) enqueued (its event recorded).  Caller's thread only.
+sp_status pump(sp_ctx *c) {
+    while (c->xfer_enq < c->planned) {
+        const long long b = c->xfer_enq, dep = b - c->P - 1;
+        if (dep >= 0 && c->trained <= dep) break;
+        const int r = (int)(b % RING);
+        cudaStream_t xs = c->xfer_s;
+        CK(cudaStreamWaitEvent(xs, c->ev_plan[r], 0));
+        if (dep >= 0) CK(cudaStreamWaitEvent(xs, c->ev_train[dep % RING], 0));
+        // RAW-4 + staging reuse: the CPU write-back of batch b-F-1 has landed
+        const long long need = b - c->F;  // scattered >= b-F
+        if (need > 0) {
+            wait_value64_fn wv = wait_value64();
+            if (!wv) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 unavailable");
+            CUresult cr = wv((CUstream)xs, (CUdeviceptr)c->d_scat, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ);
+            if (cr != CUDA_SUCCESS) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 failed");
+        }
+        XferArgs a{};
+        a.g = c->g;
+        a.bb = c->ring[r];
+        a.storage = c->d_storage;
+        a.host = c->d_host;
+        a.wb_stage = c->d_wb + (size_t)(b % c->XSR) * c->T * c->n * c->D;
+        a.err = c->d_err;
+        CK(launch(c, SP_K_TRANSFER, b, xs, [&] { return launch_pullfill(a, c->pull_ctas, xs); }));
+        CK(cudaEventRecord(c->ev_xfer[r], xs));
+        c->xfer_enq = b + 1;
+        c->x_enqueued.store(b + 1, std::memory_order_release);
+    }
+    return SP_OK;
+}
+
+void drop_graphs(sp_ctx *c);
+
 void destroy_all(sp_ctx *c) {
     if (!c) return;
+    stop_engine(c);
+    drop_graphs(c);
     cudaSetDevice(c->device);
     if (c->plan_s) cudaStreamSynchronize(c->plan_s);
-    for (auto xs : c->xfer_s)
-        if (xs) cudaStreamSynchronize(xs);
-    if (c->wb_s) cudaStreamSynchronize(c->wb_s);
+    if (c->xfer_s) cudaStreamSynchronize(c->xfer_s);
+    if (c->d2h_s) cudaStreamSynchronize(c->d2h_s);
     cudaStreamSynchronize(c->compute);
-    harvest_profile(c, true);
-    for (auto e : c->ev_pool) cudaEventDestroy(e);
-    for (int r = 0; r < RING; r++) {
-        if (c->ev_plan[r]) cudaEventDestroy(c->ev_plan[r]);
-        if (c->ev_xfer[r]) cudaEventDestroy(c->ev_xfer[r]);
-        if (c->ev_train[r]) cudaEventDestroy(c->ev_train[r]);
-        if (c->ev_h2d[r]) cudaEventDestroy(c->ev_h2d[r]);
-        if (c->ev_wb[r]) cudaEventDestroy(c->ev_wb[r]);
+    {
+        std::lock_guard<std::mutex> lk(c->prof_mu);
+        harvest_profile(c, true);
+        for (auto e : c->ev_pool) cudaEventDestroy(e);
     }
+    for (int r = 0; r < RING; r++)
+        for (cudaEvent_t e : {c->ev_plan[r], c->ev_xfer[r], c->ev_d2h[r], c->ev_train[r], c->ev_h2d[r]})
+            if (e) cudaEventDestroy(e);
     if (c->ev_user) cudaEventDestroy(c->ev_user);
     if (c->prof_ref) cudaEventDestroy(c->prof_ref);
     for (void *p : c->allocs) cudaFree(p);
-    if (c->h_stage) cudaFreeHost(c->h_stage);
-    if (c->h_err) cudaFreeHost(c->h_err);
+    for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb,
+                    (void *)c->hl_ready, (void *)c->hl_m, (void *)c->hl_ent})
+        if (p) cudaFreeHost(p);
     if (c->registered)
         for (int t = 0; t < c->T; t++) cudaHostUnregister(c->host[t]);
     if (c->plan_s) cudaStreamDestroy(c->plan_s);
-    for (auto xs : c->xfer_s)
-        if (xs) cudaStreamDestroy(xs);
-    if (c->wb_s) cudaStreamDestroy(c->wb_s);
+    if (c->xfer_s) cudaStreamDestroy(c->xfer_s);
+    if (c->d2h_s) cudaStreamDestroy(c->d2h_s);
+    if (c->cap_s) cudaStreamDestroy(c->cap_s);
     (void)cudaGetLastError();
     delete c;
 }
@@ -383,6 +675,31 @@ void destroy_all(sp_ctx *c) {
 extern "C" {
 
 int32_t sp_abi_version(void) { return SP_ABI_VERSION; }
+
+sp_status sp_host_alloc(size_t bytes, void **out) {
+    if (!out || !bytes) return SP_ERR_INVALID_ARG;
+    *out = nullptr;
+    void *p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return SP_ERR_OOM;
+    madvise(p, bytes, MADV_HUGEPAGE);  // best effort (THP "madvise" mode)
+    // pinning faults the pages in, so they come up as 2 MB pages when possible
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        munmap(p, bytes);
+        return e == cudaErrorMemoryAllocation ? SP_ERR_OOM : SP_ERR_CUDA;
+    }
+    *out = p;
+    return SP_OK;
+}
+
+sp_status sp_host_free(void *ptr, size_t bytes) {
+    if (!ptr || !bytes) return SP_ERR_INVALID_ARG;
+    cudaHostUnregister(ptr);
+    (void)cudaGetLastError();
+    munmap(ptr, bytes);
+    return SP_OK;
+}
 
 sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     if (!out) return SP_ERR_INVALID_ARG;
@@ -412,6 +729,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->device = d->device;
     c->flags = d->flags;
     c->compute = (cudaStream_t)d->stream;
+    c->profiling = (d->flags & SP_FLAG_PROFILE) != 0;
     c->g.T = c->T;
     c->g.N = c->N;
     c->g.L = c->L;
@@ -443,6 +761,9 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     }
     for (int t = 0; t < c->T; t++) c->slot_base[t + 1] = c->slot_base[t] + (uint32_t)c->slots[t];
     c->hit_total = c->row_off[c->T];
+    c->XSR = std::max(4, c->F + 2);  // >= F+1: Transfer(b) waits for scatter(b-F-1) >= b-XSR
+    c->host_threads = d->host_threads > 0 ? d->host_threads : 6;
+    c->pull_ctas = 8;
 
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) {
@@ -454,13 +775,13 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         destroy_all(c);
         return s;
     };
-#define CKC(call)                                                          \
-    do {                                                                   \
-        cudaError_t e_ = (call);                                           \
-        if (e_ != cudaSuccess) {                                           \
-            (void)cudaGetLastError();                                      \
+#define CKC(call)                                                                  \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            (void)cudaGetLastError();                                              \
             return bail(e_ == cudaErrorMemoryAllocation ? SP_ERR_OOM : SP_ERR_CUDA); \
-        }                                                                  \
+        }                                                                          \
     } while (0)
     // host tables: registration / mapped device pointers
     if (c->flags & SP_FLAG_REGISTER_HOST) {
@@ -485,20 +806,18 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         }
         hdev[t] = static_cast<float *>(p);
     }
-    CKC(cudaStreamCreateWithPriority(&c->plan_s, cudaStreamNonBlocking, -1));
-    c->nx = std::min(c->F + 1, (int)sp_ctx::MAX_XFER_STREAMS);
-    for (int k = 0; k < c->nx; k++) CKC(cudaStreamCreateWithFlags(&c->xfer_s[k], cudaStreamNonBlocking));
-    CKC(cudaStreamCreateWithFlags(&c->wb_s, cudaStreamNonBlocking));
-    for (int r = 0; r < RING; r++) {
-        CKC(cudaEventCreateWithFlags(&c->ev_plan[r], cudaEventDisableTiming));
-        CKC(cudaEventCreateWithFlags(&c->ev_xfer[r], cudaEventDisableTiming));
-        CKC(cudaEventCreateWithFlags(&c->ev_train[r], cudaEventDisableTiming));
-        CKC(cudaEventCreateWithFlags(&c->ev_h2d[r], cudaEventDisableTiming));
-        CKC(cudaEventCreateWithFlags(&c->ev_wb[r], cudaEventDisableTiming));
+    {   // Plan is the serial critical chain: its CTAs get scheduled first
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        CKC(cudaStreamCreateWithPriority(&c->plan_s, cudaStreamNonBlocking, hi));
     }
+    CKC(cudaStreamCreateWithFlags(&c->xfer_s, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->d2h_s, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->cap_s, cudaStreamNonBlocking));
+    for (int r = 0; r < RING; r++)
+        for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_d2h[r], &c->ev_train[r], &c->ev_h2d[r]})
+            CKC(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
-    c->pull_ctas = d->pull_ctas > 0 ? d->pull_ctas : 16;
-    c->wb_ctas = d->writeback_ctas > 0 ? d->writeback_ctas : 2;
     CKC(configure_push_kernel());
 
     // device allocations
@@ -534,11 +853,12 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     if (c->n > SMEM_SORT_MAX) CKC(dalloc(c, &c->d_sort_tmp, 4 * Tn));
     CKC(dalloc(c, &c->d_partial, (size_t)c->T * c->g.nc * c->D));
     CKC(dalloc(c, &c->d_host, c->T));
-    CKC(dalloc(c, &c->d_stage, (size_t)RING * Tn * c->D));
+    CKC(dalloc(c, &c->d_ctl, RING));
+    CKC(dalloc(c, &c->d_wb, (size_t)c->XSR * Tn * c->D));
     c->idx_bytes = Tn * ((c->flags & SP_FLAG_INDEX_I32) ? 4 : 8);
     for (int r = 0; r < RING; r++) {
         cudaError_t st;
-        c->ring[r] = carve(c, r, &st);
+        c->ring[r] = carve(c, &st);
         CKC(st);
         void *p = nullptr;
         CKC(cudaMalloc(&p, c->idx_bytes));
@@ -548,6 +868,30 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaHostAlloc(&c->h_stage, c->idx_bytes * RING, cudaHostAllocDefault));
     CKC(cudaHostAlloc((void **)&c->h_err, sizeof(unsigned long long), cudaHostAllocDefault));
     *c->h_err = NO_ERR;
+    CKC(cudaHostAlloc((void **)&c->h_errflag, sizeof(unsigned long long), cudaHostAllocMapped));
+    *c->h_errflag = 0;
+    CKC(cudaHostGetDevicePointer((void **)&c->d_errflag, c->h_errflag, 0));
+    CKC(cudaHostAlloc((void **)&c->h_scat, sizeof(unsigned long long), cudaHostAllocMapped));
+    *c->h_scat = 0;
+    CKC(cudaHostGetDevicePointer((void **)&c->d_scat, c->h_scat, 0));
+    CKC(cudaHostAlloc((void **)&c->h_wb, (size_t)c->XSR * Tn * c->D * sizeof(float), cudaHostAllocDefault));
+    CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
+    CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
+    CKC(cudaHostAlloc((void **)&c->hl_ent, (size_t)RING * Tn * sizeof(uint2), cudaHostAllocMapped));
+    std::memset(c->hl_ready, 0, (size_t)RING * c->T * sizeof(unsigned long long));
+    {
+        unsigned long long *dr;
+        uint32_t *dm;
+        uint2 *de;
+        CKC(cudaHostGetDevicePointer((void **)&dr, c->hl_ready, 0));
+        CKC(cudaHostGetDevicePointer((void **)&dm, c->hl_m, 0));
+        CKC(cudaHostGetDevicePointer((void **)&de, c->hl_ent, 0));
+        for (int r = 0; r < RING; r++) {
+            c->hl_dev[r].ready = dr + (size_t)r * c->T;
+            c->hl_dev[r].m = dm + (size_t)r * c->T;
+            c->hl_dev[r].ent = de + (size_t)r * Tn;
+        }
+    }
 
     // initial state
     std::vector<long long> rows64(c->rows.begin(), c->rows.end());
@@ -578,6 +922,9 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaMemset(c->d_storage, 0, (size_t)c->S_total * c->D * sizeof(float)));
     CKC(cudaDeviceSynchronize());
 #undef CKC
+    // transfer engine: helpers + worker
+    c->spool.start(c->host_threads);
+    c->scatter_worker = std::thread(scatter_main, c);
     *out = c;
     return SP_OK;
 }
@@ -591,10 +938,12 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     if (j >= RING && c->trained < j - RING + 1)
         return fail(c, SP_ERR_STATE, "sp_plan: more than 16 batches ahead of sp_train");
     CK(cudaSetDevice(c->device));
-    if (j >= RING) {
-        CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));
-        CK(cudaStreamWaitEvent(c->plan_s, c->ev_wb[r], 0));  // WriteBack(j-RING) reads ring slot r
-    }
+    // Plan(b) runs beside dedup(j) once B(b+F) = B(j-1) has been deduped
+    const long long b = j - c->F - 1;
+    const bool do_plan = b >= 0 && b == c->planned;
+    if (do_plan)
+        if (sp_status s = wait_list_slot(c, b)) return s;
+    if (j >= RING) CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));  // ring slot r reused
     const void *dev_idx;
     if (on_device) {
         // indices produced on the caller's stream
@@ -612,27 +961,24 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
         dev_idx = c->d_idx[r];
     }
     PushArgs a = push_args(c);
-    c->cur_batch = j;
     a.has_new = 1;
     a.j = j;
     a.idx = dev_idx;
     a.nb = c->ring[r];
-    // Plan(b) runs beside dedup(j) once B(b+F) = B(j-1) has been deduped
-    const long long b = j - c->F - 1;
-    a.do_plan = (b >= 0 && b == c->planned) ? 1 : 0;
-    if (a.do_plan) {
+    a.do_plan = do_plan ? 1 : 0;
+    if (do_plan) {
         a.b = b;
         a.pb = c->ring[b % RING];
+        a.hl = c->hl_dev[b % RING];
         a.has_future = 1;
         a.fb = c->ring[(b + c->F) % RING];
     }
-    CK(launch(c, SP_K_PLAN, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
-    if (a.do_plan) {
+    CK(launch(c, SP_K_PLAN, do_plan ? b : j, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
+    if (do_plan) {
         CK(cudaEventRecord(c->ev_plan[b % RING], c->plan_s));
         c->planned = b + 1;
     }
     c->pushed = j + 1;
-    CK(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->plan_s));
     return pump(c);
 }
 
@@ -656,13 +1002,14 @@ sp_status sp_copy_batch_stats(sp_ctx *c, int64_t b, uint32_t *host_out) {
 sp_status sp_set_profiling(sp_ctx *c, int32_t on) {
     if (!c) return SP_ERR_INVALID_ARG;
     CK(cudaSetDevice(c->device));
+    std::lock_guard<std::mutex> lk(c->prof_mu);
     if (on) {
-        c->flags |= SP_FLAG_PROFILE;
         if (!c->prof_ref) CK(cudaEventCreate(&c->prof_ref));
         CK(cudaEventRecord(c->prof_ref, c->compute));
         c->timeline.clear();
+        c->profiling = true;
     } else {
-        c->flags &= ~SP_FLAG_PROFILE;
+        c->profiling = false;
     }
     return SP_OK;
 }
@@ -672,6 +1019,7 @@ sp_status sp_get_timeline(sp_ctx *c, int32_t *kind, int64_t *batch, double *star
     if (!c || !n) return SP_ERR_INVALID_ARG;
     CK(cudaSetDevice(c->device));
     CK(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(c->prof_mu);
     harvest_profile(c, true);
     *n = (int64_t)c->timeline.size();
     for (int64_t i = 0; i < std::min<int64_t>(cap, *n); i++) {
@@ -690,7 +1038,6 @@ sp_status sp_end_of_data(sp_ctx *c) {
     c->eod = true;
     while (c->planned < c->pushed)
         if (sp_status s = enqueue_plan_only(c, c->planned)) return s;
-    CK(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->plan_s));
     return pump(c);
 }
 
@@ -703,15 +1050,11 @@ sp_status sp_forward(sp_ctx *c, float *pooled) {
         return fail(c, SP_ERR_STATE, "sp_forward: batch not planned yet (push B(b+F+1) or call sp_end_of_data)");
     CK(cudaSetDevice(c->device));
     if (sp_status s = pump(c)) return s;
-    if (c->transferred <= b) return fail(c, SP_ERR_STATE, "sp_forward: transfer not schedulable");
-    // every slot B(b) reads was filled by some Transfer(<= b): the last nx
-    // transfers may still be running on their own streams
-    for (int k = 0; k < c->nx && b - k >= 0; k++)
-        CK(cudaStreamWaitEvent(c->compute, c->ev_xfer[(b - k) % RING], 0));
+    if (c->xfer_enq <= b) return fail(c, SP_ERR_STATE, "sp_forward: transfer not schedulable");
+    CK(cudaStreamWaitEvent(c->compute, c->ev_xfer[b % RING], 0));
     TrainArgs a = train_args(c, b);
-    c->cur_batch = b;
     a.pooled = pooled;
-    CK(launch(c, SP_K_FORWARD, c->compute, [&] { return launch_forward(a, c->compute); }));
+    CK(launch(c, SP_K_FORWARD, b, c->compute, [&] { return launch_forward(a, c->compute); }));
     c->forwarded = b + 1;
     c->fwd_pending = true;
     return SP_OK;
@@ -724,15 +1067,15 @@ sp_status sp_train(sp_ctx *c, const float *grad, float lr) {
     CK(cudaSetDevice(c->device));
     const long long b = c->trained;
     TrainArgs a = train_args(c, b);
-    c->cur_batch = b;
     a.grad = grad;
     a.lr = lr;
-    CK(launch(c, SP_K_BACKWARD, c->compute, [&] {
+    CK(launch(c, SP_K_BACKWARD, b, c->compute, [&] {
         cudaError_t e = launch_backward(a, c->compute);
         return e != cudaSuccess ? e : launch_backward_hot(a, c->compute);
     }));
     CK(cudaEventRecord(c->ev_train[b % RING], c->compute));
     c->trained = b + 1;
+    c->trained_pub.store(b + 1, std::memory_order_release);
     c->fwd_pending = false;
     return pump(c);
 }
@@ -743,7 +1086,7 @@ sp_status sp_surrogate_grad(sp_ctx *c, const float *pooled, float *grad, int64_t
     if (c->poisoned != SP_OK) return c->poisoned;
     CK(cudaSetDevice(c->device));
     if (count == 0) count = (long long)c->T * c->N * c->D;
-    CK(launch(c, SP_K_SURROGATE, c->compute,
+    CK(launch(c, SP_K_SURROGATE, c->trained, c->compute,
               [&] { return launch_surrogate(pooled, grad, count, gamma, delta, c->compute); }));
     return SP_OK;
 }
@@ -754,9 +1097,12 @@ sp_status sp_flush(sp_ctx *c) {
     if (c->trained != c->pushed || c->fwd_pending)
         return fail(c, SP_ERR_STATE, "sp_flush: every pushed batch must be trained first");
     CK(cudaSetDevice(c->device));
+    // the transfer engine writes back every victim of every batch
+    if (sp_status s = wait_engine(c, [&] { return c->x_scattered.load(std::memory_order_acquire) >= c->planned; }))
+        return s;
     CK(cudaStreamSynchronize(c->plan_s));
-    for (int k = 0; k < c->nx; k++) CK(cudaStreamSynchronize(c->xfer_s[k]));
-    CK(cudaStreamSynchronize(c->wb_s));
+    CK(cudaStreamSynchronize(c->xfer_s));
+    CK(cudaStreamSynchronize(c->d2h_s));
     CK(cudaStreamSynchronize(c->compute));
     if (sp_status s = sync_error(c)) return s;
     FlushArgs a{};
@@ -766,9 +1112,154 @@ sp_status sp_flush(sp_ctx *c) {
     a.resident = c->d_resident;
     a.storage = c->d_storage;
     a.host = c->d_host;
-    CK(launch(c, SP_K_FLUSH, c->compute, [&] { return launch_flush(a, c->compute); }));
+    CK(launch(c, SP_K_FLUSH, c->trained, c->compute, [&] { return launch_flush(a, c->compute); }));
     CK(cudaStreamSynchronize(c->compute));
     c->eod = false;  // a flush is a checkpoint: the caller may continue pushing
+    return SP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+void drop_graphs(sp_ctx *c) {
+    for (int r = 0; r < RING; r++) {
+        if (c->gplan[r]) cudaGraphExecDestroy(c->gplan[r]);
+        if (c->gcomp[r]) cudaGraphExecDestroy(c->gcomp[r]);
+        c->gplan[r] = c->gcomp[r] = nullptr;
+    }
+    c->g_next_j = -1;
+}
+
+// Capture the two graphs of residue r = k % RING for step k: the push of
+// B(j = k+F+P+1) with Plan(k+P), and forward / surrogate / train of batch k.
+sp_status capture_step(sp_ctx *c, int r) {
+    const long long ahead = c->F + c->P + 1;
+    const int rj = (int)((r + ahead) % RING), rb = (int)((r + c->P) % RING),
+              rf = (int)((r + c->P + c->F) % RING);
+    const sp_ctx::GraphKey &k = c->gkey;
+    cudaGraph_t gr = nullptr;
+    // plan stream: [wait Train(j - RING): ring slot reuse] -> k_push -> [record ev_plan]
+    PushArgs a = push_args(c);
+    a.has_new = 1;
+    a.do_plan = 1;
+    a.has_future = 1;
+    a.idx = k.trace;
+    a.nb = c->ring[rj];
+    a.pb = c->ring[rb];
+    a.hl = c->hl_dev[rb];
+    a.fb = c->ring[rf];
+    a.ctl = c->d_ctl;
+    a.ctl_r = r;
+    a.idx_stride = k.stride;
+    CK(cudaStreamBeginCapture(c->cap_s, cudaStreamCaptureModeThreadLocal));
+    cudaStreamWaitEvent(c->cap_s, c->ev_train[rj], cudaEventWaitExternal);
+    launch_push(a, c->cap_s);
+    cudaEventRecordWithFlags(c->ev_plan[rb], c->cap_s, cudaEventRecordExternal);
+    CK(cudaStreamEndCapture(c->cap_s, &gr));
+    CK(cudaGraphInstantiate(&c->gplan[r], gr, 0));
+    cudaGraphDestroy(gr);
+    // compute stream: [wait Transfer(k)] -> forward -> surrogate -> backward -> [record ev_train]
+    TrainArgs ta = train_args(c, r);
+    ta.pooled = k.pooled;
+    TrainArgs tb = train_args(c, r);
+    tb.grad = k.grad;
+    tb.lr = k.lr;
+    CK(cudaStreamBeginCapture(c->cap_s, cudaStreamCaptureModeThreadLocal));
+    cudaStreamWaitEvent(c->cap_s, c->ev_xfer[r], cudaEventWaitExternal);
+    launch_forward(ta, c->cap_s);
+    launch_surrogate(k.pooled, k.grad, (long long)c->T * c->N * c->D, k.gamma, k.delta, c->cap_s);
+    launch_backward(tb, c->cap_s);
+    launch_backward_hot(tb, c->cap_s);
+    cudaEventRecordWithFlags(c->ev_train[r], c->cap_s, cudaEventRecordExternal);
+    CK(cudaStreamEndCapture(c->cap_s, &gr));
+    CK(cudaGraphInstantiate(&c->gcomp[r], gr, 0));
+    cudaGraphDestroy(gr);
+    return SP_OK;
+}
+
+// one steady-state step k through the graphs (2 graph launches)
+sp_status graph_step(sp_ctx *c) {
+    const long long k = c->trained, j = c->pushed, b = c->planned;  // j = k+F+P+1, b = k+P = j-F-1
+    const int r = (int)(k % RING);
+    if (!c->gplan[r])
+        if (sp_status s = capture_step(c, r)) return s;
+    if (c->g_next_j != j)  // (re)enter graph mode: seed the device batch-index chain
+        CK(cudaMemcpyAsync(c->d_ctl + r, &j, sizeof j, cudaMemcpyHostToDevice, c->plan_s));
+    auto t0 = std::chrono::steady_clock::now();
+    if (sp_status s = wait_list_slot(c, b)) return s;
+    auto t1 = std::chrono::steady_clock::now();
+    c->wait_list_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    CK(cudaGraphLaunch(c->gplan[r], c->plan_s));
+    c->pushed = j + 1;
+    c->planned = b + 1;
+    c->g_next_j = j + 1;
+    if (sp_status s = pump(c)) return s;
+    if (c->xfer_enq <= k) return fail(c, SP_ERR_STATE, "graph step: transfer not schedulable");
+    CK(cudaGraphLaunch(c->gcomp[r], c->compute));
+    c->forwarded = k + 1;
+    c->trained = k + 1;
+    c->trained_pub.store(k + 1, std::memory_order_release);
+    c->graph_steps++;
+    if (sp_status s = pump(c)) return s;
+    {
+        std::lock_guard<std::mutex> lk(c->prof_mu);
+        for (int kind : {SP_K_PLAN, SP_K_FORWARD, SP_K_SURROGATE, SP_K_BACKWARD}) c->launches[kind] += 1;
+    }
+    return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sp_status sp_run_steps(sp_ctx *c, const void *indices, int64_t num_batches, int64_t stride,
+                       int64_t steps, float *pooled, float *grad, float gamma, float delta,
+                       float lr, uint32_t *stats_out) {
+    if (!c || !indices || !pooled || !grad || num_batches < 0 || stride <= 0 || steps < 0)
+        return SP_ERR_INVALID_ARG;
+    if (c->fwd_pending) return fail(c, SP_ERR_STATE, "sp_run_steps between sp_forward and sp_train");
+    CK(cudaSetDevice(c->device));
+    const long long ahead = c->F + c->P + 1;
+    const char *base = static_cast<const char *>(indices);
+    sp_ctx::GraphKey key;
+    key.trace = indices;
+    key.stride = stride;
+    key.pooled = pooled;
+    key.grad = grad;
+    key.gamma = gamma;
+    key.delta = delta;
+    key.lr = lr;
+    if (!(key == c->gkey)) {
+        drop_graphs(c);
+        c->gkey = key;
+    }
+    const bool graphs_ok = !stats_out && !getenv("SP_NO_GRAPHS");
+    for (int64_t k = 0; k < steps; k++) {
+        if (sp_status s = check_async_error(c)) return s;
+        // steady state: the look-ahead is full and one push per step keeps it so
+        const bool steady = graphs_ok && !c->eod && !c->profiling.load() && c->pushed == c->trained + ahead &&
+                            c->planned == c->trained + c->P && c->pushed + 1 <= num_batches &&
+                            c->trained >= RING;
+        if (steady) {
+            if (sp_status s = graph_step(c)) return s;
+            continue;
+        }
+        c->g_next_j = -1;
+        // keep the look-ahead full (first call: F+P+1 batches)
+        while (c->pushed < std::min<long long>(num_batches, c->trained + ahead + 1) && !c->eod)
+            if (sp_status s = plan_impl(c, base + c->pushed * stride, true)) return s;
+        // the trace is exhausted and the next Plan needs a future that will
+        // never come: truncate the window (sp_end_of_data)
+        if (c->planned <= c->trained && c->pushed >= num_batches && !c->eod)
+            if (sp_status s = sp_end_of_data(c)) return s;
+        const long long b = c->trained;
+        if (sp_status s = sp_forward(c, pooled)) return s;
+        if (sp_status s = sp_surrogate_grad(c, pooled, grad, 0, gamma, delta)) return s;
+        if (sp_status s = sp_train(c, grad, lr)) return s;
+        if (stats_out)
+            if (sp_status s = sp_copy_batch_stats(c, b, stats_out + (size_t)k * c->T * 4)) return s;
+    }
     return SP_OK;
 }
 
@@ -796,7 +1287,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     cudaSetDevice(c->device);
     o->pushed = c->pushed;
     o->planned = c->planned;
-    o->transferred = c->transferred;
+    o->transferred = c->x_enqueued.load();
     o->forwarded = c->forwarded;
     o->trained = c->trained;
     unsigned long long cum[4] = {0, 0, 0, 0};
@@ -811,9 +1302,17 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->h2d_index_bytes = c->h2d_index_bytes;
     o->h2d_row_bytes = (int64_t)cum[2] * c->D * 4;
     o->d2h_row_bytes = (int64_t)cum[3] * c->D * 4;
+    std::lock_guard<std::mutex> lk(c->prof_mu);
+    o->host_gather_ms = 0.0;  // the GPU pulls the missed rows itself
+    o->host_scatter_ms = c->x_scatter_ns.load() * 1e-6;
+    o->host_rows_gathered = c->x_rows_g.load();
+    o->host_rows_scattered = c->x_rows_s.load();
+    o->wait_xfer_ms = c->wait_xfer_ns * 1e-6;
+    o->wait_list_ms = c->wait_list_ns * 1e-6;
+    o->graph_steps = c->graph_steps;
     if (!c->prof_pending.empty()) {
-        for (int k = 0; k < c->nx; k++) cudaStreamSynchronize(c->xfer_s[k]);
-        cudaStreamSynchronize(c->wb_s);
+        cudaStreamSynchronize(c->xfer_s);
+        cudaStreamSynchronize(c->d2h_s);
         cudaStreamSynchronize(c->compute);
         harvest_profile(c, true);
     }

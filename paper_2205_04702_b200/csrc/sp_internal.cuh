@@ -72,6 +72,14 @@ struct Geometry {
     int n, n1, nc, nh;    // strides
 };
 
+// Fill lists of one Plan, mirrored into pinned host memory by the plan kernel
+// for the CPU side of the transfer engine (per ring slot, per table).
+struct HostList {
+    unsigned long long *ready;  // [T] = b + 1 once table t's list of batch b is complete
+    uint32_t *m;                // [T] fills of table t
+    uint2 *ent;                 // [T][n] {missed row, previous resident (EMPTY if vacant)}
+};
+
 struct PushArgs {
     Geometry g;
     int P, F;
@@ -85,6 +93,7 @@ struct PushArgs {
     const unsigned long long *log_base, *log_cap;
     unsigned long long *log_head, *log_tail;
     unsigned long long *err;
+    unsigned long long *err_host;  // pinned mapped flag: set on any device error
     unsigned long long *cum;  // [4] cumulative U, hits, misses, evictions
     uint32_t *miss_u, *victims;  // plan scratch [T*n]
     uint32_t *sort_tmp;          // [4][T*n] scratch for the large-n radix path
@@ -100,6 +109,12 @@ struct PushArgs {
     BatchBufs pb;
     int has_future;
     BatchBufs fb;
+    HostList hl;                 // pinned mirror of Plan(b)'s fill lists
+    // graph replay: j is read from ctl[ctl_r] (b = j - F - 1, idx = idx + j*stride)
+    // and ctl[(ctl_r + 1) % RING] = j + 1 is written for the next step
+    long long *ctl;
+    int ctl_r;
+    long long idx_stride;
 };
 
 struct TrainArgs {
@@ -117,10 +132,11 @@ struct XferArgs {
     Geometry g;
     BatchBufs bb;
     float *storage;
-    float *stage;        // [T][n][D] victim rows of this batch, staged in HBM
-    float *const *host;  // [T] device-visible host table pointers
+    float *const *host;       // [T] device-visible host table pointers
+    float *wb_stage;          // [sum m][D] victims (D2H DMA, then CPU scatter)
     const unsigned long long *err;
 };
+
 
 struct FlushArgs {
     Geometry g;
@@ -176,8 +192,7 @@ cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s);
 cudaError_t launch_backward_hot(const TrainArgs &a, cudaStream_t s);
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
                              float delta, cudaStream_t s);
-cudaError_t launch_pull(const XferArgs &a, int ctas, cudaStream_t s);
-cudaError_t launch_writeback(const XferArgs &a, int ctas, cudaStream_t s);
+cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
 size_t push_smem_bytes(int n);
 cudaError_t configure_push_kernel();

@@ -10,9 +10,15 @@ from paper_2205_04702_b200.harness import run_loop
 from workload import init_rows_np, init_table, sample_trace
 
 
-def pinned_tables(rows, D, seed, device="cuda", pin=True):
+def pinned_tables(rows, D, seed, device="cuda", pin=True, host_alloc=False):
     out = []
     for t, R in enumerate(rows):
+        if host_alloc:  # sp_host_alloc: THP-backed, registered by the library allocator
+            from paper_2205_04702_b200 import HostTable
+            ht = HostTable(R, D)
+            init_table(seed, t, R, D, device=device, out=ht.tensor)
+            out.append(ht)
+            continue
         h = torch.empty((R, D), dtype=torch.float32)
         if pin:
             h = h.pin_memory()
@@ -45,12 +51,13 @@ def compare_tables(got: np.ndarray, want: np.ndarray, init: np.ndarray):
 def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init_seed=4702,
                gde=(0.5, 0.01, 0.01), index_dtype="int64", index_on_device=False, log_factor=0,
                check_plans=True, check_slots=True, check_pooled=True, trace=None,
-               register_host=False, profile=False, sample_rows=None):
+               register_host=False, profile=False, sample_rows=None, host_alloc=False):
     g, d, e = gde
     if trace is None:
         trace = sample_trace(rows, N, L, alpha, nb, trace_seed)
     trace_np = trace.numpy()
-    tables = pinned_tables(rows, D, init_seed, pin=not register_host)
+    tables = pinned_tables(rows, D, init_seed, pin=not register_host, host_alloc=host_alloc)
+    views = [t.tensor if host_alloc else t for t in tables]
     feed = trace.to(torch.int32 if index_dtype == "int32" else torch.int64)
     if index_on_device:
         feed = feed.cuda()
@@ -99,7 +106,7 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
             touched = np.sort(np.random.default_rng(t).choice(touched, sample_rows, replace=False))
         if len(touched):
             want = orc.rows_of(t, touched)
-            got = tables[t][torch.from_numpy(touched)].numpy()
+            got = views[t][torch.from_numpy(touched)].numpy()
             c = compare_tables(got, want, init_rows_np(init_seed, t, touched, D))
             worst["max_rel"] = max(worst["max_rel"], c["max_rel"])
             worst["mismatch"] += c["mismatch"]
@@ -108,7 +115,7 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
         # untouched rows keep their initial values
         untouched = np.setdiff1d(np.arange(min(R, 512)), orc.touched(t))
         if len(untouched):
-            assert np.array_equal(tables[t][torch.from_numpy(untouched)].numpy(),
+            assert np.array_equal(views[t][torch.from_numpy(untouched)].numpy(),
                                   init_rows_np(init_seed, t, untouched, D))
     report["tables"] = worst
     report["stats"] = sp.stats()

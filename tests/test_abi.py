@@ -47,7 +47,7 @@ def test_invalid_descriptors_rejected_before_touching_a_device():
     tabs = (ctypes.c_void_p * 1)(1)
     base = dict(num_tables=1, rows=rows, host_tables=tabs, dim=16, slots=slots, window=3, past=-1,
                 future=-1, batch_size=4, pooling=2, device=0, stream=None, flags=0, log_factor=0,
-                pull_ctas=0, writeback_ctas=0)
+                host_threads=0, reserved=0)
     for bad in [dict(dim=6), dict(dim=0), dict(num_tables=0), dict(batch_size=0),
                 dict(past=1, future=3)]:
         d = B.SpDesc(**{**base, **bad})

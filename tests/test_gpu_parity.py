@@ -103,6 +103,14 @@ def test_register_host_flag():
     _assert_tables(rep)
 
 
+def test_host_alloc_tables():
+    """Host tables from sp_host_alloc (THP-backed, registered by the library)."""
+    c = CONFIGS["tiny"]
+    rep = run_parity(c.rows, c.slots, c.dim, c.batch, c.pooling, c.num_batches, 3, 2,
+                     alpha=c.alpha, host_alloc=True)
+    _assert_tables(rep)
+
+
 def test_capacity_error_at_oracle_batch_and_table():
     rows, D, N, L, nb = [400, 400], 8, 8, 2, 40
     tr = sample_trace(rows, N, L, 0.5, nb, 3)
@@ -174,3 +182,33 @@ def test_kaggle_full_size_parity_sampled():
                      sample_rows=4000)
     assert rep["plans"] == nb and rep["evictions"] > 1000
     _assert_tables(rep, exact=False)
+
+
+def test_run_steps_graph_replay_matches_oracle():
+    """sp_run_steps (C driver loop; CUDA-graph replay of the steady-state step
+    after the first RING batches) gives the same plans, pooled values and
+    final tables as the oracle."""
+    from oracle import UncachedTrainer
+    rows, D, N, L, nb = [2000, 300, 50], 16, 64, 2, 60
+    tr = sample_trace(rows, N, L, 0.9, nb, 12)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 8) for t, R in enumerate(rows)]
+    tables = pinned_tables(rows, D, 4702)
+    sp = ScratchPipe(rows, tables, D, slots, N, L, index_dtype="int32", index_on_device=True)
+    dev = tr.to(torch.int32).cuda().contiguous()
+    pooled = torch.empty((3, N, D), device="cuda")
+    grad = torch.empty_like(pooled)
+    g, d, e = 0.5, 0.01, 0.05
+    sp.run_steps(dev, 25, pooled, grad, g, d, e)        # mixes eager and graph steps
+    sp.run_steps(dev, nb - 25, pooled, grad, g, d, e)   # ... and the trace tail
+    sp.flush()
+    st = sp.stats()
+    assert st["trained"] == nb
+    orc = UncachedTrainer(rows, D, N, L, 4702)
+    for b in range(nb):
+        orc.step(tr.numpy()[b], g, d, e)
+    for t, R in enumerate(rows):
+        touched = orc.touched(t)
+        got = tables[t][torch.from_numpy(touched)].numpy()
+        want = orc.rows_of(t, touched)
+        assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-4)) <= TOL
+    sp.close()
