@@ -62,6 +62,7 @@ def lib():
                                      f32p, i32p]
         L.orc_train_get_row.argtypes = [P, ctypes.c_int32, ctypes.c_int64, f32p]
         L.orc_train_set_padding.argtypes = [P, ctypes.c_int32]
+        L.orc_train_set_table_ids.argtypes = [P, P]
         L.orc_train_touched.restype = ctypes.c_int64
         L.orc_train_touched.argtypes = [P, ctypes.c_int32, i64p, ctypes.c_int64]
         L.orc_policy_create.restype = P
@@ -108,7 +109,7 @@ class UncachedTrainer:
     """Part A: uncached EmbeddingBag training with sparse SGD (ground truth)."""
 
     def __init__(self, rows: Sequence[int], dim: int, batch: int, pooling: int, init_seed: int,
-                 allow_padding: bool = False):
+                 allow_padding: bool = False, table_ids: Optional[Sequence[int]] = None):
         self.rows = np.asarray(rows, dtype=np.int64)
         self.T, self.D, self.N, self.L = len(rows), dim, batch, pooling
         self._h = lib().orc_train_create(self.T, _p(self.rows, ctypes.c_int64), dim, batch,
@@ -117,6 +118,9 @@ class UncachedTrainer:
             raise ValueError("bad oracle config")
         if allow_padding:
             lib().orc_train_set_padding(self._h, 1)
+        if table_ids is not None:  # global table ids (table-wise sharding)
+            self._gid = np.ascontiguousarray(table_ids, dtype=np.int32)
+            lib().orc_train_set_table_ids(self._h, _p(self._gid, ctypes.c_int32))
         self.step_count = 0
 
     def close(self):

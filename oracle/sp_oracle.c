@@ -52,6 +52,7 @@ float orc_init_value(uint64_t seed, int32_t t, int64_t row, int32_t col) {
 /* ------------------------------------------------------------------------ */
 typedef struct {
     int64_t rows;
+    int32_t gid;          /* global table id the init values are keyed by */
     int64_t *pool_of_row; /* row -> index into pool (-1 = untouched) */
     float *pool;          /* [cap][D] */
     int64_t used, cap;
@@ -82,7 +83,7 @@ static float *lazy_row(orc_train *o, int32_t t, int64_t row) {
         k = lt->used++;
         lt->pool_of_row[row] = k;
         for (int32_t j = 0; j < o->D; j++)
-            lt->pool[k * o->D + j] = orc_init_value(o->seed, t, row, j);
+            lt->pool[k * o->D + j] = orc_init_value(o->seed, lt->gid, row, j);
     }
     return &lt->pool[k * o->D];
 }
@@ -95,6 +96,7 @@ orc_train *orc_train_create(int32_t T, const int64_t *rows, int32_t D, int32_t N
     o->tab = (lazy_table *)calloc((size_t)T, sizeof(lazy_table));
     for (int32_t t = 0; t < T; t++) {
         o->tab[t].rows = rows[t];
+        o->tab[t].gid = t;
         o->tab[t].pool_of_row = (int64_t *)malloc((size_t)rows[t] * sizeof(int64_t));
         for (int64_t r = 0; r < rows[t]; r++) o->tab[t].pool_of_row[r] = -1;
     }
@@ -192,11 +194,19 @@ int32_t orc_train_step(orc_train *o, const int64_t *ids, const float *grad_in,
 
 void orc_train_set_padding(orc_train *o, int32_t allow) { o->allow_pad = allow; }
 
+/* Table-wise sharding (one cache-manager instance per table):
+ * a trainer holding a subset of the tables keys their initial values by the
+ * GLOBAL table id, so per-rank trainers together equal one trainer over all
+ * tables. */
+void orc_train_set_table_ids(orc_train *o, const int32_t *gid) {
+    for (int32_t t = 0; t < o->T; t++) o->tab[t].gid = gid[t];
+}
+
 void orc_train_get_row(const orc_train *o, int32_t t, int64_t row, float *out) {
     const lazy_table *lt = &o->tab[t];
     int64_t k = lt->pool_of_row[row];
     for (int32_t j = 0; j < o->D; j++)
-        out[j] = k < 0 ? orc_init_value(o->seed, t, row, j) : lt->pool[k * o->D + j];
+        out[j] = k < 0 ? orc_init_value(o->seed, lt->gid, row, j) : lt->pool[k * o->D + j];
 }
 
 int64_t orc_train_touched(const orc_train *o, int32_t t, int64_t *out, int64_t cap) {

@@ -48,6 +48,8 @@ int32_t orc_train_step(orc_train *o, const int64_t *ids, const float *grad_in,
 void orc_train_get_row(const orc_train *o, int32_t t, int64_t row, float *out);
 /* allow id == -1 as "no lookup" (ragged bags; used only to pin Fig. 2) */
 void orc_train_set_padding(orc_train *o, int32_t allow);
+/* init values of local table t keyed by global table id gid[t] (sharding) */
+void orc_train_set_table_ids(orc_train *o, const int32_t *gid);
 /* sorted list of rows ever touched in table t; returns count (writes <= cap) */
 int64_t orc_train_touched(const orc_train *o, int32_t t, int64_t *out, int64_t cap);
 
