@@ -1,0 +1,71 @@
+"""Map ncu SASS-level warp-stall samples of one kernel to CUDA source lines.
+
+    python tools/stall_by_line.py <report.ncu-rep> <kernel-regex> <cubin> [launch-index]
+
+ncu's `--page source --csv` gives per-SASS-instruction samples with runtime
+addresses; `nvdisasm --print-line-info` on the same cubin gives per-offset
+source lines (the library is built with -lineinfo).  Offsets are taken
+relative to the first instruction of the kernel in both listings.
+"""
+from __future__ import annotations
+
+import collections
+import csv
+import io
+import re
+import subprocess
+import sys
+
+
+def sass_samples(rep, kernel, idx):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kernel}",
+                          "--launch-skip", str(idx), "--launch-count", "1"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    hdr = rows[hdr_i]
+    si = hdr.index("Warp Stall Sampling (All Samples)")
+    out = []
+    for r in rows[hdr_i + 1:]:
+        if len(r) > si and r[0].startswith("0x"):
+            out.append((int(r[0], 16), r[1].strip(), int(r[si] or 0)))
+    return out
+
+
+def line_map(cubin, func_regex):
+    txt = subprocess.run(["nvdisasm", "--print-line-info", "-c", cubin], capture_output=True, text=True).stdout
+    cur_fn, cur_line, m = None, None, {}
+    for ln in txt.splitlines():
+        if ln.startswith(".text.") and ln.strip().endswith(":"):
+            cur_fn = ln.strip()[:-1].replace(".text.", "")
+            continue
+        lm = re.search(r'line (\d+)', ln)
+        if "//##" in ln and lm:
+            cur_line = int(lm.group(1))
+            continue
+        am = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+        if am and cur_fn and re.search(func_regex, cur_fn):
+            m.setdefault(cur_fn, {})[int(am.group(1), 16)] = cur_line
+    return m
+
+
+def main():
+    rep, kernel, cubin = sys.argv[1:4]
+    idx = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    smp = sass_samples(rep, kernel, idx)
+    base = smp[0][0]
+    maps = line_map(cubin, kernel.replace("^", ""))
+    # pick the function whose instruction count matches best
+    fn = min(maps, key=lambda f: abs(len(maps[f]) - len(smp)))
+    lm = maps[fn]
+    by = collections.Counter()
+    for a, _, n in smp:
+        by[lm.get(a - base)] += n
+    tot = sum(by.values()) or 1
+    print(f"{fn}: {tot} samples")
+    for line, n in by.most_common(40):
+        print(f"{n:7d} {100 * n / tot:5.1f}%  line {line}")
+
+
+if __name__ == "__main__":
+    main()
