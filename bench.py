@@ -3,7 +3,7 @@
 
 One "step" = one pass of the whole hot path over one synthetic mini-batch:
 sp_plan (index ingest + dedup + Hit-Map probe + hit/miss + window-safe victim
-selection + bookkeeping), the fused zero-copy Collect/Exchange/Insert
+selection + bookkeeping), the fused TMA Collect/Exchange/Insert
 transfer, sp_forward (EmbeddingBag gather-reduce), the MLP stand-in
 (surrogate gradient kernel) and sp_train (coalescing segmented reduce + fused
 SGD).  Workload at N=1: BASELINE configs[1], Criteo-Kaggle-shaped (the config
@@ -56,7 +56,7 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, index: int, period_s: float = 0.002):
+    def __init__(self, index: int, period_s: float = 0.0005):
         self.samples, self.reasons, self.ok = [], 0, False
         self.period = period_s
         try:
@@ -192,6 +192,20 @@ def cpu_baseline(cfg, trace_dev, seconds):
     return {"value": n / el, "unit": "iters/s", "cores": 1, "kind": "oracle",
             "sample": f"first {n} batches of the bench trace from a cold scratchpad: reference policy "
                       f"(Part B) + uncached EmbeddingBag SGD (Part A), single thread, {el:.1f} s"}
+
+
+def _plan_roles(p0, p1):
+    """k_push critical chain: mean per-launch wall time of each table's Plan
+    CTA and dedup CTA over the profiling window (globaltimer, in-kernel)."""
+    out = {}
+    for role, key, li in (("plan", "plan_us", 0), ("dedup", "dedup_us", 1)):
+        n0, n1 = p0["launches"][li], p1["launches"][li]
+        if n1 <= n0:
+            continue
+        per = [(b * n1 - a * n0) / (n1 - n0) for a, b in zip(p0[key], p1[key])]
+        out[role] = {"max_table_us": round(max(per), 2), "mean_us": round(sum(per) / len(per), 2),
+                     "argmax_table": int(max(range(len(per)), key=lambda i: per[i]))}
+    return out
 
 
 def run_ours(args):
@@ -345,8 +359,10 @@ def run_ours(args):
     gpu_launches = sum(v for k, v in launches.items() if k in KERNEL_ONLY)
     # ---- profiling pass: per-kernel CUDA-event durations (separate from the timed region)
     sp.set_profiling(True)
+    pp0 = sp.debug_plan_profile()
     value_loop(KP)
     sp.set_profiling(False)
+    pp1 = sp.debug_plan_profile()
     st2 = sp.stats()
     if os.environ.get("SP_TIMELINE"):
         json.dump(sp.timeline(), open(os.environ["SP_TIMELINE"], "w"))
@@ -386,16 +402,15 @@ def run_ours(args):
         # pooled grad in + occurrence list + per-unique segment/slot words + SGD read+write
         "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 8 * D * U,
         "surrogate": 8 * D * Tg * N,
-        "transfer": 8 * D * m + 8 * D * ev,      # k_fill: staged rows in + slot write, victims out
-        "h2d": 4 * D * m,                        # copy engine: gathered missed rows
-        "d2h": 4 * D * m,                        # copy engine: staged victims (one row per fill)
+        # k_exchange, host-link bytes: missed rows pulled (H2D) + victims written back (D2H)
+        "transfer": 4 * D * m + 4 * D * ev,
         "plan": 4 * Tg * n,
     }
     peak, peak_kind = peaks()
     traffic = load_traffic()
     total_ms = sum(kms.values()) or 1.0
     kernels = {}
-    for k in ["plan", "transfer", "h2d", "d2h", "forward", "backward", "surrogate"]:
+    for k in ["plan", "transfer", "forward", "backward", "surrogate"]:
         gbs = alg_bytes[k] / (avg_ms[k] * 1e-3) / 1e9 if avg_ms[k] else None
         kernels[k] = {"avg_us": round(avg_ms[k] * 1e3, 3), "share": round(kms[k] / total_ms, 4),
                       "alg_bytes_per_launch": int(alg_bytes[k]), "alg_GBs": None if gbs is None else round(gbs, 1)}
@@ -411,8 +426,9 @@ def run_ours(args):
                                   else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
     train_ms = avg_ms["forward"] + avg_ms["backward"]
     train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
-    link_GBs = alg_bytes["h2d"] / (avg_ms["h2d"] * 1e-3) / 1e9 if avg_ms.get("h2d") else None
-    wb_GBs = alg_bytes["d2h"] / (avg_ms["d2h"] * 1e-3) / 1e9 if avg_ms.get("d2h") else None
+    xs = avg_ms["transfer"] * 1e-3
+    link_GBs = 4 * D * m / xs / 1e9 if xs else None
+    wb_GBs = 4 * D * ev / xs / 1e9 if xs else None
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
@@ -428,24 +444,21 @@ def run_ours(args):
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
-        "host_link": {"path": "CPU gather/scatter + copy-engine DMA (both directions)",
-                      "h2d_bytes_per_batch": int(alg_bytes["h2d"]),
+        "host_link": {"path": "k_exchange: TMA bulk copies, victims HBM->host rows and missed rows "
+                              "host->HBM slots, both directions in one kernel (no CPU copies)",
+                      "h2d_bytes_per_batch": int(4 * D * m),
                       "h2d_GBs": None if link_GBs is None else round(link_GBs, 2),
-                      "d2h_bytes_per_batch": int(alg_bytes["d2h"]),
+                      "d2h_bytes_per_batch": int(4 * D * ev),
                       "d2h_GBs": None if wb_GBs is None else round(wb_GBs, 2),
                       "peak_h2d_GBs": 55.6, "peak_d2h_GBs": 57.0,
                       "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)"},
         "kernels": kernels,
+        "plan_ctas": _plan_roles(pp0, pp1),
         "per_step": {"uniques": round(U, 1), "misses": round(m, 1), "evictions": round(ev, 1)},
-        "host_engine": {"gather_us_per_batch": round(1e3 * (st2["host_gather_ms"] - st1["host_gather_ms"]) / KP, 2),
-                        "scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1["host_scatter_ms"]) / KP, 2),
-                        "threads": "gather + scatter threads, 8 row-copy helpers"},
         "gpu_launches": int(gpu_launches),
         "launches_per_step": {k: v / K for k, v in launches.items()},
         "clocks": sampler.summary(),
         "host_issue_us_per_step": round(1e6 * t_host_issue / K, 2),
-        "host_waits_us_per_step": {"transfer": round(1e3 * (st1["wait_xfer_ms"] - st0["wait_xfer_ms"]) / K, 2),
-                                   "list_slot": round(1e3 * (st1["wait_list_ms"] - st0["wait_list_ms"]) / K, 2)},
         "graph_steps": st1["graph_steps"] - st0["graph_steps"],
         "e2e": {"value": round(e2e_value, 2), "unit": "iters/s", "h2d_bytes_per_step": idx_bytes,
                 "d2h_bytes_per_step": stats_bytes, "ms_per_step": round(ms_e2e / K, 5),

@@ -255,6 +255,13 @@ sp_status sp_debug_resident(sp_ctx *c, int32_t t, int64_t *ids, int64_t cap, int
  * never used).  Arrays of slots[t] entries. */
 sp_status sp_debug_slots(sp_ctx *c, int32_t t, int64_t *resident, int64_t *last_use);
 /* Copy Storage rows [first, first+count) of table t to host (synchronises). */
+/* k_push per-CTA wall time while profiling is on (sp_set_profiling / SP_FLAG_PROFILE),
+ * from %globaltimer at CTA entry and exit.  out[2T+2] (caller-owned host array):
+ * out[t] = summed ns of the Plan CTA of table t, out[T+t] = summed ns of the
+ * dedup CTA of table t, out[2T] / out[2T+1] = CTAs timed per role (summed
+ * over tables).  Synchronises the plan stream.  Diagnostics only. */
+sp_status sp_debug_plan_profile(sp_ctx *c, uint64_t *out);
+
 sp_status sp_debug_storage(sp_ctx *c, int32_t t, int64_t first, int64_t count, float *out);
 
 #ifdef __cplusplus

@@ -93,7 +93,8 @@ def _load():
                        ("sp_debug_plan", [P, ctypes.c_int64, ctypes.c_int32, i64p, i64p, i64p, i64p, i64p]),
                        ("sp_debug_resident", [P, ctypes.c_int32, i64p, ctypes.c_int64, i64p]),
                        ("sp_debug_slots", [P, ctypes.c_int32, i64p, i64p]),
-                       ("sp_debug_storage", [P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, P])]:
+                       ("sp_debug_storage", [P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, P]),
+                       ("sp_debug_plan_profile", [P, P])]:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = S
@@ -336,6 +337,17 @@ class ScratchPipe:
         res, lu = np.empty(S, np.int64), np.empty(S, np.int64)
         self._check(lib.sp_debug_slots(self._h, t, _i64(res), _i64(lu)))
         return res, lu
+
+    def debug_plan_profile(self) -> dict:
+        """k_push per-CTA wall time while profiling: mean us per launch of the
+        Plan CTA and of the dedup CTA of each table (sp_debug_plan_profile)."""
+        T = len(self._slots)
+        out = np.zeros(2 * T + 2, np.uint64)
+        self._check(lib.sp_debug_plan_profile(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        npl, nde = max(1, int(out[2 * T]) // T), max(1, int(out[2 * T + 1]) // T)
+        return {"plan_us": (out[:T].astype(np.float64) / npl / 1e3).tolist(),
+                "dedup_us": (out[T:2 * T].astype(np.float64) / nde / 1e3).tolist(),
+                "launches": [int(out[2 * T]) // T, int(out[2 * T + 1]) // T]}
 
     def debug_storage(self, t: int, first: int = 0, count: Optional[int] = None) -> np.ndarray:
         if count is None:

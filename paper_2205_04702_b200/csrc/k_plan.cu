@@ -9,7 +9,8 @@
 //   D2  stable LSD radix sort of (id, occurrence) pairs by id; heads,
 //       unique IDs, segment offsets (Alg. 1 walks raw IDs; deduplicating
 //       first is equivalent, reading R5)
-//   D3  backward work list: chunk records of <= CH occurrences per unique
+//   D3  backward work lists: one chunk record per unique with <= CH
+//       occurrences, one hot record per unique with more
 //
 // CTAs [0, T) — Plan(b), b = j - F - 1, on the scratchpad state of table t:
 //   P1  future probe: resident IDs of B(b+F) (deduped by the previous
@@ -175,6 +176,7 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
     }
     // D1: ingest + range check
     int bad = 0;
+#pragma unroll 4
     for (int i = tid; i < n; i += blockDim.x) {
         long long id = A.idx_i32 ? (long long)((const int32_t *)idx)[(size_t)t * n + i]
                                  : ((const long long *)idx)[(size_t)t * n + i];
@@ -218,44 +220,57 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
     const uint32_t U = carry;
     if (tid == 0) { seg_off[U] = (uint32_t)n; nb.U[t] = U; }
     __syncthreads();
-    // D3a: chunk headers (one per <= CH occurrences of a unique) + hot rows
+    // D3a: backward work lists.  A unique with <= CH occurrences is one chunk
+    // record (its bag indices inline); a hot unique (> CH occurrences, the
+    // Zipf head) is cut into segments of <= hs occurrences, one hot record
+    // each, folded by one CTA of k_bwd.
     ChunkRec *rec = nb.chunk_rec + (size_t)t * g.nc;
     uint4 *hot = nb.hot_rec + (size_t)t * g.nh;
+    uint32_t *hcnt = nb.hot_cnt + (size_t)t * g.nh;
     uint32_t *chunk_first = sw ? ka : kb;  // the sort's free buffer (>= n entries)
+    const uint32_t hs = (uint32_t)g.hs;
     carry = 0;
     uint32_t hcarry = 0;
     for (uint32_t u0 = 0; u0 < U; u0 += blockDim.x) {
         const uint32_t u = u0 + tid;
-        uint32_t nch = 0, lo = 0, hi = 0;
+        uint32_t lo = 0, len = 0;
         if (u < U) {
             lo = seg_off[u];
-            hi = seg_off[u + 1];
-            nch = (hi - lo + CH - 1) / CH;
+            len = seg_off[u + 1] - lo;
         }
+        const bool normal = u < U && len <= (uint32_t)CH, is_hot = u < U && len > (uint32_t)CH;
+        const uint32_t nseg = is_hot ? (len + hs - 1) / hs : 0u;
         uint32_t tot, htot;
-        const uint32_t ex = block_scan(nch, &tot);
-        const uint32_t hx = block_scan(nch > 1 ? 1u : 0u, &htot);
-        if (u < U) chunk_first[u] = carry + ex;
-        const uint32_t multi = nch > 1 ? 0x80000000u : 0u;
-        for (uint32_t k = 0; k < nch; k++) {
-            ChunkRec &r = rec[carry + ex + k];
-            r.slot = u;
-            r.meta = min(hi - lo - k * CH, (uint32_t)CH) | multi;
+        const uint32_t ex = block_scan(normal ? 1u : 0u, &tot);
+        const uint32_t hx = block_scan(nseg, &htot);
+        if (normal) {
+            const uint32_t c = carry + ex;
+            chunk_first[u] = c;
+            rec[c].slot = u;
+            rec[c].meta = len;
+        } else if (is_hot) {
+            chunk_first[u] = EMPTY;
+            const uint32_t h0 = hcarry + hx;
+            for (uint32_t k = 0; k < nseg; k++)
+                hot[h0 + k] = make_uint4(u, lo + k * hs, min(hs, len - k * hs), k | (nseg << 16));
+            hcnt[h0] = 0u;
         }
-        if (nch > 1) hot[hcarry + hx] = make_uint4(u, carry + ex, nch, 0u);
         carry += tot;
         hcarry += htot;
     }
     if (tid == 0) {
         nb.nchunks[t] = carry;
         nb.nhot[t] = hcarry;
+        if (t == 0)
+            for (int k = 0; k < (g.T + 63) / 64; k++) nb.work[k] = 0u;  // k_bwd work counters
     }
     __syncthreads();
-    // D3b: inline bag indices, one occurrence per thread
+    // D3b: inline bag indices of the single-chunk rows, one occurrence per thread
+#pragma unroll 4
     for (int i = tid; i < n; i += blockDim.x) {
         const uint32_t u = sorted_uid[i];
-        const uint32_t r = (uint32_t)i - seg_off[u];
-        rec[chunk_first[u] + r / CH].bag[r % CH] = vals[i] / (uint32_t)g.L;
+        const uint32_t c = chunk_first[u];
+        if (c != EMPTY) rec[c].bag[(uint32_t)i - seg_off[u]] = vals[i] / (uint32_t)g.L;
     }
 }
 
@@ -369,7 +384,6 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
     uint32_t *fill_row = pb.fill_row + (size_t)t * n;
     uint32_t *evict_row = pb.evict_row + (size_t)t * n;
     uint32_t nev = 0;
-    uint2 *hent = A.hl.ent + (size_t)t * n;  // pinned host mirror (zero-copy, ~8 B per fill)
     for (uint32_t k = tid; k < m; k += blockDim.x) {
         const uint32_t u = miss_u[k], s = victims[k], id = uniq_id[u];
         const uint32_t old = A.resident[s];
@@ -385,18 +399,10 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
         fill_slot[k] = s;
         fill_row[k] = id;
         evict_row[k] = old;
-        hent[k] = make_uint2(id, old);
     }
     uint32_t ev_total;
     (void)block_scan(nev, &ev_total);  // barriers: P4 writes visible below
-    if (tid == 0) {
-        pb.m[t] = m;  // device copy for k_fill, published before the ready flag
-        A.hl.m[t] = m;
-        // the CTA's host-list writes precede this fence through the barrier
-        // above (causality order), so one system-scope fence publishes them all
-        __threadfence_system();
-        *(volatile unsigned long long *)&A.hl.ready[t] = (unsigned long long)(b + 1);
-    }
+    if (tid == 0) pb.m[t] = m;  // fills of table t for k_exchange
 
     // P5: LRU log append (after an in-place compaction if it would overflow)
     const unsigned long long head = s_head;
@@ -445,12 +451,26 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
     const uint32_t *sorted_occ = pb.sorted_occ + (size_t)t * n;
     const uint32_t *sorted_uid = pb.sorted_uid + (size_t)t * n;
     uint32_t *slot_of_occ = pb.slot_of_occ + (size_t)t * n;
-    for (int i = tid; i < n; i += blockDim.x) slot_of_occ[sorted_occ[i]] = slot_u[sorted_uid[i]];
+    // (4 elements per thread per round: their independent loads are in flight
+    // together instead of one dependent pair per loop trip)
+    for (int i0 = tid; i0 < n; i0 += 4 * (int)blockDim.x) {
+        uint32_t o[4], u[4], sl[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int i = i0 + q * (int)blockDim.x;
+            if (i < n) { o[q] = sorted_occ[i]; u[q] = sorted_uid[i]; }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (i0 + q * (int)blockDim.x < n) sl[q] = slot_u[u[q]];
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (i0 + q * (int)blockDim.x < n) slot_of_occ[o[q]] = sl[q];
+    }
     ChunkRec *rec = pb.chunk_rec + (size_t)t * g.nc;
-    const uint32_t nch = pb.nchunks[t];
-    for (uint32_t c = tid; c < nch; c += blockDim.x) rec[c].slot = slot_u[rec[c].slot];
     uint4 *hot = pb.hot_rec + (size_t)t * g.nh;
-    const uint32_t nhot = pb.nhot[t];
+    const uint32_t nch = pb.nchunks[t], nhot = pb.nhot[t];
+    for (uint32_t c = tid; c < nch; c += blockDim.x) rec[c].slot = slot_u[rec[c].slot];
     for (uint32_t h = tid; h < nhot; h += blockDim.x) hot[h].x = slot_u[hot[h].x];
 }
 
@@ -468,10 +488,22 @@ __global__ void __launch_bounds__(PUSH_THREADS, 2) k_push(PushArgs A) {
         idx = static_cast<const char *>(A.idx) + j * A.idx_stride;
         if (blockIdx.x == 0 && threadIdx.x == 0) A.ctl[(A.ctl_r + 1) % RING] = j + 1;
     }
-    if ((int)blockIdx.x < T) {
+    unsigned long long t_start = 0;
+    if (A.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    const bool role_plan = (int)blockIdx.x < T;
+    if (role_plan) {
         if (A.do_plan) plan_table(A, blockIdx.x, b);
     } else if (A.has_new) {
         dedup_table(A, blockIdx.x - T, smem_raw, j, idx);
+    }
+    if (A.prof && (role_plan ? A.do_plan : A.has_new)) {  // per-CTA wall time, by role and table
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t_end;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            atomicAdd(&A.prof[blockIdx.x], t_end - t_start);
+            atomicAdd(&A.prof[2 * T + (role_plan ? 0 : 1)], 1ull);
+        }
     }
 }
 

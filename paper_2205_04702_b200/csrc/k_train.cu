@@ -8,12 +8,11 @@
 //           all L row loads of a bag issued before the fold.
 //   k_bwd   gradient duplication + coalescing fused with the SGD
 //           update: per unique row, the gradients of its
-//           occurrences (ascending occurrence order, contiguous in the sorted
-//           occurrence list built at Plan) are summed in fp64 and the row is
-//           updated in place, w = fmaf(-lr, (float)sum, w).  One owner per
-//           unique row -> no atomics on Storage.  Long (hot, Zipf-skewed)
-//           segments are split into chunks of CH occurrences whose fp64
-//           partials are folded in chunk order by the last chunk to finish.
+//           occurrences (contiguous in the sorted occurrence list built at
+//           dedup) are summed in fp64 and the row is updated in place,
+//           w = fmaf(-lr, (float)sum, w).  One owner per unique row -> no
+//           atomics on Storage.  Hot (Zipf-head) rows are folded by a whole
+//           CTA with a fixed tree; the rest by one lane group each.
 //   k_surrogate  the harness's MLP stand-in g = fmaf(gamma, pooled, delta).
 #include "sp_internal.cuh"
 
@@ -121,79 +120,174 @@ __device__ __forceinline__ float4 sgd(const float4 &w, const Acc4 &a, float lr) 
     return r;
 }
 
-// Pass 1.  Work item = one chunk record of one table: up to CH occurrences of
-// one unique row with their bag indices inline, so a chunk costs one record
-// load, then its gradient rows (RB per round, all issued before folding),
-// while the Storage row is prefetched.  Single-chunk rows (the common case)
-// are updated here; hot rows write one fp64 partial per chunk, folded by
-// k_bwd_hot (pass 2).
+// One launch, two kinds of work item (lists built at dedup, slots at Plan):
+//  H  a hot row (> CH occurrences, the Zipf head): one CTA.  Lane group gi
+//     folds occurrences gi, gi+gpb, gi+2gpb, ... of the row (ascending) in
+//     fp64, RB gradient rows in flight; a fixed binary tree over the groups in
+//     shared memory gives the row sum; group 0 applies the SGD update.  No
+//     partials leave the CTA and no second pass runs; the fold shape depends
+//     only on the occurrence count (deterministic, grid-independent).
+//  N  a chunk record (<= CH occurrences, bag indices inline): one lane group,
+//     one record load, then its gradient rows, the Storage row prefetched
+//     beside them, update in the epilogue.  Groups take records dynamically
+//     (one atomic per CTA per round), so CTAs that folded hot rows take fewer.
+// One owner per unique row: no atomics on Storage.
 template <int G, int VPL>
-__global__ void __launch_bounds__(256, 3) k_bwd(TrainArgs A) {
+__global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
     const int D4 = g.D / 4;
     __shared__ uint32_t s_pref[65];
+    __shared__ uint32_t s_base;
+    __shared__ double4 s_red[256];
     const int gpb = blockDim.x / G;
+    const int gi = threadIdx.x / G;
     const int lane = threadIdx.x % G;
     const float4 *grad = reinterpret_cast<const float4 *>(A.grad);
     float4 *st = reinterpret_cast<float4 *>(A.storage);
-    constexpr int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);  // gradient rows per round
+    constexpr int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);   // hot rows: gradient rows in flight per group
+    constexpr int RBN = VPL >= 4 ? 1 : (VPL == 2 ? 2 : 4);  // chunk records (mostly 1-2 occurrences)
+    // ---- H: hot-row segments, one CTA each (RB rows per group: one round)
+    __shared__ uint32_t s_last;
+    for (int t0 = 0; t0 < g.T; t0 += 64) {
+        const int tcount = min(64, g.T - t0);
+        table_prefix(A.bb.nhot, t0, tcount, s_pref);
+        const uint32_t total = s_pref[tcount];
+        for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
+            const int tl = find_table(s_pref, tcount, item);
+            const int t = t0 + tl;
+            const uint32_t h = item - s_pref[tl];
+            const uint4 hr = A.bb.hot_rec[(size_t)t * g.nh + h];
+            const uint32_t slot = hr.x, lo = hr.y, len = hr.z, k = hr.w & 0xFFFFu, nseg = hr.w >> 16;
+            const uint32_t *occ = A.bb.sorted_occ + (size_t)t * g.n + lo;
+            const float4 *gb = grad + (size_t)t * g.N * D4 + lane;
+            Acc4 acc[VPL];
+#pragma unroll
+            for (int v = 0; v < VPL; v++) acc[v] = Acc4{0.0, 0.0, 0.0, 0.0};
+            for (uint32_t k0 = gi; k0 < len; k0 += (uint32_t)gpb * RB) {
+                float4 r[RB][VPL];
+#pragma unroll
+                for (int q = 0; q < RB; q++) {
+                    const uint32_t kq = k0 + (uint32_t)q * gpb;
+                    if (kq < len) {
+                        const uint32_t bag = __ldg(occ + kq) / (uint32_t)g.L;
+#pragma unroll
+                        for (int v = 0; v < VPL; v++) r[q][v] = ldg4(gb + (size_t)bag * D4 + v * G);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < RB; q++)
+                    if (k0 + (uint32_t)q * gpb < len)
+#pragma unroll
+                        for (int v = 0; v < VPL; v++) acc_add(acc[v], r[q][v]);
+            }
+            // fixed tree over the groups, one float4 column block at a time;
+            // group 0 ends with the segment sum
+            double4 *part = reinterpret_cast<double4 *>(A.partial + ((size_t)t * g.nh + h) * g.D) + lane;
+#pragma unroll
+            for (int v = 0; v < VPL; v++) {
+                __syncthreads();
+                s_red[threadIdx.x] = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
+                __syncthreads();
+                for (int hh = 1; hh < gpb; hh <<= 1) {
+                    if ((gi % (2 * hh)) == 0 && gi + hh < gpb) {
+                        const double4 o = s_red[threadIdx.x + hh * G];
+                        double4 &m = s_red[threadIdx.x];
+                        m.x += o.x; m.y += o.y; m.z += o.z; m.w += o.w;
+                    }
+                    __syncthreads();
+                }
+                if (gi == 0) {
+                    const double4 m = s_red[lane];
+                    if (nseg == 1) {
+                        float4 *wp = st + (size_t)slot * D4 + lane + v * G;
+                        *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
+                    } else {
+                        part[v * G] = m;
+                    }
+                }
+            }
+            if (nseg > 1) {  // the last segment to arrive folds the row's partials in k order
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0) s_last = atomicAdd(&A.bb.hot_cnt[(size_t)t * g.nh + (h - k)], 1u) == nseg - 1;
+                __syncthreads();
+                if (s_last) {
+                    __threadfence();
+                    const double2 *p0 = reinterpret_cast<const double2 *>(A.partial + ((size_t)t * g.nh + (h - k)) * g.D);
+                    for (int col = threadIdx.x; col < D4; col += blockDim.x) {
+                        // L2 loads (__ldcg): the partials were written by other SMs
+                        double2 lo2 = __ldcg(p0 + 2 * col), hi2 = __ldcg(p0 + 2 * col + 1);
+                        double4 m = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);
+                        for (uint32_t kk = 1; kk < nseg; kk++) {
+                            lo2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col);
+                            hi2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col + 1);
+                            m.x += lo2.x; m.y += lo2.y; m.z += hi2.x; m.w += hi2.y;
+                        }
+                        float4 *wp = st + (size_t)slot * D4 + col;
+                        *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
+                    }
+                }
+            }
+        }
+    }
+    // ---- N: single-chunk rows, taken dynamically one record per group
     for (int t0 = 0; t0 < g.T; t0 += 64) {
         const int tcount = min(64, g.T - t0);
         table_prefix(A.bb.nchunks, t0, tcount, s_pref);
         const uint32_t total = s_pref[tcount];
-        for (uint32_t item = blockIdx.x * gpb + threadIdx.x / G; item < total; item += gridDim.x * gpb) {
+        uint32_t *ctr = A.bb.work + t0 / 64;
+        while (true) {
+            __syncthreads();
+            if (threadIdx.x == 0) s_base = atomicAdd(ctr, (uint32_t)gpb);
+            __syncthreads();
+            const uint32_t base = s_base;
+            if (base >= total) break;
+            const uint32_t item = base + gi;
+            if (item >= total) continue;
             const int tl = find_table(s_pref, tcount, item);
             const int t = t0 + tl;
             const uint32_t c = item - s_pref[tl];
             const uint4 *rp = reinterpret_cast<const uint4 *>(A.bb.chunk_rec + (size_t)t * g.nc + c);
             uint4 q4[5];
             q4[0] = __ldg(rp);
-            const uint32_t slot = q4[0].x, meta = q4[0].y;
-            const uint32_t len = meta & 0xFFFFu;
-            const bool multi = (meta >> 31) != 0;
+            const uint32_t slot = q4[0].x, len = q4[0].y;
 #pragma unroll
             for (int k = 1; k < 5; k++) q4[k] = (uint32_t)(4 * k - 2) < len ? __ldg(rp + k) : make_uint4(0, 0, 0, 0);
             const uint32_t *bag = reinterpret_cast<const uint32_t *>(q4) + 2;
             const float4 *gb = grad + (size_t)t * g.N * D4 + lane;
-            float4 w[VPL];
             float4 *wp = st + (size_t)slot * D4 + lane;
-            if (!multi) {
+            float4 w[VPL];
 #pragma unroll
-                for (int v = 0; v < VPL; v++) w[v] = wp[v * G];
-            }
+            for (int v = 0; v < VPL; v++) w[v] = wp[v * G];
             Acc4 acc[VPL];
 #pragma unroll
             for (int v = 0; v < VPL; v++) acc[v] = Acc4{0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int q0 = 0; q0 < CH; q0 += RB) {
+            for (int q0 = 0; q0 < CH; q0 += RBN) {
                 if ((uint32_t)q0 < len) {
-                    float4 r[RB][VPL];
+                    float4 r[RBN][VPL];
 #pragma unroll
-                    for (int q = 0; q < RB; q++)
+                    for (int q = 0; q < RBN; q++)
                         if ((uint32_t)(q0 + q) < len)
 #pragma unroll
                             for (int v = 0; v < VPL; v++) r[q][v] = ldg4(gb + (size_t)bag[q0 + q] * D4 + v * G);
 #pragma unroll
-                    for (int q = 0; q < RB; q++)
+                    for (int q = 0; q < RBN; q++)
                         if ((uint32_t)(q0 + q) < len)
 #pragma unroll
                             for (int v = 0; v < VPL; v++) acc_add(acc[v], r[q][v]);
                 }
             }
-            if (!multi) {
 #pragma unroll
-                for (int v = 0; v < VPL; v++) wp[v * G] = sgd(w[v], acc[v], A.lr);
-            } else {
-                double4 *part = reinterpret_cast<double4 *>(A.partial + ((size_t)t * g.nc + c) * g.D) + lane;
-#pragma unroll
-                for (int v = 0; v < VPL; v++) part[v * G] = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
-            }
+            for (int v = 0; v < VPL; v++) wp[v * G] = sgd(w[v], acc[v], A.lr);
         }
     }
 }
 
-// generic D: one warp per chunk, strided columns
+// generic D (D/4 not a power-of-two multiple of 32): one warp per row,
+// strided columns; hot rows and chunk records both folded in ascending
+// occurrence order by that warp (sequential fp64 fold)
 __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
@@ -202,81 +296,31 @@ __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
     const float4 *grad = reinterpret_cast<const float4 *>(A.grad);
     float4 *st = reinterpret_cast<float4 *>(A.storage);
     const int wpb = blockDim.x / 32;
+    const long long w0 = (long long)blockIdx.x * wpb + threadIdx.x / 32, ws = (long long)gridDim.x * wpb;
     for (int t = 0; t < g.T; t++) {
-        const uint32_t total = A.bb.nchunks[t];
-        for (uint32_t c = blockIdx.x * wpb + threadIdx.x / 32; c < total; c += gridDim.x * wpb) {
-            const ChunkRec &rc = A.bb.chunk_rec[(size_t)t * g.nc + c];
-            const uint32_t slot = rc.slot, len = rc.meta & 0xFFFFu;
-            const bool multi = (rc.meta >> 31) != 0;
-            double *part = A.partial + ((size_t)t * g.nc + c) * g.D;
+        const float4 *gb = grad + (size_t)t * g.N * D4;
+        const uint32_t nhot = A.bb.nhot[t];
+        for (long long h = w0; h < nhot; h += ws) {
+            const uint4 hr = A.bb.hot_rec[(size_t)t * g.nh + h];
+            if ((hr.w & 0xFFFFu) != 0) continue;  // segment 0 owns the whole row
+            const uint32_t nseg = hr.w >> 16;
+            uint32_t len = 0;
+            for (uint32_t k = 0; k < nseg; k++) len += A.bb.hot_rec[(size_t)t * g.nh + h + k].z;
+            const uint32_t *occ = A.bb.sorted_occ + (size_t)t * g.n + hr.y;
             for (int col = lane; col < D4; col += 32) {
                 Acc4 a{0.0, 0.0, 0.0, 0.0};
-                for (uint32_t i = 0; i < len; i++)
-                    acc_add(a, grad[((size_t)t * g.N + rc.bag[i]) * D4 + col]);
-                if (!multi) st[(size_t)slot * D4 + col] = sgd(st[(size_t)slot * D4 + col], a, A.lr);
-                else reinterpret_cast<double4 *>(part)[col] = make_double4(a.x, a.y, a.z, a.w);
+                for (uint32_t i = 0; i < len; i++) acc_add(a, gb[(size_t)(occ[i] / (uint32_t)g.L) * D4 + col]);
+                st[(size_t)hr.x * D4 + col] = sgd(st[(size_t)hr.x * D4 + col], a, A.lr);
             }
         }
-    }
-}
-
-// Pass 2: one CTA per hot row folds its chunk partials: thread (p, col) sums
-// partials p, p+PL, p+2PL, ... in order, then a fixed-shape tree over p
-// (deterministic, independent of the grid), then the SGD update.
-__global__ void __launch_bounds__(256) k_bwd_hot(TrainArgs A) {
-    if (*A.err != NO_ERR) return;
-    const Geometry g = A.g;
-    const int D4 = g.D / 4;
-    __shared__ double4 s_acc[256];
-    __shared__ uint32_t s_pref[65];
-    const int PL = D4 >= 256 ? 1 : 256 / D4;          // partial lanes per column (<= 256/D4)
-    float4 *st = reinterpret_cast<float4 *>(A.storage);
-    for (int t0 = 0; t0 < g.T; t0 += 64) {
-        const int tcount = min(64, g.T - t0);
-        table_prefix(A.bb.nhot, t0, tcount, s_pref);
-        const uint32_t total = s_pref[tcount];
-        for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-            const int tl = find_table(s_pref, tcount, item);
-            const int t = t0 + tl;
-            const uint4 hr = A.bb.hot_rec[(size_t)t * g.nh + (item - s_pref[tl])];
-            const uint32_t slot = hr.x, c0 = hr.y, nch = hr.z;
-            const double4 *part = reinterpret_cast<const double4 *>(A.partial + ((size_t)t * g.nc + c0) * g.D);
-            for (int col0 = 0; col0 < D4; col0 += 256 / PL) {
-                const int p = threadIdx.x / (256 / PL > D4 ? D4 : 256 / PL);
-                const int colw = 256 / PL > D4 ? D4 : 256 / PL;
-                const int col = col0 + threadIdx.x % colw;
+        const uint32_t total = A.bb.nchunks[t];
+        for (long long c = w0; c < total; c += ws) {
+            const ChunkRec &rc = A.bb.chunk_rec[(size_t)t * g.nc + c];
+            const uint32_t slot = rc.slot, len = rc.meta;
+            for (int col = lane; col < D4; col += 32) {
                 Acc4 a{0.0, 0.0, 0.0, 0.0};
-                if (p < PL && col < D4) {
-                    uint32_t q = p;
-                    for (; q + 3 * PL < nch; q += 4 * PL) {  // 4 partials in flight, folded in order
-                        double4 d[4];
-#pragma unroll
-                        for (int k = 0; k < 4; k++) d[k] = part[(size_t)(q + k * PL) * D4 + col];
-#pragma unroll
-                        for (int k = 0; k < 4; k++) { a.x += d[k].x; a.y += d[k].y; a.z += d[k].z; a.w += d[k].w; }
-                    }
-                    for (; q < nch; q += PL) {
-                        const double4 d = part[(size_t)q * D4 + col];
-                        a.x += d.x; a.y += d.y; a.z += d.z; a.w += d.w;
-                    }
-                }
-                __syncthreads();
-                if (p < PL && col < D4) s_acc[p * colw + (col - col0)] = make_double4(a.x, a.y, a.z, a.w);
-                __syncthreads();
-                for (int half = 1; half < PL; half <<= 1) {   // fixed tree over p
-                    if (p < PL && col < D4 && (p % (2 * half)) == 0 && p + half < PL) {
-                        const double4 o = s_acc[(p + half) * colw + (col - col0)];
-                        double4 &m = s_acc[p * colw + (col - col0)];
-                        m.x += o.x; m.y += o.y; m.z += o.z; m.w += o.w;
-                    }
-                    __syncthreads();
-                }
-                if (p == 0 && col < D4) {
-                    const double4 m = s_acc[col - col0];
-                    float4 *wp = st + (size_t)slot * D4 + col;
-                    *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
-                }
-                __syncthreads();
+                for (uint32_t i = 0; i < len; i++) acc_add(a, gb[(size_t)rc.bag[i] * D4 + col]);
+                st[(size_t)slot * D4 + col] = sgd(st[(size_t)slot * D4 + col], a, A.lr);
             }
         }
     }
@@ -349,19 +393,25 @@ cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// occurrences per hot-row segment: one round of RB rows per lane group of
+// the k_bwd instance that D dispatches to (generic D: 64)
+int backward_hot_segment(int D) {
+    int G = 32, VPL = 1;
+    switch (D / 4) {
+        case 1: case 2: case 4: case 8: case 16: case 32: G = D / 4; VPL = 1; break;
+        case 64: VPL = 2; break;
+        case 128: VPL = 4; break;
+        case 256: VPL = 8; break;
+        default: return 64;
+    }
+    const int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);
+    return (256 / G) * RB;
+}
+
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
     // upper bound of work items: all chunks of all tables
     SP_DISPATCH_D(D4, k_bwd, (long long)a.g.T * a.g.nc, a, s);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_backward_hot(const TrainArgs &a, cudaStream_t s) {
-    long long upper = (long long)a.g.T * a.g.nh;
-    const long long cap = (long long)num_sms() * 4;
-    int grid = (int)(upper < cap ? upper : cap);
-    if (grid < 1) grid = 1;
-    k_bwd_hot<<<grid, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -42,14 +42,16 @@ __host__ __device__ inline unsigned long long err_key(long long b, int t, unsign
 //   n1 = n + 1       (seg_off)
 //   nc = n + n/CH + 1 (chunk_rec)
 //   nh = n/CH + 1     (hot_rec)
-// chunk_rec[c]: up to CH consecutive occurrences (in ascending occurrence
-// order) of one unique row, with their bag indices inline so that the
-// backward pass needs one record load before the gradient rows.
-// hot_rec[h] = {u -> slot, first chunk, nch, 0} for every row with more than
-// CH occurrences (its chunk partials are folded by k_bwd_hot).
+// chunk_rec[c]: one unique row with <= CH occurrences, their bag indices inline
+// (ascending occurrence order), so the backward pass needs one record load
+// before the gradient rows.
+// hot_rec[h] = {u -> slot, first sorted occurrence, occurrences, k | nseg<<16}:
+// segment k of nseg of a row with more than CH occurrences (Zipf head), at most
+// hs occurrences each.  One CTA of k_bwd folds a segment from sorted_occ; a
+// row's segments meet through fp64 partials and hot_cnt (last arriver folds).
 struct ChunkRec {
     uint32_t slot;      // unique index at dedup, Storage slot after Plan
-    uint32_t meta;      // occurrences in this chunk | 0x80000000 if the row has > 1 chunk
+    uint32_t meta;      // occurrences (1..CH)
     uint32_t bag[CH];   // table-local bag (sample) index of each occurrence
     uint32_t pad[2];
 };
@@ -61,23 +63,18 @@ struct BatchBufs {
     uint32_t *nchunks;
     uint4 *hot_rec;
     uint32_t *nhot;
+    uint32_t *hot_cnt;  // [T][nh] arrivals per hot row (at its segment-0 index)
     uint32_t *slot_u, *slot_of_occ;
     uint8_t *hit;
     uint32_t *fill_slot, *fill_row, *evict_row, *m;
     uint32_t *stats;  // [T][4] U, hits, misses, evictions
+    uint32_t *work;   // [ceil(T/64)] k_bwd dynamic work counters (zeroed at dedup)
 };
 
 struct Geometry {
     int T, N, L, D;
     int n, n1, nc, nh;    // strides
-};
-
-// Fill lists of one Plan, mirrored into pinned host memory by the plan kernel
-// for the CPU side of the transfer engine (per ring slot, per table).
-struct HostList {
-    unsigned long long *ready;  // [T] = b + 1 once table t's list of batch b is complete
-    uint32_t *m;                // [T] fills of table t
-    uint2 *ent;                 // [T][n] {missed row, previous resident (EMPTY if vacant)}
+    int hs;               // occurrences per hot-row segment (k_bwd: one CTA round)
 };
 
 struct PushArgs {
@@ -109,12 +106,14 @@ struct PushArgs {
     BatchBufs pb;
     int has_future;
     BatchBufs fb;
-    HostList hl;                 // pinned mirror of Plan(b)'s fill lists
     // graph replay: j is read from ctl[ctl_r] (b = j - F - 1, idx = idx + j*stride)
     // and ctl[(ctl_r + 1) % RING] = j + 1 is written for the next step
     long long *ctl;
     int ctl_r;
     long long idx_stride;
+    // profiling (nullable): [0,T) plan-CTA ns, [T,2T) dedup-CTA ns summed over
+    // launches, [2T] plan launches, [2T+1] dedup launches
+    unsigned long long *prof;
 };
 
 struct TrainArgs {
@@ -124,7 +123,7 @@ struct TrainArgs {
     const float *grad;   // bwd
     float *pooled;       // fwd
     float lr;
-    double *partial;     // [T][nc][D] fp64 chunk partials of hot rows
+    double *partial;     // [T][nh][D] fp64 partial sums of hot-row segments
     const unsigned long long *err;
 };
 
@@ -132,8 +131,7 @@ struct XferArgs {
     Geometry g;
     BatchBufs bb;
     float *storage;
-    float *const *host;       // [T] device-visible host table pointers
-    float *wb_stage;          // [sum m][D] victims (D2H DMA, then CPU scatter)
+    float *const *host;       // [T] device-visible (mapped) host table pointers
     const unsigned long long *err;
 };
 
@@ -189,10 +187,12 @@ __device__ __forceinline__ int find_table(const uint32_t *s_pref, int tcount, ui
 cudaError_t launch_push(const PushArgs &a, cudaStream_t s);
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s);
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s);
-cudaError_t launch_backward_hot(const TrainArgs &a, cudaStream_t s);
+int backward_hot_segment(int D);
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
                              float delta, cudaStream_t s);
-cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
+cudaError_t launch_exchange(const XferArgs &a, int ctas, cudaStream_t s);
+cudaError_t configure_exchange_kernel(int D);
+size_t exchange_smem_bytes(int D);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
 size_t push_smem_bytes(int n);
 cudaError_t configure_push_kernel();

@@ -18,7 +18,7 @@ import sys
 
 
 def sass_samples(rep, kernel, idx):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kernel}",
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kernel}", "--kernel-name-base", "demangled",
                           "--launch-skip", str(idx), "--launch-count", "1"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
@@ -52,19 +52,22 @@ def line_map(cubin, func_regex):
 def main():
     rep, kernel, cubin = sys.argv[1:4]
     idx = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    want = sys.argv[5] if len(sys.argv) > 5 else None  # mangled cubin function name
     smp = sass_samples(rep, kernel, idx)
     base = smp[0][0]
-    maps = line_map(cubin, kernel.replace("^", ""))
+    maps = line_map(cubin, ".")
     # pick the function whose instruction count matches best
-    fn = min(maps, key=lambda f: abs(len(maps[f]) - len(smp)))
+    fn = want if want else min(maps, key=lambda f: abs(len(maps[f]) - len(smp)))
     lm = maps[fn]
     by = collections.Counter()
     for a, _, n in smp:
         by[lm.get(a - base)] += n
     tot = sum(by.values()) or 1
     print(f"{fn}: {tot} samples")
+    src = open(sys.argv[6]).read().splitlines() if len(sys.argv) > 6 else []
     for line, n in by.most_common(40):
-        print(f"{n:7d} {100 * n / tot:5.1f}%  line {line}")
+        txt = src[line - 1].strip()[:90] if src and line and line <= len(src) else ""
+        print(f"{n:7d} {100 * n / tot:5.1f}%  line {line}  {txt}")
 
 
 if __name__ == "__main__":
