@@ -3,7 +3,8 @@
 
 One "step" = one pass of the whole hot path over one synthetic mini-batch:
 sp_plan (index ingest + dedup + Hit-Map probe + hit/miss + window-safe victim
-selection + bookkeeping), the fused TMA Collect/Exchange/Insert
+selection + bookkeeping), the Collect/Exchange/Insert transfer (GPU pull of
+missed rows, victims staged in HBM -> D2H DMA -> CPU scatter)
 transfer, sp_forward (EmbeddingBag gather-reduce), the MLP stand-in
 (surrogate gradient kernel) and sp_train (coalescing segmented reduce + fused
 SGD).  Workload at N=1: BASELINE configs[1], Criteo-Kaggle-shaped (the config
@@ -14,9 +15,9 @@ regime), then W warm-up steps, then K timed steps.
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config kaggle]
 
 Prints ONE JSON line on rank 0.  `value` times device-resident int32 indices
-(inputs in HBM); `e2e` times the same steps through sp_plan with indices in
-pinned host memory (H2D inside the timed region) plus a D2H read of every
-step's Plan counters.
+(inputs in HBM); `e2e` times the same steps one library call per step with
+the indices in pinned host memory (their H2D inside the timed region) plus a
+D2H read of every step's Plan counters that the host waits for.
 """
 from __future__ import annotations
 
@@ -235,7 +236,8 @@ def run_ours(args):
     P, F = cfg.window, max(cfg.window - 1, 0)
     ahead = P + F + 1
     nb_dev = pre + W + K + KP          # device-index phase (incl. the `ahead` pushed first)
-    nb_host = W + K                    # host-index (e2e) phase
+    WE = max(W, 18)                    # e2e warm-up: also (re)captures the 16 step graphs
+    nb_host = WE + K                   # host-index (e2e) phase
     nb = nb_dev + ahead + nb_host
 
     # ---- inputs: host tables (pinned), trace (device int32; host int32 part pinned)
@@ -261,7 +263,7 @@ def run_ours(args):
                      index_dtype="int32", index_on_device=False)
     pooled = torch.empty((len(mine), N, D), dtype=torch.float32, device=dev)
     grad = torch.empty_like(pooled)
-    stats_host = torch.zeros((K + W + 8, len(mine), 4), dtype=torch.int32).pin_memory()
+    stats_host = torch.zeros((K + max(W, 18) + 8, len(mine), 4), dtype=torch.int32).pin_memory()
     state = {"pushed": 0, "trained": 0}
 
     def push_dev():
@@ -368,17 +370,34 @@ def run_ours(args):
         json.dump(sp.timeline(), open(os.environ["SP_TIMELINE"], "w"))
     state["pushed"] = nb_dev + ahead
     state["trained"] = nb_dev
-    # ---- e2e: host indices through the public API, D2H of every step's Plan counters
-    for k in range(W):
-        train_step(push_host, read_stats_slot=k)
+    # ---- e2e: host indices (pinned) through the public API, and a D2H of every
+    # step's result (its Plan counters) that the host waits for and reads one
+    # step later (lag 1 keeps the pipeline full)
+    evs = [torch.cuda.Event() for _ in range(2)]
     hits_seen = []
+    h0 = nb_dev + ahead  # host_trace[i] is batch h0 + i
+
+    def e2e_one(slot):
+        if world == 1:  # the library's step call: plan kernel reads B(j) over the host link
+            sp.run_steps(host_trace, 1, pooled, grad, g_, d_, e_, first_batch=h0)
+            state["pushed"] += 1
+            sp.copy_batch_stats(state["trained"], stats_host[slot])
+            state["trained"] += 1
+        else:           # per-call API (sp_plan copies B(j) H2D) + NCCL exchange
+            train_step(push_host, read_stats_slot=slot)
+        evs[slot % 2].record(stream)
+
+    for k in range(WE):
+        e2e_one(k)
+    torch.cuda.synchronize()
 
     def e2e_step(k):
-        train_step(push_host, read_stats_slot=W + k)
-        if k >= 1:  # read the previous step's result (lag 1 keeps the pipeline full)
-            hits_seen.append(int(stats_host[W + k - 1, :, 1].sum()))
+        e2e_one(WE + k)
+        if k >= 1:
+            evs[(WE + k - 1) % 2].synchronize()
+            hits_seen.append(int(stats_host[WE + k - 1, :, 1].sum()))
     ms_e2e, _ = timed(e2e_step, K)
-    hits_seen.append(int(stats_host[W + K - 1, :, 1].sum()))
+    hits_seen.append(int(stats_host[WE + K - 1, :, 1].sum()))
     e2e_value = K / (ms_e2e / 1e3)
     st3 = sp.stats()
     idx_bytes = len(mine) * N * L * 4
@@ -402,15 +421,17 @@ def run_ours(args):
         # pooled grad in + occurrence list + per-unique segment/slot words + SGD read+write
         "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 8 * D * U,
         "surrogate": 8 * D * Tg * N,
-        # k_exchange, host-link bytes: missed rows pulled (H2D) + victims written back (D2H)
-        "transfer": 4 * D * m + 4 * D * ev,
+        # k_pullfill: missed rows pulled over the host link (zero-copy) + victims
+        # staged HBM->HBM (4*D*e read + 4*D*e written)
+        "transfer": 4 * D * m + 8 * D * ev,
+        "d2h": 4 * D * ev,                       # copy engine: staged victims
         "plan": 4 * Tg * n,
     }
     peak, peak_kind = peaks()
     traffic = load_traffic()
     total_ms = sum(kms.values()) or 1.0
     kernels = {}
-    for k in ["plan", "transfer", "forward", "backward", "surrogate"]:
+    for k in ["plan", "transfer", "d2h", "forward", "backward", "surrogate"]:
         gbs = alg_bytes[k] / (avg_ms[k] * 1e-3) / 1e9 if avg_ms[k] else None
         kernels[k] = {"avg_us": round(avg_ms[k] * 1e3, 3), "share": round(kms[k] / total_ms, 4),
                       "alg_bytes_per_launch": int(alg_bytes[k]), "alg_GBs": None if gbs is None else round(gbs, 1)}
@@ -428,7 +449,7 @@ def run_ours(args):
     train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
     xs = avg_ms["transfer"] * 1e-3
     link_GBs = 4 * D * m / xs / 1e9 if xs else None
-    wb_GBs = 4 * D * ev / xs / 1e9 if xs else None
+    wb_GBs = alg_bytes["d2h"] / (avg_ms["d2h"] * 1e-3) / 1e9 if avg_ms.get("d2h") else None
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
@@ -444,8 +465,8 @@ def run_ours(args):
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
-        "host_link": {"path": "k_exchange: TMA bulk copies, victims HBM->host rows and missed rows "
-                              "host->HBM slots, both directions in one kernel (no CPU copies)",
+        "host_link": {"path": "H2D: k_pullfill zero-copy pull of missed rows by a bounded grid; "
+                              "D2H: victims staged in HBM, copy-engine DMA, CPU scatter threads",
                       "h2d_bytes_per_batch": int(4 * D * m),
                       "h2d_GBs": None if link_GBs is None else round(link_GBs, 2),
                       "d2h_bytes_per_batch": int(4 * D * ev),
@@ -454,6 +475,9 @@ def run_ours(args):
                       "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)"},
         "kernels": kernels,
         "plan_ctas": _plan_roles(pp0, pp1),
+        "host_engine": {"scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1["host_scatter_ms"]) / KP, 2),
+                        "threads": "1 scatter thread + row-copy helpers"},
+        "host_waits_us_per_step": {"list_slot": round(1e3 * (st1["wait_list_ms"] - st0["wait_list_ms"]) / K, 2)},
         "per_step": {"uniques": round(U, 1), "misses": round(m, 1), "evictions": round(ev, 1)},
         "gpu_launches": int(gpu_launches),
         "launches_per_step": {k: v / K for k, v in launches.items()},
@@ -462,8 +486,11 @@ def run_ours(args):
         "graph_steps": st1["graph_steps"] - st0["graph_steps"],
         "e2e": {"value": round(e2e_value, 2), "unit": "iters/s", "h2d_bytes_per_step": idx_bytes,
                 "d2h_bytes_per_step": stats_bytes, "ms_per_step": round(ms_e2e / K, 5),
-                "path": "sp_plan(host int32 indices, pinned) -> H2D on the plan stream; "
-                        "sp_copy_batch_stats D2H each step, read one step later"},
+                "path": ("sp_run_steps(1 step) on pinned host int32 indices (the plan kernel reads "
+                         "the batch over the host link); sp_copy_batch_stats D2H each step, waited "
+                         "for and read one step later") if world == 1 else
+                        "sp_plan(host int32 indices, pinned) -> H2D on the plan stream; NCCL exchange; "
+                        "sp_copy_batch_stats D2H each step, waited for and read one step later"},
         "preroll_s": round(t_pre, 2),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

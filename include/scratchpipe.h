@@ -212,7 +212,9 @@ sp_status sp_get_timeline(sp_ctx *c, int32_t *kind, int64_t *batch, double *star
  *   once the trace is exhausted and the next batch cannot be planned otherwise),
  *   sp_forward(pooled), sp_surrogate_grad(pooled, grad, 0, gamma, delta),
  *   sp_train(grad, lr)
- * The first call pushes F+P+1 batches ahead.  `indices` is a DEVICE array of
+ * The first call pushes F+P+1 batches ahead.  `indices` is a DEVICE array, or
+ * a PINNED HOST array (cudaHostAlloc / registered; the plan kernel then reads
+ * each batch over the host link, so its H2D is part of the step), of
  * `num_batches` batches [T][N][L] (index width per SP_FLAG_INDEX_I32) with
  * `stride` bytes between batches; batch j of the trace is pushed at most once
  * (the loop continues from the context's counters).  pooled / grad: device

@@ -241,13 +241,15 @@ class ScratchPipe:
         self._check(lib.sp_copy_batch_stats(self._h, b, ctypes.c_void_p(host_out.data_ptr())))
 
     def run_steps(self, trace_dev, steps: int, pooled, grad, gamma: float, delta: float, lr: float,
-                  stats_out=None):
-        """C driver loop over a device-resident trace [nb][T][N][L] (see sp_run_steps)."""
-        if not trace_dev.is_cuda or not trace_dev.is_contiguous():
-            raise TypeError("trace must be a contiguous CUDA tensor")
+                  stats_out=None, first_batch: int = 0):
+        """C driver loop over a trace [nb][T][N][L] (see sp_run_steps) in device
+        memory or pinned host memory.  trace[i] is batch first_batch + i."""
+        if not trace_dev.is_contiguous() or not (trace_dev.is_cuda or trace_dev.is_pinned()):
+            raise TypeError("trace must be a contiguous CUDA tensor or pinned host tensor")
         self._last_idx = trace_dev
         stride = trace_dev[0].numel() * trace_dev.element_size()
-        self._check(lib.sp_run_steps(self._h, ctypes.c_void_p(trace_dev.data_ptr()), trace_dev.shape[0],
+        base = trace_dev.data_ptr() - first_batch * stride  # batch j at base + j*stride
+        self._check(lib.sp_run_steps(self._h, ctypes.c_void_p(base), first_batch + trace_dev.shape[0],
                                      stride, steps, ctypes.c_void_p(pooled.data_ptr()),
                                      ctypes.c_void_p(grad.data_ptr()), float(gamma), float(delta), float(lr),
                                      None if stats_out is None else ctypes.c_void_p(stats_out.data_ptr())))

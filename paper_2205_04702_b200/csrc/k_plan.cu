@@ -85,10 +85,12 @@ __device__ __forceinline__ int bit_width_u64(unsigned long long x) { return x ? 
 // ranks a contiguous run of the tile in rounds of 32 (match_any), so equal
 // digits keep their input order: stable.  Returns true if the result ends
 // in (kb, vb).
+// (histogram and per-warp digit counts shared by both instantiations)
+__shared__ uint32_t s_hist[256];
+__shared__ uint32_t s_wcnt[NW][256];
+
 template <int IPT>
 __device__ bool radix_sort_pairs(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, int n, int bits) {
-    __shared__ uint32_t s_hist[256];
-    __shared__ uint32_t s_wcnt[NW][256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int TILE = PUSH_THREADS * IPT;
     bool swapped = false;
@@ -190,8 +192,8 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
     }
     // D2: sort by id (stable: occurrences stay ascending within an id)
     const int bits = bit_width_u64((unsigned long long)(R - 1));
-    const bool sw = small ? radix_sort_pairs<4>(ka, va, kb, vb, n, bits)
-                          : radix_sort_pairs<8>(ka, va, kb, vb, n, bits);
+    const bool sw = small ? radix_sort_pairs<2048 / PUSH_THREADS>(ka, va, kb, vb, n, bits)
+                          : radix_sort_pairs<4096 / PUSH_THREADS>(ka, va, kb, vb, n, bits);
     const uint32_t *keys = sw ? kb : ka;
     const uint32_t *vals = sw ? vb : va;
     __syncthreads();
@@ -384,6 +386,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
     uint32_t *fill_row = pb.fill_row + (size_t)t * n;
     uint32_t *evict_row = pb.evict_row + (size_t)t * n;
     uint32_t nev = 0;
+    uint2 *hent = A.hl.ent + (size_t)t * n;  // pinned host mirror (zero-copy, ~8 B per fill)
     for (uint32_t k = tid; k < m; k += blockDim.x) {
         const uint32_t u = miss_u[k], s = victims[k], id = uniq_id[u];
         const uint32_t old = A.resident[s];
@@ -399,10 +402,18 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
         fill_slot[k] = s;
         fill_row[k] = id;
         evict_row[k] = old;
+        hent[k] = make_uint2(id, old);
     }
     uint32_t ev_total;
     (void)block_scan(nev, &ev_total);  // barriers: P4 writes visible below
-    if (tid == 0) pb.m[t] = m;  // fills of table t for k_exchange
+    if (tid == 0) {
+        pb.m[t] = m;  // device copy for k_pullfill, published before the ready flag
+        A.hl.m[t] = m;
+        // the CTA's host-list writes precede this fence through the barrier
+        // above (causality order), so one system-scope fence publishes them all
+        __threadfence_system();
+        *(volatile unsigned long long *)&A.hl.ready[t] = (unsigned long long)(b + 1);
+    }
 
     // P5: LRU log append (after an in-place compaction if it would overflow)
     const unsigned long long head = s_head;
@@ -476,7 +487,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(PUSH_THREADS, 2) k_push(PushArgs A) {
+__global__ void __launch_bounds__(PUSH_THREADS, PUSH_THREADS >= 1024 ? 1 : 2) k_push(PushArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (*A.err != NO_ERR) return;  // poisoned: nothing more is planned
     const int T = A.g.T;

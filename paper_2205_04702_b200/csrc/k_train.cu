@@ -41,47 +41,57 @@ __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
 }  // namespace
 
 // ---------------------------------------------------------------- forward
-// G lanes per bag, VPL float4 per lane (D/4 = G*VPL).
+// G lanes per bag, VPL float4 per lane (D/4 = G*VPL).  A lane group folds BU
+// bags at a time (bags g, g+S, ..., S = all groups of the grid): their slot
+// indices, then their rows for lookup position p, are all in flight together,
+// so even L = 1 (one row per bag) keeps BU rows per group outstanding.  Each
+// bag is still a left fold in ascending p (bit-exact with the oracle).
 template <int G, int VPL>
 __global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
     if (*A.err != NO_ERR) return;
+    constexpr int BU = VPL >= 4 ? 1 : (VPL == 2 ? 2 : 4);
     const int L = A.g.L, D4 = A.g.D / 4;
     const long long nbags = (long long)A.g.T * A.g.N;
     const int gpb = blockDim.x / G;
     const int lane = threadIdx.x % G;
-    const float4 *st = reinterpret_cast<const float4 *>(A.storage);
-    float4 *out = reinterpret_cast<float4 *>(A.pooled);
-    for (long long bag = (long long)blockIdx.x * gpb + threadIdx.x / G; bag < nbags;
-         bag += (long long)gridDim.x * gpb) {
-        const uint32_t *so = A.bb.slot_of_occ + bag * L;
-        float4 acc[VPL];
-        {
-            const uint32_t s = __ldg(so);
+    const float4 *st = reinterpret_cast<const float4 *>(A.storage) + lane;
+    float4 *out = reinterpret_cast<float4 *>(A.pooled) + lane;
+    const long long S = (long long)gridDim.x * gpb;
+    for (long long bag0 = (long long)blockIdx.x * gpb + threadIdx.x / G; bag0 < nbags; bag0 += BU * S) {
+        const uint32_t *so[BU];
+        bool ok[BU];
+        float4 acc[BU][VPL];
 #pragma unroll
-            for (int v = 0; v < VPL; v++) acc[v] = ldg4(st + (size_t)s * D4 + lane + v * G);
+        for (int u = 0; u < BU; u++) {
+            const long long bag = bag0 + u * S;
+            ok[u] = bag < nbags;
+            so[u] = A.bb.slot_of_occ + (ok[u] ? bag : 0) * L;
         }
-        int p = 1;
-        for (; p + 4 <= L; p += 4) {  // 4 rows in flight, folded in p order
-            uint32_t s[4];
+        uint32_t s[BU];
 #pragma unroll
-            for (int q = 0; q < 4; q++) s[q] = __ldg(so + p + q);
-            float4 r[4][VPL];
+        for (int u = 0; u < BU; u++) s[u] = __ldg(so[u]);
 #pragma unroll
-            for (int q = 0; q < 4; q++)
+        for (int u = 0; u < BU; u++)
 #pragma unroll
-                for (int v = 0; v < VPL; v++) r[q][v] = ldg4(st + (size_t)s[q] * D4 + lane + v * G);
+            for (int v = 0; v < VPL; v++) acc[u][v] = ldg4(st + (size_t)s[u] * D4 + v * G);
+        for (int p = 1; p < L; p++) {
 #pragma unroll
-            for (int q = 0; q < 4; q++)
+            for (int u = 0; u < BU; u++) s[u] = __ldg(so[u] + p);
+            float4 r[BU][VPL];
 #pragma unroll
-                for (int v = 0; v < VPL; v++) add4(acc[v], r[q][v]);
+            for (int u = 0; u < BU; u++)
+#pragma unroll
+                for (int v = 0; v < VPL; v++) r[u][v] = ldg4(st + (size_t)s[u] * D4 + v * G);
+#pragma unroll
+            for (int u = 0; u < BU; u++)
+#pragma unroll
+                for (int v = 0; v < VPL; v++) add4(acc[u][v], r[u][v]);
         }
-        for (; p < L; p++) {
-            const uint32_t s = __ldg(so + p);
 #pragma unroll
-            for (int v = 0; v < VPL; v++) add4(acc[v], ldg4(st + (size_t)s * D4 + lane + v * G));
-        }
+        for (int u = 0; u < BU; u++)
+            if (ok[u])
 #pragma unroll
-        for (int v = 0; v < VPL; v++) __stcs(out + bag * D4 + lane + v * G, acc[v]);
+                for (int v = 0; v < VPL; v++) __stcs(out + (bag0 + u * S) * D4 + v * G, acc[u][v]);
     }
 }
 

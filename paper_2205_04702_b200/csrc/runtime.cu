@@ -1,23 +1,28 @@
 // runtime.cu — host runtime behind include/scratchpipe.h.
 //
 // Pipeline schedule: PAPER.md Fig. 8 re-expressed with CUDA
-// streams and events instead of lock-step cycles:
+// streams, events and a native transfer-engine thread instead of lock-step
+// cycles:
 //
 //   plan stream     push(j): [H2D of B(j)] -> k_push: dedup B(j) beside
-//                   Plan(b = j-F-1) -> record ev_plan[b]
+//                   Plan(b = j-F-1) -> record ev_plan[b]; Plan(b) also
+//                   mirrors its fill lists into pinned host memory
 //   transfer stream Transfer(b) once Train(b-P-1) is enqueued (past window,
-//                   P:840-861): waits ev_plan[b] and ev_train[b-P-1] ->
-//                   k_exchange ([Collect] + [Exchange] + [Insert]: victims
-//                   written back to their host rows, missed rows pulled into
-//                   the freed slots, both by TMA bulk copies) -> ev_xfer[b].
-//                   Transfers run in batch order, so a row written back at
-//                   Transfer(b) lands before any later pull of it (RAW-4)
+//                   P:840-861): waits ev_plan[b], ev_train[b-P-1] and, on the
+//                   GPU, for the pinned counter "scattered >= b-F" (RAW-4,
+//                   the CPU write-back of batch b-F-1 has landed)
+//                   -> k_pullfill ([Collect] + [Insert] on the GPU side:
+//                   victims staged in HBM, missed rows pulled by zero-copy
+//                   reads into the freed slots) -> record ev_xfer[b]
+//   transfer engine (scatter thread + row-copy helpers): for b in order,
+//                   D2H DMA of the staged victims ([Exchange]) and CPU scatter
+//                   into the host tables ([Insert]), then scattered = b+1
 //   compute stream  forward(b) waits ev_xfer[b]; train(b) -> record ev_train[b]
 //
-// No host thread moves rows and the caller's thread never synchronises in
-// the steady state.
+// No host synchronisation on the caller's thread in the steady state.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <immintrin.h>
 #include <sys/mman.h>
 
 #include <algorithm>
@@ -28,6 +33,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/scratchpipe.h"
@@ -49,6 +55,91 @@ struct TimelineRec {
     double start_ms, end_ms;  // relative to the profiling reference event
 };
 
+// Fork-join pool of spinning threads copying rows between host tables and
+// pinned staging (the CPU side of Collect / Insert).
+struct RowPool {
+    std::vector<std::thread> th;
+    std::atomic<uint64_t> gen{0};
+    std::atomic<long> next{0};
+    std::atomic<int> done{0};
+    std::atomic<bool> stop{false};
+    const float *const *src = nullptr;
+    float *const *dst = nullptr;
+    long n = 0;
+    size_t bytes = 0;
+
+    static constexpr long CHUNK = 16;
+
+    void run_chunks() {
+        for (;;) {
+            const long i0 = next.fetch_add(CHUNK, std::memory_order_relaxed);
+            if (i0 >= n) break;
+            const long i1 = std::min(n, i0 + CHUNK);
+            // all source lines of the chunk in flight first (random host rows:
+            // memory-level parallelism, not bandwidth, bounds a core here)
+            for (long i = i0; i < i1; i++) {
+                const char *p = reinterpret_cast<const char *>(src[i]);
+                for (size_t o = 0; o < bytes; o += 64) __builtin_prefetch(p + o, 0, 2);
+            }
+            // non-temporal stores: a random destination row costs no
+            // read-for-ownership, and staging never pollutes the caches
+            for (long i = i0; i < i1; i++) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(src[i]) | reinterpret_cast<uintptr_t>(dst[i]);
+                if ((a & 15) == 0 && (bytes & 15) == 0) {
+                    const __m128i *sp = reinterpret_cast<const __m128i *>(src[i]);
+                    __m128i *dp = reinterpret_cast<__m128i *>(dst[i]);
+                    for (size_t q = 0; q < bytes / 16; q++) _mm_stream_si128(dp + q, _mm_load_si128(sp + q));
+                } else {
+                    std::memcpy(dst[i], src[i], bytes);
+                }
+            }
+            _mm_sfence();
+        }
+    }
+
+    void helper() {
+        uint64_t seen = 0;
+        int idle = 0;
+        while (!stop.load(std::memory_order_relaxed)) {
+            const uint64_t g = gen.load(std::memory_order_acquire);
+            if (g == seen) {
+                if (++idle > 4096) std::this_thread::yield();
+                else _mm_pause();
+                continue;
+            }
+            idle = 0;
+            seen = g;
+            run_chunks();
+            done.fetch_add(1, std::memory_order_acq_rel);
+        }
+    }
+
+    void start(int nthreads) {
+        for (int i = 0; i < nthreads; i++) th.emplace_back([this] { helper(); });
+    }
+
+    void copy(const float *const *s, float *const *d, long count, size_t row_bytes) {
+        if (count <= 0) return;
+        src = s;
+        dst = d;
+        n = count;
+        bytes = row_bytes;
+        next.store(0, std::memory_order_relaxed);
+        done.store(0, std::memory_order_relaxed);
+        gen.fetch_add(1, std::memory_order_acq_rel);
+        run_chunks();
+        while (done.load(std::memory_order_acquire) < (int)th.size()) _mm_pause();
+    }
+
+    void shutdown() {
+        stop = true;
+        for (auto &t : th) t.join();
+        th.clear();
+    }
+};
+
+enum : int { K_H2D = SP_K_H2D, K_D2H = SP_K_D2H };
+
 }  // namespace
 
 struct sp_ctx {
@@ -66,6 +157,7 @@ struct sp_ctx {
     Geometry g{};
     cudaStream_t compute = nullptr, plan_s = nullptr, xfer_s = nullptr;
     cudaStream_t own_plan_s = nullptr, own_xfer_s = nullptr;  // created by the library
+    cudaStream_t d2h_s = nullptr;  // victims' D2H on its own stream (other copy engine)
     // device memory
     std::vector<void *> allocs;
     unsigned long long *d_row_off = nullptr;
@@ -74,7 +166,6 @@ struct sp_ctx {
     uint32_t *d_hitmap = nullptr, *d_resident = nullptr;
     int32_t *d_last_use = nullptr, *d_next_need = nullptr;
     float *d_storage = nullptr;
-    double *d_partial = nullptr;  // [T][nh][D] hot-row segment partials (k_bwd)
     uint32_t *d_log_slot = nullptr;
     int32_t *d_log_stamp = nullptr;
     unsigned long long *d_log_base = nullptr, *d_log_cap = nullptr, *d_log_head = nullptr,
@@ -83,12 +174,23 @@ struct sp_ctx {
     unsigned long long *d_pprof = nullptr;  // k_push per-CTA timing [2T+2] (profiling only)
     uint32_t *d_miss_u = nullptr, *d_victims = nullptr;
     uint32_t *d_sort_tmp = nullptr;
+    double *d_partial = nullptr;  // [T][nh][D] hot-row segment partials (k_bwd)
     float **d_host = nullptr;
     void *d_idx[RING] = {};
     BatchBufs ring[RING];
-    int xchg_ctas = 16;                        // k_exchange grid (one warp per CTA)
-    bool diag_no_xchg = false;                 // SP_DIAG_NO_XCHG=1 (timing diagnostic only)
+    // transfer staging of the victims: XSR slots of sum(m) rows (<= T*n)
+    int XSR = 4;
+    float *d_wb = nullptr;                     // device [XSR][T*n][D]
+    float *h_wb = nullptr;                     // pinned [XSR][T*n][D]
+    unsigned long long *h_scat = nullptr;      // pinned mapped: batches scattered
+    unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
+    int pull_ctas = 8;
     long long xfer_enq = 0;                    // transfers enqueued (caller's thread)
+    // pinned host mirror of the fill lists, per ring slot
+    unsigned long long *hl_ready = nullptr;    // [RING][T]
+    uint32_t *hl_m = nullptr;                  // [RING][T]
+    uint2 *hl_ent = nullptr;                   // [RING][T][n]
+    HostList hl_dev[RING];                     // mapped device pointers of the same
     // pinned index staging
     void *h_stage = nullptr;
     unsigned long long *h_err = nullptr;      // exact device error key (sync copies)
@@ -96,12 +198,23 @@ struct sp_ctx {
     unsigned long long *d_errflag = nullptr;  // device alias of h_errflag
     size_t idx_bytes = 0;
     // events
-    cudaEvent_t ev_plan[RING] = {}, ev_xfer[RING] = {}, ev_train[RING] = {}, ev_h2d[RING] = {};
+    cudaEvent_t ev_plan[RING] = {}, ev_xfer[RING] = {}, ev_d2h[RING] = {}, ev_train[RING] = {},
+                ev_h2d[RING] = {};
     cudaEvent_t ev_user = nullptr;
     bool h2d_used[RING] = {};
     // schedule state (caller's thread)
     long long pushed = 0, planned = 0, forwarded = 0, trained = 0;
     bool eod = false, fwd_pending = false;
+    // published to the transfer engine
+    std::atomic<long long> trained_pub{0};
+    std::atomic<long long> x_enqueued{0}, x_scattered{0};
+    std::atomic<int> x_error{0};
+    std::atomic<long long> x_gather_ns{0}, x_scatter_ns{0}, x_rows_g{0}, x_rows_s{0};
+    std::string x_errmsg;
+    std::thread scatter_worker;
+    std::atomic<bool> stop{false};
+    RowPool spool;  // scatter helpers
+    int host_threads = 6;
     // errors
     sp_status poisoned = SP_OK;
     std::string err = "no error";
@@ -135,6 +248,7 @@ struct sp_ctx {
     } gkey;
     long long g_next_j = -1;                    // j the device chain expects next
     long long graph_steps = 0;
+    long long wait_xfer_ns = 0, wait_list_ns = 0;  // caller-thread waits on the engine
 };
 
 namespace {
@@ -281,6 +395,11 @@ sp_status check_async_error(sp_ctx *c) {
         c->err = buf;
         return c->poisoned;
     }
+    if (c->x_error.load(std::memory_order_acquire)) {
+        c->poisoned = SP_ERR_CUDA;
+        c->err = "transfer engine: " + c->x_errmsg;
+        return c->poisoned;
+    }
     return SP_OK;
 }
 
@@ -292,6 +411,18 @@ sp_status sync_error(sp_ctx *c) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->plan_s);
     if (e != cudaSuccess) return cuda_fail(c, e, "sync_error");
     return check_async_error(c);
+}
+
+// spin until pred() (the transfer engine made progress) or an error shows up
+template <typename Pred>
+sp_status wait_engine(sp_ctx *c, Pred pred) {
+    int idle = 0;
+    while (!pred()) {
+        if (sp_status s = check_async_error(c)) return s;
+        if (++idle > 1024) std::this_thread::yield();
+        else _mm_pause();
+    }
+    return SP_OK;
 }
 
 PushArgs push_args(sp_ctx *c) {
@@ -323,12 +454,22 @@ PushArgs push_args(sp_ctx *c) {
     return a;
 }
 
+// The host-list ring slot of Plan(b) is reused by Plan(b + RING): the transfer
+// engine must be done with batch b (gathered and scattered) first.
+sp_status wait_list_slot(sp_ctx *c, long long b) {
+    const long long prev = b - RING;
+    if (prev < 0) return SP_OK;
+    return wait_engine(c, [&] { return c->x_scattered.load(std::memory_order_acquire) > prev; });
+}
+
 sp_status enqueue_plan_only(sp_ctx *c, long long b) {
+    if (sp_status s = wait_list_slot(c, b)) return s;
     PushArgs a = push_args(c);
     a.has_new = 0;
     a.do_plan = 1;
     a.b = b;
     a.pb = c->ring[b % RING];
+    a.hl = c->hl_dev[b % RING];
     a.has_future = (b + c->F < c->pushed) ? 1 : 0;  // future window truncates at the end
     a.fb = c->ring[(b + c->F) % RING];
     CK(launch(c, SP_K_PLAN, b, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
@@ -347,7 +488,125 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     return a;
 }
 
-// --------------------------------------------------------------- transfer
+// --------------------------------------------------------------- transfer engine
+void engine_fail(sp_ctx *c, cudaError_t e, const char *where) {
+    c->x_errmsg = std::string(where) + ": " + cudaGetErrorString(e);
+    c->x_error.store(1, std::memory_order_release);
+}
+
+// [Insert] CPU scatter of batch s's victims into the host tables once its D2H
+// has landed, in batch order, on its own thread: it overlaps the gather of
+// later batches (rows evicted at s are not in B(s+1..s+F)).
+void scatter_main(sp_ctx *c) {
+    cudaSetDevice(c->device);
+    const size_t rowb = (size_t)c->D * sizeof(float);
+    const size_t slab = (size_t)c->T * c->n * c->D;
+    std::vector<const float *> src;
+    std::vector<float *> dst;
+    std::vector<uint32_t> pref(c->T + 1);
+    long long s = 0, d = 0;  // next batch to scatter / to issue the D2H for
+    int idle = 0;
+    auto ready = [&](long long b) {
+        const int r = (int)(b % RING);
+        for (int t = 0; t < c->T; t++)
+            if (((volatile unsigned long long *)c->hl_ready)[(size_t)r * c->T + t] != (unsigned long long)(b + 1))
+                return false;
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return true;
+    };
+    auto rows_of = [&](long long b) {
+        const int r = (int)(b % RING);
+        pref[0] = 0;
+        for (int t = 0; t < c->T; t++) pref[t + 1] = pref[t] + c->hl_m[(size_t)r * c->T + t];
+        return (size_t)pref[c->T];
+    };
+    while (!c->stop.load(std::memory_order_relaxed)) {
+        if (*(volatile unsigned long long *)c->h_errflag) break;
+        bool progressed = false;
+        // [Exchange] D2H of the staged victims of batch d once Transfer(d) is
+        // enqueued (ev_xfer exists) and its lists are known; the staging slot
+        // d % XSR is free because Transfer(d) waited for scatter(d-F-1)
+        if (d < s + c->XSR && d < c->x_enqueued.load(std::memory_order_acquire) && ready(d)) {
+            const int r = (int)(d % RING);
+            const size_t bytes = rows_of(d) * rowb;
+            cudaError_t e = cudaStreamWaitEvent(c->d2h_s, c->ev_xfer[r], 0);
+            if (e == cudaSuccess && bytes)
+                e = launch(c, K_D2H, d, c->d2h_s, [&] {
+                    return cudaMemcpyAsync(c->h_wb + (size_t)(d % c->XSR) * slab,
+                                           c->d_wb + (size_t)(d % c->XSR) * slab, bytes,
+                                           cudaMemcpyDeviceToHost, c->d2h_s);
+                });
+            if (e == cudaSuccess) e = cudaEventRecord(c->ev_d2h[r], c->d2h_s);
+            if (e != cudaSuccess) {
+                engine_fail(c, e, "D2H enqueue");
+                break;
+            }
+            d++;
+            progressed = true;
+        }
+        // [Insert] CPU scatter of batch s once its D2H has landed, in order
+        if (s < d) {
+            cudaError_t q = cudaEventQuery(c->ev_d2h[s % RING]);
+            if (q == cudaSuccess) {
+                const int r = (int)(s % RING);
+                rows_of(s);
+                src.clear();
+                dst.clear();
+                const float *wb = c->h_wb + (size_t)(s % c->XSR) * slab;
+                for (int t = 0; t < c->T; t++) {
+                    const uint2 *ent = c->hl_ent + ((size_t)r * c->T + t) * c->n;
+                    for (uint32_t k = 0; k < pref[t + 1] - pref[t]; k++)
+                        if (ent[k].y != EMPTY) {
+                            src.push_back(wb + (size_t)(pref[t] + k) * c->D);
+                            dst.push_back(c->host[t] + (size_t)ent[k].y * c->D);
+                        }
+                }
+                const auto t0 = std::chrono::steady_clock::now();
+                c->spool.copy(src.data(), dst.data(), (long)src.size(), rowb);
+                c->x_scatter_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                       std::chrono::steady_clock::now() - t0).count();
+                c->x_rows_s += (long long)src.size();
+                s++;
+                c->x_scattered.store(s, std::memory_order_release);
+                std::atomic_thread_fence(std::memory_order_seq_cst);
+                *(volatile unsigned long long *)c->h_scat = (unsigned long long)s;  // GPU wait-value
+                progressed = true;
+            } else if (q != cudaErrorNotReady) {
+                engine_fail(c, q, "ev_d2h");
+                break;
+            }
+        }
+        if (progressed) {
+            idle = 0;
+        } else if (++idle > 2048) {
+            std::this_thread::yield();
+        } else {
+            _mm_pause();
+        }
+    }
+}
+
+void stop_engine(sp_ctx *c) {
+    c->stop = true;
+    if (c->scatter_worker.joinable()) c->scatter_worker.join();
+    c->spool.shutdown();
+}
+
+// stream wait on a 64-bit pinned counter (cuStreamWaitValue64 through the
+// runtime's driver entry point: no link-time dependency on libcuda)
+typedef CUresult (*wait_value64_fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+wait_value64_fn wait_value64() {
+    static wait_value64_fn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<wait_value64_fn>(p);
+    }
+    return fn;
+}
+
 // Enqueue every Transfer(b) whose preconditions exist: Plan(b) enqueued and
 // Train(b-P-1) enqueued (its event recorded).  Caller's thread only.
 sp_status pump(sp_ctx *c) {
@@ -358,16 +617,25 @@ sp_status pump(sp_ctx *c) {
         cudaStream_t xs = c->xfer_s;
         CK(cudaStreamWaitEvent(xs, c->ev_plan[r], 0));
         if (dep >= 0) CK(cudaStreamWaitEvent(xs, c->ev_train[dep % RING], 0));
+        // RAW-4 + staging reuse: the CPU write-back of batch b-F-1 has landed
+        const long long need = b - c->F;  // scattered >= b-F
+        if (need > 0) {
+            wait_value64_fn wv = wait_value64();
+            if (!wv) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 unavailable");
+            CUresult cr = wv((CUstream)xs, (CUdeviceptr)c->d_scat, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ);
+            if (cr != CUDA_SUCCESS) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 failed");
+        }
         XferArgs a{};
         a.g = c->g;
         a.bb = c->ring[r];
         a.storage = c->d_storage;
         a.host = c->d_host;
+        a.wb_stage = c->d_wb + (size_t)(b % c->XSR) * c->T * c->n * c->D;
         a.err = c->d_err;
-        if (c->diag_no_xchg) a.g.T = 0;  // diagnostic: launch, move nothing
-        CK(launch(c, SP_K_TRANSFER, b, xs, [&] { return launch_exchange(a, c->xchg_ctas, xs); }));
+        CK(launch(c, SP_K_TRANSFER, b, xs, [&] { return launch_pullfill(a, c->pull_ctas, xs); }));
         CK(cudaEventRecord(c->ev_xfer[r], xs));
         c->xfer_enq = b + 1;
+        c->x_enqueued.store(b + 1, std::memory_order_release);
     }
     return SP_OK;
 }
@@ -376,10 +644,12 @@ void drop_graphs(sp_ctx *c);
 
 void destroy_all(sp_ctx *c) {
     if (!c) return;
+    stop_engine(c);
     drop_graphs(c);
     cudaSetDevice(c->device);
     if (c->plan_s) cudaStreamSynchronize(c->plan_s);
     if (c->xfer_s) cudaStreamSynchronize(c->xfer_s);
+    if (c->d2h_s) cudaStreamSynchronize(c->d2h_s);
     cudaStreamSynchronize(c->compute);
     {
         std::lock_guard<std::mutex> lk(c->prof_mu);
@@ -387,17 +657,19 @@ void destroy_all(sp_ctx *c) {
         for (auto e : c->ev_pool) cudaEventDestroy(e);
     }
     for (int r = 0; r < RING; r++)
-        for (cudaEvent_t e : {c->ev_plan[r], c->ev_xfer[r], c->ev_train[r], c->ev_h2d[r]})
+        for (cudaEvent_t e : {c->ev_plan[r], c->ev_xfer[r], c->ev_d2h[r], c->ev_train[r], c->ev_h2d[r]})
             if (e) cudaEventDestroy(e);
     if (c->ev_user) cudaEventDestroy(c->ev_user);
     if (c->prof_ref) cudaEventDestroy(c->prof_ref);
     for (void *p : c->allocs) cudaFree(p);
-    for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag})
+    for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb,
+                    (void *)c->hl_ready, (void *)c->hl_m, (void *)c->hl_ent})
         if (p) cudaFreeHost(p);
     if (c->registered)
         for (int t = 0; t < c->T; t++) cudaHostUnregister(c->host[t]);
     if (c->own_plan_s) cudaStreamDestroy(c->own_plan_s);
     if (c->own_xfer_s) cudaStreamDestroy(c->own_xfer_s);
+    if (c->d2h_s) cudaStreamDestroy(c->d2h_s);
     if (c->cap_s) cudaStreamDestroy(c->cap_s);
     (void)cudaGetLastError();
     delete c;
@@ -495,8 +767,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     }
     for (int t = 0; t < c->T; t++) c->slot_base[t + 1] = c->slot_base[t] + (uint32_t)c->slots[t];
     c->hit_total = c->row_off[c->T];
-    if (const char *e = getenv("SP_XCHG_CTAS")) c->xchg_ctas = std::max(1, atoi(e));
-    if (const char *e = getenv("SP_DIAG_NO_XCHG")) c->diag_no_xchg = atoi(e) == 1;
+    c->XSR = std::max(4, c->F + 2);  // >= F+1: Transfer(b) waits for scatter(b-F-1) >= b-XSR
+    c->host_threads = d->host_threads > 0 ? d->host_threads : 6;
+    c->pull_ctas = 8;
+    if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
 
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) {
@@ -538,30 +812,27 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
             return bail(SP_ERR_INVALID_ARG);  // not pinned / registered
         }
         hdev[t] = static_cast<float *>(p);
-        // TMA bulk copies move whole rows: 16-byte aligned row starts
-        if ((reinterpret_cast<uintptr_t>(p) & 15) != 0) return bail(SP_ERR_INVALID_ARG);
     }
-    {   // Plan and Transfer are long serial chains of few CTAs: their CTAs are
-        // scheduled ahead of the wide Train grids when SM slots free up
+    {   // Plan is the serial critical chain: its CTAs get scheduled first
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         CKC(cudaStreamCreateWithPriority(&c->plan_s, cudaStreamNonBlocking, hi));
-        const char *xp = getenv("SP_XFER_PRIO");
-        CKC(cudaStreamCreateWithPriority(&c->xfer_s, cudaStreamNonBlocking, (xp && atoi(xp) == 0) ? lo : hi));
+        const char *xp = getenv("SP_XFER_PRIO");  // 1: transfer CTAs also scheduled first
+        CKC(cudaStreamCreateWithPriority(&c->xfer_s, cudaStreamNonBlocking, (xp && atoi(xp) == 1) ? hi : lo));
         c->own_plan_s = c->plan_s;
         c->own_xfer_s = c->xfer_s;
-        // diagnostic: SP_DIAG_SERIAL=1 runs every stage on the caller's stream
-        // (no stage overlap) to measure kernel durations free of interference
+        // diagnostic: SP_DIAG_SERIAL=1 runs every GPU stage on the caller's
+        // stream (no stage overlap) to time kernels free of interference
         if (const char *ds = getenv("SP_DIAG_SERIAL"))
             if (atoi(ds) == 1) c->plan_s = c->xfer_s = c->compute;
     }
+    CKC(cudaStreamCreateWithFlags(&c->d2h_s, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithFlags(&c->cap_s, cudaStreamNonBlocking));
     for (int r = 0; r < RING; r++)
-        for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_train[r], &c->ev_h2d[r]})
+        for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_d2h[r], &c->ev_train[r], &c->ev_h2d[r]})
             CKC(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
     CKC(configure_push_kernel());
-    CKC(configure_exchange_kernel(c->D));
 
     // device allocations
     const size_t Tn = (size_t)c->T * c->n;
@@ -591,14 +862,15 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_log_tail, c->T));
     CKC(dalloc(c, &c->d_err, 1));
     CKC(dalloc(c, &c->d_cum, 4));
-    CKC(dalloc(c, &c->d_partial, (size_t)c->T * c->g.nh * c->D));
-    CKC(dalloc(c, &c->d_pprof, 2 * (size_t)c->T + 2));
-    CKC(cudaMemset(c->d_pprof, 0, (2 * (size_t)c->T + 2) * sizeof(unsigned long long)));
     CKC(dalloc(c, &c->d_miss_u, Tn));
     CKC(dalloc(c, &c->d_victims, Tn));
     if (c->n > SMEM_SORT_MAX) CKC(dalloc(c, &c->d_sort_tmp, 4 * Tn));
+    CKC(dalloc(c, &c->d_partial, (size_t)c->T * c->g.nh * c->D));
+    CKC(dalloc(c, &c->d_pprof, 2 * (size_t)c->T + 2));
+    CKC(cudaMemset(c->d_pprof, 0, (2 * (size_t)c->T + 2) * sizeof(unsigned long long)));
     CKC(dalloc(c, &c->d_host, c->T));
     CKC(dalloc(c, &c->d_ctl, RING));
+    CKC(dalloc(c, &c->d_wb, (size_t)c->XSR * Tn * c->D));
     c->idx_bytes = Tn * ((c->flags & SP_FLAG_INDEX_I32) ? 4 : 8);
     for (int r = 0; r < RING; r++) {
         cudaError_t st;
@@ -615,7 +887,27 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaHostAlloc((void **)&c->h_errflag, sizeof(unsigned long long), cudaHostAllocMapped));
     *c->h_errflag = 0;
     CKC(cudaHostGetDevicePointer((void **)&c->d_errflag, c->h_errflag, 0));
-
+    CKC(cudaHostAlloc((void **)&c->h_scat, sizeof(unsigned long long), cudaHostAllocMapped));
+    *c->h_scat = 0;
+    CKC(cudaHostGetDevicePointer((void **)&c->d_scat, c->h_scat, 0));
+    CKC(cudaHostAlloc((void **)&c->h_wb, (size_t)c->XSR * Tn * c->D * sizeof(float), cudaHostAllocDefault));
+    CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
+    CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
+    CKC(cudaHostAlloc((void **)&c->hl_ent, (size_t)RING * Tn * sizeof(uint2), cudaHostAllocMapped));
+    std::memset(c->hl_ready, 0, (size_t)RING * c->T * sizeof(unsigned long long));
+    {
+        unsigned long long *dr;
+        uint32_t *dm;
+        uint2 *de;
+        CKC(cudaHostGetDevicePointer((void **)&dr, c->hl_ready, 0));
+        CKC(cudaHostGetDevicePointer((void **)&dm, c->hl_m, 0));
+        CKC(cudaHostGetDevicePointer((void **)&de, c->hl_ent, 0));
+        for (int r = 0; r < RING; r++) {
+            c->hl_dev[r].ready = dr + (size_t)r * c->T;
+            c->hl_dev[r].m = dm + (size_t)r * c->T;
+            c->hl_dev[r].ent = de + (size_t)r * Tn;
+        }
+    }
 
     // initial state
     std::vector<long long> rows64(c->rows.begin(), c->rows.end());
@@ -646,6 +938,9 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaMemset(c->d_storage, 0, (size_t)c->S_total * c->D * sizeof(float)));
     CKC(cudaDeviceSynchronize());
 #undef CKC
+    // transfer engine: helpers + worker
+    c->spool.start(c->host_threads);
+    c->scatter_worker = std::thread(scatter_main, c);
     *out = c;
     return SP_OK;
 }
@@ -662,6 +957,8 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     // Plan(b) runs beside dedup(j) once B(b+F) = B(j-1) has been deduped
     const long long b = j - c->F - 1;
     const bool do_plan = b >= 0 && b == c->planned;
+    if (do_plan)
+        if (sp_status s = wait_list_slot(c, b)) return s;
     if (j >= RING) CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));  // ring slot r reused
     const void *dev_idx;
     if (on_device) {
@@ -688,6 +985,7 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     if (do_plan) {
         a.b = b;
         a.pb = c->ring[b % RING];
+        a.hl = c->hl_dev[b % RING];
         a.has_future = 1;
         a.fb = c->ring[(b + c->F) % RING];
     }
@@ -792,6 +1090,7 @@ sp_status sp_train(sp_ctx *c, const float *grad, float lr) {
     }));
     CK(cudaEventRecord(c->ev_train[b % RING], c->compute));
     c->trained = b + 1;
+    c->trained_pub.store(b + 1, std::memory_order_release);
     c->fwd_pending = false;
     return pump(c);
 }
@@ -813,9 +1112,12 @@ sp_status sp_flush(sp_ctx *c) {
     if (c->trained != c->pushed || c->fwd_pending)
         return fail(c, SP_ERR_STATE, "sp_flush: every pushed batch must be trained first");
     CK(cudaSetDevice(c->device));
-    // every Transfer has written its victims back once the streams drain
+    // the transfer engine writes back every victim of every batch
+    if (sp_status s = wait_engine(c, [&] { return c->x_scattered.load(std::memory_order_acquire) >= c->planned; }))
+        return s;
     CK(cudaStreamSynchronize(c->plan_s));
     CK(cudaStreamSynchronize(c->xfer_s));
+    CK(cudaStreamSynchronize(c->d2h_s));
     CK(cudaStreamSynchronize(c->compute));
     if (sp_status s = sync_error(c)) return s;
     FlushArgs a{};
@@ -860,6 +1162,7 @@ sp_status capture_step(sp_ctx *c, int r) {
     a.idx = k.trace;
     a.nb = c->ring[rj];
     a.pb = c->ring[rb];
+    a.hl = c->hl_dev[rb];
     a.fb = c->ring[rf];
     a.ctl = c->d_ctl;
     a.ctl_r = r;
@@ -897,6 +1200,10 @@ sp_status graph_step(sp_ctx *c) {
         if (sp_status s = capture_step(c, r)) return s;
     if (c->g_next_j != j)  // (re)enter graph mode: seed the device batch-index chain
         CK(cudaMemcpyAsync(c->d_ctl + r, &j, sizeof j, cudaMemcpyHostToDevice, c->plan_s));
+    auto t0 = std::chrono::steady_clock::now();
+    if (sp_status s = wait_list_slot(c, b)) return s;
+    auto t1 = std::chrono::steady_clock::now();
+    c->wait_list_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
     CK(cudaGraphLaunch(c->gplan[r], c->plan_s));
     c->pushed = j + 1;
     c->planned = b + 1;
@@ -906,6 +1213,7 @@ sp_status graph_step(sp_ctx *c) {
     CK(cudaGraphLaunch(c->gcomp[r], c->compute));
     c->forwarded = k + 1;
     c->trained = k + 1;
+    c->trained_pub.store(k + 1, std::memory_order_release);
     c->graph_steps++;
     if (sp_status s = pump(c)) return s;
     {
@@ -926,6 +1234,18 @@ sp_status sp_run_steps(sp_ctx *c, const void *indices, int64_t num_batches, int6
         return SP_ERR_INVALID_ARG;
     if (c->fwd_pending) return fail(c, SP_ERR_STATE, "sp_run_steps between sp_forward and sp_train");
     CK(cudaSetDevice(c->device));
+    {   // device memory, or pinned + mapped host memory read by k_push over the
+        // host link (the batch's H2D is then part of the plan kernel)
+        // (checked at the next batch to push: `indices` itself may be a base
+        // offset below the caller's array, batch j living at indices + j*stride)
+        const void *first = static_cast<const char *>(indices) + c->pushed * stride;
+        cudaPointerAttributes pa{};
+        if (steps > 0 && c->pushed < num_batches && (cudaPointerGetAttributes(&pa, first) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered ||
+                          (pa.type == cudaMemoryTypeHost && pa.devicePointer != first))) {
+            (void)cudaGetLastError();
+            return fail(c, SP_ERR_INVALID_ARG, "sp_run_steps: indices must be device memory or pinned host memory");
+        }
+    }
     const long long ahead = c->F + c->P + 1;
     const char *base = static_cast<const char *>(indices);
     sp_ctx::GraphKey key;
@@ -993,7 +1313,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     cudaSetDevice(c->device);
     o->pushed = c->pushed;
     o->planned = c->planned;
-    o->transferred = c->xfer_enq;
+    o->transferred = c->x_enqueued.load();
     o->forwarded = c->forwarded;
     o->trained = c->trained;
     unsigned long long cum[4] = {0, 0, 0, 0};
@@ -1009,10 +1329,16 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->h2d_row_bytes = (int64_t)cum[2] * c->D * 4;
     o->d2h_row_bytes = (int64_t)cum[3] * c->D * 4;
     std::lock_guard<std::mutex> lk(c->prof_mu);
-    // host_* / wait_* fields stay 0: no host thread moves rows (ABI 1 layout)
+    o->host_gather_ms = 0.0;  // the GPU pulls the missed rows itself
+    o->host_scatter_ms = c->x_scatter_ns.load() * 1e-6;
+    o->host_rows_gathered = c->x_rows_g.load();
+    o->host_rows_scattered = c->x_rows_s.load();
+    o->wait_xfer_ms = c->wait_xfer_ns * 1e-6;
+    o->wait_list_ms = c->wait_list_ns * 1e-6;
     o->graph_steps = c->graph_steps;
     if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);
+        cudaStreamSynchronize(c->d2h_s);
         cudaStreamSynchronize(c->compute);
         harvest_profile(c, true);
     }

@@ -26,7 +26,7 @@ constexpr uint32_t EMPTY = 0xFFFFFFFFu;     // empty Hit-Map entry / vacant slot
 constexpr int32_t VACANT = INT32_MIN;       // last_use of a never-used slot
 constexpr int32_t NEVER = INT32_MIN;        // next_need of a slot with no future use
 constexpr int CH = 16;                      // occurrences per backward chunk
-constexpr int PUSH_THREADS = 512;
+constexpr int PUSH_THREADS = 1024;            // one CTA per table and role (k_push)
 constexpr int SMEM_SORT_MAX = 8192;         // n handled by the shared-memory radix sort
 constexpr unsigned long long NO_ERR = ~0ull;
 
@@ -77,6 +77,14 @@ struct Geometry {
     int hs;               // occurrences per hot-row segment (k_bwd: one CTA round)
 };
 
+// Fill lists of one Plan, mirrored into pinned host memory by the plan kernel
+// for the CPU side of the transfer engine (per ring slot, per table).
+struct HostList {
+    unsigned long long *ready;  // [T] = b + 1 once table t's list of batch b is complete
+    uint32_t *m;                // [T] fills of table t
+    uint2 *ent;                 // [T][n] {missed row, previous resident (EMPTY if vacant)}
+};
+
 struct PushArgs {
     Geometry g;
     int P, F;
@@ -106,6 +114,7 @@ struct PushArgs {
     BatchBufs pb;
     int has_future;
     BatchBufs fb;
+    HostList hl;                 // pinned mirror of Plan(b)'s fill lists
     // graph replay: j is read from ctl[ctl_r] (b = j - F - 1, idx = idx + j*stride)
     // and ctl[(ctl_r + 1) % RING] = j + 1 is written for the next step
     long long *ctl;
@@ -132,6 +141,7 @@ struct XferArgs {
     BatchBufs bb;
     float *storage;
     float *const *host;       // [T] device-visible (mapped) host table pointers
+    float *wb_stage;          // [sum m][D] victims (D2H DMA, then CPU scatter)
     const unsigned long long *err;
 };
 
@@ -190,9 +200,7 @@ cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s);
 int backward_hot_segment(int D);
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
                              float delta, cudaStream_t s);
-cudaError_t launch_exchange(const XferArgs &a, int ctas, cudaStream_t s);
-cudaError_t configure_exchange_kernel(int D);
-size_t exchange_smem_bytes(int D);
+cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
 size_t push_smem_bytes(int n);
 cudaError_t configure_push_kernel();

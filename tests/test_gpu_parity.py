@@ -212,3 +212,43 @@ def test_run_steps_graph_replay_matches_oracle():
         want = orc.rows_of(t, touched)
         assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-4)) <= TOL
     sp.close()
+
+
+@pytest.mark.gpu
+def test_run_steps_pinned_host_trace_matches_oracle():
+    """sp_run_steps over a PINNED HOST trace (the plan kernel reads each batch
+    over the host link; bench.py's e2e path), switched mid-run from a device
+    trace and driven one step per call, gives the oracle's final tables."""
+    from oracle import UncachedTrainer
+    rows, D, N, L, nb = [2000, 300, 50], 16, 64, 2, 70
+    tr = sample_trace(rows, N, L, 0.9, nb, 13)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 8) for t, R in enumerate(rows)]
+    tables = pinned_tables(rows, D, 4702)
+    sp = ScratchPipe(rows, tables, D, slots, N, L, index_dtype="int32", index_on_device=True)
+    t32 = tr.to(torch.int32).contiguous()
+    dev = t32.cuda()
+    pooled = torch.empty((3, N, D), device="cuda")
+    grad = torch.empty_like(pooled)
+    g, d, e = 0.5, 0.01, 0.05
+    sp.run_steps(dev[:30], 20, pooled, grad, g, d, e)              # device trace, pushes up to 26
+    j0 = sp.stats()["pushed"]
+    host = t32[j0:].pin_memory()                                    # the rest from pinned host memory
+    while sp.stats()["trained"] < nb:
+        sp.run_steps(host, 1, pooled, grad, g, d, e, first_batch=j0)
+    sp.flush()
+    orc = UncachedTrainer(rows, D, N, L, 4702)
+    for b in range(nb):
+        orc.step(tr.numpy()[b], g, d, e)
+    for t, R in enumerate(rows):
+        touched = orc.touched(t)
+        got = tables[t][torch.from_numpy(touched)].numpy()
+        want = orc.rows_of(t, touched)
+        assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-4)) <= TOL
+    with pytest.raises(Exception):  # pageable host memory is refused
+        sp2 = ScratchPipe(rows, pinned_tables(rows, D, 4702), D, slots, N, L, index_dtype="int32",
+                          index_on_device=True)
+        try:
+            sp2.run_steps(t32.clone(), 1, pooled, grad, g, d, e)
+        finally:
+            sp2.close()
+    sp.close()
