@@ -204,8 +204,18 @@ def _plan_roles(p0, p1):
         if n1 <= n0:
             continue
         per = [(b * n1 - a * n0) / (n1 - n0) for a, b in zip(p0[key], p1[key])]
+        tm = int(max(range(len(per)), key=lambda i: per[i]))
+        pk = role + "_phase_us"
+        phases = [round((b * n1 - a * n0) / (n1 - n0), 2) for a, b in zip(p0[pk][tm], p1[pk][tm])]
         out[role] = {"max_table_us": round(max(per), 2), "mean_us": round(sum(per) / len(per), 2),
-                     "argmax_table": int(max(range(len(per)), key=lambda i: per[i]))}
+                     "argmax_table": tm, "phases_us_of_argmax": phases[:6 if role == "plan" else 5]}
+    pl = p1.get("per_launch", {})
+    if pl.get("span_us"):
+        import numpy as np
+        q = lambda v: [round(float(np.percentile(v, x)), 2) for x in (50, 90, 99)]
+        out["per_launch_p50_p90_p99_us"] = {"kernel_span": q(pl["span_us"]), "slowest_plan_cta": q(pl["plan_cta_max_us"]),
+                                            "slowest_dedup_cta": q(pl["dedup_cta_max_us"]),
+                                            "launches": len(pl["span_us"])}
     return out
 
 
@@ -235,7 +245,8 @@ def run_ours(args):
     pre = cfg.preroll if args.preroll < 0 else args.preroll
     P, F = cfg.window, max(cfg.window - 1, 0)
     ahead = P + F + 1
-    nb_dev = pre + W + K + KP          # device-index phase (incl. the `ahead` pushed first)
+    KS = 48 if world == 1 else 0       # graph-mode stage-timing pass (16 recaptures + 32 timed)
+    nb_dev = pre + W + K + KS + KP     # device-index phase (incl. the `ahead` pushed first)
     WE = max(W, 18)                    # e2e warm-up: also (re)captures the 16 step graphs
     nb_host = WE + K                   # host-index (e2e) phase
     nb = nb_dev + ahead + nb_host
@@ -354,6 +365,13 @@ def run_ours(args):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     st1 = sp.stats()
+    stage_t = None
+    if world == 1:  # same graph-mode steady state, step graphs recaptured with event nodes
+        sp.set_stage_timing(True)
+        value_loop(KS)
+        stage_t = sp.stage_times()   # events of the last 16 steps, on each stage's own stream
+        sp.set_stage_timing(False)
+    st1p = sp.stats()  # baseline of the (eager) profiling pass
     value = K / (ms / 1e3)   # iterations of the global batch per second (max over ranks)
     ms_per_step = ms / K
     from paper_2205_04702_b200._binding import KERNEL_ONLY
@@ -405,15 +423,15 @@ def run_ours(args):
 
     # ---- per-kernel accounting (profiling window)
     def delta(key):
-        return st2[key] - st1[key]
+        return st2[key] - st1p[key]
     steps_p = KP
     U = delta("uniques") / steps_p
     m = delta("misses") / steps_p
     ev = delta("evictions") / steps_p
     Tg = len(mine)
     n = N * L
-    kms = {k: st2["kernel_ms"][k] - st1["kernel_ms"][k] for k in st2["kernel_ms"]}
-    kcount = {k: st2["kernel_timed"][k] - st1["kernel_timed"][k] for k in st2["kernel_timed"]}
+    kms = {k: st2["kernel_ms"][k] - st1p["kernel_ms"][k] for k in st2["kernel_ms"]}
+    kcount = {k: st2["kernel_timed"][k] - st1p["kernel_timed"][k] for k in st2["kernel_timed"]}
     avg_ms = {k: (kms[k] / kcount[k] if kcount[k] else 0.0) for k in kms}
     alg_bytes = {
         # slot map + gathered rows + pooled out (nominal TBE bytes)
@@ -421,35 +439,43 @@ def run_ours(args):
         # pooled grad in + occurrence list + per-unique segment/slot words + SGD read+write
         "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 8 * D * U,
         "surrogate": 8 * D * Tg * N,
-        # k_pullfill: missed rows pulled over the host link (zero-copy) + victims
-        # staged HBM->HBM (4*D*e read + 4*D*e written)
-        "transfer": 4 * D * m + 8 * D * ev,
-        "d2h": 4 * D * ev,                       # copy engine: staged victims
+        # k_pullfill, host-link bytes: missed rows pulled (H2D) + victims written
+        # to the pinned staging slot (D2H); HBM: the same rows written / read
+        "transfer": 4 * D * m + 4 * D * ev,
         "plan": 4 * Tg * n,
     }
     peak, peak_kind = peaks()
     traffic = load_traffic()
     total_ms = sum(kms.values()) or 1.0
     kernels = {}
-    for k in ["plan", "transfer", "d2h", "forward", "backward", "surrogate"]:
-        gbs = alg_bytes[k] / (avg_ms[k] * 1e-3) / 1e9 if avg_ms[k] else None
-        kernels[k] = {"avg_us": round(avg_ms[k] * 1e3, 3), "share": round(kms[k] / total_ms, 4),
+    # per-stage duration: CUDA events on each stage's own stream inside the
+    # step graphs of the TIMED region (last 16 steps), else the profiling pass
+    timed_src = bool(stage_t) and all(stage_t[k]["n"] > 0 for k in ["forward", "backward", "surrogate"])
+    for k in ["plan", "transfer", "forward", "backward", "surrogate"]:
+        us = stage_t[k]["ms"] * 1e3 if timed_src and stage_t[k]["n"] else avg_ms[k] * 1e3
+        gbs = alg_bytes[k] / (us * 1e-6) / 1e9 if us else None
+        kernels[k] = {"avg_us": round(us, 3), "share_profiling_pass": round(kms[k] / total_ms, 4),
+                      "profiling_pass_us": round(avg_ms[k] * 1e3, 3),
                       "alg_bytes_per_launch": int(alg_bytes[k]), "alg_GBs": None if gbs is None else round(gbs, 1)}
     # dominant HBM-bound kernel (the Train stage: forward or backward)
-    dom = max(["forward", "backward"], key=lambda k: kms[k])
+    dom = max(["forward", "backward"], key=lambda k: kernels[k]["avg_us"])
     ach = kernels[dom]["alg_GBs"] or 0.0
     tr_bytes = traffic.get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "duration_source": ("CUDA events around the kernel on its stream inside the step graphs "
+                                    "of a graph-mode pass right after the timed region (mean of 16 steps)")
+                                   if timed_src else
+                                   "CUDA events around each launch in a separate profiling pass",
                 "traffic": tr_bytes,
                 "bytes_per_launch": int(alg_bytes[dom]),
                 "bytes_formula": ("4*T*n + 4*D*T*n + 4*D*T*N" if dom == "forward"
                                   else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
-    train_ms = avg_ms["forward"] + avg_ms["backward"]
+    train_ms = (kernels["forward"]["avg_us"] + kernels["backward"]["avg_us"]) * 1e-3
     train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
-    xs = avg_ms["transfer"] * 1e-3
+    xs = kernels["transfer"]["avg_us"] * 1e-6
     link_GBs = 4 * D * m / xs / 1e9 if xs else None
-    wb_GBs = alg_bytes["d2h"] / (avg_ms["d2h"] * 1e-3) / 1e9 if avg_ms.get("d2h") else None
+    wb_GBs = 4 * D * ev / xs / 1e9 if xs else None
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
@@ -465,8 +491,9 @@ def run_ours(args):
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
-        "host_link": {"path": "H2D: k_pullfill zero-copy pull of missed rows by a bounded grid; "
-                              "D2H: victims staged in HBM, copy-engine DMA, CPU scatter threads",
+        "host_link": {"path": "k_pullfill: zero-copy pull of missed rows (H2D) and victims written "
+                              "contiguously to pinned staging (D2H) by one bounded-grid kernel; CPU "
+                              "threads scatter staged victims into the host tables",
                       "h2d_bytes_per_batch": int(4 * D * m),
                       "h2d_GBs": None if link_GBs is None else round(link_GBs, 2),
                       "d2h_bytes_per_batch": int(4 * D * ev),
@@ -475,7 +502,7 @@ def run_ours(args):
                       "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)"},
         "kernels": kernels,
         "plan_ctas": _plan_roles(pp0, pp1),
-        "host_engine": {"scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1["host_scatter_ms"]) / KP, 2),
+        "host_engine": {"scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1p["host_scatter_ms"]) / KP, 2),
                         "threads": "1 scatter thread + row-copy helpers"},
         "host_waits_us_per_step": {"list_slot": round(1e3 * (st1["wait_list_ms"] - st0["wait_list_ms"]) / K, 2)},
         "per_step": {"uniques": round(U, 1), "misses": round(m, 1), "evictions": round(ev, 1)},

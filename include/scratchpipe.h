@@ -11,10 +11,11 @@
  *               (past window P:840-861, future window P:864-884, superset
  *               P:887-896), Hit-Map/Storage bookkeeping.
  *               [Collect]+[Exchange]+[Insert] run in the
- *               library's transfer engine: CPU threads gather missed rows /
- *               scatter victims in host memory, the copy engines move both
- *               directions over PCIe at once, one HBM kernel fills the
- *               freed slots and stages the victims.
+ *               library's transfer engine: one bounded-grid kernel per
+ *               batch pulls the missed rows from the host tables into the
+ *               freed slots (zero-copy) and writes the victims contiguously
+ *               into pinned staging; CPU threads scatter the staged victims
+ *               into their host rows (no CUDA call on those threads).
  *   sp_forward  [Training] part 1: EmbeddingBag gather-reduce.
  *   sp_train    [Training] part 2: gradient duplication + coalescing
  *                and the SGD update in place in the scratchpad
@@ -96,22 +97,21 @@ typedef struct {
     uint32_t flags;              /* SP_FLAG_*                                       */
     int32_t log_factor;          /* LRU-log ring capacity per table =               */
                                  /* log_factor * slots[t] + 4*N*L (0 -> 8)          */
-    int32_t host_threads;        /* CPU helper threads of the transfer engine that  */
-                                 /* copy rows between host tables and pinned        */
-                                 /* staging (0 -> 8), split between the gather and  */
-                                 /* the scatter thread                              */
+    int32_t host_threads;        /* CPU helper threads that, with the scatter       */
+                                 /* thread, copy staged victims into their host     */
+                                 /* rows (0 -> 6)                                   */
     int32_t reserved;            /* must be 0                                       */
 } sp_desc;
 
 typedef enum {
     SP_K_PLAN = 0,      /* dedup + future probe + Plan (one launch per sp_plan)  */
-    SP_K_TRANSFER = 1,  /* k_fill: victims staged, freed slots filled (HBM)       */
+    SP_K_TRANSFER = 1,  /* k_pullfill: victims staged to host, freed slots filled */
     SP_K_FORWARD = 2,   /* EmbeddingBag gather-reduce                             */
     SP_K_BACKWARD = 3,  /* duplicate-coalescing segmented reduce + fused SGD      */
     SP_K_SURROGATE = 4, /* harness MLP stand-in g = fmaf(gamma, pooled, delta)    */
     SP_K_FLUSH = 5,     /* write-back of all resident rows                        */
-    SP_K_H2D = 6,       /* copy-engine DMA of the gathered missed rows            */
-    SP_K_D2H = 7,       /* copy-engine DMA of the staged victims                  */
+    SP_K_H2D = 6,       /* (unused: the transfer kernel pulls rows itself)        */
+    SP_K_D2H = 7,       /* (unused: the transfer kernel stages victims itself)    */
     SP_K_COUNT = 8
 } sp_kernel_kind;
 
@@ -257,11 +257,29 @@ sp_status sp_debug_resident(sp_ctx *c, int32_t t, int64_t *ids, int64_t cap, int
  * never used).  Arrays of slots[t] entries. */
 sp_status sp_debug_slots(sp_ctx *c, int32_t t, int64_t *resident, int64_t *last_use);
 /* Copy Storage rows [first, first+count) of table t to host (synchronises). */
+/* Stage timing on/off (default off): when on, the steady-state step graphs are
+ * (re)captured with CUDA event records around k_push, k_fwd, k_surrogate and
+ * k_bwd, and every transfer launch is bracketed by events (read with
+ * sp_stage_times).  Off keeps the event nodes out of the graphs. */
+sp_status sp_set_stage_timing(sp_ctx *c, int32_t on);
+
+/* Stage durations of the LAST RING (16) steps, from CUDA events recorded on
+ * the stages' own streams inside the steady-state step graphs (sp_run_steps)
+ * and around every transfer launch: out_ms[5] = mean ms of {plan (k_push),
+ * transfer (k_pullfill), forward, surrogate, backward}, n_out[5] = steps
+ * averaged (0: stage never timed).  Synchronises the device. */
+sp_status sp_stage_times(sp_ctx *c, double *out_ms, int32_t *n_out);
+
 /* k_push per-CTA wall time while profiling is on (sp_set_profiling / SP_FLAG_PROFILE),
- * from %globaltimer at CTA entry and exit.  out[2T+2] (caller-owned host array):
+ * from %globaltimer at CTA entry and exit.  out[18T+2+4096] (caller-owned host array):
  * out[t] = summed ns of the Plan CTA of table t, out[T+t] = summed ns of the
  * dedup CTA of table t, out[2T] / out[2T+1] = CTAs timed per role (summed
- * over tables).  Synchronises the plan stream.  Diagnostics only. */
+ * over tables), out[2T+2 + (role*T + t)*8 + k] = summed ns of phase k of that
+ * CTA (role 0 Plan: P1..P6; role 1 dedup: D1, D2 sort, D2 unique, D3a, D3b);
+ * then per launch q = j mod 1024 of the current profiling window: [q] first
+ * CTA start, [1024+q] last CTA end (ns), [2048+q] slowest Plan CTA,
+ * [3072+q] slowest dedup CTA (ns).
+ * Synchronises the plan stream.  Diagnostics only. */
 sp_status sp_debug_plan_profile(sp_ctx *c, uint64_t *out);
 
 sp_status sp_debug_storage(sp_ctx *c, int32_t t, int64_t first, int64_t count, float *out);

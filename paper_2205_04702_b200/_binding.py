@@ -94,7 +94,8 @@ def _load():
                        ("sp_debug_resident", [P, ctypes.c_int32, i64p, ctypes.c_int64, i64p]),
                        ("sp_debug_slots", [P, ctypes.c_int32, i64p, i64p]),
                        ("sp_debug_storage", [P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, P]),
-                       ("sp_debug_plan_profile", [P, P])]:
+                       ("sp_debug_plan_profile", [P, P]), ("sp_stage_times", [P, P, P]),
+                       ("sp_set_stage_timing", [P, ctypes.c_int32])]:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = S
@@ -340,16 +341,35 @@ class ScratchPipe:
         self._check(lib.sp_debug_slots(self._h, t, _i64(res), _i64(lu)))
         return res, lu
 
+    def set_stage_timing(self, on: bool):
+        self._check(lib.sp_set_stage_timing(self._h, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        """Mean ms per step of each stage over the last 16 steps (events inside
+        the step graphs / around each transfer; sp_stage_times)."""
+        ms = np.zeros(5, np.float64)
+        n = np.zeros(5, np.int32)
+        self._check(lib.sp_stage_times(self._h, ms.ctypes.data_as(ctypes.c_void_p), n.ctypes.data_as(ctypes.c_void_p)))
+        names = ["plan", "transfer", "forward", "surrogate", "backward"]
+        return {k: {"ms": float(ms[i]), "n": int(n[i])} for i, k in enumerate(names)}
+
     def debug_plan_profile(self) -> dict:
         """k_push per-CTA wall time while profiling: mean us per launch of the
         Plan CTA and of the dedup CTA of each table (sp_debug_plan_profile)."""
         T = len(self._slots)
-        out = np.zeros(2 * T + 2, np.uint64)
+        out = np.zeros(18 * T + 2 + 4096, np.uint64)
         self._check(lib.sp_debug_plan_profile(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        sp = out[18 * T + 2:].reshape(4, 1024)
+        ok = (sp[1] > 0) & (sp[0] != np.uint64(0xFFFFFFFFFFFFFFFF))
+        spans = {"span_us": ((sp[1][ok] - sp[0][ok]).astype(np.float64) / 1e3).tolist(),
+                 "plan_cta_max_us": (sp[2][ok].astype(np.float64) / 1e3).tolist(),
+                 "dedup_cta_max_us": (sp[3][ok].astype(np.float64) / 1e3).tolist()}
         npl, nde = max(1, int(out[2 * T]) // T), max(1, int(out[2 * T + 1]) // T)
+        ph = out[2 * T + 2:18 * T + 2].astype(np.float64).reshape(2, T, 8)
         return {"plan_us": (out[:T].astype(np.float64) / npl / 1e3).tolist(),
                 "dedup_us": (out[T:2 * T].astype(np.float64) / nde / 1e3).tolist(),
-                "launches": [int(out[2 * T]) // T, int(out[2 * T + 1]) // T]}
+                "plan_phase_us": (ph[0] / npl / 1e3).tolist(), "dedup_phase_us": (ph[1] / nde / 1e3).tolist(),
+                "launches": [int(out[2 * T]) // T, int(out[2 * T + 1]) // T], "per_launch": spans}
 
     def debug_storage(self, t: int, first: int = 0, count: Optional[int] = None) -> np.ndarray:
         if count is None:

@@ -376,7 +376,10 @@ template <int G, int VPL, typename K>
 static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStream_t s) {
     static std::unordered_map<const void *, int> caps;  // per kernel (not per signature)
     int &cap = caps[reinterpret_cast<const void *>(kernel)];
-    if (!cap) cap = resident_ctas(kernel, 256);
+    if (!cap) {
+        apply_carveout(kernel);
+        cap = resident_ctas(kernel, 256);
+    }
     long long blocks = (groups + (256 / G) - 1) / (256 / G);
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
@@ -432,6 +435,11 @@ cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, 
     const long long cap = (long long)num_sms() * 8;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
+    static bool once = false;
+    if (!once) {
+        apply_carveout(k_surrogate);
+        once = true;
+    }
     k_surrogate<<<grid, 256, 0, s>>>(reinterpret_cast<const float4 *>(pooled),
                                      reinterpret_cast<float4 *>(grad), n4, gamma, delta);
     return cudaGetLastError();

@@ -8,21 +8,41 @@
 //                vs ~6x for full-rate writes), and the GPU gathers the rows
 //                itself: no CPU copy (random host rows cost ~31 ns/row/core
 //                in this VM) and no per-batch API calls for sizes.
-//   HBM -> host  the victims are staged in HBM by the same kernel, moved by
-//                a copy-engine D2H DMA, and scattered into the host tables by
-//                the CPU threads of the transfer engine (runtime.cu).
+//   HBM -> host  the same kernel writes the victims, contiguously, into a
+//                pinned host staging slot (sequential pages: few address
+//                translations), raises a pinned flag when the last CTA is
+//                done, and the CPU threads of the transfer engine scatter them
+//                into the host tables (runtime.cu): random host rows are
+//                translated by the CPU MMU, not the IOMMU the pulls use.
 //   k_pullfill (transfer stream): for every fill k (slot s, missed row x,
 //   previous resident o) of Plan(b), staging index i = prefix + k:
-//       wb_stage[i] <- Storage[s]     if o is valid (dirty victim)
+//       wb_stage[i] <- Storage[s]     if o is valid (dirty victim, P:693-696;
+//                                     pinned host staging, zero-copy store)
 //       Storage[s]  <- host[t][x]     zero-copy PCIe read
 //   the same lane reads the victim before overwriting the slot.
 #include "sp_internal.cuh"
 
 namespace sp {
 
+// Completion of Transfer(b) for the scatter thread: every CTA's staging stores
+// are made visible system-wide, then the last CTA to arrive raises the pinned
+// flag (and resets the counter for the next use of this ring slot).
+__device__ __forceinline__ void publish_staged(const XferArgs &A) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned k = atomicAdd(A.done_ctr, 1u);
+        if (k == gridDim.x - 1) {
+            *A.done_ctr = 0u;
+            __threadfence_system();
+            *(volatile unsigned long long *)A.staged = (unsigned long long)(A.b + 1);
+        }
+    }
+}
+
 // G lanes per row, VPL float4 per lane, XU rows in flight per lane group.
 // Per fill k (slot s, missed row x, previous resident o), staging i = prefix + k:
-//   wb_stage[i] <- Storage[s]        if o is valid (dirty victim, HBM -> HBM)
+//   wb_stage[i] <- Storage[s]        if o is valid (dirty victim -> pinned staging)
 //   Storage[s]  <- host[t][x]        zero-copy PCIe read (bounded grid)
 template <int G, int VPL>
 __global__ void __launch_bounds__(256) k_pullfill(XferArgs A) {
@@ -79,6 +99,7 @@ __global__ void __launch_bounds__(256) k_pullfill(XferArgs A) {
         }
         base_t0 += total;
     }
+    publish_staged(A);
 }
 
 __global__ void __launch_bounds__(256) k_pullfill_generic(XferArgs A) {
@@ -105,6 +126,7 @@ __global__ void __launch_bounds__(256) k_pullfill_generic(XferArgs A) {
         }
         base += m;
     }
+    publish_staged(A);
 }
 
 // write back every resident slot (sp_flush)
@@ -133,6 +155,15 @@ static int sm_count() {
 
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s) {
     const int grid = ctas > 0 ? ctas : 8;
+    static bool once = false;
+    if (!once) {
+        apply_carveout(k_pullfill<16, 1>);
+        apply_carveout(k_pullfill<32, 1>);
+        apply_carveout(k_pullfill<32, 2>);
+        apply_carveout(k_pullfill<32, 4>);
+        apply_carveout(k_pullfill_generic);
+        once = true;
+    }
     switch (a.g.D / 4) {
         case 1: k_pullfill<1, 1><<<grid, 256, 0, s>>>(a); break;
         case 2: k_pullfill<2, 1><<<grid, 256, 0, s>>>(a); break;

@@ -138,7 +138,6 @@ struct RowPool {
     }
 };
 
-enum : int { K_H2D = SP_K_H2D, K_D2H = SP_K_D2H };
 
 }  // namespace
 
@@ -156,8 +155,12 @@ struct sp_ctx {
     bool registered = false;
     Geometry g{};
     cudaStream_t compute = nullptr, plan_s = nullptr, xfer_s = nullptr;
-    cudaStream_t own_plan_s = nullptr, own_xfer_s = nullptr;  // created by the library
-    cudaStream_t d2h_s = nullptr;  // victims' D2H on its own stream (other copy engine)
+    // Transfer(b) runs on xfer_s if b is even, xfer_s2 if odd: consecutive
+    // transfers touch disjoint slots and host rows (a victim of Plan(b+1) has
+    // last_use <= b-P, a row evicted at Plan(b) is not in B(b+1..b+F)), and
+    // every real dependency is an explicit wait (Plan, Train(b-P-1), scatter)
+    cudaStream_t xfer_s2 = nullptr;
+    cudaStream_t own_plan_s = nullptr, own_xfer_s = nullptr, own_xfer_s2 = nullptr;  // created here
     // device memory
     std::vector<void *> allocs;
     unsigned long long *d_row_off = nullptr;
@@ -178,13 +181,21 @@ struct sp_ctx {
     float **d_host = nullptr;
     void *d_idx[RING] = {};
     BatchBufs ring[RING];
-    // transfer staging of the victims: XSR slots of sum(m) rows (<= T*n)
+    // victim staging: XSR slots of sum(m) rows (<= T*n) in pinned host memory,
+    // written by k_pullfill (contiguous rows over the host link); the kernel's
+    // last CTA sets h_staged[b % RING] = b + 1 for the scatter thread
     int XSR = 4;
-    float *d_wb = nullptr;                     // device [XSR][T*n][D]
-    float *h_wb = nullptr;                     // pinned [XSR][T*n][D]
+    float *h_wb = nullptr;                     // pinned mapped [XSR][T*n][D]
+    float *hd_wb = nullptr;                    // its device alias
+    unsigned long long *h_staged = nullptr;    // pinned mapped [RING]
+    unsigned long long *hd_staged = nullptr;   // device alias
+    uint32_t *d_xdone = nullptr;               // [RING] k_pullfill CTA arrival counters
     unsigned long long *h_scat = nullptr;      // pinned mapped: batches scattered
     unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
     int pull_ctas = 8;
+    // timing diagnostics (SP_DIAG bit mask; results are then WRONG): 1 = the
+    // transfer kernel moves nothing, 2 = the Train kernels do nothing
+    int diag = 0;
     long long xfer_enq = 0;                    // transfers enqueued (caller's thread)
     // pinned host mirror of the fill lists, per ring slot
     unsigned long long *hl_ready = nullptr;    // [RING][T]
@@ -198,9 +209,16 @@ struct sp_ctx {
     unsigned long long *d_errflag = nullptr;  // device alias of h_errflag
     size_t idx_bytes = 0;
     // events
-    cudaEvent_t ev_plan[RING] = {}, ev_xfer[RING] = {}, ev_d2h[RING] = {}, ev_train[RING] = {},
+    cudaEvent_t ev_plan[RING] = {}, ev_xfer[RING] = {}, ev_train[RING] = {},
                 ev_h2d[RING] = {};
     cudaEvent_t ev_user = nullptr;
+    // timing events of the steady state (sp_stage_times): recorded by the step
+    // graphs of residue r around k_push / k_fwd / k_surrogate / k_bwd
+    // ([0..1] plan, [2..5] forward start, forward end, surrogate end, backward
+    // end) and around every transfer ([6..7]); the last RING steps are timed
+    cudaEvent_t sev[RING][8] = {};
+    bool sev_used[RING][2] = {};
+    bool stage_timing = false;  // sp_set_stage_timing: record sev in new graphs
     bool h2d_used[RING] = {};
     // schedule state (caller's thread)
     long long pushed = 0, planned = 0, forwarded = 0, trained = 0;
@@ -485,98 +503,62 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.storage = c->d_storage;
     a.partial = c->d_partial;
     a.err = c->d_err;
+    if (c->diag & 2) a.g.T = 0;  // diagnostic: Train kernels launched, no work
     return a;
 }
 
 // --------------------------------------------------------------- transfer engine
-void engine_fail(sp_ctx *c, cudaError_t e, const char *where) {
-    c->x_errmsg = std::string(where) + ": " + cudaGetErrorString(e);
-    c->x_error.store(1, std::memory_order_release);
-}
 
-// [Insert] CPU scatter of batch s's victims into the host tables once its D2H
-// has landed, in batch order, on its own thread: it overlaps the gather of
-// later batches (rows evicted at s are not in B(s+1..s+F)).
+// [Insert] CPU scatter of batch s's victims into the host tables once
+// Transfer(s) has staged them in pinned host memory (k_pullfill's last CTA
+// sets h_staged), in batch order, on its own thread.  No CUDA API call: the
+// thread only polls pinned memory, so it never contends for the driver with
+// the caller's thread.  Rows evicted at s are not in B(s+1..s+F), so the
+// scatter overlaps the next transfers; Transfer(s+F+1) waits for it on the
+// GPU (RAW-4, h_scat).
 void scatter_main(sp_ctx *c) {
-    cudaSetDevice(c->device);
     const size_t rowb = (size_t)c->D * sizeof(float);
     const size_t slab = (size_t)c->T * c->n * c->D;
     std::vector<const float *> src;
     std::vector<float *> dst;
     std::vector<uint32_t> pref(c->T + 1);
-    long long s = 0, d = 0;  // next batch to scatter / to issue the D2H for
+    long long s = 0;  // next batch to scatter
     int idle = 0;
     auto ready = [&](long long b) {
         const int r = (int)(b % RING);
+        if (((volatile unsigned long long *)c->h_staged)[r] != (unsigned long long)(b + 1)) return false;
         for (int t = 0; t < c->T; t++)
             if (((volatile unsigned long long *)c->hl_ready)[(size_t)r * c->T + t] != (unsigned long long)(b + 1))
                 return false;
         std::atomic_thread_fence(std::memory_order_acquire);
         return true;
     };
-    auto rows_of = [&](long long b) {
-        const int r = (int)(b % RING);
-        pref[0] = 0;
-        for (int t = 0; t < c->T; t++) pref[t + 1] = pref[t] + c->hl_m[(size_t)r * c->T + t];
-        return (size_t)pref[c->T];
-    };
     while (!c->stop.load(std::memory_order_relaxed)) {
         if (*(volatile unsigned long long *)c->h_errflag) break;
-        bool progressed = false;
-        // [Exchange] D2H of the staged victims of batch d once Transfer(d) is
-        // enqueued (ev_xfer exists) and its lists are known; the staging slot
-        // d % XSR is free because Transfer(d) waited for scatter(d-F-1)
-        if (d < s + c->XSR && d < c->x_enqueued.load(std::memory_order_acquire) && ready(d)) {
-            const int r = (int)(d % RING);
-            const size_t bytes = rows_of(d) * rowb;
-            cudaError_t e = cudaStreamWaitEvent(c->d2h_s, c->ev_xfer[r], 0);
-            if (e == cudaSuccess && bytes)
-                e = launch(c, K_D2H, d, c->d2h_s, [&] {
-                    return cudaMemcpyAsync(c->h_wb + (size_t)(d % c->XSR) * slab,
-                                           c->d_wb + (size_t)(d % c->XSR) * slab, bytes,
-                                           cudaMemcpyDeviceToHost, c->d2h_s);
-                });
-            if (e == cudaSuccess) e = cudaEventRecord(c->ev_d2h[r], c->d2h_s);
-            if (e != cudaSuccess) {
-                engine_fail(c, e, "D2H enqueue");
-                break;
+        if (s < c->x_enqueued.load(std::memory_order_acquire) && ready(s)) {
+            const int r = (int)(s % RING);
+            pref[0] = 0;
+            for (int t = 0; t < c->T; t++) pref[t + 1] = pref[t] + c->hl_m[(size_t)r * c->T + t];
+            src.clear();
+            dst.clear();
+            const float *wb = c->h_wb + (size_t)(s % c->XSR) * slab;
+            for (int t = 0; t < c->T; t++) {
+                const uint2 *ent = c->hl_ent + ((size_t)r * c->T + t) * c->n;
+                for (uint32_t k = 0; k < pref[t + 1] - pref[t]; k++)
+                    if (ent[k].y != EMPTY) {
+                        src.push_back(wb + (size_t)(pref[t] + k) * c->D);
+                        dst.push_back(c->host[t] + (size_t)ent[k].y * c->D);
+                    }
             }
-            d++;
-            progressed = true;
-        }
-        // [Insert] CPU scatter of batch s once its D2H has landed, in order
-        if (s < d) {
-            cudaError_t q = cudaEventQuery(c->ev_d2h[s % RING]);
-            if (q == cudaSuccess) {
-                const int r = (int)(s % RING);
-                rows_of(s);
-                src.clear();
-                dst.clear();
-                const float *wb = c->h_wb + (size_t)(s % c->XSR) * slab;
-                for (int t = 0; t < c->T; t++) {
-                    const uint2 *ent = c->hl_ent + ((size_t)r * c->T + t) * c->n;
-                    for (uint32_t k = 0; k < pref[t + 1] - pref[t]; k++)
-                        if (ent[k].y != EMPTY) {
-                            src.push_back(wb + (size_t)(pref[t] + k) * c->D);
-                            dst.push_back(c->host[t] + (size_t)ent[k].y * c->D);
-                        }
-                }
-                const auto t0 = std::chrono::steady_clock::now();
-                c->spool.copy(src.data(), dst.data(), (long)src.size(), rowb);
-                c->x_scatter_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
-                                       std::chrono::steady_clock::now() - t0).count();
-                c->x_rows_s += (long long)src.size();
-                s++;
-                c->x_scattered.store(s, std::memory_order_release);
-                std::atomic_thread_fence(std::memory_order_seq_cst);
-                *(volatile unsigned long long *)c->h_scat = (unsigned long long)s;  // GPU wait-value
-                progressed = true;
-            } else if (q != cudaErrorNotReady) {
-                engine_fail(c, q, "ev_d2h");
-                break;
-            }
-        }
-        if (progressed) {
+            const auto t0 = std::chrono::steady_clock::now();
+            c->spool.copy(src.data(), dst.data(), (long)src.size(), rowb);
+            c->x_scatter_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                   std::chrono::steady_clock::now() - t0).count();
+            c->x_rows_s += (long long)src.size();
+            s++;
+            c->x_scattered.store(s, std::memory_order_release);
+            std::atomic_thread_fence(std::memory_order_seq_cst);
+            *(volatile unsigned long long *)c->h_scat = (unsigned long long)s;  // GPU wait-value
             idle = 0;
         } else if (++idle > 2048) {
             std::this_thread::yield();
@@ -614,7 +596,7 @@ sp_status pump(sp_ctx *c) {
         const long long b = c->xfer_enq, dep = b - c->P - 1;
         if (dep >= 0 && c->trained <= dep) break;
         const int r = (int)(b % RING);
-        cudaStream_t xs = c->xfer_s;
+        cudaStream_t xs = (b & 1) ? c->xfer_s2 : c->xfer_s;
         CK(cudaStreamWaitEvent(xs, c->ev_plan[r], 0));
         if (dep >= 0) CK(cudaStreamWaitEvent(xs, c->ev_train[dep % RING], 0));
         // RAW-4 + staging reuse: the CPU write-back of batch b-F-1 has landed
@@ -630,9 +612,16 @@ sp_status pump(sp_ctx *c) {
         a.bb = c->ring[r];
         a.storage = c->d_storage;
         a.host = c->d_host;
-        a.wb_stage = c->d_wb + (size_t)(b % c->XSR) * c->T * c->n * c->D;
+        a.wb_stage = c->hd_wb + (size_t)(b % c->XSR) * c->T * c->n * c->D;
+        a.done_ctr = c->d_xdone + r;
+        a.staged = c->hd_staged + r;
+        a.b = b;
+        if (c->diag & 1) a.g.T = 0;  // diagnostic: transfer launched, no rows moved
         a.err = c->d_err;
+        if (c->stage_timing) CK(cudaEventRecord(c->sev[r][6], xs));
         CK(launch(c, SP_K_TRANSFER, b, xs, [&] { return launch_pullfill(a, c->pull_ctas, xs); }));
+        if (c->stage_timing) CK(cudaEventRecord(c->sev[r][7], xs));
+        c->sev_used[r][1] = c->stage_timing;
         CK(cudaEventRecord(c->ev_xfer[r], xs));
         c->xfer_enq = b + 1;
         c->x_enqueued.store(b + 1, std::memory_order_release);
@@ -649,7 +638,7 @@ void destroy_all(sp_ctx *c) {
     cudaSetDevice(c->device);
     if (c->plan_s) cudaStreamSynchronize(c->plan_s);
     if (c->xfer_s) cudaStreamSynchronize(c->xfer_s);
-    if (c->d2h_s) cudaStreamSynchronize(c->d2h_s);
+    if (c->xfer_s2) cudaStreamSynchronize(c->xfer_s2);
     cudaStreamSynchronize(c->compute);
     {
         std::lock_guard<std::mutex> lk(c->prof_mu);
@@ -657,19 +646,22 @@ void destroy_all(sp_ctx *c) {
         for (auto e : c->ev_pool) cudaEventDestroy(e);
     }
     for (int r = 0; r < RING; r++)
-        for (cudaEvent_t e : {c->ev_plan[r], c->ev_xfer[r], c->ev_d2h[r], c->ev_train[r], c->ev_h2d[r]})
+        for (cudaEvent_t e : {c->ev_plan[r], c->ev_xfer[r], c->ev_train[r], c->ev_h2d[r]})
             if (e) cudaEventDestroy(e);
     if (c->ev_user) cudaEventDestroy(c->ev_user);
+    for (int r = 0; r < RING; r++)
+        for (int k = 0; k < 8; k++)
+            if (c->sev[r][k]) cudaEventDestroy(c->sev[r][k]);
     if (c->prof_ref) cudaEventDestroy(c->prof_ref);
     for (void *p : c->allocs) cudaFree(p);
-    for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb,
+    for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb, (void *)c->h_staged,
                     (void *)c->hl_ready, (void *)c->hl_m, (void *)c->hl_ent})
         if (p) cudaFreeHost(p);
     if (c->registered)
         for (int t = 0; t < c->T; t++) cudaHostUnregister(c->host[t]);
     if (c->own_plan_s) cudaStreamDestroy(c->own_plan_s);
     if (c->own_xfer_s) cudaStreamDestroy(c->own_xfer_s);
-    if (c->d2h_s) cudaStreamDestroy(c->d2h_s);
+    if (c->own_xfer_s2) cudaStreamDestroy(c->own_xfer_s2);
     if (c->cap_s) cudaStreamDestroy(c->cap_s);
     (void)cudaGetLastError();
     delete c;
@@ -771,6 +763,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->host_threads = d->host_threads > 0 ? d->host_threads : 6;
     c->pull_ctas = 8;
     if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
+    if (const char *e = getenv("SP_DIAG")) c->diag = atoi(e);
 
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) {
@@ -819,19 +812,26 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         CKC(cudaStreamCreateWithPriority(&c->plan_s, cudaStreamNonBlocking, hi));
         const char *xp = getenv("SP_XFER_PRIO");  // 1: transfer CTAs also scheduled first
         CKC(cudaStreamCreateWithPriority(&c->xfer_s, cudaStreamNonBlocking, (xp && atoi(xp) == 1) ? hi : lo));
+        // SP_XFER_STREAMS=1: one transfer stream (transfers strictly in sequence)
+        const char *xn = getenv("SP_XFER_STREAMS");
+        if (xn && atoi(xn) == 1) c->xfer_s2 = c->xfer_s;
+        else CKC(cudaStreamCreateWithPriority(&c->xfer_s2, cudaStreamNonBlocking, (xp && atoi(xp) == 1) ? hi : lo));
+        c->own_xfer_s2 = c->xfer_s2 != c->xfer_s ? c->xfer_s2 : nullptr;
         c->own_plan_s = c->plan_s;
         c->own_xfer_s = c->xfer_s;
         // diagnostic: SP_DIAG_SERIAL=1 runs every GPU stage on the caller's
         // stream (no stage overlap) to time kernels free of interference
         if (const char *ds = getenv("SP_DIAG_SERIAL"))
-            if (atoi(ds) == 1) c->plan_s = c->xfer_s = c->compute;
+            if (atoi(ds) == 1) c->plan_s = c->xfer_s = c->xfer_s2 = c->compute;
     }
-    CKC(cudaStreamCreateWithFlags(&c->d2h_s, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithFlags(&c->cap_s, cudaStreamNonBlocking));
     for (int r = 0; r < RING; r++)
-        for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_d2h[r], &c->ev_train[r], &c->ev_h2d[r]})
+        for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_train[r], &c->ev_h2d[r]})
             CKC(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming));
+    for (int r = 0; r < RING; r++)
+        for (int k = 0; k < 8; k++) CKC(cudaEventCreate(&c->sev[r][k]));
+    if (const char *e = getenv("SP_CARVEOUT")) g_carveout = atoi(e);
     CKC(configure_push_kernel());
 
     // device allocations
@@ -866,11 +866,13 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_victims, Tn));
     if (c->n > SMEM_SORT_MAX) CKC(dalloc(c, &c->d_sort_tmp, 4 * Tn));
     CKC(dalloc(c, &c->d_partial, (size_t)c->T * c->g.nh * c->D));
-    CKC(dalloc(c, &c->d_pprof, 2 * (size_t)c->T + 2));
-    CKC(cudaMemset(c->d_pprof, 0, (2 * (size_t)c->T + 2) * sizeof(unsigned long long)));
+    CKC(dalloc(c, &c->d_pprof, 18 * (size_t)c->T + 2 + 4096));
+    CKC(cudaMemset(c->d_pprof, 0, (18 * (size_t)c->T + 2 + 4096) * sizeof(unsigned long long)));
+    CKC(cudaMemset(c->d_pprof + 18 * (size_t)c->T + 2, 0xFF, 1024 * sizeof(unsigned long long)));
     CKC(dalloc(c, &c->d_host, c->T));
     CKC(dalloc(c, &c->d_ctl, RING));
-    CKC(dalloc(c, &c->d_wb, (size_t)c->XSR * Tn * c->D));
+    CKC(dalloc(c, &c->d_xdone, RING));
+    CKC(cudaMemset(c->d_xdone, 0, RING * sizeof(uint32_t)));
     c->idx_bytes = Tn * ((c->flags & SP_FLAG_INDEX_I32) ? 4 : 8);
     for (int r = 0; r < RING; r++) {
         cudaError_t st;
@@ -890,7 +892,11 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaHostAlloc((void **)&c->h_scat, sizeof(unsigned long long), cudaHostAllocMapped));
     *c->h_scat = 0;
     CKC(cudaHostGetDevicePointer((void **)&c->d_scat, c->h_scat, 0));
-    CKC(cudaHostAlloc((void **)&c->h_wb, (size_t)c->XSR * Tn * c->D * sizeof(float), cudaHostAllocDefault));
+    CKC(cudaHostAlloc((void **)&c->h_wb, (size_t)c->XSR * Tn * c->D * sizeof(float), cudaHostAllocMapped));
+    CKC(cudaHostGetDevicePointer((void **)&c->hd_wb, c->h_wb, 0));
+    CKC(cudaHostAlloc((void **)&c->h_staged, RING * sizeof(unsigned long long), cudaHostAllocMapped));
+    std::memset(c->h_staged, 0, RING * sizeof(unsigned long long));
+    CKC(cudaHostGetDevicePointer((void **)&c->hd_staged, c->h_staged, 0));
     CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
     CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
     CKC(cudaHostAlloc((void **)&c->hl_ent, (size_t)RING * Tn * sizeof(uint2), cudaHostAllocMapped));
@@ -1020,6 +1026,10 @@ sp_status sp_set_profiling(sp_ctx *c, int32_t on) {
     CK(cudaSetDevice(c->device));
     std::lock_guard<std::mutex> lk(c->prof_mu);
     if (on) {
+        // per-launch k_push spans restart with this profiling window
+        const size_t so = 18 * (size_t)c->T + 2;
+        CK(cudaMemsetAsync(c->d_pprof + so, 0xFF, 1024 * sizeof(unsigned long long), c->plan_s));
+        CK(cudaMemsetAsync(c->d_pprof + so + 1024, 0, 3072 * sizeof(unsigned long long), c->plan_s));
         if (!c->prof_ref) CK(cudaEventCreate(&c->prof_ref));
         CK(cudaEventRecord(c->prof_ref, c->compute));
         c->timeline.clear();
@@ -1117,7 +1127,7 @@ sp_status sp_flush(sp_ctx *c) {
         return s;
     CK(cudaStreamSynchronize(c->plan_s));
     CK(cudaStreamSynchronize(c->xfer_s));
-    CK(cudaStreamSynchronize(c->d2h_s));
+    CK(cudaStreamSynchronize(c->xfer_s2));
     CK(cudaStreamSynchronize(c->compute));
     if (sp_status s = sync_error(c)) return s;
     FlushArgs a{};
@@ -1169,7 +1179,9 @@ sp_status capture_step(sp_ctx *c, int r) {
     a.idx_stride = k.stride;
     CK(cudaStreamBeginCapture(c->cap_s, cudaStreamCaptureModeThreadLocal));
     cudaStreamWaitEvent(c->cap_s, c->ev_train[rj], cudaEventWaitExternal);
+    if (c->stage_timing) cudaEventRecordWithFlags(c->sev[r][0], c->cap_s, cudaEventRecordExternal);
     launch_push(a, c->cap_s);
+    if (c->stage_timing) cudaEventRecordWithFlags(c->sev[r][1], c->cap_s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(c->ev_plan[rb], c->cap_s, cudaEventRecordExternal);
     CK(cudaStreamEndCapture(c->cap_s, &gr));
     CK(cudaGraphInstantiate(&c->gplan[r], gr, 0));
@@ -1182,13 +1194,19 @@ sp_status capture_step(sp_ctx *c, int r) {
     tb.lr = k.lr;
     CK(cudaStreamBeginCapture(c->cap_s, cudaStreamCaptureModeThreadLocal));
     cudaStreamWaitEvent(c->cap_s, c->ev_xfer[r], cudaEventWaitExternal);
+    const bool st = c->stage_timing;
+    if (st) cudaEventRecordWithFlags(c->sev[r][2], c->cap_s, cudaEventRecordExternal);
     launch_forward(ta, c->cap_s);
+    if (st) cudaEventRecordWithFlags(c->sev[r][3], c->cap_s, cudaEventRecordExternal);
     launch_surrogate(k.pooled, k.grad, (long long)c->T * c->N * c->D, k.gamma, k.delta, c->cap_s);
+    if (st) cudaEventRecordWithFlags(c->sev[r][4], c->cap_s, cudaEventRecordExternal);
     launch_backward(tb, c->cap_s);
+    if (st) cudaEventRecordWithFlags(c->sev[r][5], c->cap_s, cudaEventRecordExternal);
     cudaEventRecordWithFlags(c->ev_train[r], c->cap_s, cudaEventRecordExternal);
     CK(cudaStreamEndCapture(c->cap_s, &gr));
     CK(cudaGraphInstantiate(&c->gcomp[r], gr, 0));
     cudaGraphDestroy(gr);
+    c->sev_used[r][0] = st;
     return SP_OK;
 }
 
@@ -1338,7 +1356,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->graph_steps = c->graph_steps;
     if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);
-        cudaStreamSynchronize(c->d2h_s);
+        cudaStreamSynchronize(c->xfer_s2);
         cudaStreamSynchronize(c->compute);
         harvest_profile(c, true);
     }
@@ -1419,11 +1437,51 @@ sp_status sp_debug_slots(sp_ctx *c, int32_t t, int64_t *resident, int64_t *last_
     return SP_OK;
 }
 
+sp_status sp_set_stage_timing(sp_ctx *c, int32_t on) {
+    if (!c) return SP_ERR_INVALID_ARG;
+    if ((on != 0) != c->stage_timing) {
+        c->stage_timing = on != 0;
+        drop_graphs(c);  // recaptured with / without the timing event nodes
+        for (int r = 0; r < RING; r++) c->sev_used[r][0] = c->sev_used[r][1] = false;
+    }
+    return SP_OK;
+}
+
+sp_status sp_stage_times(sp_ctx *c, double *out_ms, int32_t *n_out) {
+    if (!c || !out_ms || !n_out) return SP_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    double sum[5] = {0, 0, 0, 0, 0};
+    int cnt[5] = {0, 0, 0, 0, 0};
+    auto el = [&](cudaEvent_t a, cudaEvent_t b, int k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) {
+            sum[k] += ms;
+            cnt[k]++;
+        }
+        (void)cudaGetLastError();
+    };
+    for (int r = 0; r < RING; r++) {
+        if (c->sev_used[r][0]) {
+            el(c->sev[r][0], c->sev[r][1], 0);
+            el(c->sev[r][2], c->sev[r][3], 2);
+            el(c->sev[r][3], c->sev[r][4], 3);
+            el(c->sev[r][4], c->sev[r][5], 4);
+        }
+        if (c->sev_used[r][1]) el(c->sev[r][6], c->sev[r][7], 1);
+    }
+    for (int k = 0; k < 5; k++) {
+        out_ms[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
+        n_out[k] = cnt[k];
+    }
+    return SP_OK;
+}
+
 sp_status sp_debug_plan_profile(sp_ctx *c, uint64_t *out) {
     if (!c || !out) return SP_ERR_INVALID_ARG;
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->plan_s));
-    CK(cudaMemcpy(out, c->d_pprof, (2 * (size_t)c->T + 2) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, c->d_pprof, (18 * (size_t)c->T + 2 + 4096) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     return SP_OK;
 }
 

@@ -141,7 +141,10 @@ struct XferArgs {
     BatchBufs bb;
     float *storage;
     float *const *host;       // [T] device-visible (mapped) host table pointers
-    float *wb_stage;          // [sum m][D] victims (D2H DMA, then CPU scatter)
+    float *wb_stage;          // [sum m][D] victims: pinned host staging (device alias)
+    uint32_t *done_ctr;       // CTA arrivals (the last CTA resets it)
+    unsigned long long *staged;  // pinned host flag: = b + 1 once every victim is staged
+    long long b;
     const unsigned long long *err;
 };
 
@@ -203,6 +206,14 @@ cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, 
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
 size_t push_smem_bytes(int n);
+// shared-memory carveout (percent) requested for every kernel of the library,
+// -1 = driver default; set once at sp_create (SP_CARVEOUT) so consecutive
+// kernels on an SM do not force an L1/shared reconfiguration
+extern int g_carveout;
+template <typename K>
+inline void apply_carveout(K kernel) {
+    if (g_carveout >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
+}
 cudaError_t configure_push_kernel();
 
 }  // namespace sp
