@@ -183,6 +183,81 @@ __device__ bool radix_sort_pairs(uint32_t *ka, uint32_t *va, uint32_t *kb, uint3
     return swapped;
 }
 
+// Shared-memory LSD radix sort of (key, val) pairs by key for n <= IPT *
+// PUSH_THREADS, one tile per pass.  Warp w owns the contiguous run
+// [w*32*IPT, (w+1)*32*IPT) and ranks it in rounds of 32 in input order, so
+// equal digits keep their order: stable.  Per pass: the digit peers of a lane
+// come from 9 ballots (a warp multisplit), each warp counts its digits in its
+// own row of s_wcnt, ONE block-wide exclusive scan over the (digit, warp)
+// counters in digit-major order gives every (digit, warp) its output offset,
+// and the elements are scattered.  No histogram pre-pass, no serial loop over
+// warps.  Returns true if the result ends in (kb, vb).
+template <int IPT>
+__device__ bool radix_sort_smem(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, int n, int bits) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    bool swapped = false;
+    for (int sh = 0; sh < bits; sh += 8) {
+        for (int k = threadIdx.x; k < NW * 256; k += blockDim.x) (&s_wcnt[0][0])[k] = 0;
+        __syncthreads();
+        uint32_t key[IPT], val[IPT], rk[IPT];
+        unsigned dg[IPT];
+        const int wbase = warp * 32 * IPT;
+#pragma unroll
+        for (int r = 0; r < IPT; r++) {
+            const int i = wbase + r * 32 + lane;
+            const bool ok = i < n;
+            key[r] = ok ? ka[i] : 0u;
+            val[r] = ok ? va[i] : 0u;
+            dg[r] = ok ? ((key[r] >> sh) & 255u) : 256u;
+            unsigned peers = 0xffffffffu;
+#pragma unroll
+            for (int b = 0; b < 9; b++) {
+                const bool bit = (dg[r] >> b) & 1u;
+                const unsigned bal = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bal : ~bal;
+            }
+            const uint32_t base = dg[r] < 256u ? s_wcnt[warp][dg[r]] : 0u;
+            rk[r] = base + __popc(peers & lt);
+            __syncwarp();
+            if (dg[r] < 256u && (peers & lt) == 0) s_wcnt[warp][dg[r]] = base + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        // exclusive scan of the counters in (digit, warp) order: thread t owns
+        // the NW*256/blockDim consecutive entries e = d*NW + w of its range
+        constexpr int PER = NW * 256 / PUSH_THREADS;
+        uint32_t c[PER], sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; q++) {
+            const int e = threadIdx.x * PER + q;
+            c[q] = s_wcnt[e % NW][e / NW];
+            sum += c[q];
+        }
+        uint32_t tot;
+        uint32_t run = block_scan(sum, &tot);
+#pragma unroll
+        for (int q = 0; q < PER; q++) {
+            const int e = threadIdx.x * PER + q;
+            s_wcnt[e % NW][e / NW] = run;
+            run += c[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < IPT; r++)
+            if (dg[r] < 256u) {
+                const uint32_t pos = s_wcnt[warp][dg[r]] + rk[r];
+                kb[pos] = key[r];
+                vb[pos] = val[r];
+            }
+        __syncthreads();
+        uint32_t *tk = ka, *tv = va;
+        ka = kb; va = vb; kb = tk; vb = tv;
+        swapped = !swapped;
+    }
+    return swapped;
+}
+
 // ------------------------------------------------------------------ dedup
 __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, long long j, const void *idx) {
     // (the chunk records of D3 use the sort's free ping-pong buffer as scratch)
@@ -217,13 +292,15 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
     }
     pc.mark(0);
     // D2: sort by id (stable: occurrences stay ascending within an id).  LSD
-    // radix over the table's id bits (1-3 passes): measured faster here than a
-    // shared-memory bitonic sort of packed (id, occurrence) keys (17.8 vs
-    // 13.7 us for n = 2048 on a 24-bit table, every table paying the full
-    // 66 barrier stages)
+    // radix over the table's id bits (1-3 passes of 8 bits).  (A shared-memory
+    // bitonic sort of packed (id, occurrence) keys was measured slower:
+    // 17.8 us for n = 2048, every table paying the full 66 barrier stages.)
     const int bits = bit_width_u64((unsigned long long)(R - 1));
-    const bool sw = small ? radix_sort_pairs<2048 / PUSH_THREADS>(ka, va, kb, vb, n, bits)
-                          : radix_sort_pairs<4096 / PUSH_THREADS>(ka, va, kb, vb, n, bits);
+    bool sw;
+    if (n <= 2 * PUSH_THREADS) sw = radix_sort_smem<2>(ka, va, kb, vb, n, bits);
+    else if (n <= 4 * PUSH_THREADS) sw = radix_sort_smem<4>(ka, va, kb, vb, n, bits);
+    else if (small) sw = radix_sort_smem<SMEM_SORT_MAX / PUSH_THREADS>(ka, va, kb, vb, n, bits);
+    else sw = radix_sort_pairs<4096 / PUSH_THREADS>(ka, va, kb, vb, n, bits);
     const uint32_t *keys = sw ? kb : ka;
     const uint32_t *vals = sw ? vb : va;
     __syncthreads();
@@ -314,51 +391,53 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
 }
 
 // ------------------------------------------------------------------- plan
-__device__ void plan_table(const PushArgs &A, int t, long long b) {
+__device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char *smem_raw) {
     const Geometry &g = A.g;
     const int n = g.n, tid = threadIdx.x;
     __shared__ uint32_t s_fail, s_got;
     __shared__ unsigned long long s_head, s_newhead, s_tail;
     const unsigned long long roff = A.row_off[t];
     const BatchBufs &pb = A.pb;
+    // working lists of this Plan: in the CTA's dynamic shared memory (the same
+    // 16n bytes the dedup role sorts in) when n <= SMEM_SORT_MAX, else global
+    const bool small = n <= SMEM_SORT_MAX;
+    uint32_t *w_uid = small ? reinterpret_cast<uint32_t *>(smem_raw) : nullptr;   // uniq_id of B(b)
+    uint32_t *slot_l = small ? w_uid + n : pb.slot_u + (size_t)t * n;               // slot per unique
+    uint32_t *miss_u = small ? w_uid + 2 * n : A.miss_u + (size_t)t * n;
+    uint32_t *victims = small ? w_uid + 3 * n : A.victims + (size_t)t * n;
+    uint32_t *slot_u = pb.slot_u + (size_t)t * n;                                    // global copy
 
     PhaseClock pc(A.prof, g.T, 0, t);
-    // P1: future probe of B(b+F)
-    if (A.has_future) {
-        const uint32_t Uf = A.fb.U[t];
-        const uint32_t *fid = A.fb.uniq_id + (size_t)t * n;
-        const int32_t stamp = (int32_t)(b + A.F);
-        for (uint32_t u = tid; u < Uf; u += blockDim.x) {
-            const uint32_t s = A.hitmap[roff + fid[u]];
-            if (s != EMPTY) A.next_need[s] = stamp;
-        }
-    }
-    pc.mark(0);
-    // P2: probe B(b); hits stamped, misses compacted (ascending ID)
+    // P1 + P2 in one pass (independent probes of the same Hit-Map):
+    // P1 future probe: resident IDs of B(b+F) get next_need = b+F;
+    // P2 probe of B(b): hits stamped last_use = b, misses compacted in
+    // ascending ID order (Alg. 1)
     const uint32_t Ub = pb.U[t];
+    const uint32_t Uf = A.has_future ? A.fb.U[t] : 0u;
+    const uint32_t *fid = A.fb.uniq_id + (size_t)t * n;
     const uint32_t *uniq_id = pb.uniq_id + (size_t)t * n;
-    uint32_t *slot_u = pb.slot_u + (size_t)t * n;
+    const int32_t fstamp = (int32_t)(b + A.F);
     uint8_t *hitf = pb.hit + (size_t)t * n;
-    uint32_t *miss_u = A.miss_u + (size_t)t * n;
-    uint32_t *victims = A.victims + (size_t)t * n;
+    const uint32_t Umax = Ub > Uf ? Ub : Uf;
     uint32_t carry = 0;
-    for (uint32_t u0 = 0; u0 < Ub; u0 += blockDim.x) {
+    for (uint32_t u0 = 0; u0 < Umax; u0 += blockDim.x) {
         const uint32_t u = u0 + tid;
+        const uint32_t idf = u < Uf ? fid[u] : 0u;
+        const uint32_t idb = u < Ub ? uniq_id[u] : 0u;
+        const uint32_t sf = u < Uf ? A.hitmap[roff + idf] : EMPTY;
+        const uint32_t sb = u < Ub ? A.hitmap[roff + idb] : EMPTY;
+        if (sf != EMPTY) A.next_need[sf] = fstamp;
         uint32_t miss = 0;
         if (u < Ub) {
-            const uint32_t s = A.hitmap[roff + uniq_id[u]];
-            if (s != EMPTY) {
-                A.last_use[s] = (int32_t)b;
-                slot_u[u] = s;
-                hitf[u] = 1;
-            } else {
-                slot_u[u] = EMPTY;
-                hitf[u] = 0;
-                miss = 1;
-            }
+            if (small) w_uid[u] = idb;
+            if (sb != EMPTY) A.last_use[sb] = (int32_t)b;
+            else miss = 1;
+            slot_l[u] = sb;
+            if (small) slot_u[u] = sb;
+            hitf[u] = sb != EMPTY;
         }
         uint32_t tot;
-        const uint32_t ex = block_scan(miss, &tot);  // barriers: P1 and stamps visible below
+        const uint32_t ex = block_scan(miss, &tot);  // barriers: stamps visible below
         if (miss) miss_u[carry + ex] = u;
         carry += tot;
     }
@@ -366,6 +445,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
     const uint32_t nhit = Ub - m;
     __syncthreads();
 
+    pc.mark(0);
     pc.mark(1);
     // P3: victim selection over the per-table LRU log
     const unsigned long long cap = A.log_cap[t], lbase = A.log_base[t];
@@ -429,7 +509,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
     uint32_t nev = 0;
     uint2 *hent = A.hl.ent + (size_t)t * n;  // pinned host mirror (zero-copy, ~8 B per fill)
     for (uint32_t k = tid; k < m; k += blockDim.x) {
-        const uint32_t u = miss_u[k], s = victims[k], id = uniq_id[u];
+        const uint32_t u = miss_u[k], s = victims[k], id = small ? w_uid[u] : uniq_id[u];
         const uint32_t old = A.resident[s];
         if (old != EMPTY) {
             A.hitmap[roff + old] = EMPTY;
@@ -439,7 +519,8 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
         A.resident[s] = id;
         A.last_use[s] = (int32_t)b;
         A.next_need[s] = NEVER;
-        slot_u[u] = s;
+        slot_l[u] = s;
+        if (small) slot_u[u] = s;
         fill_slot[k] = s;
         fill_row[k] = id;
         evict_row[k] = old;
@@ -487,7 +568,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
     }
     for (uint32_t u = tid; u < Ub; u += blockDim.x) {
         const size_t ix = (size_t)(lbase + (tail + u) % cap);
-        lslot[ix] = slot_u[u];
+        lslot[ix] = slot_l[u];
         lstamp[ix] = (int32_t)b;
     }
     if (tid == 0) {
@@ -516,7 +597,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
         }
 #pragma unroll
         for (int q = 0; q < 4; q++)
-            if (i0 + q * (int)blockDim.x < n) sl[q] = slot_u[u[q]];
+            if (i0 + q * (int)blockDim.x < n) sl[q] = slot_l[u[q]];
 #pragma unroll
         for (int q = 0; q < 4; q++)
             if (i0 + q * (int)blockDim.x < n) slot_of_occ[o[q]] = sl[q];
@@ -524,8 +605,8 @@ __device__ void plan_table(const PushArgs &A, int t, long long b) {
     ChunkRec *rec = pb.chunk_rec + (size_t)t * g.nc;
     uint4 *hot = pb.hot_rec + (size_t)t * g.nh;
     const uint32_t nch = pb.nchunks[t], nhot = pb.nhot[t];
-    for (uint32_t c = tid; c < nch; c += blockDim.x) rec[c].slot = slot_u[rec[c].slot];
-    for (uint32_t h = tid; h < nhot; h += blockDim.x) hot[h].x = slot_u[hot[h].x];
+    for (uint32_t c = tid; c < nch; c += blockDim.x) rec[c].slot = slot_l[rec[c].slot];
+    for (uint32_t h = tid; h < nhot; h += blockDim.x) hot[h].x = slot_l[hot[h].x];
     if (A.prof) {
         __syncthreads();
         pc.mark(5);
@@ -550,7 +631,7 @@ __global__ void __launch_bounds__(PUSH_THREADS, PUSH_THREADS >= 1024 ? 1 : 2) k_
     if (A.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     const bool role_plan = (int)blockIdx.x < T;
     if (role_plan) {
-        if (A.do_plan) plan_table(A, blockIdx.x, b);
+        if (A.do_plan) plan_table(A, blockIdx.x, b, smem_raw);
     } else if (A.has_new) {
         dedup_table(A, blockIdx.x - T, smem_raw, j, idx);
     }

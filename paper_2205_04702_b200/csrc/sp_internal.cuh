@@ -26,7 +26,10 @@ constexpr uint32_t EMPTY = 0xFFFFFFFFu;     // empty Hit-Map entry / vacant slot
 constexpr int32_t VACANT = INT32_MIN;       // last_use of a never-used slot
 constexpr int32_t NEVER = INT32_MIN;        // next_need of a slot with no future use
 constexpr int CH = 16;                      // occurrences per backward chunk
-constexpr int PUSH_THREADS = 1024;            // one CTA per table and role (k_push)
+#ifndef SP_PUSH_THREADS
+#define SP_PUSH_THREADS 1024
+#endif
+constexpr int PUSH_THREADS = SP_PUSH_THREADS;  // one CTA per table and role (k_push)
 constexpr int SMEM_SORT_MAX = 8192;         // n handled by the shared-memory radix sort
 constexpr unsigned long long NO_ERR = ~0ull;
 
