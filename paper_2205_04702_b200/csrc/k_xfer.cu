@@ -1,25 +1,25 @@
 // k_xfer.cu — the GPU side of [Collect] / [Exchange] / [Insert] (PAPER.md
 // P:688-704) and the end-of-run write-back.
 //
-// Direction by direction, on measurements of this platform
-// (profiles/r01_interference_microbench.txt, r01_host_gather.txt):
-//   host -> HBM  SM zero-copy reads from a BOUNDED grid (8 CTAs): reads are
-//                the benign direction (~1.2-1.6x on concurrent HBM kernels
-//                vs ~6x for full-rate writes), and the GPU gathers the rows
-//                itself: no CPU copy (random host rows cost ~31 ns/row/core
-//                in this VM) and no per-batch API calls for sizes.
+// Direction by direction, on measurements of this platform (
+// profiles/r01_host_tlb_microbench.txt, r01_tma_xfer_microbench*.txt):
+//   host -> HBM  the GPU pulls the missed rows itself from a BOUNDED grid of
+//                one-warp CTAs (16): random host rows are bound by address
+//                translation on the host side of the link, not bandwidth,
+//                and more SMs mostly add interference with the Train
+//                kernels.  Rows move as whole-row TMA bulk copies
+//                (cp.async.bulk, one request per row instead of 16-B loads).
 //   HBM -> host  the same kernel writes the victims, contiguously, into a
-//                pinned host staging slot (sequential pages: few address
+//                pinned host staging slot (sequential pages: few
 //                translations), raises a pinned flag when the last CTA is
-//                done, and the CPU threads of the transfer engine scatter them
-//                into the host tables (runtime.cu): random host rows are
-//                translated by the CPU MMU, not the IOMMU the pulls use.
-//   k_pullfill (transfer stream): for every fill k (slot s, missed row x,
-//   previous resident o) of Plan(b), staging index i = prefix + k:
-//       wb_stage[i] <- Storage[s]     if o is valid (dirty victim, P:693-696;
-//                                     pinned host staging, zero-copy store)
-//       Storage[s]  <- host[t][x]     zero-copy PCIe read
-//   the same lane reads the victim before overwriting the slot.
+//                done, and the CPU threads of the transfer engine scatter
+//                them into the host tables (runtime.cu): random host rows
+//                are translated by the CPU MMU, not the IOMMU the pulls use.
+//   for every fill k (slot s, missed row x, previous resident o) of Plan(b),
+//   staging index i = prefix + k:
+//       smem <- Storage[s], smem' <- host[t][x]   (both land before any store)
+//       wb_stage[i] <- smem      if o is valid (dirty victim)
+//       Storage[s]  <- smem'     (the freed slot gets the missed row)
 #include "sp_internal.cuh"
 
 namespace sp {
@@ -40,93 +40,132 @@ __device__ __forceinline__ void publish_staged(const XferArgs &A) {
     }
 }
 
-// G lanes per row, VPL float4 per lane, XU rows in flight per lane group.
-// Per fill k (slot s, missed row x, previous resident o), staging i = prefix + k:
-//   wb_stage[i] <- Storage[s]        if o is valid (dirty victim -> pinned staging)
-//   Storage[s]  <- host[t][x]        zero-copy PCIe read (bounded grid)
-template <int G, int VPL>
-__global__ void __launch_bounds__(256) k_pullfill(XferArgs A) {
-    if (*A.err != NO_ERR) return;
-    constexpr int XU = 4;
-    const Geometry g = A.g;
-    const int D4 = g.D / 4;
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "SP_MBW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra SP_MBW;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global (HBM or mapped host) -> shared, completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// shared -> global (HBM or mapped host), bulk async-group of the issuing thread
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+}  // namespace
+
+// k_pullfill (one warp per CTA): per fill, the victim row
+// (HBM) and the missed row (host, zero-copy) are brought into shared memory
+// by cp.async.bulk, then stored by cp.async.bulk to the staging row (host,
+// contiguous) and the slot (HBM).  A whole 256-B row moves as one bulk
+// request instead of sixteen 16-B loads.  The flattened fill list is split
+// into contiguous shares, one per CTA, moved in rounds of nb items (one per
+// lane) through XS shared-memory stages.
+constexpr int XS = 4;
+
+__global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t bar[XS];
     __shared__ uint32_t s_pref[65];
-    const int gpb = blockDim.x / G;
-    const int lane = threadIdx.x % G;
-    float4 *st = reinterpret_cast<float4 *>(A.storage);
-    float4 *wbs = reinterpret_cast<float4 *>(A.wb_stage);
-    uint32_t base_t0 = 0;  // staging rows of the tables before t0
+    __shared__ uint32_t s_slot[XS][32], s_stage[XS][32];
+    if (*A.err != NO_ERR) return;
+    const Geometry g = A.g;
+    const uint32_t rowb = (uint32_t)g.D * 4u;
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+        for (int s = 0; s < XS; s++) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase_ctr = 0;  // rounds issued so far over all stages (parity source)
+    uint32_t base_t0 = 0;    // staging rows of the tables before t0
     for (int t0 = 0; t0 < g.T; t0 += 64) {
         const int tcount = min(64, g.T - t0);
-        table_prefix(A.bb.m, t0, tcount, s_pref);
+        table_prefix(A.bb.m, t0, tcount, s_pref);  // (32 threads: one warp)
         const uint32_t total = s_pref[tcount];
-        const uint32_t ngroups = gridDim.x * gpb;
-        for (uint32_t base = (blockIdx.x * gpb + threadIdx.x / G) * XU; base < total; base += ngroups * XU) {
-            uint32_t slot[XU];
-            size_t idx[XU];
-            bool wb[XU];
-            const float4 *src[XU];
-#pragma unroll
-            for (int r = 0; r < XU; r++) {
-                const uint32_t item = base + r;
-                slot[r] = EMPTY;
-                if (item < total) {
-                    const int tl = find_table(s_pref, tcount, item);
-                    const size_t kk = (size_t)(t0 + tl) * g.n + (item - s_pref[tl]);
-                    idx[r] = (size_t)base_t0 + item;
-                    slot[r] = A.bb.fill_slot[kk];
-                    wb[r] = A.bb.evict_row[kk] != EMPTY;
-                    src[r] = reinterpret_cast<const float4 *>(A.host[t0 + tl] + (size_t)A.bb.fill_row[kk] * g.D);
-                }
+        const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+        const uint32_t lo = min(total, blockIdx.x * per), hi = min(total, lo + per);
+        const uint32_t nround = hi > lo ? (hi - lo + nb - 1) / nb : 0;
+        auto vbuf = [&](int s, int i) { return sm + ((size_t)s * nb + i) * 2 * rowb; };
+        auto issue = [&](uint32_t r) {
+            const int s = (int)((phase_ctr + r) % XS);
+            const uint32_t k0 = lo + r * nb;
+            const uint32_t cnt = min((uint32_t)nb, hi - k0);
+            uint32_t bytes = 0, slot = EMPTY, stage = EMPTY;
+            const float *src_host = nullptr;
+            if ((uint32_t)lane < cnt) {
+                const uint32_t item = k0 + lane;
+                const int tl = find_table(s_pref, tcount, item);
+                const int t = t0 + tl;
+                const size_t kk = (size_t)t * g.n + (item - s_pref[tl]);
+                slot = A.bb.fill_slot[kk];
+                src_host = A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
+                if (A.bb.evict_row[kk] != EMPTY) stage = base_t0 + item;
+                bytes = rowb * (stage != EMPTY ? 2u : 1u);
             }
-            float4 x[XU][VPL];
-#pragma unroll
-            for (int r = 0; r < XU; r++)  // PCIe reads in flight first
-                if (slot[r] != EMPTY)
-#pragma unroll
-                    for (int q = 0; q < VPL; q++) x[r][q] = __ldcv(src[r] + lane + q * G);
-#pragma unroll
-            for (int r = 0; r < XU; r++)  // victims staged while the reads fly
-                if (slot[r] != EMPTY && wb[r])
-#pragma unroll
-                    for (int q = 0; q < VPL; q++)
-                        wbs[idx[r] * D4 + lane + q * G] = st[(size_t)slot[r] * D4 + lane + q * G];
-#pragma unroll
-            for (int r = 0; r < XU; r++)
-                if (slot[r] != EMPTY)
-#pragma unroll
-                    for (int q = 0; q < VPL; q++) st[(size_t)slot[r] * D4 + lane + q * G] = x[r][q];
+            s_slot[s][lane] = slot;
+            s_stage[s][lane] = stage;
+            const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
+            if (lane == 0) mbar_expect_tx(&bar[s], tot);
+            __syncwarp();
+            if (slot != EMPTY) {
+                if (stage != EMPTY) bulk_g2s(vbuf(s, lane), A.storage + (size_t)slot * g.D, rowb, &bar[s]);
+                bulk_g2s(vbuf(s, lane) + rowb, src_host, rowb, &bar[s]);
+            }
+        };
+        for (uint32_t r = 0; r < min((uint32_t)XS, nround); r++) issue(r);
+        for (uint32_t r = 0; r < nround; r++) {
+            const int s = (int)((phase_ctr + r) % XS);
+            mbar_wait(&bar[s], ((phase_ctr + r) / XS) & 1u);
+            const uint32_t slot = s_slot[s][lane], stage = s_stage[s][lane];
+            if (slot != EMPTY) {
+                if (stage != EMPTY) bulk_s2g(A.wb_stage + (size_t)stage * g.D, vbuf(s, lane), rowb);
+                bulk_s2g(A.storage + (size_t)slot * g.D, vbuf(s, lane) + rowb, rowb);
+            }
+            bulk_commit();
+            if (r + XS < nround) {
+                bulk_wait_read0();  // stage s has been read out: refill it
+                __syncwarp();
+                issue(r + XS);
+            }
         }
+        phase_ctr += nround;
         base_t0 += total;
+        bulk_wait0();
+        __syncwarp();
     }
+    bulk_wait0();
     publish_staged(A);
 }
 
-__global__ void __launch_bounds__(256) k_pullfill_generic(XferArgs A) {
-    if (*A.err != NO_ERR) return;
-    const Geometry g = A.g;
-    const int D4 = g.D / 4;
-    const int lane = threadIdx.x & 31;
-    float4 *st = reinterpret_cast<float4 *>(A.storage);
-    float4 *wbs = reinterpret_cast<float4 *>(A.wb_stage);
-    const int wpb = blockDim.x / 32;
-    size_t base = 0;
-    for (int t = 0; t < g.T; t++) {
-        const uint32_t m = A.bb.m[t];
-        const float *h = A.host[t];
-        for (uint32_t k = blockIdx.x * wpb + threadIdx.x / 32; k < m; k += gridDim.x * wpb) {
-            const size_t kk = (size_t)t * g.n + k, i = base + k;
-            const uint32_t s = A.bb.fill_slot[kk], x = A.bb.fill_row[kk];
-            const bool wb = A.bb.evict_row[kk] != EMPTY;
-            for (int c = lane; c < D4; c += 32) {
-                const float4 in = __ldcv(reinterpret_cast<const float4 *>(h + (size_t)x * g.D) + c);
-                if (wb) wbs[i * D4 + c] = st[(size_t)s * D4 + c];
-                st[(size_t)s * D4 + c] = in;
-            }
-        }
-        base += m;
-    }
-    publish_staged(A);
+int pullfill_tma_items(int D) {
+    const size_t budget = 192 * 1024, per_item = (size_t)2 * D * 4 * XS;
+    size_t nb = budget / per_item;
+    return (int)(nb > 32 ? 32 : (nb < 1 ? 1 : nb));
 }
 
 // write back every resident slot (sp_flush)
@@ -154,28 +193,15 @@ static int sm_count() {
 }
 
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s) {
-    const int grid = ctas > 0 ? ctas : 8;
+    const int nb = pullfill_tma_items(a.g.D);
+    const size_t smem = (size_t)nb * 2 * a.g.D * 4 * XS;
     static bool once = false;
     if (!once) {
-        apply_carveout(k_pullfill<16, 1>);
-        apply_carveout(k_pullfill<32, 1>);
-        apply_carveout(k_pullfill<32, 2>);
-        apply_carveout(k_pullfill<32, 4>);
-        apply_carveout(k_pullfill_generic);
+        cudaFuncSetAttribute(k_pullfill, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
+        apply_carveout(k_pullfill);
         once = true;
     }
-    switch (a.g.D / 4) {
-        case 1: k_pullfill<1, 1><<<grid, 256, 0, s>>>(a); break;
-        case 2: k_pullfill<2, 1><<<grid, 256, 0, s>>>(a); break;
-        case 4: k_pullfill<4, 1><<<grid, 256, 0, s>>>(a); break;
-        case 8: k_pullfill<8, 1><<<grid, 256, 0, s>>>(a); break;
-        case 16: k_pullfill<16, 1><<<grid, 256, 0, s>>>(a); break;
-        case 32: k_pullfill<32, 1><<<grid, 256, 0, s>>>(a); break;
-        case 64: k_pullfill<32, 2><<<grid, 256, 0, s>>>(a); break;
-        case 128: k_pullfill<32, 4><<<grid, 256, 0, s>>>(a); break;
-        case 256: k_pullfill<32, 8><<<grid, 256, 0, s>>>(a); break;
-        default: k_pullfill_generic<<<grid, 256, 0, s>>>(a); break;
-    }
+    k_pullfill<<<ctas > 0 ? ctas : 16, 32, smem, s>>>(a, nb);
     return cudaGetLastError();
 }
 

@@ -192,7 +192,7 @@ struct sp_ctx {
     uint32_t *d_xdone = nullptr;               // [RING] k_pullfill CTA arrival counters
     unsigned long long *h_scat = nullptr;      // pinned mapped: batches scattered
     unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
-    int pull_ctas = 8;
+    int pull_ctas = 16;  // k_pullfill grid (one warp per CTA); SP_PULL_CTAS overrides
     // timing diagnostics (SP_DIAG bit mask; results are then WRONG): 1 = the
     // transfer kernel moves nothing, 2 = the Train kernels do nothing
     int diag = 0;
@@ -761,7 +761,6 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->hit_total = c->row_off[c->T];
     c->XSR = std::max(4, c->F + 2);  // >= F+1: Transfer(b) waits for scatter(b-F-1) >= b-XSR
     c->host_threads = d->host_threads > 0 ? d->host_threads : 6;
-    c->pull_ctas = 8;
     if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_DIAG")) c->diag = atoi(e);
 
@@ -805,6 +804,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
             return bail(SP_ERR_INVALID_ARG);  // not pinned / registered
         }
         hdev[t] = static_cast<float *>(p);
+        // the transfer kernel moves whole rows with cp.async.bulk: 16-B aligned
+        if ((reinterpret_cast<uintptr_t>(p) & 15) != 0) return bail(SP_ERR_INVALID_ARG);
     }
     {   // Plan is the serial critical chain: its CTAs get scheduled first
         int lo = 0, hi = 0;

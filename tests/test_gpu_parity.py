@@ -252,3 +252,31 @@ def test_run_steps_pinned_host_trace_matches_oracle():
         finally:
             sp2.close()
     sp.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D", [64, 128, 256])
+def test_hot_row_segments_last_arriver_fold(D):
+    """Rows with more occurrences than one k_bwd segment (hs = 128 / 64 / 32
+    for D = 64 / 128 / 256): several CTAs fold segments, write fp64 partials,
+    and the last to arrive folds them in segment order (plus plain chunk
+    records from the large table in the same launch)."""
+    rows, N, L, nb = [3, 5, 4000], 512, 4, 8
+    tr = sample_trace(rows, N, L, 1.05, nb, 21 + D)
+    slots = [3, 5, min(4000, max_window_union(tr.numpy(), 2, 3, 2) + 5)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr,
+                     gde=(float(np.float32(0.5 / N)), float(np.float32(0.01 / N)), 0.5))
+    _assert_tables(rep, exact=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,L", [(750, 4), (1500, 4)])
+def test_smem_radix_tile_sizes(N, L):
+    """n = N*L = 3000 and 6000: the 4- and 8-element-per-thread shared-memory
+    radix passes of the dedup CTA (n = 2048 uses 2 per thread)."""
+    rows, D, nb = [50000, 700], 16, 8
+    tr = sample_trace(rows, N, L, 1.0, nb, N)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 10) for t, R in enumerate(rows)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr,
+                     gde=(float(np.float32(0.5 / N)), float(np.float32(0.01 / N)), 1.0))
+    _assert_tables(rep, exact=False)
