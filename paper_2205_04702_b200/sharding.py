@@ -40,6 +40,19 @@ def tables_of(owner: Sequence[int], rank: int) -> List[int]:
     return [t for t, r in enumerate(owner) if r == rank]
 
 
+def _all_to_all(recv, send, counts_in, counts_out, group):
+    """all_to_all_single; over a backend without CUDA all-to-all (gloo, used by
+    the tests to run several ranks on one GPU) the buffers go through host
+    memory.  NCCL moves CUDA tensors directly over NVLink."""
+    import torch.distributed as dist
+    if send.is_cuda and dist.get_backend(group) != "nccl":
+        r = recv.cpu()
+        dist.all_to_all_single(r, send.cpu(), counts_in, counts_out, group=group)
+        recv.copy_(r)
+    else:
+        dist.all_to_all_single(recv, send, counts_in, counts_out, group=group)
+
+
 def _split_bags(N: int, world: int) -> List[int]:
     base, rem = divmod(N, world)
     return [base + (1 if r < rem else 0) for r in range(world)]
@@ -49,14 +62,13 @@ def exchange_forward(pooled_local: torch.Tensor, owner: Sequence[int], rank: int
                      group=None) -> torch.Tensor:
     """[T_g][N][D] (this rank's tables, ascending table id) -> [T][N_r][D]
     (all tables, this rank's slice of the batch), via one all_to_all."""
-    import torch.distributed as dist
     Tg, N, D = pooled_local.shape
     nb = _split_bags(N, world)
     send = torch.cat([pooled_local[:, sum(nb[:h]):sum(nb[:h + 1])].reshape(-1) for h in range(world)])
     counts_in = [len(tables_of(owner, h)) * nb[rank] * D for h in range(world)]
     counts_out = [Tg * nb[h] * D for h in range(world)]
     recv = send.new_empty(sum(counts_in))
-    dist.all_to_all_single(recv, send, counts_in, counts_out, group=group)
+    _all_to_all(recv, send, counts_in, counts_out, group)
     out = recv.new_empty((len(owner), nb[rank], D))
     off = 0
     for h in range(world):
@@ -71,7 +83,6 @@ def exchange_forward(pooled_local: torch.Tensor, owner: Sequence[int], rank: int
 def exchange_backward(grad_batch: torch.Tensor, owner: Sequence[int], rank: int, world: int,
                       N: int, group=None) -> torch.Tensor:
     """Inverse of exchange_forward: [T][N_r][D] -> [T_g][N][D]."""
-    import torch.distributed as dist
     T, Nr, D = grad_batch.shape
     nb = _split_bags(N, world)
     mine = tables_of(owner, rank)
@@ -79,7 +90,7 @@ def exchange_backward(grad_batch: torch.Tensor, owner: Sequence[int], rank: int,
     counts_out = [len(tables_of(owner, h)) * Nr * D for h in range(world)]
     counts_in = [len(mine) * nb[h] * D for h in range(world)]
     recv = send.new_empty(sum(counts_in))
-    dist.all_to_all_single(recv, send, counts_in, counts_out, group=group)
+    _all_to_all(recv, send, counts_in, counts_out, group)
     out = recv.new_empty((len(mine), N, D))
     off = 0
     for h in range(world):

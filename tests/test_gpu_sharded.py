@@ -1,0 +1,95 @@
+"""Table-wise sharding on the GPU path (§6.7): two ranks,
+each with its own ScratchPipe context over its tables, exchange pooled
+embeddings and gradients with the all-to-all of bench.py's N>1 path.  The
+exchange is pure data movement and the surrogate is element-wise, so every
+rank's tables must match the single-process oracle.  Both ranks share cuda:0
+here (gloo process group; the driver's GPU box has one GPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle import UncachedTrainer
+        from paper_2205_04702_b200 import ScratchPipe
+        from paper_2205_04702_b200.sharding import (exchange_backward, exchange_forward, lpt_assign,
+                                                    table_weights, tables_of)
+        from tests.gpu_helpers import max_window_union, pinned_tables
+        from workload import sample_trace
+        rows, D, N, L, nb = [3000, 500, 1200, 40, 800], 32, 64, 3, 30
+        tr = sample_trace(rows, N, L, 0.95, nb, 77)
+        slots_all = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 6) for t, R in enumerate(rows)]
+        owner = lpt_assign(table_weights(rows, slots_all, N * L, D), world)
+        mine = tables_of(owner, rank)
+        torch.cuda.set_device(0)
+        tables_all = pinned_tables(rows, D, 4702)
+        tables = [tables_all[t] for t in mine]
+        sp = ScratchPipe([rows[t] for t in mine], tables, D, [slots_all[t] for t in mine], N, L,
+                         index_dtype="int32", index_on_device=True)
+        trace = tr[:, mine].to(torch.int32).cuda().contiguous()
+        g, d, e = 0.5, 0.01, 0.05
+        pooled = torch.empty((len(mine), N, D), device="cuda")
+        ahead = sp.F + sp.P + 1
+        for j in range(ahead):
+            sp.plan_device(trace[j])
+        for b in range(nb):
+            if b + ahead < nb:
+                sp.plan_device(trace[b + ahead])
+            elif b + ahead == nb:
+                sp.end_of_data()
+            sp.forward(pooled)
+            pb = exchange_forward(pooled, owner, rank, world)        # [T][N/2][D]
+            gb = sp.surrogate(pb, g, d)
+            gl = exchange_backward(gb, owner, rank, world, N)         # [T_mine][N][D]
+            sp.train(gl.contiguous(), e)
+        sp.flush()
+        torch.cuda.synchronize()
+        orc = UncachedTrainer(rows, D, N, L, 4702)
+        for b in range(nb):
+            orc.step(tr.numpy()[b], g, d, e)
+        worst = 0.0
+        for i, t in enumerate(mine):
+            touched = orc.touched(t)
+            got = tables[i][torch.from_numpy(touched)].numpy()
+            want = orc.rows_of(t, touched)
+            worst = max(worst, float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-4))))
+        sp.close()
+        q.put((rank, len(mine), worst, None))
+        dist.destroy_process_group()
+    except Exception as ex:  # pragma: no cover - reported to the parent
+        q.put((rank, 0, 1.0, repr(ex)))
+
+
+def test_two_ranks_tablewise_match_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=120)
+    for rank, ntab, worst, err in res:
+        assert err is None, err
+        assert ntab >= 1
+        assert worst <= 1e-5, (rank, worst)

@@ -11,7 +11,7 @@ python paper_2205_04702_b200/build.py > $O/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/ref.json 2> $O/ref.err
-KR='regex:^(k_push|k_pullfill|k_fwd|k_bwd|k_bwd_hot|k_surrogate)'
+KR='regex:^(k_push|k_pullfill|k_fwd|k_bwd|k_surrogate)'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KR" -s 3000 -c 600 --csv \
   --log-file $O/launches.csv python bench.py --steps 200 --warmup 5 --no-cpu-baseline --profile-steps 5 > $O/ncu_list.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k "$KR" -s 3000 -c 12 \
