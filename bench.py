@@ -460,7 +460,8 @@ def run_ours(args):
     # dominant HBM-bound kernel (the Train stage: forward or backward)
     dom = max(["forward", "backward"], key=lambda k: kernels[k]["avg_us"])
     ach = kernels[dom]["alg_GBs"] or 0.0
-    tr_bytes = traffic.get(dom)
+    # ncu DRAM traffic applies to the configuration it was captured on
+    tr_bytes = traffic.get(dom) if traffic.get("config", "kaggle") == args.config else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "duration_source": ("CUDA events around the kernel on its stream inside the step graphs "

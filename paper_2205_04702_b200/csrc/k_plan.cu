@@ -507,7 +507,6 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
     uint32_t *fill_row = pb.fill_row + (size_t)t * n;
     uint32_t *evict_row = pb.evict_row + (size_t)t * n;
     uint32_t nev = 0;
-    uint2 *hent = A.hl.ent + (size_t)t * n;  // pinned host mirror (zero-copy, ~8 B per fill)
     for (uint32_t k = tid; k < m; k += blockDim.x) {
         const uint32_t u = miss_u[k], s = victims[k], id = small ? w_uid[u] : uniq_id[u];
         const uint32_t old = A.resident[s];
@@ -524,18 +523,10 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
         fill_slot[k] = s;
         fill_row[k] = id;
         evict_row[k] = old;
-        hent[k] = make_uint2(id, old);
     }
     uint32_t ev_total;
     (void)block_scan(nev, &ev_total);  // barriers: P4 writes visible below
-    if (tid == 0) {
-        pb.m[t] = m;  // device copy for k_pullfill, published before the ready flag
-        A.hl.m[t] = m;
-        // the CTA's host-list writes precede this fence through the barrier
-        // above (causality order), so one system-scope fence publishes them all
-        __threadfence_system();
-        *(volatile unsigned long long *)&A.hl.ready[t] = (unsigned long long)(b + 1);
-    }
+    if (tid == 0) pb.m[t] = m;  // fills of table t for k_pullfill
 
     pc.mark(3);
     // P5: LRU log append (after an in-place compaction if it would overflow)

@@ -337,16 +337,32 @@ __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
 }
 
 // -------------------------------------------------------------- surrogate
+// Streaming: each thread keeps SU float4 loads in flight (loads first, then
+// the fmas and stores), so latency, not occupancy, is covered; element i's
+// result does not depend on the grid.
+constexpr int SU = 4;
 __global__ void __launch_bounds__(256) k_surrogate(const float4 *p, float4 *g, long long n4,
                                                    float gamma, float delta) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-         i += (long long)gridDim.x * blockDim.x) {
-        float4 x = __ldcs(p + i), y;
-        y.x = fmaf(gamma, x.x, delta);
-        y.y = fmaf(gamma, x.y, delta);
-        y.z = fmaf(gamma, x.z, delta);
-        y.w = fmaf(gamma, x.w, delta);
-        g[i] = y;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += SU * stride) {
+        float4 x[SU];
+#pragma unroll
+        for (int u = 0; u < SU; u++) {
+            const long long i = i0 + u * stride;
+            if (i < n4) x[u] = __ldcs(p + i);
+        }
+#pragma unroll
+        for (int u = 0; u < SU; u++) {
+            const long long i = i0 + u * stride;
+            if (i < n4) {
+                float4 y;
+                y.x = fmaf(gamma, x[u].x, delta);
+                y.y = fmaf(gamma, x[u].y, delta);
+                y.z = fmaf(gamma, x[u].z, delta);
+                y.w = fmaf(gamma, x[u].w, delta);
+                g[i] = y;
+            }
+        }
     }
 }
 
@@ -431,7 +447,7 @@ cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
                              float delta, cudaStream_t s) {
     long long n4 = count / 4;
-    long long blocks = (n4 + 255) / 256;
+    long long blocks = (n4 + 256 * SU - 1) / (256 * SU);
     const long long cap = (long long)num_sms() * 8;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;

@@ -25,15 +25,17 @@
 namespace sp {
 
 // Completion of Transfer(b) for the scatter thread: every CTA's staging stores
-// are made visible system-wide, then the last CTA to arrive raises the pinned
-// flag (and resets the counter for the next use of this ring slot).
-__device__ __forceinline__ void publish_staged(const XferArgs &A) {
+// (rows and their destination addresses) are made visible system-wide, then
+// the last CTA to arrive writes the item count and raises the pinned flag
+// (and resets the counter for the next use of this ring slot).
+__device__ __forceinline__ void publish_staged(const XferArgs &A, unsigned long long nstaged) {
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned k = atomicAdd(A.done_ctr, 1u);
         if (k == gridDim.x - 1) {
             *A.done_ctr = 0u;
+            *(volatile unsigned long long *)A.staged_cnt = nstaged;
             __threadfence_system();
             *(volatile unsigned long long *)A.staged = (unsigned long long)(A.b + 1);
         }
@@ -124,7 +126,11 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 const size_t kk = (size_t)t * g.n + (item - s_pref[tl]);
                 slot = A.bb.fill_slot[kk];
                 src_host = A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
-                if (A.bb.evict_row[kk] != EMPTY) stage = base_t0 + item;
+                const uint32_t old = A.bb.evict_row[kk];
+                if (old != EMPTY) stage = base_t0 + item;
+                // the scatter thread's work list: where the staged row goes
+                A.wb_dst[base_t0 + item] =
+                    old != EMPTY ? (unsigned long long)(uintptr_t)(A.host[t] + (size_t)old * g.D) : 0ull;
                 bytes = rowb * (stage != EMPTY ? 2u : 1u);
             }
             s_slot[s][lane] = slot;
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
         __syncwarp();
     }
     bulk_wait0();
-    publish_staged(A);
+    publish_staged(A, base_t0);  // base_t0 = sum over tables of m[t]
 }
 
 int pullfill_tma_items(int D) {

@@ -2,21 +2,22 @@
 //
 // Pipeline schedule: PAPER.md Fig. 8 re-expressed with CUDA
 // streams, events and a native transfer-engine thread instead of lock-step
-// cycles (DESIGN.md §3):
+// cycles (DESIGN.md §5.2):
 //
 //   plan stream     push(j): [H2D of B(j)] -> k_push: dedup B(j) beside
-//                   Plan(b = j-F-1) -> record ev_plan[b]; Plan(b) also
-//                   mirrors its fill lists into pinned host memory
-//   transfer stream Transfer(b) once Train(b-P-1) is enqueued (past window,
-//                   P:840-861): waits ev_plan[b], ev_train[b-P-1] and, on the
-//                   GPU, for the pinned counter "scattered >= b-F" (RAW-4,
-//                   the CPU write-back of batch b-F-1 has landed)
-//                   -> k_pullfill ([Collect] + [Insert] on the GPU side:
-//                   victims staged in HBM, missed rows pulled by zero-copy
-//                   reads into the freed slots) -> record ev_xfer[b]
-//   transfer engine (scatter thread + row-copy helpers): for b in order,
-//                   D2H DMA of the staged victims ([Exchange]) and CPU scatter
-//                   into the host tables ([Insert]), then scattered = b+1
+//                   Plan(b = j-F-1) -> record ev_plan[b]
+//   transfer streams (two, alternating batches) Transfer(b) once
+//                   Train(b-P-1) is enqueued (past window): waits
+//                   ev_plan[b], ev_train[b-P-1] and, on the GPU, for the
+//                   pinned counter "scattered >= b-F" (RAW-4: the
+//                   CPU write-back of batch b-F-1 has landed) -> k_pullfill
+//                   ([Collect] + [Exchange]: missed rows pulled into the freed
+//                   slots, victims written to pinned staging with their host
+//                   addresses; the last CTA raises h_staged[b]) -> ev_xfer[b]
+//   transfer engine (scatter thread + row-copy helpers, no CUDA calls): for
+//                   b in order, once h_staged[b] is up, CPU scatter of the
+//                   staged victims into the host tables ([Insert]), then
+//                   scattered = b+1
 //   compute stream  forward(b) waits ev_xfer[b]; train(b) -> record ev_train[b]
 //
 // No host synchronisation on the caller's thread in the steady state.
@@ -189,6 +190,10 @@ struct sp_ctx {
     float *hd_wb = nullptr;                    // its device alias
     unsigned long long *h_staged = nullptr;    // pinned mapped [RING]
     unsigned long long *hd_staged = nullptr;   // device alias
+    unsigned long long *h_wbdst = nullptr;     // pinned mapped [XSR][T*n]: host row of each staged victim
+    unsigned long long *hd_wbdst = nullptr;    // device alias
+    unsigned long long *h_scnt = nullptr;      // pinned mapped [RING]: staged items of the batch
+    unsigned long long *hd_scnt = nullptr;     // device alias
     uint32_t *d_xdone = nullptr;               // [RING] k_pullfill CTA arrival counters
     unsigned long long *h_scat = nullptr;      // pinned mapped: batches scattered
     unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
@@ -197,11 +202,6 @@ struct sp_ctx {
     // transfer kernel moves nothing, 2 = the Train kernels do nothing
     int diag = 0;
     long long xfer_enq = 0;                    // transfers enqueued (caller's thread)
-    // pinned host mirror of the fill lists, per ring slot
-    unsigned long long *hl_ready = nullptr;    // [RING][T]
-    uint32_t *hl_m = nullptr;                  // [RING][T]
-    uint2 *hl_ent = nullptr;                   // [RING][T][n]
-    HostList hl_dev[RING];                     // mapped device pointers of the same
     // pinned index staging
     void *h_stage = nullptr;
     unsigned long long *h_err = nullptr;      // exact device error key (sync copies)
@@ -254,6 +254,10 @@ struct sp_ctx {
     long long *d_ctl = nullptr;                 // [RING] device batch-index chain
     cudaGraphExec_t gplan[RING] = {}, gcomp[RING] = {};
     cudaStream_t cap_s = nullptr;
+    // plan graphs are captured on a high-priority stream: a captured kernel
+    // node keeps the priority of its capture stream, and k_push must stay
+    // ahead of the wide Train grids in graph mode as in eager mode
+    cudaStream_t cap_hi = nullptr;
     struct GraphKey {
         const void *trace = nullptr;
         long long stride = 0;
@@ -472,22 +476,12 @@ PushArgs push_args(sp_ctx *c) {
     return a;
 }
 
-// The host-list ring slot of Plan(b) is reused by Plan(b + RING): the transfer
-// engine must be done with batch b (gathered and scattered) first.
-sp_status wait_list_slot(sp_ctx *c, long long b) {
-    const long long prev = b - RING;
-    if (prev < 0) return SP_OK;
-    return wait_engine(c, [&] { return c->x_scattered.load(std::memory_order_acquire) > prev; });
-}
-
 sp_status enqueue_plan_only(sp_ctx *c, long long b) {
-    if (sp_status s = wait_list_slot(c, b)) return s;
     PushArgs a = push_args(c);
     a.has_new = 0;
     a.do_plan = 1;
     a.b = b;
     a.pb = c->ring[b % RING];
-    a.hl = c->hl_dev[b % RING];
     a.has_future = (b + c->F < c->pushed) ? 1 : 0;  // future window truncates at the end
     a.fb = c->ring[(b + c->F) % RING];
     CK(launch(c, SP_K_PLAN, b, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
@@ -525,31 +519,23 @@ void scatter_main(sp_ctx *c) {
     long long s = 0;  // next batch to scatter
     int idle = 0;
     auto ready = [&](long long b) {
-        const int r = (int)(b % RING);
-        if (((volatile unsigned long long *)c->h_staged)[r] != (unsigned long long)(b + 1)) return false;
-        for (int t = 0; t < c->T; t++)
-            if (((volatile unsigned long long *)c->hl_ready)[(size_t)r * c->T + t] != (unsigned long long)(b + 1))
-                return false;
+        if (((volatile unsigned long long *)c->h_staged)[b % RING] != (unsigned long long)(b + 1)) return false;
         std::atomic_thread_fence(std::memory_order_acquire);
         return true;
     };
     while (!c->stop.load(std::memory_order_relaxed)) {
         if (*(volatile unsigned long long *)c->h_errflag) break;
         if (s < c->x_enqueued.load(std::memory_order_acquire) && ready(s)) {
-            const int r = (int)(s % RING);
-            pref[0] = 0;
-            for (int t = 0; t < c->T; t++) pref[t + 1] = pref[t] + c->hl_m[(size_t)r * c->T + t];
+            const size_t cnt = (size_t)((volatile unsigned long long *)c->h_scnt)[s % RING];
             src.clear();
             dst.clear();
             const float *wb = c->h_wb + (size_t)(s % c->XSR) * slab;
-            for (int t = 0; t < c->T; t++) {
-                const uint2 *ent = c->hl_ent + ((size_t)r * c->T + t) * c->n;
-                for (uint32_t k = 0; k < pref[t + 1] - pref[t]; k++)
-                    if (ent[k].y != EMPTY) {
-                        src.push_back(wb + (size_t)(pref[t] + k) * c->D);
-                        dst.push_back(c->host[t] + (size_t)ent[k].y * c->D);
-                    }
-            }
+            const unsigned long long *wd = c->h_wbdst + (size_t)(s % c->XSR) * c->T * c->n;
+            for (size_t i = 0; i < cnt; i++)
+                if (wd[i]) {
+                    src.push_back(wb + i * c->D);
+                    dst.push_back(reinterpret_cast<float *>((uintptr_t)wd[i]));
+                }
             const auto t0 = std::chrono::steady_clock::now();
             c->spool.copy(src.data(), dst.data(), (long)src.size(), rowb);
             c->x_scatter_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -615,6 +601,8 @@ sp_status pump(sp_ctx *c) {
         a.wb_stage = c->hd_wb + (size_t)(b % c->XSR) * c->T * c->n * c->D;
         a.done_ctr = c->d_xdone + r;
         a.staged = c->hd_staged + r;
+        a.wb_dst = c->hd_wbdst + (size_t)(b % c->XSR) * c->T * c->n;
+        a.staged_cnt = c->hd_scnt + r;
         a.b = b;
         if (c->diag & 1) a.g.T = 0;  // diagnostic: transfer launched, no rows moved
         a.err = c->d_err;
@@ -655,7 +643,7 @@ void destroy_all(sp_ctx *c) {
     if (c->prof_ref) cudaEventDestroy(c->prof_ref);
     for (void *p : c->allocs) cudaFree(p);
     for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb, (void *)c->h_staged,
-                    (void *)c->hl_ready, (void *)c->hl_m, (void *)c->hl_ent})
+                    (void *)c->h_wbdst, (void *)c->h_scnt})
         if (p) cudaFreeHost(p);
     if (c->registered)
         for (int t = 0; t < c->T; t++) cudaHostUnregister(c->host[t]);
@@ -663,6 +651,7 @@ void destroy_all(sp_ctx *c) {
     if (c->own_xfer_s) cudaStreamDestroy(c->own_xfer_s);
     if (c->own_xfer_s2) cudaStreamDestroy(c->own_xfer_s2);
     if (c->cap_s) cudaStreamDestroy(c->cap_s);
+    if (c->cap_hi) cudaStreamDestroy(c->cap_hi);
     (void)cudaGetLastError();
     delete c;
 }
@@ -826,6 +815,12 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
             if (atoi(ds) == 1) c->plan_s = c->xfer_s = c->xfer_s2 = c->compute;
     }
     CKC(cudaStreamCreateWithFlags(&c->cap_s, cudaStreamNonBlocking));
+    {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        const char *gp = getenv("SP_PLAN_GRAPH_PRIO");  // 0: capture at default priority (A/B)
+        CKC(cudaStreamCreateWithPriority(&c->cap_hi, cudaStreamNonBlocking, (gp && atoi(gp) == 0) ? lo : hi));
+    }
     for (int r = 0; r < RING; r++)
         for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_train[r], &c->ev_h2d[r]})
             CKC(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
@@ -898,23 +893,11 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaHostAlloc((void **)&c->h_staged, RING * sizeof(unsigned long long), cudaHostAllocMapped));
     std::memset(c->h_staged, 0, RING * sizeof(unsigned long long));
     CKC(cudaHostGetDevicePointer((void **)&c->hd_staged, c->h_staged, 0));
-    CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
-    CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
-    CKC(cudaHostAlloc((void **)&c->hl_ent, (size_t)RING * Tn * sizeof(uint2), cudaHostAllocMapped));
-    std::memset(c->hl_ready, 0, (size_t)RING * c->T * sizeof(unsigned long long));
-    {
-        unsigned long long *dr;
-        uint32_t *dm;
-        uint2 *de;
-        CKC(cudaHostGetDevicePointer((void **)&dr, c->hl_ready, 0));
-        CKC(cudaHostGetDevicePointer((void **)&dm, c->hl_m, 0));
-        CKC(cudaHostGetDevicePointer((void **)&de, c->hl_ent, 0));
-        for (int r = 0; r < RING; r++) {
-            c->hl_dev[r].ready = dr + (size_t)r * c->T;
-            c->hl_dev[r].m = dm + (size_t)r * c->T;
-            c->hl_dev[r].ent = de + (size_t)r * Tn;
-        }
-    }
+    CKC(cudaHostAlloc((void **)&c->h_wbdst, (size_t)c->XSR * Tn * sizeof(unsigned long long), cudaHostAllocMapped));
+    CKC(cudaHostGetDevicePointer((void **)&c->hd_wbdst, c->h_wbdst, 0));
+    CKC(cudaHostAlloc((void **)&c->h_scnt, RING * sizeof(unsigned long long), cudaHostAllocMapped));
+    std::memset(c->h_scnt, 0, RING * sizeof(unsigned long long));
+    CKC(cudaHostGetDevicePointer((void **)&c->hd_scnt, c->h_scnt, 0));
 
     // initial state
     std::vector<long long> rows64(c->rows.begin(), c->rows.end());
@@ -964,8 +947,6 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     // Plan(b) runs beside dedup(j) once B(b+F) = B(j-1) has been deduped
     const long long b = j - c->F - 1;
     const bool do_plan = b >= 0 && b == c->planned;
-    if (do_plan)
-        if (sp_status s = wait_list_slot(c, b)) return s;
     if (j >= RING) CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));  // ring slot r reused
     const void *dev_idx;
     if (on_device) {
@@ -992,7 +973,6 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     if (do_plan) {
         a.b = b;
         a.pb = c->ring[b % RING];
-        a.hl = c->hl_dev[b % RING];
         a.has_future = 1;
         a.fb = c->ring[(b + c->F) % RING];
     }
@@ -1173,18 +1153,17 @@ sp_status capture_step(sp_ctx *c, int r) {
     a.idx = k.trace;
     a.nb = c->ring[rj];
     a.pb = c->ring[rb];
-    a.hl = c->hl_dev[rb];
     a.fb = c->ring[rf];
     a.ctl = c->d_ctl;
     a.ctl_r = r;
     a.idx_stride = k.stride;
-    CK(cudaStreamBeginCapture(c->cap_s, cudaStreamCaptureModeThreadLocal));
-    cudaStreamWaitEvent(c->cap_s, c->ev_train[rj], cudaEventWaitExternal);
-    if (c->stage_timing) cudaEventRecordWithFlags(c->sev[r][0], c->cap_s, cudaEventRecordExternal);
-    launch_push(a, c->cap_s);
-    if (c->stage_timing) cudaEventRecordWithFlags(c->sev[r][1], c->cap_s, cudaEventRecordExternal);
-    cudaEventRecordWithFlags(c->ev_plan[rb], c->cap_s, cudaEventRecordExternal);
-    CK(cudaStreamEndCapture(c->cap_s, &gr));
+    CK(cudaStreamBeginCapture(c->cap_hi, cudaStreamCaptureModeThreadLocal));
+    cudaStreamWaitEvent(c->cap_hi, c->ev_train[rj], cudaEventWaitExternal);
+    if (c->stage_timing) cudaEventRecordWithFlags(c->sev[r][0], c->cap_hi, cudaEventRecordExternal);
+    launch_push(a, c->cap_hi);
+    if (c->stage_timing) cudaEventRecordWithFlags(c->sev[r][1], c->cap_hi, cudaEventRecordExternal);
+    cudaEventRecordWithFlags(c->ev_plan[rb], c->cap_hi, cudaEventRecordExternal);
+    CK(cudaStreamEndCapture(c->cap_hi, &gr));
     CK(cudaGraphInstantiate(&c->gplan[r], gr, 0));
     cudaGraphDestroy(gr);
     // compute stream: [wait Transfer(k)] -> forward -> surrogate -> backward -> [record ev_train]
@@ -1219,10 +1198,6 @@ sp_status graph_step(sp_ctx *c) {
         if (sp_status s = capture_step(c, r)) return s;
     if (c->g_next_j != j)  // (re)enter graph mode: seed the device batch-index chain
         CK(cudaMemcpyAsync(c->d_ctl + r, &j, sizeof j, cudaMemcpyHostToDevice, c->plan_s));
-    auto t0 = std::chrono::steady_clock::now();
-    if (sp_status s = wait_list_slot(c, b)) return s;
-    auto t1 = std::chrono::steady_clock::now();
-    c->wait_list_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
     CK(cudaGraphLaunch(c->gplan[r], c->plan_s));
     c->pushed = j + 1;
     c->planned = b + 1;

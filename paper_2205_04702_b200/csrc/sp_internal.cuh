@@ -80,14 +80,6 @@ struct Geometry {
     int hs;               // occurrences per hot-row segment (k_bwd: one CTA round)
 };
 
-// Fill lists of one Plan, mirrored into pinned host memory by the plan kernel
-// for the CPU side of the transfer engine (per ring slot, per table).
-struct HostList {
-    unsigned long long *ready;  // [T] = b + 1 once table t's list of batch b is complete
-    uint32_t *m;                // [T] fills of table t
-    uint2 *ent;                 // [T][n] {missed row, previous resident (EMPTY if vacant)}
-};
-
 struct PushArgs {
     Geometry g;
     int P, F;
@@ -117,7 +109,6 @@ struct PushArgs {
     BatchBufs pb;
     int has_future;
     BatchBufs fb;
-    HostList hl;                 // pinned mirror of Plan(b)'s fill lists
     // graph replay: j is read from ctl[ctl_r] (b = j - F - 1, idx = idx + j*stride)
     // and ctl[(ctl_r + 1) % RING] = j + 1 is written for the next step
     long long *ctl;
@@ -145,6 +136,8 @@ struct XferArgs {
     float *storage;
     float *const *host;       // [T] device-visible (mapped) host table pointers
     float *wb_stage;          // [sum m][D] victims: pinned host staging (device alias)
+    unsigned long long *wb_dst;  // [sum m] host address of each staged victim's row (0: none)
+    unsigned long long *staged_cnt;  // pinned: sum m of this batch (written before `staged`)
     uint32_t *done_ctr;       // CTA arrivals (the last CTA resets it)
     unsigned long long *staged;  // pinned host flag: = b + 1 once every victim is staged
     long long b;

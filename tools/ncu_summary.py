@@ -95,6 +95,7 @@ def main():
         traffic[st] += statistics.mean(v)
     traffic = {k: int(v) for k, v in traffic.items()}
     traffic["source"] = f"{src}/full.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum, mean per launch)"
+    traffic["config"] = sys.argv[3] if len(sys.argv) > 3 else "kaggle"
     lines.append("# DRAM bytes per launch by stage: " + json.dumps(traffic))
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w").write("\n".join(lines) + "\n")
