@@ -799,7 +799,9 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     {   // Plan is the serial critical chain: its CTAs get scheduled first
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        CKC(cudaStreamCreateWithPriority(&c->plan_s, cudaStreamNonBlocking, hi));
+        const char *pp = getenv("SP_PLAN_PRIO");  // 0: plan stream at default priority (A/B)
+        const bool plan_hi = !(pp && atoi(pp) == 0);
+        CKC(cudaStreamCreateWithPriority(&c->plan_s, cudaStreamNonBlocking, plan_hi ? hi : lo));
         const char *xp = getenv("SP_XFER_PRIO");  // 1: transfer CTAs also scheduled first
         CKC(cudaStreamCreateWithPriority(&c->xfer_s, cudaStreamNonBlocking, (xp && atoi(xp) == 1) ? hi : lo));
         // SP_XFER_STREAMS=1: one transfer stream (transfers strictly in sequence)
@@ -818,8 +820,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        const char *gp = getenv("SP_PLAN_GRAPH_PRIO");  // 0: capture at default priority (A/B)
-        CKC(cudaStreamCreateWithPriority(&c->cap_hi, cudaStreamNonBlocking, (gp && atoi(gp) == 0) ? lo : hi));
+        const char *pp = getenv("SP_PLAN_PRIO");  // the plan graphs get the plan stream's priority
+        CKC(cudaStreamCreateWithPriority(&c->cap_hi, cudaStreamNonBlocking, (pp && atoi(pp) == 0) ? lo : hi));
     }
     for (int r = 0; r < RING; r++)
         for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_train[r], &c->ev_h2d[r]})
