@@ -3,9 +3,10 @@
 
 One "step" = one pass of the whole hot path over one synthetic mini-batch:
 sp_plan (index ingest + dedup + Hit-Map probe + hit/miss + window-safe victim
-selection + bookkeeping), the Collect/Exchange/Insert transfer (GPU pull of
-missed rows, victims staged in HBM -> D2H DMA -> CPU scatter)
-transfer, sp_forward (EmbeddingBag gather-reduce), the MLP stand-in
+selection + bookkeeping), the Collect/Exchange/Insert transfer (one kernel
+pulls the missed rows into the freed slots and stages the victims in pinned
+host memory; CPU threads scatter them into their host rows),
+sp_forward (EmbeddingBag gather-reduce), the MLP stand-in
 (surrogate gradient kernel) and sp_train (coalescing segmented reduce + fused
 SGD).  Workload at N=1: BASELINE configs[1], Criteo-Kaggle-shaped (the config
 the metric is quoted on that fits one GPU), in steady state: `preroll`
@@ -66,6 +67,11 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # warm the query path: the first calls can take tens of ms, longer
+            # than a whole timed region at ~50 us/step
+            for _ in range(3):
+                pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             self.ok = True
         except Exception as e:  # pragma: no cover
             self.err = str(e)

@@ -408,6 +408,20 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
     uint32_t *slot_u = pb.slot_u + (size_t)t * n;                                    // global copy
 
     PhaseClock pc(A.prof, g.T, 0, t);
+    // P3's first window of the LRU log, loaded now: its entries (slot, stamp)
+    // are not touched before P3, so the loads overlap P1 + P2
+    const unsigned long long cap = A.log_cap[t], lbase = A.log_base[t];
+    uint32_t *lslot = A.log_slot;
+    int32_t *lstamp = A.log_stamp;
+    const unsigned long long head0 = A.log_head[t], tail0 = A.log_tail[t];
+    const bool inr0 = head0 + tid < tail0;
+    uint32_t slot0 = 0;
+    int32_t stamp0 = 0;
+    if (inr0) {
+        const size_t ix = (size_t)(lbase + (head0 + tid) % cap);
+        slot0 = lslot[ix];
+        stamp0 = lstamp[ix];
+    }
     // P1 + P2 in one pass (independent probes of the same Hit-Map):
     // P1 future probe: resident IDs of B(b+F) get next_need = b+F;
     // P2 probe of B(b): hits stamped last_use = b, misses compacted in
@@ -448,35 +462,42 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
     pc.mark(0);
     pc.mark(1);
     // P3: victim selection over the per-table LRU log
-    const unsigned long long cap = A.log_cap[t], lbase = A.log_base[t];
-    uint32_t *lslot = A.log_slot;
-    int32_t *lstamp = A.log_stamp;
     if (tid == 0) {
-        s_head = A.log_head[t];
-        s_tail = A.log_tail[t];
+        s_head = head0;
+        s_tail = tail0;
         s_got = 0;
         s_fail = 0;
     }
     __syncthreads();
     const long long limit = b - A.P - 1;
+    bool first = true;
     while (true) {
         const unsigned long long head = s_head, tail = s_tail;
         const uint32_t got = s_got;
         if (got >= m) break;
         const unsigned long long pos = head + tid;
-        const bool inr = pos < tail;
+        bool inr;
         uint32_t slot = 0;
         int32_t stamp = 0;
-        if (inr) {
-            const size_t ix = (size_t)(lbase + pos % cap);
-            slot = lslot[ix];
-            stamp = lstamp[ix];
+        if (first) {  // head == head0: the prefetched window
+            inr = inr0;
+            slot = slot0;
+            stamp = stamp0;
+            first = false;
+        } else {
+            inr = pos < tail;
+            if (inr) {
+                const size_t ix = (size_t)(lbase + pos % cap);
+                slot = lslot[ix];
+                stamp = lstamp[ix];
+            }
         }
         const bool elig = inr && (long long)stamp <= limit;  // stamps are non-decreasing
         const bool cand = elig && A.last_use[slot] == stamp && (long long)A.next_need[slot] <= b;
-        uint32_t n_elig, n_cand;
-        (void)block_scan(elig ? 1u : 0u, &n_elig);
-        const uint32_t r = block_scan(cand ? 1u : 0u, &n_cand);
+        // one scan for both counts (<= blockDim each): eligible in the high half
+        uint32_t tot2;
+        const uint32_t ex2 = block_scan((elig ? 0x10000u : 0u) | (cand ? 1u : 0u), &tot2);
+        const uint32_t n_elig = tot2 >> 16, n_cand = tot2 & 0xFFFFu, r = ex2 & 0xFFFFu;
         const uint32_t need = m - got;
         if (cand && r < need) {
             victims[got + r] = slot;
