@@ -43,6 +43,18 @@
  *   errors the context is poisoned: only sp_error_string, sp_last_error_batch,
  *   sp_get_stats and sp_destroy remain valid.
  * - One context per GPU; a context is not thread-safe.
+ *
+ * Environment (read at sp_create; tuning experiments and diagnostics only,
+ * the defaults are the measured best on B200):
+ *   SP_PULL_CTAS=n        transfer-kernel grid (one-warp CTAs, default 16)
+ *   SP_XFER_STREAMS=1     one transfer stream instead of two alternating ones
+ *   SP_XFER_PRIO=1        transfer streams at the highest priority
+ *   SP_PLAN_PRIO=0        plan stream / plan graphs at the default priority
+ *   SP_CARVEOUT=pct       shared-memory carveout hint for every kernel
+ *   SP_DIAG_SERIAL=1      every GPU stage on the caller's stream (no overlap)
+ *   SP_DIAG=mask          1: the transfer kernel moves nothing, 2: the Train
+ *                         kernels do nothing -- RESULTS ARE WRONG (timing only)
+ *   SP_NO_GRAPHS=1        sp_run_steps without CUDA-graph replay
  */
 #ifndef SCRATCHPIPE_H
 #define SCRATCHPIPE_H

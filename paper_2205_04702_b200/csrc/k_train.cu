@@ -223,19 +223,52 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
                 if (threadIdx.x == 0) s_last = atomicAdd(&A.bb.hot_cnt[(size_t)t * g.nh + (h - k)], 1u) == nseg - 1;
                 __syncthreads();
                 if (s_last) {
+                    // fold the nseg partials: PL lanes per column each sum the
+                    // partials kk = p, p+PL, ... in order, then a fixed tree
+                    // over the lanes (shape depends on nseg only)
                     __threadfence();
                     const double2 *p0 = reinterpret_cast<const double2 *>(A.partial + ((size_t)t * g.nh + (h - k)) * g.D);
-                    for (int col = threadIdx.x; col < D4; col += blockDim.x) {
-                        // L2 loads (__ldcg): the partials were written by other SMs
-                        double2 lo2 = __ldcg(p0 + 2 * col), hi2 = __ldcg(p0 + 2 * col + 1);
-                        double4 m = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);
-                        for (uint32_t kk = 1; kk < nseg; kk++) {
-                            lo2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col);
-                            hi2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col + 1);
-                            m.x += lo2.x; m.y += lo2.y; m.z += hi2.x; m.w += hi2.y;
+                    const int PL = D4 >= 256 ? 1 : 256 / D4;
+                    for (int col0 = 0; col0 < D4; col0 += 256) {
+                        const int col = col0 + (int)threadIdx.x % (D4 < 256 ? D4 : 256);
+                        const int p = (int)threadIdx.x / (D4 < 256 ? D4 : 256);
+                        double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
+                        if (p < PL && col < D4) {
+                            uint32_t kk = (uint32_t)p;
+                            for (; kk + 3u * PL < nseg; kk += 4u * PL) {  // 4 partials in flight
+                                double2 lo[4], hi[4];
+#pragma unroll
+                                for (int q = 0; q < 4; q++) {
+                                    // L2 loads (__ldcg): the partials were written by other SMs
+                                    lo[q] = __ldcg(p0 + (size_t)(kk + q * PL) * 2 * D4 + 2 * col);
+                                    hi[q] = __ldcg(p0 + (size_t)(kk + q * PL) * 2 * D4 + 2 * col + 1);
+                                }
+#pragma unroll
+                                for (int q = 0; q < 4; q++) { m.x += lo[q].x; m.y += lo[q].y; m.z += hi[q].x; m.w += hi[q].y; }
+                            }
+                            for (; kk < nseg; kk += PL) {
+                                const double2 lo2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col);
+                                const double2 hi2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col + 1);
+                                m.x += lo2.x; m.y += lo2.y; m.z += hi2.x; m.w += hi2.y;
+                            }
                         }
-                        float4 *wp = st + (size_t)slot * D4 + col;
-                        *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
+                        __syncthreads();
+                        s_red[threadIdx.x] = m;
+                        __syncthreads();
+                        const int W = D4 < 256 ? D4 : 256;
+                        for (int hh = 1; hh < PL; hh <<= 1) {
+                            if (p < PL && (p % (2 * hh)) == 0 && p + hh < PL) {
+                                const double4 o = s_red[threadIdx.x + hh * W];
+                                double4 &mm = s_red[threadIdx.x];
+                                mm.x += o.x; mm.y += o.y; mm.z += o.z; mm.w += o.w;
+                            }
+                            __syncthreads();
+                        }
+                        if (p == 0 && col < D4) {
+                            const double4 f = s_red[threadIdx.x];
+                            float4 *wp = st + (size_t)slot * D4 + col;
+                            *wp = sgd(*wp, Acc4{f.x, f.y, f.z, f.w}, A.lr);
+                        }
                     }
                 }
             }
@@ -247,14 +280,20 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
         table_prefix(A.bb.nchunks, t0, tcount, s_pref);
         const uint32_t total = s_pref[tcount];
         uint32_t *ctr = A.bb.work + t0 / 64;
+        // the next round's grab is issued before this round's record is
+        // folded, so the atomic's latency overlaps the gradient loads
+        __syncthreads();
+        if (threadIdx.x == 0) s_base = atomicAdd(ctr, (uint32_t)gpb);
+        __syncthreads();
+        uint32_t next = s_base;
         while (true) {
-            __syncthreads();
-            if (threadIdx.x == 0) s_base = atomicAdd(ctr, (uint32_t)gpb);
-            __syncthreads();
-            const uint32_t base = s_base;
+            const uint32_t base = next;
             if (base >= total) break;
+            __syncthreads();  // every thread has read s_base
+            uint32_t nx = 0;
+            if (threadIdx.x == 0) nx = atomicAdd(ctr, (uint32_t)gpb);
             const uint32_t item = base + gi;
-            if (item >= total) continue;
+            if (item < total) {
             const int tl = find_table(s_pref, tcount, item);
             const int t = t0 + tl;
             const uint32_t c = item - s_pref[tl];
@@ -291,6 +330,10 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
             }
 #pragma unroll
             for (int v = 0; v < VPL; v++) wp[v * G] = sgd(w[v], acc[v], A.lr);
+            }
+            if (threadIdx.x == 0) s_base = nx;
+            __syncthreads();
+            next = s_base;
         }
     }
 }
@@ -424,6 +467,9 @@ cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s) {
 
 // occurrences per hot-row segment: one round of RB rows per lane group of
 // the k_bwd instance that D dispatches to (generic D: 64)
+// occurrences per hot-row segment: one round of RB rows per lane group of
+// the k_bwd instance that D dispatches to (generic D: 64).  (Half-width lane
+// groups, two float4 per lane, were measured slower: 20.7 vs 16.4 us.)
 int backward_hot_segment(int D) {
     int G = 32, VPL = 1;
     switch (D / 4) {
