@@ -518,6 +518,8 @@ def run_ours(args):
         "clocks": sampler.summary(),
         "host_issue_us_per_step": round(1e6 * t_host_issue / K, 2),
         "graph_steps": st1["graph_steps"] - st0["graph_steps"],
+        "graph_step_host_us": round(1e3 * (st1["graph_step_host_ms"] - st0["graph_step_host_ms"]) /
+                                    max(1, st1["graph_steps"] - st0["graph_steps"]), 2),
         "e2e": {"value": round(e2e_value, 2), "unit": "iters/s", "h2d_bytes_per_step": idx_bytes,
                 "d2h_bytes_per_step": stats_bytes, "ms_per_step": round(ms_e2e / K, 5),
                 "path": ("sp_run_steps(1 step) on pinned host int32 indices (the plan kernel reads "

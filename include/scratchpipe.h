@@ -145,6 +145,7 @@ typedef struct {
     double wait_xfer_ms;            /* caller thread waiting for the transfer     */
     double wait_list_ms;            /* engine (forward / host-list ring reuse)    */
     int64_t graph_steps;            /* sp_run_steps steps replayed as CUDA graphs */
+    double graph_step_host_ms;      /* caller-thread wall time spent issuing them */
 } sp_stats;
 
 int32_t sp_abi_version(void);

@@ -64,7 +64,7 @@ class SpStats(ctypes.Structure):
         ("host_gather_ms", ctypes.c_double), ("host_scatter_ms", ctypes.c_double),
         ("host_rows_gathered", ctypes.c_int64), ("host_rows_scattered", ctypes.c_int64),
         ("wait_xfer_ms", ctypes.c_double), ("wait_list_ms", ctypes.c_double),
-        ("graph_steps", ctypes.c_int64),
+        ("graph_steps", ctypes.c_int64), ("graph_step_host_ms", ctypes.c_double),
     ]
 
 
@@ -312,7 +312,7 @@ class ScratchPipe:
         out["kernel_ms"] = dict(zip(KERNEL_KINDS, list(s.kernel_ms)))
         out["kernel_timed"] = dict(zip(KERNEL_KINDS, list(s.kernel_timed)))
         for k in ("host_gather_ms", "host_scatter_ms", "host_rows_gathered", "host_rows_scattered",
-                  "wait_xfer_ms", "wait_list_ms", "graph_steps"):
+                  "wait_xfer_ms", "wait_list_ms", "graph_steps", "graph_step_host_ms"):
             out[k] = getattr(s, k)
         out["status"] = st
         return out

@@ -270,6 +270,7 @@ struct sp_ctx {
     } gkey;
     long long g_next_j = -1;                    // j the device chain expects next
     long long graph_steps = 0;
+    long long graph_step_ns = 0;  // caller-thread time issuing graph steps
     long long wait_xfer_ns = 0, wait_list_ns = 0;  // caller-thread waits on the engine
 };
 
@@ -822,6 +823,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         const char *pp = getenv("SP_PLAN_PRIO");  // the plan graphs get the plan stream's priority
         CKC(cudaStreamCreateWithPriority(&c->cap_hi, cudaStreamNonBlocking, (pp && atoi(pp) == 0) ? lo : hi));
+
     }
     for (int r = 0; r < RING; r++)
         for (cudaEvent_t *ev : {&c->ev_plan[r], &c->ev_xfer[r], &c->ev_train[r], &c->ev_h2d[r]})
@@ -1264,7 +1266,10 @@ sp_status sp_run_steps(sp_ctx *c, const void *indices, int64_t num_batches, int6
                             c->planned == c->trained + c->P && c->pushed + 1 <= num_batches &&
                             c->trained >= RING;
         if (steady) {
+            const auto g0 = std::chrono::steady_clock::now();
             if (sp_status s = graph_step(c)) return s;
+            c->graph_step_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                    std::chrono::steady_clock::now() - g0).count();
             continue;
         }
         c->g_next_j = -1;
@@ -1332,6 +1337,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->wait_xfer_ms = c->wait_xfer_ns * 1e-6;
     o->wait_list_ms = c->wait_list_ns * 1e-6;
     o->graph_steps = c->graph_steps;
+    o->graph_step_host_ms = c->graph_step_ns * 1e-6;
     if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);
         cudaStreamSynchronize(c->xfer_s2);

@@ -280,3 +280,47 @@ def test_smem_radix_tile_sizes(N, L):
     rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr,
                      gde=(float(np.float32(0.5 / N)), float(np.float32(0.01 / N)), 1.0))
     _assert_tables(rep, exact=False)
+
+
+@pytest.mark.gpu
+def test_stage_timing_and_plan_profile_introspection():
+    """sp_set_stage_timing / sp_stage_times (events inside the recaptured step
+    graphs) and sp_debug_plan_profile (per-CTA %globaltimer) report positive,
+    self-consistent durations, and turning stage timing on and off does not
+    change the results of the run."""
+    from oracle import UncachedTrainer
+    rows, D, N, L, nb = [3000, 400], 32, 128, 2, 80
+    tr = sample_trace(rows, N, L, 1.0, nb, 31)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 8) for t, R in enumerate(rows)]
+    tables = pinned_tables(rows, D, 4702)
+    sp = ScratchPipe(rows, tables, D, slots, N, L, index_dtype="int32", index_on_device=True)
+    dev = tr.to(torch.int32).cuda().contiguous()
+    pooled = torch.empty((2, N, D), device="cuda")
+    grad = torch.empty_like(pooled)
+    g, d, e = 0.5, 0.01, 0.05
+    sp.run_steps(dev, 20, pooled, grad, g, d, e)
+    sp.set_stage_timing(True)
+    sp.run_steps(dev, 30, pooled, grad, g, d, e)          # recaptured with event nodes
+    st = sp.stage_times()
+    sp.set_stage_timing(False)
+    for k in ("plan", "transfer", "forward", "surrogate", "backward"):
+        assert st[k]["n"] > 0 and st[k]["ms"] > 0, (k, st[k])
+    sp.set_profiling(True)
+    sp.run_steps(dev, 10, pooled, grad, g, d, e)          # eager profiled steps
+    prof = sp.debug_plan_profile()
+    sp.set_profiling(False)
+    pl = prof["per_launch"]
+    assert len(pl["span_us"]) >= 5
+    assert all(s > 0 for s in pl["span_us"])
+    assert all(sp_ >= c - 1e-3 for sp_, c in zip(pl["span_us"], pl["plan_cta_max_us"]))
+    sp.run_steps(dev, nb - 60, pooled, grad, g, d, e)
+    sp.flush()
+    orc = UncachedTrainer(rows, D, N, L, 4702)
+    for b in range(nb):
+        orc.step(tr.numpy()[b], g, d, e)
+    for t, R in enumerate(rows):
+        touched = orc.touched(t)
+        got = tables[t][torch.from_numpy(touched)].numpy()
+        want = orc.rows_of(t, touched)
+        assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-4)) <= TOL
+    sp.close()
