@@ -43,6 +43,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="kaggle")
+    ap.add_argument("--variant", default="pipelined", choices=["pipelined", "serial", "resident"],
+                    help="design points of PAPER.md Fig. 10 / Table 1 from the same kernels: "
+                         "pipelined (ScratchPipe), serial (straw-man: every stage on one stream, "
+                         "no overlap), resident (slots = rows: the all-in-HBM 'GPU-only' ceiling)")
     ap.add_argument("--preroll", type=int, default=-1, help="untimed steady-state fill batches (-1: config)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -201,6 +205,15 @@ def cpu_baseline(cfg, trace_dev, seconds):
                       f"(Part B) + uncached EmbeddingBag SGD (Part A), single thread, {el:.1f} s"}
 
 
+def _overlap(kernels, step_us):
+    streams = {"plan": kernels["plan"]["avg_us"], "transfer": kernels["transfer"]["avg_us"],
+               "compute": sum(kernels[k]["avg_us"] for k in ("forward", "surrogate", "backward"))}
+    tot, mx = sum(streams.values()), max(streams.values())
+    eff = (tot - step_us) / (tot - mx) if tot > mx else None
+    return {"step_us": round(step_us, 2), "stream_us": {k: round(v, 2) for k, v in streams.items()},
+            "serial_sum_us": round(tot, 2), "efficiency": None if eff is None else round(eff, 3)}
+
+
 def _plan_roles(p0, p1):
     """k_push critical chain: mean per-launch wall time of each table's Plan
     CTA and dedup CTA over the profiling window (globaltimer, in-kernel)."""
@@ -239,6 +252,10 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
+    if args.variant == "resident":
+        cfg = cfg.with_(slot_frac=1.0, slots_fixed=None)
+    if args.variant == "serial":
+        os.environ["SP_DIAG_SERIAL"] = "1"
     T, D, N, L = cfg.num_tables, cfg.dim, cfg.batch, cfg.pooling
     slots_all = cfg.slots
     owner = lpt_assign(table_weights(cfg.rows, slots_all, N * L, D), world)
@@ -494,7 +511,8 @@ def run_ours(args):
                    "l2": "no flush: inputs larger than L2 (Storage %.2f GB, Hit-Map %.0f MB, host tables "
                          "%.1f GB); every step reads a fresh batch" % (
                              sum(slots_all) * D * 4 / 1e9, sum(cfg.rows) * 4 / 1e6, sum(cfg.rows) * D * 4 / 1e9),
-                   "parallelism": f"table-wise x{world}" if world > 1 else "single GPU"},
+                   "parallelism": f"table-wise x{world}" if world > 1 else "single GPU",
+                   "variant": args.variant},
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
@@ -506,7 +524,15 @@ def run_ours(args):
                       "d2h_bytes_per_batch": int(4 * D * ev),
                       "d2h_GBs": None if wb_GBs is None else round(wb_GBs, 2),
                       "peak_h2d_GBs": 55.6, "peak_d2h_GBs": 57.0,
-                      "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)"},
+                      "h2d_frac": None if link_GBs is None else round(link_GBs / 55.6, 4),
+                      "d2h_frac": None if wb_GBs is None else round(wb_GBs / 57.0, 4),
+                      "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)",
+                      "note": "random 256-B host rows are bound by host-side address translation "
+                              "(~32 us per 1,800 fresh rows, profiles/r01_host_tlb_microbench.txt), "
+                              "not by link bandwidth"},
+        # stage overlap in the graph-mode steady state: 1.0 = the step costs
+        # only its slowest stream, 0.0 = the stages run back to back
+        "overlap": _overlap(kernels, ms_per_step * 1e3) if timed_src else None,
         "kernels": kernels,
         "plan_ctas": _plan_roles(pp0, pp1),
         "host_engine": {"scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1p["host_scatter_ms"]) / KP, 2),

@@ -351,9 +351,18 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
         }
         const bool normal = u < U && len <= (uint32_t)CH, is_hot = u < U && len > (uint32_t)CH;
         const uint32_t nseg = is_hot ? (len + hs - 1) / hs : 0u;
-        uint32_t tot, htot;
-        const uint32_t ex = block_scan(normal ? 1u : 0u, &tot);
-        const uint32_t hx = block_scan(nseg, &htot);
+        uint32_t tot, htot, ex, hx;
+        if (n <= 65535) {  // one scan: segment counts sum to < n/CH + blockDim < 2^16
+            uint32_t t2;
+            const uint32_t e2 = block_scan((normal ? 1u : 0u) | (nseg << 16), &t2);
+            ex = e2 & 0xFFFFu;
+            hx = e2 >> 16;
+            tot = t2 & 0xFFFFu;
+            htot = t2 >> 16;
+        } else {
+            ex = block_scan(normal ? 1u : 0u, &tot);
+            hx = block_scan(nseg, &htot);
+        }
         if (normal) {
             const uint32_t c = carry + ex;
             chunk_first[u] = c;
