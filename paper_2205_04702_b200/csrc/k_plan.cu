@@ -443,26 +443,66 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
     uint8_t *hitf = pb.hit + (size_t)t * n;
     const uint32_t Umax = Ub > Uf ? Ub : Uf;
     uint32_t carry = 0;
-    for (uint32_t u0 = 0; u0 < Umax; u0 += blockDim.x) {
-        const uint32_t u = u0 + tid;
-        const uint32_t idf = u < Uf ? fid[u] : 0u;
-        const uint32_t idb = u < Ub ? uniq_id[u] : 0u;
-        const uint32_t sf = u < Uf ? A.hitmap[roff + idf] : EMPTY;
-        const uint32_t sb = u < Ub ? A.hitmap[roff + idb] : EMPTY;
-        if (sf != EMPTY) A.next_need[sf] = fstamp;
-        uint32_t miss = 0;
-        if (u < Ub) {
-            if (small) w_uid[u] = idb;
-            if (sb != EMPTY) A.last_use[sb] = (int32_t)b;
-            else miss = 1;
-            slot_l[u] = sb;
-            if (small) slot_u[u] = sb;
-            hitf[u] = sb != EMPTY;
+    if (small) {
+        // probes first, PU uniques per thread per round with all their loads
+        // in flight (the per-round scans below only compact the misses)
+        constexpr int PU = 4;
+        for (uint32_t u0 = tid; u0 < Umax; u0 += PU * blockDim.x) {
+            uint32_t idf[PU], idb[PU], sf[PU], sb[PU];
+#pragma unroll
+            for (int q = 0; q < PU; q++) {
+                const uint32_t u = u0 + q * blockDim.x;
+                idf[q] = u < Uf ? fid[u] : 0u;
+                idb[q] = u < Ub ? uniq_id[u] : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < PU; q++) {
+                const uint32_t u = u0 + q * blockDim.x;
+                sf[q] = u < Uf ? A.hitmap[roff + idf[q]] : EMPTY;
+                sb[q] = u < Ub ? A.hitmap[roff + idb[q]] : EMPTY;
+            }
+#pragma unroll
+            for (int q = 0; q < PU; q++) {
+                const uint32_t u = u0 + q * blockDim.x;
+                if (sf[q] != EMPTY) A.next_need[sf[q]] = fstamp;
+                if (u < Ub) {
+                    w_uid[u] = idb[q];
+                    if (sb[q] != EMPTY) A.last_use[sb[q]] = (int32_t)b;
+                    slot_l[u] = sb[q];
+                    slot_u[u] = sb[q];
+                    hitf[u] = sb[q] != EMPTY;
+                }
+            }
         }
-        uint32_t tot;
-        const uint32_t ex = block_scan(miss, &tot);  // barriers: stamps visible below
-        if (miss) miss_u[carry + ex] = u;
-        carry += tot;
+        __syncthreads();
+        for (uint32_t u0 = 0; u0 < Ub; u0 += blockDim.x) {  // misses, ascending ID order
+            const uint32_t u = u0 + tid;
+            const uint32_t miss = (u < Ub && slot_l[u] == EMPTY) ? 1u : 0u;
+            uint32_t tot;
+            const uint32_t ex = block_scan(miss, &tot);
+            if (miss) miss_u[carry + ex] = u;
+            carry += tot;
+        }
+    } else {
+        for (uint32_t u0 = 0; u0 < Umax; u0 += blockDim.x) {
+            const uint32_t u = u0 + tid;
+            const uint32_t idf = u < Uf ? fid[u] : 0u;
+            const uint32_t idb = u < Ub ? uniq_id[u] : 0u;
+            const uint32_t sf = u < Uf ? A.hitmap[roff + idf] : EMPTY;
+            const uint32_t sb = u < Ub ? A.hitmap[roff + idb] : EMPTY;
+            if (sf != EMPTY) A.next_need[sf] = fstamp;
+            uint32_t miss = 0;
+            if (u < Ub) {
+                if (sb != EMPTY) A.last_use[sb] = (int32_t)b;
+                else miss = 1;
+                slot_l[u] = sb;
+                hitf[u] = sb != EMPTY;
+            }
+            uint32_t tot;
+            const uint32_t ex = block_scan(miss, &tot);  // barriers: stamps visible below
+            if (miss) miss_u[carry + ex] = u;
+            carry += tot;
+        }
     }
     const uint32_t m = carry;
     const uint32_t nhit = Ub - m;

@@ -751,6 +751,9 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->hit_total = c->row_off[c->T];
     c->XSR = std::max(4, c->F + 2);  // >= F+1: Transfer(b) waits for scatter(b-F-1) >= b-XSR
     c->host_threads = d->host_threads > 0 ? d->host_threads : 6;
+    // transfer grid: 16 one-warp CTAs for up to ~56k lookups per step (Kaggle),
+    // more for larger batches (more rows to pull), at most 48
+    c->pull_ctas = (int)std::min<long long>(48, std::max<long long>(16, (long long)c->T * c->n / 3500));
     if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_DIAG")) c->diag = atoi(e);
 
