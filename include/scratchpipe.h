@@ -53,7 +53,8 @@
  *   SP_CARVEOUT=pct       shared-memory carveout hint for every kernel
  *   SP_DIAG_SERIAL=1      every GPU stage on the caller's stream (no overlap)
  *   SP_DIAG=mask          1: the transfer kernel moves nothing, 2: the Train
- *                         kernels do nothing -- RESULTS ARE WRONG (timing only)
+ *                         kernels do nothing, 4: victims are not staged --
+ *                         RESULTS ARE WRONG (timing only)
  *   SP_NO_GRAPHS=1        sp_run_steps without CUDA-graph replay
  */
 #ifndef SCRATCHPIPE_H
@@ -242,6 +243,13 @@ sp_status sp_run_steps(sp_ctx *c, const void *indices, int64_t num_batches, int6
  * host tables are coherent.  Requires every pushed batch to be trained (call
  * sp_end_of_data first).  Synchronises the device. */
 sp_status sp_flush(sp_ctx *c);
+
+/* All-resident warm start, the paper's GPU-only design point (Table 1;
+ * SURVEY §8(f) f3): with slots[t] == rows[t] for every table, copy every host
+ * row into Storage (slot_base[t] + id) and map it in the Hit-Map before the
+ * first sp_plan, so no batch ever misses.  SP_ERR_INVALID_ARG unless every
+ * table is fully resident, SP_ERR_STATE after the first sp_plan.  Synchronous. */
+sp_status sp_prefill(sp_ctx *c);
 
 /* Free everything (unregisters host tables registered by the library). */
 sp_status sp_destroy(sp_ctx *c);

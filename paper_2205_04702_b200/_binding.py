@@ -87,7 +87,7 @@ def _load():
                        ("sp_get_timeline", [P, P, P, P, P, ctypes.c_int64, i64p]), ("sp_end_of_data", [P]), ("sp_forward", [P, P]),
                        ("sp_train", [P, P, ctypes.c_float]),
                        ("sp_surrogate_grad", [P, P, P, ctypes.c_int64, ctypes.c_float, ctypes.c_float]),
-                       ("sp_flush", [P]), ("sp_destroy", [P]),
+                       ("sp_flush", [P]), ("sp_destroy", [P]), ("sp_prefill", [P]),
                        ("sp_last_error_batch", [P, i64p, ctypes.POINTER(ctypes.c_int32)]),
                        ("sp_get_stats", [P, ctypes.POINTER(SpStats)]),
                        ("sp_debug_plan", [P, ctypes.c_int64, ctypes.c_int32, i64p, i64p, i64p, i64p, i64p]),
@@ -296,6 +296,10 @@ class ScratchPipe:
 
     def flush(self):
         self._check(lib.sp_flush(self._h))
+
+    def prefill(self):
+        """All rows resident before the first batch (needs slots == rows)."""
+        self._check(lib.sp_prefill(self._h))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -676,7 +676,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
 
 }  // namespace
 
-__global__ void __launch_bounds__(PUSH_THREADS, PUSH_THREADS >= 1024 ? 1 : 2) k_push(PushArgs A) {
+__global__ void __launch_bounds__(PUSH_THREADS, SP_PUSH_MIN_BLOCKS) k_push(PushArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (*A.err != NO_ERR) return;  // poisoned: nothing more is planned
     const int T = A.g.T;

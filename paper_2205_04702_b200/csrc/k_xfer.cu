@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 slot = A.bb.fill_slot[kk];
                 src_host = A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
                 const uint32_t old = A.bb.evict_row[kk];
-                if (old != EMPTY) stage = base_t0 + item;
+                if (old != EMPTY && !A.diag_nowb) stage = base_t0 + item;
                 // the scatter thread's work list: where the staged row goes
                 A.wb_dst[base_t0 + item] =
                     old != EMPTY ? (unsigned long long)(uintptr_t)(A.host[t] + (size_t)old * g.D) : 0ull;
@@ -172,6 +172,30 @@ int pullfill_tma_items(int D) {
     const size_t budget = 192 * 1024, per_item = (size_t)2 * D * 4 * XS;
     size_t nb = budget / per_item;
     return (int)(nb > 32 ? 32 : (nb < 1 ? 1 : nb));
+}
+
+// sp_prefill (slots == rows for every table): slot slot_base[t] + id holds
+// row id of table t; Storage itself is filled by a contiguous H2D copy
+__global__ void __launch_bounds__(256) k_prefill_map(const uint32_t *slot_base, const unsigned long long *row_off,
+                                                     int T, long long S_total, uint32_t *resident, uint32_t *hitmap) {
+    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < S_total;
+         s += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = T;  // slot_base[lo] <= s < slot_base[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((long long)slot_base[mid] <= s) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t id = (uint32_t)(s - slot_base[lo]);
+        resident[s] = id;
+        hitmap[row_off[lo] + id] = (uint32_t)s;
+    }
+}
+
+cudaError_t launch_prefill_map(const uint32_t *slot_base, const unsigned long long *row_off, int T,
+                               long long S_total, uint32_t *resident, uint32_t *hitmap, cudaStream_t s) {
+    k_prefill_map<<<148 * 8, 256, 0, s>>>(slot_base, row_off, T, S_total, resident, hitmap);
+    return cudaGetLastError();
 }
 
 // write back every resident slot (sp_flush)

@@ -199,7 +199,8 @@ struct sp_ctx {
     unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
     int pull_ctas = 16;  // k_pullfill grid (one warp per CTA); SP_PULL_CTAS overrides
     // timing diagnostics (SP_DIAG bit mask; results are then WRONG): 1 = the
-    // transfer kernel moves nothing, 2 = the Train kernels do nothing
+    // transfer kernel moves nothing, 2 = the Train kernels do nothing, 4 = the
+    // transfer kernel pulls but does not stage the victims
     int diag = 0;
     long long xfer_enq = 0;                    // transfers enqueued (caller's thread)
     // pinned index staging
@@ -606,6 +607,7 @@ sp_status pump(sp_ctx *c) {
         a.staged_cnt = c->hd_scnt + r;
         a.b = b;
         if (c->diag & 1) a.g.T = 0;  // diagnostic: transfer launched, no rows moved
+        if (c->diag & 4) a.diag_nowb = 1;  // diagnostic: victims not staged (pull only)
         a.err = c->d_err;
         if (c->stage_timing) CK(cudaEventRecord(c->sev[r][6], xs));
         CK(launch(c, SP_K_TRANSFER, b, xs, [&] { return launch_pullfill(a, c->pull_ctas, xs); }));
@@ -751,9 +753,9 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->hit_total = c->row_off[c->T];
     c->XSR = std::max(4, c->F + 2);  // >= F+1: Transfer(b) waits for scatter(b-F-1) >= b-XSR
     c->host_threads = d->host_threads > 0 ? d->host_threads : 6;
-    // transfer grid: 16 one-warp CTAs for up to ~56k lookups per step (Kaggle),
-    // more for larger batches (more rows to pull), at most 48
-    c->pull_ctas = (int)std::min<long long>(48, std::max<long long>(16, (long long)c->T * c->n / 3500));
+    // transfer grid: 16 one-warp CTAs (measured best on Kaggle and Terabyte;
+    // 30 / 48 CTAs were 11% / 18% slower on Terabyte: more SMs add interference,
+    // not host-link throughput)
     if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_DIAG")) c->diag = atoi(e);
 
@@ -1101,6 +1103,21 @@ sp_status sp_surrogate_grad(sp_ctx *c, const float *pooled, float *grad, int64_t
     if (count == 0) count = (long long)c->T * c->N * c->D;
     CK(launch(c, SP_K_SURROGATE, c->trained, c->compute,
               [&] { return launch_surrogate(pooled, grad, count, gamma, delta, c->compute); }));
+    return SP_OK;
+}
+
+sp_status sp_prefill(sp_ctx *c) {
+    if (!c) return SP_ERR_INVALID_ARG;
+    if (sp_status s = check_async_error(c)) return s;
+    if (c->pushed != 0) return fail(c, SP_ERR_STATE, "sp_prefill: only before the first sp_plan");
+    for (int t = 0; t < c->T; t++)
+        if (c->slots[t] != c->rows[t]) return fail(c, SP_ERR_INVALID_ARG, "sp_prefill: needs slots == rows for every table");
+    CK(cudaSetDevice(c->device));
+    for (int t = 0; t < c->T; t++)
+        CK(cudaMemcpyAsync(c->d_storage + (size_t)c->slot_base[t] * c->D, c->host[t],
+                           (size_t)c->rows[t] * c->D * sizeof(float), cudaMemcpyHostToDevice, c->plan_s));
+    CK(launch_prefill_map(c->d_slot_base, c->d_row_off, c->T, c->S_total, c->d_resident, c->d_hitmap, c->plan_s));
+    CK(cudaStreamSynchronize(c->plan_s));
     return SP_OK;
 }
 

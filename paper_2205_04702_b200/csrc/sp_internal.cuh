@@ -30,6 +30,9 @@ constexpr int CH = 16;                      // occurrences per backward chunk
 #define SP_PUSH_THREADS 1024
 #endif
 constexpr int PUSH_THREADS = SP_PUSH_THREADS;  // one CTA per table and role (k_push)
+#ifndef SP_PUSH_MIN_BLOCKS
+#define SP_PUSH_MIN_BLOCKS (SP_PUSH_THREADS >= 1024 ? 1 : 2)  // resident k_push CTAs per SM
+#endif
 constexpr int SMEM_SORT_MAX = 8192;         // n handled by the shared-memory radix sort
 constexpr unsigned long long NO_ERR = ~0ull;
 
@@ -138,6 +141,7 @@ struct XferArgs {
     float *wb_stage;          // [sum m][D] victims: pinned host staging (device alias)
     unsigned long long *wb_dst;  // [sum m] host address of each staged victim's row (0: none)
     unsigned long long *staged_cnt;  // pinned: sum m of this batch (written before `staged`)
+    int diag_nowb;                // timing diagnostic: skip the victims' staging stores
     uint32_t *done_ctr;       // CTA arrivals (the last CTA resets it)
     unsigned long long *staged;  // pinned host flag: = b + 1 once every victim is staged
     long long b;
@@ -201,6 +205,8 @@ cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, 
                              float delta, cudaStream_t s);
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
+cudaError_t launch_prefill_map(const uint32_t *slot_base, const unsigned long long *row_off, int T,
+                               long long S_total, uint32_t *resident, uint32_t *hitmap, cudaStream_t s);
 size_t push_smem_bytes(int n);
 // shared-memory carveout (percent) requested for every kernel of the library,
 // -1 = driver default; set once at sp_create (SP_CARVEOUT) so consecutive

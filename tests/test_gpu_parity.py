@@ -324,3 +324,37 @@ def test_stage_timing_and_plan_profile_introspection():
         want = orc.rows_of(t, touched)
         assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-4)) <= TOL
     sp.close()
+
+
+@pytest.mark.gpu
+def test_prefill_all_resident_no_misses_matches_oracle():
+    """sp_prefill (slots == rows, every row loaded before the first batch):
+    no batch misses or evicts, and training still equals the oracle; prefill
+    is refused when a table is not fully resident."""
+    from oracle import UncachedTrainer
+    rows, D, N, L, nb = [900, 60, 333], 16, 32, 3, 25
+    tr = sample_trace(rows, N, L, 1.0, nb, 41)
+    tables = pinned_tables(rows, D, 4702)
+    sp = ScratchPipe(rows, tables, D, list(rows), N, L, index_dtype="int32", index_on_device=True)
+    sp.prefill()
+    dev = tr.to(torch.int32).cuda().contiguous()
+    pooled = torch.empty((3, N, D), device="cuda")
+    grad = torch.empty_like(pooled)
+    g, d, e = 0.5, 0.01, 0.05
+    sp.run_steps(dev, nb, pooled, grad, g, d, e)
+    sp.flush()
+    st = sp.stats()
+    assert st["misses"] == 0 and st["evictions"] == 0 and st["hits"] == st["uniques"] > 0
+    orc = UncachedTrainer(rows, D, N, L, 4702)
+    for b in range(nb):
+        orc.step(tr.numpy()[b], g, d, e)
+    for t, R in enumerate(rows):
+        touched = orc.touched(t)
+        got = tables[t][torch.from_numpy(touched)].numpy()
+        want = orc.rows_of(t, touched)
+        assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-4)) <= TOL
+    sp.close()
+    sp2 = ScratchPipe(rows, pinned_tables(rows, D, 4702), D, [900, 60, 300], N, L)
+    with pytest.raises(SpError):
+        sp2.prefill()
+    sp2.close()
