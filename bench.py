@@ -539,6 +539,7 @@ def run_ours(args):
         "kernels": kernels,
         "plan_ctas": _plan_roles(pp0, pp1),
         "host_engine": {"scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1p["host_scatter_ms"]) / KP, 2),
+                        "gather_us_per_batch": round(1e3 * (st2["host_gather_ms"] - st1p["host_gather_ms"]) / KP, 2),
                         "threads": "1 scatter thread + row-copy helpers"},
         "host_waits_us_per_step": {"list_slot": round(1e3 * (st1["wait_list_ms"] - st0["wait_list_ms"]) / K, 2)},
         "per_step": {"uniques": round(U, 1), "misses": round(m, 1), "evictions": round(ev, 1)},

@@ -11,11 +11,12 @@
  *               (past window P:840-861, future window P:864-884, superset
  *               P:887-896), Hit-Map/Storage bookkeeping.
  *               [Collect]+[Exchange]+[Insert] run in the
- *               library's transfer engine: one bounded-grid kernel per
- *               batch pulls the missed rows from the host tables into the
- *               freed slots (zero-copy) and writes the victims contiguously
- *               into pinned staging; CPU threads scatter the staged victims
- *               into their host rows (no CUDA call on those threads).
+ *               library's transfer engine: CPU threads gather the missed
+ *               rows into a contiguous pinned slot, one bounded-grid kernel
+ *               per batch moves them into the freed slots and writes the
+ *               victims contiguously into pinned staging (zero-copy, TMA
+ *               bulk copies), CPU threads scatter the staged victims into
+ *               their host rows (no CUDA call on those threads).
  *   sp_forward  [Training] part 1: EmbeddingBag gather-reduce.
  *   sp_train    [Training] part 2: gradient duplication + coalescing
  *                and the SGD update in place in the scratchpad
@@ -46,6 +47,9 @@
  *
  * Environment (read at sp_create; tuning experiments and diagnostics only,
  * the defaults are the measured best on B200):
+ *   SP_CPU_GATHER=0       the transfer kernel pulls the missed rows from their
+ *                         random host rows itself (default: CPU threads gather
+ *                         them into a contiguous pinned slot first)
  *   SP_PULL_CTAS=n        transfer-kernel grid (one-warp CTAs, default 16)
  *   SP_XFER_STREAMS=1     one transfer stream instead of two alternating ones
  *   SP_XFER_PRIO=1        transfer streams at the highest priority

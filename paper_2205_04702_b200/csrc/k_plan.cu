@@ -593,10 +593,20 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
         fill_slot[k] = s;
         fill_row[k] = id;
         evict_row[k] = old;
+        if (A.hl.row) A.hl.row[(size_t)t * n + k] = id;  // pinned mirror (zero-copy)
     }
     uint32_t ev_total;
     (void)block_scan(nev, &ev_total);  // barriers: P4 writes visible below
-    if (tid == 0) pb.m[t] = m;  // fills of table t for k_pullfill
+    if (tid == 0) {
+        pb.m[t] = m;  // fills of table t for k_pullfill
+        if (A.hl.row) {
+            // the CTA's mirror writes precede this fence through the barrier
+            // above (causality order): one system-scope fence publishes them
+            A.hl.m[t] = m;
+            __threadfence_system();
+            *(volatile unsigned long long *)&A.hl.ready[t] = (unsigned long long)(b + 1);
+        }
+    }
 
     pc.mark(3);
     // P5: LRU log append (after an in-place compaction if it would overflow)

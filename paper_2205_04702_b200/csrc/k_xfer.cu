@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 const int t = t0 + tl;
                 const size_t kk = (size_t)t * g.n + (item - s_pref[tl]);
                 slot = A.bb.fill_slot[kk];
-                src_host = A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
+                src_host = A.in_stage ? A.in_stage + (size_t)(base_t0 + item) * g.D  // CPU-gathered, contiguous
+                                      : A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
                 const uint32_t old = A.bb.evict_row[kk];
                 if (old != EMPTY && !A.diag_nowb) stage = base_t0 + item;
                 // the scatter thread's work list: where the staged row goes

@@ -234,6 +234,22 @@ struct sp_ctx {
     std::atomic<bool> stop{false};
     RowPool spool;  // scatter helpers
     int host_threads = 6;
+    // CPU gather of the missed rows (default; SP_CPU_GATHER=0 lets the transfer
+    // kernel pull random host rows itself): Plan mirrors its
+    // missed-row lists to pinned memory, the gather thread copies the rows
+    // into a contiguous pinned slot, the transfer kernel reads that slot
+    // (sequential pages) instead of random host rows
+    bool cpu_gather = false;
+    std::thread gather_worker;
+    RowPool gpool;  // gather helpers
+    unsigned long long *hl_ready = nullptr;    // pinned mapped [RING][T]
+    uint32_t *hl_m = nullptr;                  // pinned mapped [RING][T]
+    uint32_t *hl_row = nullptr;                // pinned mapped [RING][T][n]
+    HostList hl_dev[RING];                     // device aliases
+    float *h_in = nullptr, *hd_in = nullptr;   // pinned mapped [XSR][T*n][D] gathered rows
+    unsigned long long *h_gathered = nullptr;  // pinned mapped: batches gathered
+    unsigned long long *d_gathered = nullptr;  // device alias (stream wait-value)
+    std::atomic<long long> x_gathered{0};
     // errors
     sp_status poisoned = SP_OK;
     std::string err = "no error";
@@ -478,12 +494,16 @@ PushArgs push_args(sp_ctx *c) {
     return a;
 }
 
+sp_status wait_gather_slot(sp_ctx *c, long long b);
+
 sp_status enqueue_plan_only(sp_ctx *c, long long b) {
+    if (sp_status s = wait_gather_slot(c, b)) return s;
     PushArgs a = push_args(c);
     a.has_new = 0;
     a.do_plan = 1;
     a.b = b;
     a.pb = c->ring[b % RING];
+    if (c->cpu_gather) a.hl = c->hl_dev[b % RING];
     a.has_future = (b + c->F < c->pushed) ? 1 : 0;  // future window truncates at the end
     a.fb = c->ring[(b + c->F) % RING];
     CK(launch(c, SP_K_PLAN, b, c->plan_s, [&] { return launch_push(a, c->plan_s); }));
@@ -504,6 +524,16 @@ TrainArgs train_args(sp_ctx *c, long long b) {
 }
 
 // --------------------------------------------------------------- transfer engine
+
+// On a device error or at teardown the engine threads stop; the GPU stream
+// waits on their progress counters are released so that queued transfers run
+// (and return at once on the latched error) instead of blocking forever.
+void release_engine_waits(sp_ctx *c) {
+    const unsigned long long all = 1ull << 62;
+    if (c->h_scat) *(volatile unsigned long long *)c->h_scat = all;
+    if (c->h_gathered) *(volatile unsigned long long *)c->h_gathered = all;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+}
 
 // [Insert] CPU scatter of batch s's victims into the host tables once
 // Transfer(s) has staged them in pinned host memory (k_pullfill's last CTA
@@ -526,7 +556,10 @@ void scatter_main(sp_ctx *c) {
         return true;
     };
     while (!c->stop.load(std::memory_order_relaxed)) {
-        if (*(volatile unsigned long long *)c->h_errflag) break;
+        if (*(volatile unsigned long long *)c->h_errflag) {
+            release_engine_waits(c);
+            break;
+        }
         if (s < c->x_enqueued.load(std::memory_order_acquire) && ready(s)) {
             const size_t cnt = (size_t)((volatile unsigned long long *)c->h_scnt)[s % RING];
             src.clear();
@@ -556,10 +589,83 @@ void scatter_main(sp_ctx *c) {
     }
 }
 
+// [Collect] CPU gather of batch b's missed rows into the contiguous pinned
+// slot b % XSR, in batch order, once Plan(b) has mirrored its lists, the
+// write-back of batch b-F-1 has landed in the host tables (RAW-4: a row
+// evicted at b-F-1 or earlier may be missed again at b) and Transfer(b-XSR)
+// has finished reading the slot.  Publishes gathered = b + 1 (the transfer
+// stream waits on it).  No CUDA API call.
+void gather_main(sp_ctx *c) {
+    const size_t rowb = (size_t)c->D * sizeof(float);
+    const size_t slab = (size_t)c->T * c->n * c->D;
+    std::vector<const float *> src;
+    std::vector<float *> dst;
+    long long g = 0;
+    int idle = 0;
+    auto ready = [&](long long b) {
+        const int r = (int)(b % RING);
+        for (int t = 0; t < c->T; t++)
+            if (((volatile unsigned long long *)c->hl_ready)[(size_t)r * c->T + t] != (unsigned long long)(b + 1))
+                return false;
+        if (c->x_scattered.load(std::memory_order_acquire) < b - c->F) return false;
+        const long long prev = b - c->XSR;
+        if (prev >= 0 && ((volatile unsigned long long *)c->h_staged)[prev % RING] < (unsigned long long)(prev + 1))
+            return false;
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return true;
+    };
+    while (!c->stop.load(std::memory_order_relaxed)) {
+        if (*(volatile unsigned long long *)c->h_errflag) {
+            release_engine_waits(c);
+            break;
+        }
+        if (ready(g)) {
+            const int r = (int)(g % RING);
+            src.clear();
+            dst.clear();
+            float *in = c->h_in + (size_t)(g % c->XSR) * slab;
+            size_t k0 = 0;
+            for (int t = 0; t < c->T; t++) {
+                const uint32_t m = c->hl_m[(size_t)r * c->T + t];
+                const uint32_t *rows = c->hl_row + ((size_t)r * c->T + t) * c->n;
+                for (uint32_t k = 0; k < m; k++) {
+                    src.push_back(c->host[t] + (size_t)rows[k] * c->D);
+                    dst.push_back(in + (k0 + k) * c->D);
+                }
+                k0 += m;
+            }
+            const auto t0 = std::chrono::steady_clock::now();
+            c->gpool.copy(src.data(), dst.data(), (long)src.size(), rowb);
+            c->x_gather_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                  std::chrono::steady_clock::now() - t0).count();
+            c->x_rows_g += (long long)src.size();
+            g++;
+            c->x_gathered.store(g, std::memory_order_release);
+            std::atomic_thread_fence(std::memory_order_seq_cst);
+            *(volatile unsigned long long *)c->h_gathered = (unsigned long long)g;
+            idle = 0;
+        } else if (++idle > 2048) {
+            std::this_thread::yield();
+        } else {
+            _mm_pause();
+        }
+    }
+}
+
+// Plan(b) reuses the missed-row mirror slot of Plan(b - RING): the gather
+// thread must be done with it (CPU gather only).
+sp_status wait_gather_slot(sp_ctx *c, long long b) {
+    if (!c->cpu_gather || b - RING < 0) return SP_OK;
+    return wait_engine(c, [&] { return c->x_gathered.load(std::memory_order_acquire) > b - RING; });
+}
+
 void stop_engine(sp_ctx *c) {
     c->stop = true;
+    release_engine_waits(c);
     if (c->scatter_worker.joinable()) c->scatter_worker.join();
+    if (c->gather_worker.joinable()) c->gather_worker.join();
     c->spool.shutdown();
+    c->gpool.shutdown();
 }
 
 // stream wait on a 64-bit pinned counter (cuStreamWaitValue64 through the
@@ -595,9 +701,16 @@ sp_status pump(sp_ctx *c) {
             CUresult cr = wv((CUstream)xs, (CUdeviceptr)c->d_scat, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ);
             if (cr != CUDA_SUCCESS) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 failed");
         }
+        if (c->cpu_gather) {  // the CPU has gathered batch b's missed rows
+            wait_value64_fn wv = wait_value64();
+            if (!wv) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 unavailable");
+            CUresult cr = wv((CUstream)xs, (CUdeviceptr)c->d_gathered, (cuuint64_t)(b + 1), CU_STREAM_WAIT_VALUE_GEQ);
+            if (cr != CUDA_SUCCESS) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 failed");
+        }
         XferArgs a{};
         a.g = c->g;
         a.bb = c->ring[r];
+        if (c->cpu_gather) a.in_stage = c->hd_in + (size_t)(b % c->XSR) * c->T * c->n * c->D;
         a.storage = c->d_storage;
         a.host = c->d_host;
         a.wb_stage = c->hd_wb + (size_t)(b % c->XSR) * c->T * c->n * c->D;
@@ -646,7 +759,8 @@ void destroy_all(sp_ctx *c) {
     if (c->prof_ref) cudaEventDestroy(c->prof_ref);
     for (void *p : c->allocs) cudaFree(p);
     for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb, (void *)c->h_staged,
-                    (void *)c->h_wbdst, (void *)c->h_scnt})
+                    (void *)c->h_wbdst, (void *)c->h_scnt,
+                    (void *)c->hl_ready, (void *)c->hl_m, (void *)c->hl_row, (void *)c->h_in, (void *)c->h_gathered})
         if (p) cudaFreeHost(p);
     if (c->registered)
         for (int t = 0; t < c->T; t++) cudaHostUnregister(c->host[t]);
@@ -902,6 +1016,29 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaHostAlloc((void **)&c->h_staged, RING * sizeof(unsigned long long), cudaHostAllocMapped));
     std::memset(c->h_staged, 0, RING * sizeof(unsigned long long));
     CKC(cudaHostGetDevicePointer((void **)&c->hd_staged, c->h_staged, 0));
+    c->cpu_gather = true;  // measured +8-9% (value and e2e) over GPU pulls of random host rows
+    if (const char *e = getenv("SP_CPU_GATHER")) c->cpu_gather = atoi(e) != 0;
+    if (c->cpu_gather) {
+        CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
+        CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
+        CKC(cudaHostAlloc((void **)&c->hl_row, (size_t)RING * Tn * sizeof(uint32_t), cudaHostAllocMapped));
+        std::memset(c->hl_ready, 0, (size_t)RING * c->T * sizeof(unsigned long long));
+        unsigned long long *dr;
+        uint32_t *dm, *drow;
+        CKC(cudaHostGetDevicePointer((void **)&dr, c->hl_ready, 0));
+        CKC(cudaHostGetDevicePointer((void **)&dm, c->hl_m, 0));
+        CKC(cudaHostGetDevicePointer((void **)&drow, c->hl_row, 0));
+        for (int r = 0; r < RING; r++) {
+            c->hl_dev[r].ready = dr + (size_t)r * c->T;
+            c->hl_dev[r].m = dm + (size_t)r * c->T;
+            c->hl_dev[r].row = drow + (size_t)r * Tn;
+        }
+        CKC(cudaHostAlloc((void **)&c->h_in, (size_t)c->XSR * Tn * c->D * sizeof(float), cudaHostAllocMapped));
+        CKC(cudaHostGetDevicePointer((void **)&c->hd_in, c->h_in, 0));
+        CKC(cudaHostAlloc((void **)&c->h_gathered, sizeof(unsigned long long), cudaHostAllocMapped));
+        *c->h_gathered = 0;
+        CKC(cudaHostGetDevicePointer((void **)&c->d_gathered, c->h_gathered, 0));
+    }
     CKC(cudaHostAlloc((void **)&c->h_wbdst, (size_t)c->XSR * Tn * sizeof(unsigned long long), cudaHostAllocMapped));
     CKC(cudaHostGetDevicePointer((void **)&c->hd_wbdst, c->h_wbdst, 0));
     CKC(cudaHostAlloc((void **)&c->h_scnt, RING * sizeof(unsigned long long), cudaHostAllocMapped));
@@ -940,6 +1077,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     // transfer engine: helpers + worker
     c->spool.start(c->host_threads);
     c->scatter_worker = std::thread(scatter_main, c);
+    if (c->cpu_gather) {
+        c->gpool.start(c->host_threads);
+        c->gather_worker = std::thread(gather_main, c);
+    }
     *out = c;
     return SP_OK;
 }
@@ -956,6 +1097,8 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     // Plan(b) runs beside dedup(j) once B(b+F) = B(j-1) has been deduped
     const long long b = j - c->F - 1;
     const bool do_plan = b >= 0 && b == c->planned;
+    if (do_plan)
+        if (sp_status s = wait_gather_slot(c, b)) return s;
     if (j >= RING) CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));  // ring slot r reused
     const void *dev_idx;
     if (on_device) {
@@ -982,6 +1125,7 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
     if (do_plan) {
         a.b = b;
         a.pb = c->ring[b % RING];
+        if (c->cpu_gather) a.hl = c->hl_dev[b % RING];
         a.has_future = 1;
         a.fb = c->ring[(b + c->F) % RING];
     }
@@ -1177,6 +1321,7 @@ sp_status capture_step(sp_ctx *c, int r) {
     a.idx = k.trace;
     a.nb = c->ring[rj];
     a.pb = c->ring[rb];
+    if (c->cpu_gather) a.hl = c->hl_dev[rb];
     a.fb = c->ring[rf];
     a.ctl = c->d_ctl;
     a.ctl_r = r;
@@ -1222,6 +1367,7 @@ sp_status graph_step(sp_ctx *c) {
         if (sp_status s = capture_step(c, r)) return s;
     if (c->g_next_j != j)  // (re)enter graph mode: seed the device batch-index chain
         CK(cudaMemcpyAsync(c->d_ctl + r, &j, sizeof j, cudaMemcpyHostToDevice, c->plan_s));
+    if (sp_status s = wait_gather_slot(c, b)) return s;
     CK(cudaGraphLaunch(c->gplan[r], c->plan_s));
     c->pushed = j + 1;
     c->planned = b + 1;
@@ -1350,7 +1496,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->h2d_row_bytes = (int64_t)cum[2] * c->D * 4;
     o->d2h_row_bytes = (int64_t)cum[3] * c->D * 4;
     std::lock_guard<std::mutex> lk(c->prof_mu);
-    o->host_gather_ms = 0.0;  // the GPU pulls the missed rows itself
+    o->host_gather_ms = c->x_gather_ns.load() * 1e-6;
     o->host_scatter_ms = c->x_scatter_ns.load() * 1e-6;
     o->host_rows_gathered = c->x_rows_g.load();
     o->host_rows_scattered = c->x_rows_s.load();

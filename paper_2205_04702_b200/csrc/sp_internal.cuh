@@ -83,6 +83,14 @@ struct Geometry {
     int hs;               // occurrences per hot-row segment (k_bwd: one CTA round)
 };
 
+// Missed-row lists of one Plan, mirrored into pinned host memory by the plan
+// kernel for the CPU gather of the transfer engine (per ring slot, per table).
+struct HostList {
+    unsigned long long *ready;  // [T] = b + 1 once table t's list of batch b is complete
+    uint32_t *m;                // [T] fills of table t
+    uint32_t *row;              // [T][n] missed row of each fill
+};
+
 struct PushArgs {
     Geometry g;
     int P, F;
@@ -112,6 +120,7 @@ struct PushArgs {
     BatchBufs pb;
     int has_future;
     BatchBufs fb;
+    HostList hl;                 // pinned mirror of Plan(b)'s missed rows (CPU gather)
     // graph replay: j is read from ctl[ctl_r] (b = j - F - 1, idx = idx + j*stride)
     // and ctl[(ctl_r + 1) % RING] = j + 1 is written for the next step
     long long *ctl;
@@ -142,6 +151,9 @@ struct XferArgs {
     unsigned long long *wb_dst;  // [sum m] host address of each staged victim's row (0: none)
     unsigned long long *staged_cnt;  // pinned: sum m of this batch (written before `staged`)
     int diag_nowb;                // timing diagnostic: skip the victims' staging stores
+    const float *in_stage;        // [sum m][D] missed rows gathered by the CPU into pinned
+                                  // host memory (contiguous, flattened over tables), or
+                                  // nullptr: pull each row from its host table
     uint32_t *done_ctr;       // CTA arrivals (the last CTA resets it)
     unsigned long long *staged;  // pinned host flag: = b + 1 once every victim is staged
     long long b;
