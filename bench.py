@@ -3,9 +3,10 @@
 
 One "step" = one pass of the whole hot path over one synthetic mini-batch:
 sp_plan (index ingest + dedup + Hit-Map probe + hit/miss + window-safe victim
-selection + bookkeeping), the Collect/Exchange/Insert transfer (one kernel
-pulls the missed rows into the freed slots and stages the victims in pinned
-host memory; CPU threads scatter them into their host rows),
+selection + bookkeeping), the Collect/Exchange/Insert transfer (CPU threads
+gather the missed rows into pinned memory, one kernel moves them into the
+freed slots and stages the victims in pinned memory, CPU threads scatter the
+victims into their host rows),
 sp_forward (EmbeddingBag gather-reduce), the MLP stand-in
 (surrogate gradient kernel) and sp_train (coalescing segmented reduce + fused
 SGD).  Workload at N=1: BASELINE configs[1], Criteo-Kaggle-shaped (the config
@@ -519,9 +520,10 @@ def run_ours(args):
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
-        "host_link": {"path": "k_pullfill: zero-copy pull of missed rows (H2D) and victims written "
-                              "contiguously to pinned staging (D2H) by one bounded-grid kernel; CPU "
-                              "threads scatter staged victims into the host tables",
+        "host_link": {"path": "CPU threads gather the missed rows into a contiguous pinned slot; "
+                              "k_pullfill moves it into the freed slots (H2D) and writes the victims "
+                              "contiguously to pinned staging (D2H), TMA bulk copies, 16 one-warp CTAs; "
+                              "CPU threads scatter the staged victims into the host tables",
                       "h2d_bytes_per_batch": int(4 * D * m),
                       "h2d_GBs": None if link_GBs is None else round(link_GBs, 2),
                       "d2h_bytes_per_batch": int(4 * D * ev),
@@ -530,9 +532,10 @@ def run_ours(args):
                       "h2d_frac": None if link_GBs is None else round(link_GBs / 55.6, 4),
                       "d2h_frac": None if wb_GBs is None else round(wb_GBs / 57.0, 4),
                       "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)",
-                      "note": "random 256-B host rows are bound by host-side address translation "
-                              "(~32 us per 1,800 fresh rows, profiles/r01_host_tlb_microbench.txt), "
-                              "not by link bandwidth"},
+                      "note": "the kernel moves contiguous pinned slots; random host rows are "
+                              "handled by CPU threads (GPU reads of random host rows are bound by "
+                              "host-side address translation, ~32 us per 1,800 fresh rows, "
+                              "profiles/r01_host_tlb_microbench.txt)"},
         # stage overlap in the graph-mode steady state: 1.0 = the step costs
         # only its slowest stream, 0.0 = the stages run back to back
         "overlap": _overlap(kernels, ms_per_step * 1e3) if timed_src else None,

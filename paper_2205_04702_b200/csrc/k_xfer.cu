@@ -3,21 +3,21 @@
 //
 // Direction by direction, on measurements of this platform (
 // profiles/r01_host_tlb_microbench.txt, r01_tma_xfer_microbench*.txt):
-//   host -> HBM  the GPU pulls the missed rows itself from a BOUNDED grid of
-//                one-warp CTAs (16): random host rows are bound by address
-//                translation on the host side of the link, not bandwidth,
-//                and more SMs mostly add interference with the Train
-//                kernels.  Rows move as whole-row TMA bulk copies
-//                (cp.async.bulk, one request per row instead of 16-B loads).
+//   host -> HBM  by default the CPU gather thread has copied the missed rows
+//                into a contiguous pinned slot (A.in_stage); the kernel moves
+//                that slot into the freed Storage slots.  GPU reads of random
+//                host rows are bound by host-side address translation and
+//                slow the concurrent Train kernels; with in_stage == nullptr
+//                (SP_CPU_GATHER=0) the kernel pulls each row from its table.
+//                Rows move as whole-row TMA bulk copies (cp.async.bulk, one
+//                request per row) from a bounded grid of 16 one-warp CTAs.
 //   HBM -> host  the same kernel writes the victims, contiguously, into a
-//                pinned host staging slot (sequential pages: few
-//                translations), raises a pinned flag when the last CTA is
-//                done, and the CPU threads of the transfer engine scatter
-//                them into the host tables (runtime.cu): random host rows
-//                are translated by the CPU MMU, not the IOMMU the pulls use.
+//                pinned staging slot with their host addresses, raises a
+//                pinned flag when the last CTA is done, and the CPU threads of
+//                the transfer engine scatter them into the host tables.
 //   for every fill k (slot s, missed row x, previous resident o) of Plan(b),
 //   staging index i = prefix + k:
-//       smem <- Storage[s], smem' <- host[t][x]   (both land before any store)
+//       smem <- Storage[s], smem' <- in_stage[i] (or host[t][x])   (both land first)
 //       wb_stage[i] <- smem      if o is valid (dirty victim)
 //       Storage[s]  <- smem'     (the freed slot gets the missed row)
 #include "sp_internal.cuh"
