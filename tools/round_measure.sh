@@ -14,6 +14,12 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/ref.json 
 KR='regex:^(k_push|k_pullfill|k_fwd|k_bwd|k_surrogate)'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KR" -s 3000 -c 600 --csv \
   --log-file $O/launches.csv python bench.py --steps 200 --warmup 5 --no-cpu-baseline --profile-steps 5 > $O/ncu_list.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k "$KR" -s 3000 -c 12 \
+# The full capture runs with the GPU pull (SP_CPU_GATHER=0): ncu serialises
+# every launch, which deadlocks the CPU gather handshake (a transfer waits for
+# the gather thread, which waits for a Plan ncu has not let run yet).  The
+# Train kernels it measures are the same; the launch list above is timed in
+# the default configuration.
+KF='regex:^(k_push|k_pullfill|k_fwd|k_bwd|k_surrogate)'
+SP_CPU_GATHER=0 timeout 1200 ncu --set full --clock-control none --import-source on -k "$KF" -s 3000 -c 12 \
   -o $O/full python bench.py --steps 40 --warmup 5 --no-cpu-baseline --profile-steps 5 > $O/ncu_full.log 2>&1
 ls -la $O
