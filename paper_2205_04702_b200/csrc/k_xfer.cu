@@ -112,7 +112,11 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
         const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
         const uint32_t lo = min(total, blockIdx.x * per), hi = min(total, lo + per);
         const uint32_t nround = hi > lo ? (hi - lo + nb - 1) / nb : 0;
-        auto vbuf = [&](int s, int i) { return sm + ((size_t)s * nb + i) * 2 * rowb; };
+        // per stage: nb victim rows, then nb new rows (contiguous, so a gathered
+        // round moves as one bulk copy each way)
+        auto vbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + i) * rowb; };
+        auto nbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + nb + i) * rowb; };
+        const bool gathered = A.in_stage != nullptr && !A.diag_nowb;
         auto issue = [&](uint32_t r) {
             const int s = (int)((phase_ctr + r) % XS);
             const uint32_t k0 = lo + r * nb;
@@ -139,20 +143,28 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
             const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
             if (lane == 0) mbar_expect_tx(&bar[s], tot);
             __syncwarp();
-            if (slot != EMPTY) {
-                if (stage != EMPTY) bulk_g2s(vbuf(s, lane), A.storage + (size_t)slot * g.D, rowb, &bar[s]);
-                bulk_g2s(vbuf(s, lane) + rowb, src_host, rowb, &bar[s]);
+            if (gathered) {  // the round's new rows: one contiguous bulk copy
+                if (lane == 0 && cnt) bulk_g2s(nbuf(s, 0), A.in_stage + (size_t)(base_t0 + k0) * g.D, cnt * rowb, &bar[s]);
+            } else if (slot != EMPTY) {
+                bulk_g2s(nbuf(s, lane), src_host, rowb, &bar[s]);
             }
+            if (slot != EMPTY && stage != EMPTY) bulk_g2s(vbuf(s, lane), A.storage + (size_t)slot * g.D, rowb, &bar[s]);
         };
         for (uint32_t r = 0; r < min((uint32_t)XS, nround); r++) issue(r);
         for (uint32_t r = 0; r < nround; r++) {
             const int s = (int)((phase_ctr + r) % XS);
             mbar_wait(&bar[s], ((phase_ctr + r) / XS) & 1u);
             const uint32_t slot = s_slot[s][lane], stage = s_stage[s][lane];
-            if (slot != EMPTY) {
-                if (stage != EMPTY) bulk_s2g(A.wb_stage + (size_t)stage * g.D, vbuf(s, lane), rowb);
-                bulk_s2g(A.storage + (size_t)slot * g.D, vbuf(s, lane) + rowb, rowb);
+            if (gathered) {
+                // victims: one contiguous bulk store of the round's staging rows
+                // (rows of fills without a victim carry garbage; their work-list
+                // entry is 0, so the scatter skips them)
+                const uint32_t k0 = lo + r * nb, cnt = min((uint32_t)nb, hi - k0);
+                if (lane == 0 && cnt) bulk_s2g(A.wb_stage + (size_t)(base_t0 + k0) * g.D, vbuf(s, 0), cnt * rowb);
+            } else if (slot != EMPTY && stage != EMPTY) {
+                bulk_s2g(A.wb_stage + (size_t)stage * g.D, vbuf(s, lane), rowb);
             }
+            if (slot != EMPTY) bulk_s2g(A.storage + (size_t)slot * g.D, nbuf(s, lane), rowb);
             bulk_commit();
             if (r + XS < nround) {
                 bulk_wait_read0();  // stage s has been read out: refill it
