@@ -47,9 +47,10 @@
  *
  * Environment (read at sp_create; tuning experiments and diagnostics only,
  * the defaults are the measured best on B200):
- *   SP_CPU_GATHER=0       the transfer kernel pulls the missed rows from their
- *                         random host rows itself (default: CPU threads gather
- *                         them into a contiguous pinned slot first)
+ *   SP_CPU_GATHER=0|1     0: the transfer kernel pulls the missed rows from
+ *                         their random host rows itself; 1: CPU threads gather
+ *                         them into a contiguous pinned slot first (default:
+ *                         1 when T*N*L*dim*4 <= 32 MB, i.e. few rows per batch)
  *   SP_PULL_CTAS=n        transfer-kernel grid (one-warp CTAs, default 16)
  *   SP_XFER_STREAMS=1     one transfer stream instead of two alternating ones
  *   SP_XFER_PRIO=1        transfer streams at the highest priority

@@ -1016,7 +1016,11 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaHostAlloc((void **)&c->h_staged, RING * sizeof(unsigned long long), cudaHostAllocMapped));
     std::memset(c->h_staged, 0, RING * sizeof(unsigned long long));
     CKC(cudaHostGetDevicePointer((void **)&c->hd_staged, c->h_staged, 0));
-    c->cpu_gather = true;  // measured +8-9% (value and e2e) over GPU pulls of random host rows
+    // CPU gather when a batch's rows are few (latency, not copy bandwidth,
+    // dominates): +8-9% on Kaggle (T*n*D*4 = 13.6 MB); the GPU pull wins on
+    // Terabyte (54.5 MB: 7.0k vs 6.0k it/s) and high-pooling (671 MB: 96 vs
+    // 54 it/s), where the CPU copy threads become the bound
+    c->cpu_gather = (double)c->T * c->n * c->D * sizeof(float) <= 32.0 * (1 << 20);
     if (const char *e = getenv("SP_CPU_GATHER")) c->cpu_gather = atoi(e) != 0;
     if (c->cpu_gather) {
         CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
