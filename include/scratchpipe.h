@@ -51,6 +51,8 @@
  *                         their random host rows itself; 1: CPU threads gather
  *                         them into a contiguous pinned slot first (default:
  *                         1 when T*N*L*dim*4 <= 32 MB, i.e. few rows per batch)
+ *   SP_GATHER_DMA=1       with the CPU gather, copy the gathered slot to HBM by
+ *                         copy-engine DMA before the transfer kernel (default 0)
  *   SP_PULL_CTAS=n        transfer-kernel grid (one-warp CTAs, default 16)
  *   SP_XFER_STREAMS=1     one transfer stream instead of two alternating ones
  *   SP_XFER_PRIO=1        transfer streams at the highest priority

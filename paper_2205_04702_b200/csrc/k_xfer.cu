@@ -143,8 +143,15 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
             const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
             if (lane == 0) mbar_expect_tx(&bar[s], tot);
             __syncwarp();
-            if (gathered) {  // the round's new rows: one contiguous bulk copy
-                if (lane == 0 && cnt) bulk_g2s(nbuf(s, 0), A.in_stage + (size_t)(base_t0 + k0) * g.D, cnt * rowb, &bar[s]);
+            if (gathered) {  // the round's new rows: contiguous bulk copies, from the
+                             // DMA'd device copy where it reaches, else the pinned slot
+                if (lane == 0 && cnt) {
+                    const uint32_t i0 = base_t0 + k0;
+                    const uint32_t nd = A.in_dev ? min(cnt, A.in_dev_rows > i0 ? A.in_dev_rows - i0 : 0u) : 0u;
+                    if (nd) bulk_g2s(nbuf(s, 0), A.in_dev + (size_t)i0 * g.D, nd * rowb, &bar[s]);
+                    if (cnt > nd)
+                        bulk_g2s(nbuf(s, nd), A.in_stage + (size_t)(i0 + nd) * g.D, (cnt - nd) * rowb, &bar[s]);
+                }
             } else if (slot != EMPTY) {
                 bulk_g2s(nbuf(s, lane), src_host, rowb, &bar[s]);
             }

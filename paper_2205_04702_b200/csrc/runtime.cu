@@ -250,6 +250,14 @@ struct sp_ctx {
     unsigned long long *h_gathered = nullptr;  // pinned mapped: batches gathered
     unsigned long long *d_gathered = nullptr;  // device alias (stream wait-value)
     std::atomic<long long> x_gathered{0};
+    // copy-engine H2D of the gathered slot (SP_GATHER_DMA=1; off by default:
+    // measured 4% slower on Kaggle, the DMA's HBM writes slow k_fwd/k_bwd more
+    // than it saves the surrogate): the first rows of the slot go to d_in by
+    // DMA on the transfer stream; k_pullfill reads them from HBM and any rows
+    // beyond from the pinned slot (zero-copy).
+    bool gather_dma = false;
+    float *d_in = nullptr;                     // device [XSR][T*n][D]
+    std::atomic<long long> x_max_m{0};         // largest of the last 16 gathered batches (rows)
     // errors
     sp_status poisoned = SP_OK;
     std::string err = "no error";
@@ -596,6 +604,7 @@ void scatter_main(sp_ctx *c) {
 // has finished reading the slot.  Publishes gathered = b + 1 (the transfer
 // stream waits on it).  No CUDA API call.
 void gather_main(sp_ctx *c) {
+    long long recent[16] = {};
     const size_t rowb = (size_t)c->D * sizeof(float);
     const size_t slab = (size_t)c->T * c->n * c->D;
     std::vector<const float *> src;
@@ -639,6 +648,12 @@ void gather_main(sp_ctx *c) {
             c->x_gather_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
                                   std::chrono::steady_clock::now() - t0).count();
             c->x_rows_g += (long long)src.size();
+            {   // largest of the last 16 batches (cold-start bursts age out)
+                recent[g % 16] = (long long)src.size();
+                long long mx = 0;
+                for (long long v : recent) mx = std::max(mx, v);
+                c->x_max_m.store(mx, std::memory_order_relaxed);
+            }
             g++;
             c->x_gathered.store(g, std::memory_order_release);
             std::atomic_thread_fence(std::memory_order_seq_cst);
@@ -711,6 +726,18 @@ sp_status pump(sp_ctx *c) {
         a.g = c->g;
         a.bb = c->ring[r];
         if (c->cpu_gather) a.in_stage = c->hd_in + (size_t)(b % c->XSR) * c->T * c->n * c->D;
+        if (c->cpu_gather && c->gather_dma) {
+            // rows to DMA: 1.5x the largest of the last 16 gathered batches
+            // (+256), at most the slot; rows past them are read zero-copy
+            const long long Tn = (long long)c->T * c->n;
+            long long rows = c->x_max_m.load(std::memory_order_relaxed);
+            rows = rows ? std::min(Tn, rows + rows / 2 + 256) : Tn;
+            const size_t off = (size_t)(b % c->XSR) * Tn * c->D;
+            CK(cudaMemcpyAsync(c->d_in + off, c->h_in + off, (size_t)rows * c->D * sizeof(float),
+                               cudaMemcpyHostToDevice, xs));
+            a.in_dev = c->d_in + off;
+            a.in_dev_rows = (uint32_t)rows;
+        }
         a.storage = c->d_storage;
         a.host = c->d_host;
         a.wb_stage = c->hd_wb + (size_t)(b % c->XSR) * c->T * c->n * c->D;
@@ -1038,6 +1065,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
             c->hl_dev[r].row = drow + (size_t)r * Tn;
         }
         CKC(cudaHostAlloc((void **)&c->h_in, (size_t)c->XSR * Tn * c->D * sizeof(float), cudaHostAllocMapped));
+        if (const char *e = getenv("SP_GATHER_DMA")) c->gather_dma = atoi(e) != 0;
+        if (c->gather_dma) CKC(dalloc(c, &c->d_in, (size_t)c->XSR * Tn * c->D));
         CKC(cudaHostGetDevicePointer((void **)&c->hd_in, c->h_in, 0));
         CKC(cudaHostAlloc((void **)&c->h_gathered, sizeof(unsigned long long), cudaHostAllocMapped));
         *c->h_gathered = 0;

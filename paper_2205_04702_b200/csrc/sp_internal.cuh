@@ -151,6 +151,8 @@ struct XferArgs {
     unsigned long long *wb_dst;  // [sum m] host address of each staged victim's row (0: none)
     unsigned long long *staged_cnt;  // pinned: sum m of this batch (written before `staged`)
     int diag_nowb;                // timing diagnostic: skip the victims' staging stores
+    const float *in_dev;          // device copy of the first in_dev_rows rows of in_stage
+    uint32_t in_dev_rows;         //   (copy-engine DMA), or nullptr / 0
     const float *in_stage;        // [sum m][D] missed rows gathered by the CPU into pinned
                                   // host memory (contiguous, flattened over tables), or
                                   // nullptr: pull each row from its host table
