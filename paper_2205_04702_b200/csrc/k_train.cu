@@ -159,9 +159,12 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
     constexpr int RBN = VPL >= 4 ? 1 : (VPL == 2 ? 2 : 4);  // chunk records (mostly 1-2 occurrences)
     // ---- H: hot-row segments, one CTA each (RB rows per group: one round)
     __shared__ uint32_t s_last;
+    __shared__ uint32_t s_pref_n[65];  // chunk-record prefix, computed up front when T <= 64
+    const bool one_group = g.T <= 64;
+    if (one_group) table_prefix2(A.bb.nhot, A.bb.nchunks, 0, g.T, s_pref, s_pref_n);
     for (int t0 = 0; t0 < g.T; t0 += 64) {
         const int tcount = min(64, g.T - t0);
-        table_prefix(A.bb.nhot, t0, tcount, s_pref);
+        if (!one_group) table_prefix(A.bb.nhot, t0, tcount, s_pref);
         const uint32_t total = s_pref[tcount];
         for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
             const int tl = find_table(s_pref, tcount, item);
@@ -277,7 +280,13 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
     // ---- N: single-chunk rows, taken dynamically one record per group
     for (int t0 = 0; t0 < g.T; t0 += 64) {
         const int tcount = min(64, g.T - t0);
-        table_prefix(A.bb.nchunks, t0, tcount, s_pref);
+        if (one_group) {
+            __syncthreads();
+            if (threadIdx.x < 65) s_pref[threadIdx.x] = s_pref_n[threadIdx.x];
+            __syncthreads();
+        } else {
+            table_prefix(A.bb.nchunks, t0, tcount, s_pref);
+        }
         const uint32_t total = s_pref[tcount];
         uint32_t *ctr = A.bb.work + t0 / 64;
         // the next round's grab is issued before this round's record is

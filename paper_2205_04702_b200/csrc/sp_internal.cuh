@@ -198,6 +198,32 @@ __device__ __forceinline__ void table_prefix(const uint32_t *counts, int t0, int
     __syncthreads();
 }
 
+// Two prefixes at once (warp 0: counts_a -> pa, warp 1: counts_b -> pb), so
+// their global loads are in flight together.  Contains __syncthreads.
+__device__ __forceinline__ void table_prefix2(const uint32_t *counts_a, const uint32_t *counts_b, int t0,
+                                              int tcount, uint32_t *pa, uint32_t *pb) {
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        const int lane = threadIdx.x & 31;
+        const uint32_t *counts = threadIdx.x < 32 ? counts_a : counts_b;
+        uint32_t *s_pref = threadIdx.x < 32 ? pa : pb;
+        uint32_t a = lane < tcount ? counts[t0 + lane] : 0u;
+        uint32_t b = lane + 32 < tcount ? counts[t0 + lane + 32] : 0u;
+        uint32_t x = a, y = b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t xa = __shfl_up_sync(0xffffffffu, x, o);
+            uint32_t yb = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) { x += xa; y += yb; }
+        }
+        const uint32_t tot_a = __shfl_sync(0xffffffffu, x, 31);
+        s_pref[lane] = x - a;
+        s_pref[lane + 32] = tot_a + y - b;
+        if (lane == 31) s_pref[64] = tot_a + y;
+    }
+    __syncthreads();
+}
+
 // Table of a flattened work item: the tl with s_pref[tl] <= item < s_pref[tl+1]
 // (binary search; empty tables have equal prefixes and are skipped).
 __device__ __forceinline__ int find_table(const uint32_t *s_pref, int tcount, uint32_t item) {
