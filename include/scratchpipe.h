@@ -60,7 +60,8 @@
  *   SP_CARVEOUT=pct       shared-memory carveout hint for every kernel
  *   SP_DIAG_SERIAL=1      every GPU stage on the caller's stream (no overlap)
  *   SP_DIAG=mask          1: the transfer kernel moves nothing, 2: the Train
- *                         kernels do nothing, 4: victims are not staged --
+ *                         kernels do nothing, 4: victims are not staged, 8 / 16:
+ *                         k_bwd skips hot segments / chunk records --
  *                         RESULTS ARE WRONG (timing only)
  *   SP_NO_GRAPHS=1        sp_run_steps without CUDA-graph replay
  */

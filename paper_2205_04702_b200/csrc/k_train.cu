@@ -162,10 +162,17 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
     __shared__ uint32_t s_pref_n[65];  // chunk-record prefix, computed up front when T <= 64
     const bool one_group = g.T <= 64;
     if (one_group) table_prefix2(A.bb.nhot, A.bb.nchunks, 0, g.T, s_pref, s_pref_n);
+    if (A.diag & 8) {  // timing diagnostic: no hot segments
+        __syncthreads();
+        if (threadIdx.x <= 64) s_pref[threadIdx.x] = 0;
+        __syncthreads();
+    }
+    uint32_t htot = 0;  // hot segments over all tables: CTAs [0, htot) start with one
     for (int t0 = 0; t0 < g.T; t0 += 64) {
         const int tcount = min(64, g.T - t0);
         if (!one_group) table_prefix(A.bb.nhot, t0, tcount, s_pref);
         const uint32_t total = s_pref[tcount];
+        htot += total;
         for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
             const int tl = find_table(s_pref, tcount, item);
             const int t = t0 + tl;
@@ -287,20 +294,33 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
         } else {
             table_prefix(A.bb.nchunks, t0, tcount, s_pref);
         }
-        const uint32_t total = s_pref[tcount];
+        const uint32_t total = (A.diag & 16) ? 0u : s_pref[tcount];  // diagnostic: no chunk records
         uint32_t *ctr = A.bb.work + t0 / 64;
-        // the next round's grab is issued before this round's record is
-        // folded, so the atomic's latency overlaps the gradient loads
-        __syncthreads();
-        if (threadIdx.x == 0) s_base = atomicAdd(ctr, (uint32_t)gpb);
-        __syncthreads();
-        uint32_t next = s_base;
+        // The first round is static (CTA c >= hotc takes records
+        // [(c-hotc)*gpb, (c-hotc+1)*gpb)):
+        // one same-address atomic per CTA at launch cost ~5 us of serialised
+        // L2 atomics for an otherwise empty kernel.  Later rounds are grabbed
+        // from the counter, offset past the static part; the next round's
+        // grab is issued before this round's record is folded, so the
+        // atomic's latency overlaps the gradient loads.
+        // (CTAs that folded a hot segment start on the counter instead)
+        const uint32_t hotc = min(htot, gridDim.x);
+        const uint32_t static_part = (gridDim.x - hotc) * (uint32_t)gpb;
+        uint32_t next;
+        if (blockIdx.x >= hotc) {
+            next = (blockIdx.x - hotc) * (uint32_t)gpb;
+        } else {
+            __syncthreads();
+            if (threadIdx.x == 0) s_base = static_part >= total ? total : static_part + atomicAdd(ctr, (uint32_t)gpb);
+            __syncthreads();
+            next = s_base;
+        }
         while (true) {
             const uint32_t base = next;
             if (base >= total) break;
             __syncthreads();  // every thread has read s_base
             uint32_t nx = 0;
-            if (threadIdx.x == 0) nx = atomicAdd(ctr, (uint32_t)gpb);
+            if (threadIdx.x == 0) nx = static_part >= total ? total : static_part + atomicAdd(ctr, (uint32_t)gpb);
             const uint32_t item = base + gi;
             if (item < total) {
             const int tl = find_table(s_pref, tcount, item);

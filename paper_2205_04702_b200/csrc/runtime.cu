@@ -528,6 +528,7 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.partial = c->d_partial;
     a.err = c->d_err;
     if (c->diag & 2) a.g.T = 0;  // diagnostic: Train kernels launched, no work
+    a.diag = c->diag;
     return a;
 }
 

@@ -140,6 +140,7 @@ struct TrainArgs {
     float lr;
     double *partial;     // [T][nh][D] fp64 partial sums of hot-row segments
     const unsigned long long *err;
+    int diag;            // timing diagnostic (k_bwd): 8 = skip hot segments, 16 = skip chunk records
 };
 
 struct XferArgs {
