@@ -358,3 +358,21 @@ def test_prefill_all_resident_no_misses_matches_oracle():
     with pytest.raises(SpError):
         sp2.prefill()
     sp2.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"SP_CPU_GATHER": "0"}, {"SP_CPU_GATHER": "1"},
+                                 {"SP_CPU_GATHER": "1", "SP_GATHER_DMA": "1"}])
+def test_transfer_modes_match_oracle(env, monkeypatch):
+    """Every transfer mode (GPU pull of random host rows, CPU gather into a
+    pinned slot, CPU gather + copy-engine DMA) gives the oracle's plans,
+    pooled values and final tables under heavy eviction; the default picks by
+    batch size, so large configurations use the GPU pull."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rows, D, N, L, nb = [5000, 700, 90], 32, 96, 3, 40
+    tr = sample_trace(rows, N, L, 0.9, nb, 51)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 4) for t, R in enumerate(rows)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr, gde=(0.5, 0.01, 0.05))
+    assert rep["evictions"] > 200
+    _assert_tables(rep)
