@@ -16,6 +16,7 @@
 //   k_surrogate  the harness's MLP stand-in g = fmaf(gamma, pooled, delta).
 #include "sp_internal.cuh"
 
+#include <cstdlib>
 #include <unordered_map>
 
 namespace sp {
@@ -509,7 +510,11 @@ int backward_hot_segment(int D) {
         default: return 64;
     }
     const int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);
-    return (256 / G) * RB;
+    int hs = (256 / G) * RB;  // one round of RB rows per lane group
+    // SP_HOT_SEG overrides (A/B; >= CH so a hot row has >= 2 segments' worth).
+    // Measured on Kaggle: 2 and 4 rounds per segment were 16% / 51% slower.
+    if (const char *e = getenv("SP_HOT_SEG")) hs = atoi(e) >= CH ? atoi(e) : hs;
+    return hs;
 }
 
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
