@@ -64,6 +64,7 @@
  *                         k_bwd skips hot segments / chunk records --
  *                         RESULTS ARE WRONG (timing only)
  *   SP_NO_GRAPHS=1        sp_run_steps without CUDA-graph replay
+ *   SP_PDL=0              no programmatic dependent launch of k_surrogate / k_bwd
  */
 #ifndef SCRATCHPIPE_H
 #define SCRATCHPIPE_H

@@ -727,6 +727,7 @@ __global__ void __launch_bounds__(PUSH_THREADS, SP_PUSH_MIN_BLOCKS) k_push(PushA
 size_t push_smem_bytes(int n) { return n <= SMEM_SORT_MAX ? (size_t)n * 4 * sizeof(uint32_t) : 0; }
 
 int g_carveout = -1;
+int g_pdl = 1;
 
 cudaError_t configure_push_kernel() {
     apply_carveout(k_push);

@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
     __shared__ uint32_t s_pref_n[65];  // chunk-record prefix, computed up front when T <= 64
     const bool one_group = g.T <= 64;
     if (one_group) table_prefix2(A.bb.nhot, A.bb.nchunks, 0, g.T, s_pref, s_pref_n);
+    griddep_wait();  // (PDL) the surrogate's gradients are complete from here on
     if (A.diag & 8) {  // timing diagnostic: no hot segments
         __syncthreads();
         if (threadIdx.x <= 64) s_pref[threadIdx.x] = 0;
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
 constexpr int SU = 4;
 __global__ void __launch_bounds__(256) k_surrogate(const float4 *p, float4 *g, long long n4,
                                                    float gamma, float delta) {
+    griddep_wait();  // (PDL) pooled is complete from here on
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += SU * stride) {
         float4 x[SU];
@@ -461,8 +463,27 @@ static int resident_ctas(K kernel, int threads) {
     return per_sm * num_sms();
 }
 
+template <typename K, typename... Args>
+static void launch_maybe_pdl(K kernel, int grid, int block, size_t smem, cudaStream_t s, bool pdl, Args... args) {
+    if (pdl && g_pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(block);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kernel, args...);
+    } else {
+        kernel<<<grid, block, smem, s>>>(args...);
+    }
+}
+
 template <int G, int VPL, typename K>
-static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStream_t s) {
+static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStream_t s, bool pdl = false) {
     static std::unordered_map<const void *, int> caps;  // per kernel (not per signature)
     int &cap = caps[reinterpret_cast<const void *>(kernel)];
     if (!cap) {
@@ -472,31 +493,29 @@ static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStr
     long long blocks = (groups + (256 / G) - 1) / (256 / G);
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
-    kernel<<<grid, 256, 0, s>>>(a);
+    launch_maybe_pdl(kernel, grid, 256, 0, s, pdl, a);
 }
 
-#define SP_DISPATCH_D(D4, KERNEL, GROUPS, ARGS, STREAM)                                  \
-    switch (D4) {                                                                         \
-        case 1: launch_sized<1, 1>(KERNEL<1, 1>, GROUPS, ARGS, STREAM); break;            \
-        case 2: launch_sized<2, 1>(KERNEL<2, 1>, GROUPS, ARGS, STREAM); break;            \
-        case 4: launch_sized<4, 1>(KERNEL<4, 1>, GROUPS, ARGS, STREAM); break;            \
-        case 8: launch_sized<8, 1>(KERNEL<8, 1>, GROUPS, ARGS, STREAM); break;            \
-        case 16: launch_sized<16, 1>(KERNEL<16, 1>, GROUPS, ARGS, STREAM); break;         \
-        case 32: launch_sized<32, 1>(KERNEL<32, 1>, GROUPS, ARGS, STREAM); break;         \
-        case 64: launch_sized<32, 2>(KERNEL<32, 2>, GROUPS, ARGS, STREAM); break;         \
-        case 128: launch_sized<32, 4>(KERNEL<32, 4>, GROUPS, ARGS, STREAM); break;        \
-        case 256: launch_sized<32, 8>(KERNEL<32, 8>, GROUPS, ARGS, STREAM); break;        \
-        default: launch_sized<32, 1>(KERNEL##_generic, GROUPS, ARGS, STREAM); break;      \
+#define SP_DISPATCH_D(D4, KERNEL, GROUPS, ARGS, STREAM, PDL)                                   \
+    switch (D4) {                                                                              \
+        case 1: launch_sized<1, 1>(KERNEL<1, 1>, GROUPS, ARGS, STREAM, PDL); break;            \
+        case 2: launch_sized<2, 1>(KERNEL<2, 1>, GROUPS, ARGS, STREAM, PDL); break;            \
+        case 4: launch_sized<4, 1>(KERNEL<4, 1>, GROUPS, ARGS, STREAM, PDL); break;            \
+        case 8: launch_sized<8, 1>(KERNEL<8, 1>, GROUPS, ARGS, STREAM, PDL); break;            \
+        case 16: launch_sized<16, 1>(KERNEL<16, 1>, GROUPS, ARGS, STREAM, PDL); break;         \
+        case 32: launch_sized<32, 1>(KERNEL<32, 1>, GROUPS, ARGS, STREAM, PDL); break;         \
+        case 64: launch_sized<32, 2>(KERNEL<32, 2>, GROUPS, ARGS, STREAM, PDL); break;         \
+        case 128: launch_sized<32, 4>(KERNEL<32, 4>, GROUPS, ARGS, STREAM, PDL); break;        \
+        case 256: launch_sized<32, 8>(KERNEL<32, 8>, GROUPS, ARGS, STREAM, PDL); break;        \
+        default: launch_sized<32, 1>(KERNEL##_generic, GROUPS, ARGS, STREAM, false); break;    \
     }
 
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
-    SP_DISPATCH_D(D4, k_fwd, (long long)a.g.T * a.g.N, a, s);
+    SP_DISPATCH_D(D4, k_fwd, (long long)a.g.T * a.g.N, a, s, false);
     return cudaGetLastError();
 }
 
-// occurrences per hot-row segment: one round of RB rows per lane group of
-// the k_bwd instance that D dispatches to (generic D: 64)
 // occurrences per hot-row segment: one round of RB rows per lane group of
 // the k_bwd instance that D dispatches to (generic D: 64).  (Half-width lane
 // groups, two float4 per lane, were measured slower: 20.7 vs 16.4 us.)
@@ -520,7 +539,7 @@ int backward_hot_segment(int D) {
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
     // upper bound of work items: all chunks of all tables
-    SP_DISPATCH_D(D4, k_bwd, (long long)a.g.T * a.g.nc, a, s);
+    SP_DISPATCH_D(D4, k_bwd, (long long)a.g.T * a.g.nc, a, s, true);
     return cudaGetLastError();
 }
 
@@ -536,8 +555,8 @@ cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, 
         apply_carveout(k_surrogate);
         once = true;
     }
-    k_surrogate<<<grid, 256, 0, s>>>(reinterpret_cast<const float4 *>(pooled),
-                                     reinterpret_cast<float4 *>(grad), n4, gamma, delta);
+    launch_maybe_pdl(k_surrogate, grid, 256, 0, s, true, reinterpret_cast<const float4 *>(pooled),
+                     reinterpret_cast<float4 *>(grad), n4, gamma, delta);
     return cudaGetLastError();
 }
 

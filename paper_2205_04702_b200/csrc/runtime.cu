@@ -979,6 +979,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     for (int r = 0; r < RING; r++)
         for (int k = 0; k < 8; k++) CKC(cudaEventCreate(&c->sev[r][k]));
     if (const char *e = getenv("SP_CARVEOUT")) g_carveout = atoi(e);
+    if (const char *e = getenv("SP_PDL")) g_pdl = atoi(e) != 0;
     CKC(configure_push_kernel());
 
     // device allocations

@@ -253,6 +253,11 @@ size_t push_smem_bytes(int n);
 // -1 = driver default; set once at sp_create (SP_CARVEOUT) so consecutive
 // kernels on an SM do not force an L1/shared reconfiguration
 extern int g_carveout;
+// Programmatic dependent launch for k_surrogate and k_bwd (SP_PDL, default on):
+// each may be launched while its predecessor on the stream drains, runs the
+// prologue that reads no predecessor output, then griddepcontrol.wait
+extern int g_pdl;
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 template <typename K>
 inline void apply_carveout(K kernel) {
     if (g_carveout >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
