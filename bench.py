@@ -9,12 +9,14 @@ freed slots and stages the victims in pinned memory, CPU threads scatter the
 victims into their host rows),
 sp_forward (EmbeddingBag gather-reduce), the MLP stand-in
 (surrogate gradient kernel) and sp_train (coalescing segmented reduce + fused
-SGD).  Workload at N=1: BASELINE configs[1], Criteo-Kaggle-shaped (the config
-the metric is quoted on that fits one GPU), in steady state: `preroll`
-untimed batches first fill the scratchpad (cold start is not the paper's
-regime), then W warm-up steps, then K timed steps.
+SGD).  Workload at N=1: BASELINE configs[2], Criteo-Terabyte-shaped (the
+shape north_star names for the 1- and 8-GPU headline; it fits one B200), in
+steady state: `preroll` untimed batches first fill the scratchpad (cold start
+is not the paper's regime), then W warm-up steps, then K timed steps.  The
+other BASELINE configs are parity-test cases and extra runs (--config kaggle |
+highpool | tiny).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config kaggle]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config terabyte]
 
 Prints ONE JSON line on rank 0.  `value` times device-resident int32 indices
 (inputs in HBM); `e2e` times the same steps one library call per step with
@@ -43,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="kaggle")
+    ap.add_argument("--config", default="terabyte")
     ap.add_argument("--variant", default="pipelined", choices=["pipelined", "serial", "resident", "gpuonly"],
                     help="design points of PAPER.md Fig. 10 / Table 1 from the same kernels: "
                          "pipelined (ScratchPipe), serial (straw-man: every stage on one stream, "
@@ -131,6 +133,61 @@ def load_traffic():
     return {}
 
 
+def host_cpu_info():
+    """nproc and the lscpu model name of this box (cpu_baseline context)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "NUMA node(s)", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception as e:  # pragma: no cover
+        info["lscpu"] = f"unavailable: {e}"
+    return info
+
+
+def link_peaks(dev, mib=256, reps=5):
+    """Host-link peaks measured in this run: pinned cudaMemcpyAsync of `mib`
+    MiB, best of `reps`, H2D, D2H and both directions at once (two streams),
+    CUDA events.  The roofline denominators of the transfer stage."""
+    import torch
+    n = mib << 18  # float32 elements
+    h = torch.empty(n, dtype=torch.float32).pin_memory()
+    h2 = torch.empty(n, dtype=torch.float32).pin_memory()
+    d = torch.empty(n, dtype=torch.float32, device=dev)
+    d2 = torch.empty(n, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def once(kind):
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s1)
+        s2.wait_event(a)
+        with torch.cuda.stream(s1):
+            if kind in ("h2d", "bidir"):
+                d.copy_(h, non_blocking=True)
+            else:
+                h.copy_(d, non_blocking=True)
+        if kind == "bidir":
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+            s1.wait_stream(s2)
+        b.record(s1)
+        b.synchronize()
+        return a.elapsed_time(b) * 1e-3
+
+    out = {}
+    for kind in ("h2d", "d2h", "bidir"):
+        once(kind)
+        t = min(once(kind) for _ in range(reps))
+        out[kind + "_GBs"] = round((2 if kind == "bidir" else 1) * n * 4 / t / 1e9, 2)
+    out["how"] = f"pinned cudaMemcpyAsync of {mib} MiB, best of {reps}, CUDA events (bidir: both directions on two streams, bytes summed)"
+    del h, h2, d, d2
+    return out
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -173,7 +230,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": cfg.description, "note": "oracle from a cold scratchpad"},
-            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle", "host": host_cpu_info(),
                              "sample": f"{args.steps} consecutive batches after {args.warmup} warm-up, "
                                        "reference policy + uncached EmbeddingBag SGD, single thread"},
             "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -202,18 +259,62 @@ def cpu_baseline(cfg, trace_dev, seconds):
         if time.perf_counter() - t0 > seconds and n >= 3:
             break
     el = time.perf_counter() - t0
-    return {"value": n / el, "unit": "iters/s", "cores": 1, "kind": "oracle",
+    return {"value": n / el, "unit": "iters/s", "cores": 1, "kind": "oracle", "host": host_cpu_info(),
             "sample": f"first {n} batches of the bench trace from a cold scratchpad: reference policy "
                       f"(Part B) + uncached EmbeddingBag SGD (Part A), single thread, {el:.1f} s"}
 
 
-def _overlap(kernels, step_us):
-    streams = {"plan": kernels["plan"]["avg_us"], "transfer": kernels["transfer"]["avg_us"],
-               "compute": sum(kernels[k]["avg_us"] for k in ("forward", "surrogate", "backward"))}
+def _union_us(iv):
+    """Total length (us) of the union of [a, b] intervals given in ms."""
+    iv = sorted((a, b) for a, b in iv if a == a and b == b and b >= a)
+    tot, cur = 0.0, None
+    for a, b in iv:
+        if cur is None or a > cur[1]:
+            if cur:
+                tot += cur[1] - cur[0]
+            cur = [a, b]
+        else:
+            cur[1] = max(cur[1], b)
+    if cur:
+        tot += cur[1] - cur[0]
+    return tot * 1e3
+
+
+def _stream_busy(ev):
+    """Per-step busy time of each stream over the stage-event window of the
+    last 16 steps (sp_stage_events): union of that stream's intervals / steps."""
+    import numpy as np
+    rows = [r for r in range(ev.shape[0]) if not np.isnan(ev[r, 0])]
+    nst = max(1, len(rows))
+    plan = [(ev[r, 0], ev[r, 1]) for r in rows]
+    comp = [(ev[r, 2], ev[r, 5]) for r in rows]
+    xfer = [(ev[r, 6], ev[r, 7]) for r in range(ev.shape[0]) if not np.isnan(ev[r, 6])]
+    lo = np.nanmin(ev[rows][:, [0, 2]]) if rows else 0.0
+    hi = np.nanmax(ev[rows][:, [1, 5]]) if rows else 0.0
+    return {"plan": _union_us(plan) / nst, "compute": _union_us(comp) / nst,
+            "transfer": _union_us(xfer) / max(1, len(xfer)),
+            "window_us_per_step": (hi - lo) * 1e3 / nst, "steps": nst}
+
+
+def _overlap(kernels, step_us, busy=None):
+    """Stage overlap in the steady state.  busy: per-step busy
+    time of each stream = the union of its event intervals over the last 16
+    steps / 16 (so two transfers in flight on the two alternating transfer
+    streams count once).  Full overlap: step <= 1.05 x the busiest stream.
+    Spans include waiting for SM resources beside the other stages."""
+    if busy is None:
+        return None
+    streams = {k: busy[k] for k in ("plan", "transfer", "compute")}
     tot, mx = sum(streams.values()), max(streams.values())
-    eff = (tot - step_us) / (tot - mx) if tot > mx else None
-    return {"step_us": round(step_us, 2), "stream_us": {k: round(v, 2) for k, v in streams.items()},
-            "serial_sum_us": round(tot, 2), "efficiency": None if eff is None else round(eff, 3)}
+    bound = max(streams, key=streams.get)
+    return {"step_us": round(step_us, 2), "stream_busy_us_per_step": {k: round(v, 2) for k, v in streams.items()},
+            "event_window_us_per_step": round(busy["window_us_per_step"], 2),
+            "serial_sum_us": round(tot, 2), "busiest_stream": bound,
+            "step_over_busiest": round(step_us / mx, 3) if mx else None,
+            "full_overlap": bool(mx and step_us <= 1.05 * mx),
+            "transfer_hidden_behind_compute": bool(streams["transfer"] <= 1.05 * streams["compute"]),
+            "source": "sp_stage_events: CUDA events on each stage's own stream inside the step graphs, "
+                      "union of intervals per stream over the last %d steps" % busy["steps"]}
 
 
 def _plan_roles(p0, p1):
@@ -392,11 +493,12 @@ def run_ours(args):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     st1 = sp.stats()
-    stage_t = None
+    stage_t = stage_busy = None
     if world == 1:  # same graph-mode steady state, step graphs recaptured with event nodes
         sp.set_stage_timing(True)
         value_loop(KS)
         stage_t = sp.stage_times()   # events of the last 16 steps, on each stage's own stream
+        stage_busy = _stream_busy(sp.stage_events())
         sp.set_stage_timing(False)
     st1p = sp.stats()  # baseline of the (eager) profiling pass
     value = K / (ms / 1e3)   # iterations of the global batch per second (max over ranks)
@@ -436,12 +538,16 @@ def run_ours(args):
         e2e_one(k)
     torch.cuda.synchronize()
 
+    e2e_host_t = []
+
     def e2e_step(k):
         e2e_one(WE + k)
         if k >= 1:
             evs[(WE + k - 1) % 2].synchronize()
             hits_seen.append(int(stats_host[WE + k - 1, :, 1].sum()))
+        e2e_host_t.append(time.perf_counter())
     ms_e2e, _ = timed(e2e_step, K)
+    e2e_gaps = [1e6 * (b - a) for a, b in zip(e2e_host_t, e2e_host_t[1:])]
     hits_seen.append(int(stats_host[WE + K - 1, :, 1].sum()))
     e2e_value = K / (ms_e2e / 1e3)
     st3 = sp.stats()
@@ -488,7 +594,7 @@ def run_ours(args):
     dom = max(["forward", "backward"], key=lambda k: kernels[k]["avg_us"])
     ach = kernels[dom]["alg_GBs"] or 0.0
     # ncu DRAM traffic applies to the configuration it was captured on
-    tr_bytes = traffic.get(dom) if traffic.get("config", "kaggle") == args.config else None
+    tr_bytes = traffic.get(args.config, {}).get(dom)  # per config (captured on that workload)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "duration_source": ("CUDA events around the kernel on its stream inside the step graphs "
@@ -501,9 +607,21 @@ def run_ours(args):
                                   else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
     train_ms = (kernels["forward"]["avg_us"] + kernels["backward"]["avg_us"]) * 1e-3
     train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
-    xs = kernels["transfer"]["avg_us"] * 1e-6
+    # host link: the transfer stream's busy time per step (union of its event
+    # intervals: two transfers may be in flight on the alternating streams)
+    xs = (stage_busy["transfer"] if stage_busy else kernels["transfer"]["avg_us"]) * 1e-6
     link_GBs = 4 * D * m / xs / 1e9 if xs else None
     wb_GBs = 4 * D * ev / xs / 1e9 if xs else None
+    lp = link_peaks(dev)
+    mode = st2.get("transfer_mode", "?")
+    path = {"gpu_pull": "k_pullfill pulls each missed row from its host row (TMA bulk copy per row, "
+                        "zero-copy over the link) into the freed Storage slot and writes the victims "
+                        "contiguously to pinned staging; CPU threads scatter them into their host rows",
+            "cpu_gather": "CPU threads gather the missed rows into a contiguous pinned slot; k_pullfill "
+                          "moves it into the freed slots and writes the victims contiguously to pinned "
+                          "staging (TMA bulk copies); CPU threads scatter them into their host rows",
+            "cpu_gather_dma": "CPU gather into a pinned slot, copy-engine DMA of the slot, k_pullfill "
+                              "fills the slots and stages the victims; CPU scatter"}.get(mode, mode)
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
@@ -520,25 +638,21 @@ def run_ours(args):
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
-        "host_link": {"path": "CPU threads gather the missed rows into a contiguous pinned slot; "
-                              "k_pullfill moves it into the freed slots (H2D) and writes the victims "
-                              "contiguously to pinned staging (D2H), TMA bulk copies, 16 one-warp CTAs; "
-                              "CPU threads scatter the staged victims into the host tables",
+        "host_link": {"path": path, "transfer_mode": mode, "engine_threads": st2.get("engine_threads"),
                       "h2d_bytes_per_batch": int(4 * D * m),
                       "h2d_GBs": None if link_GBs is None else round(link_GBs, 2),
                       "d2h_bytes_per_batch": int(4 * D * ev),
                       "d2h_GBs": None if wb_GBs is None else round(wb_GBs, 2),
-                      "peak_h2d_GBs": 55.6, "peak_d2h_GBs": 57.0,
-                      "h2d_frac": None if link_GBs is None else round(link_GBs / 55.6, 4),
-                      "d2h_frac": None if wb_GBs is None else round(wb_GBs / 57.0, 4),
-                      "peak_source": "profiles/r01_host_link_probe.json (pinned cudaMemcpy, 1 GiB)",
-                      "note": "the kernel moves contiguous pinned slots; random host rows are "
-                              "handled by CPU threads (GPU reads of random host rows are bound by "
-                              "host-side address translation, ~32 us per 1,800 fresh rows, "
-                              "profiles/r01_host_tlb_microbench.txt)"},
+                      "peak_h2d_GBs": lp["h2d_GBs"], "peak_d2h_GBs": lp["d2h_GBs"], "peak_bidir_GBs": lp["bidir_GBs"],
+                      "h2d_frac": None if link_GBs is None else round(link_GBs / lp["h2d_GBs"], 4),
+                      "d2h_frac": None if wb_GBs is None else round(wb_GBs / lp["d2h_GBs"], 4),
+                      "bidir_frac": None if link_GBs is None else round((link_GBs + wb_GBs) / lp["bidir_GBs"], 4),
+                      "peak_source": "measured in this run: " + lp["how"],
+                      "busy_source": "transfer-stream busy time per step (union of its event intervals)"
+                                     if stage_busy else "transfer kernel span (profiling pass)"},
         # stage overlap in the graph-mode steady state: 1.0 = the step costs
         # only its slowest stream, 0.0 = the stages run back to back
-        "overlap": _overlap(kernels, ms_per_step * 1e3) if timed_src else None,
+        "overlap": _overlap(kernels, ms_per_step * 1e3, stage_busy) if timed_src else None,
         "kernels": kernels,
         "plan_ctas": _plan_roles(pp0, pp1),
         "host_engine": {"scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1p["host_scatter_ms"]) / KP, 2),
@@ -555,6 +669,8 @@ def run_ours(args):
                                     max(1, st1["graph_steps"] - st0["graph_steps"]), 2),
         "e2e": {"value": round(e2e_value, 2), "unit": "iters/s", "h2d_bytes_per_step": idx_bytes,
                 "d2h_bytes_per_step": stats_bytes, "ms_per_step": round(ms_e2e / K, 5),
+                "host_step_us_first5": [round(x, 1) for x in e2e_gaps[:5]],
+                "host_step_us_median": round(statistics.median(e2e_gaps), 1) if e2e_gaps else None,
                 "path": ("sp_run_steps(1 step) on pinned host int32 indices (the plan kernel reads "
                          "the batch over the host link); sp_copy_batch_stats D2H each step, waited "
                          "for and read one step later") if world == 1 else

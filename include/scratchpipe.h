@@ -76,7 +76,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 1
+#define SP_ABI_VERSION 2
 
 typedef struct sp_ctx sp_ctx;
 
@@ -156,7 +156,15 @@ typedef struct {
     double wait_list_ms;            /* engine (forward / host-list ring reuse)    */
     int64_t graph_steps;            /* sp_run_steps steps replayed as CUDA graphs */
     double graph_step_host_ms;      /* caller-thread wall time spent issuing them */
+    int32_t transfer_mode;          /* how missed rows reach HBM: SP_XFER_*        */
+    int32_t engine_threads;         /* CPU threads of the transfer engine (workers */
+                                    /* + row-copy helpers)                          */
 } sp_stats;
+
+/* sp_stats.transfer_mode */
+#define SP_XFER_GPU_PULL   0  /* k_pullfill reads each missed row from its host row */
+#define SP_XFER_CPU_GATHER 1  /* CPU threads gather into a contiguous pinned slot   */
+#define SP_XFER_GATHER_DMA 2  /* CPU gather, then copy-engine DMA of the slot       */
 
 int32_t sp_abi_version(void);
 
@@ -299,6 +307,14 @@ sp_status sp_set_stage_timing(sp_ctx *c, int32_t on);
  * transfer (k_pullfill), forward, surrogate, backward}, n_out[5] = steps
  * averaged (0: stage never timed).  Synchronises the device. */
 sp_status sp_stage_times(sp_ctx *c, double *out_ms, int32_t *n_out);
+
+/* Raw stage-event timestamps of the same last RING steps: out_ms[16][8] = ms
+ * of event k of ring residue r relative to the earliest plan-start event of
+ * the window (k: 0/1 plan start/end, 2 forward start, 3 forward end =
+ * surrogate start, 4 surrogate end, 5 backward end, 6/7 transfer start/end),
+ * NaN where not recorded.  Lets the caller take the union of each stream's
+ * busy intervals instead of summing spans.  Synchronises the device. */
+sp_status sp_stage_events(sp_ctx *c, double *out_ms);
 
 /* k_push per-CTA wall time while profiling is on (sp_set_profiling / SP_FLAG_PROFILE),
  * from %globaltimer at CTA entry and exit.  out[18T+2+4096] (caller-owned host array):

@@ -28,6 +28,7 @@ SP_FLAG_INDEX_DEVICE = 1 << 2
 SP_FLAG_PROFILE = 1 << 3
 KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush", "h2d", "d2h"]
 KERNEL_ONLY = ["plan", "transfer", "forward", "backward", "surrogate", "flush"]
+RING = 16  # batches in flight inside the library (sp_internal.cuh)
 
 
 class SpDesc(ctypes.Structure):
@@ -65,7 +66,11 @@ class SpStats(ctypes.Structure):
         ("host_rows_gathered", ctypes.c_int64), ("host_rows_scattered", ctypes.c_int64),
         ("wait_xfer_ms", ctypes.c_double), ("wait_list_ms", ctypes.c_double),
         ("graph_steps", ctypes.c_int64), ("graph_step_host_ms", ctypes.c_double),
+        ("transfer_mode", ctypes.c_int32), ("engine_threads", ctypes.c_int32),
     ]
+
+
+XFER_MODES = {0: "gpu_pull", 1: "cpu_gather", 2: "cpu_gather_dma"}
 
 
 def _load():
@@ -95,7 +100,7 @@ def _load():
                        ("sp_debug_slots", [P, ctypes.c_int32, i64p, i64p]),
                        ("sp_debug_storage", [P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, P]),
                        ("sp_debug_plan_profile", [P, P]), ("sp_stage_times", [P, P, P]),
-                       ("sp_set_stage_timing", [P, ctypes.c_int32])]:
+                       ("sp_set_stage_timing", [P, ctypes.c_int32]), ("sp_stage_events", [P, P])]:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = S
@@ -203,8 +208,17 @@ class ScratchPipe:
             past, future = window, max(window - 1, 0)
         self.P, self.F = past, future
         self._pooled = None
+        import collections
+        self._idx_refs = collections.deque(maxlen=RING + 2)
 
     # ------------------------------------------------------------------ core
+    def _keep(self, idx):
+        """Keep a pushed index tensor alive until its batch's Plan has run:
+        k_push reads it on the library's plan stream, up to RING (16) batches
+        after sp_plan returns, so a temporary must not be recycled by torch's
+        caching allocator before then (RING + 2 newest references are kept)."""
+        self._idx_refs.append(idx)
+
     def _check(self, st: int):
         if st != SP_OK:
             b = ctypes.c_int64(-1)
@@ -225,7 +239,7 @@ class ScratchPipe:
         if self.index_on_device != idx.is_cuda:
             raise ValueError("index device does not match index_on_device")
         idx = idx.contiguous()
-        self._last_idx = idx  # keep alive (device indices are read asynchronously)
+        self._keep(idx)  # device indices are read asynchronously on the plan stream
         self._check(lib.sp_plan(self._h, ctypes.c_void_p(idx.data_ptr())))
 
     def plan_device(self, idx):
@@ -233,7 +247,7 @@ class ScratchPipe:
         want = "int32" if self.index_dtype == "int32" else "int64"
         if not idx.is_cuda or str(idx.dtype) != f"torch.{want}" or not idx.is_contiguous():
             raise TypeError(f"device indices must be contiguous cuda {want}")
-        self._last_idx = idx
+        self._keep(idx)
         self._check(lib.sp_plan_device(self._h, ctypes.c_void_p(idx.data_ptr())))
 
     def copy_batch_stats(self, b: int, host_out):
@@ -316,8 +330,9 @@ class ScratchPipe:
         out["kernel_ms"] = dict(zip(KERNEL_KINDS, list(s.kernel_ms)))
         out["kernel_timed"] = dict(zip(KERNEL_KINDS, list(s.kernel_timed)))
         for k in ("host_gather_ms", "host_scatter_ms", "host_rows_gathered", "host_rows_scattered",
-                  "wait_xfer_ms", "wait_list_ms", "graph_steps", "graph_step_host_ms"):
+                  "wait_xfer_ms", "wait_list_ms", "graph_steps", "graph_step_host_ms", "engine_threads"):
             out[k] = getattr(s, k)
+        out["transfer_mode"] = XFER_MODES.get(s.transfer_mode, str(s.transfer_mode))
         out["status"] = st
         return out
 
@@ -356,6 +371,13 @@ class ScratchPipe:
         self._check(lib.sp_stage_times(self._h, ms.ctypes.data_as(ctypes.c_void_p), n.ctypes.data_as(ctypes.c_void_p)))
         names = ["plan", "transfer", "forward", "surrogate", "backward"]
         return {k: {"ms": float(ms[i]), "n": int(n[i])} for i, k in enumerate(names)}
+
+    def stage_events(self) -> np.ndarray:
+        """[16][8] ms of the stage events of the last 16 timed steps relative
+        to the earliest plan start (NaN: not recorded); sp_stage_events."""
+        out = np.zeros(RING * 8, np.float64)
+        self._check(lib.sp_stage_events(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out.reshape(RING, 8)
 
     def debug_plan_profile(self) -> dict:
         """k_push per-CTA wall time while profiling: mean us per launch of the

@@ -372,7 +372,7 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
             chunk_first[u] = EMPTY;
             const uint32_t h0 = hcarry + hx;
             for (uint32_t k = 0; k < nseg; k++)
-                hot[h0 + k] = make_uint4(u, lo + k * hs, min(hs, len - k * hs), k | (nseg << 16));
+                hot[h0 + k] = make_uint4(u, lo + k * hs, min(hs, len - k * hs) | (nseg << HOT_LEN_BITS), k);
             hcnt[h0] = 0u;
         }
         carry += tot;

@@ -17,7 +17,8 @@
 #include "sp_internal.cuh"
 
 #include <cstdlib>
-#include <unordered_map>
+#include <map>
+#include <mutex>
 
 namespace sp {
 
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
             const int t = t0 + tl;
             const uint32_t h = item - s_pref[tl];
             const uint4 hr = A.bb.hot_rec[(size_t)t * g.nh + h];
-            const uint32_t slot = hr.x, lo = hr.y, len = hr.z, k = hr.w & 0xFFFFu, nseg = hr.w >> 16;
+            const uint32_t slot = hr.x, lo = hr.y, len = hr.z & HOT_LEN_MASK, k = hr.w, nseg = hr.z >> HOT_LEN_BITS;
             const uint32_t *occ = A.bb.sorted_occ + (size_t)t * g.n + lo;
             const float4 *gb = grad + (size_t)t * g.N * D4 + lane;
             Acc4 acc[VPL];
@@ -386,10 +387,10 @@ __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
         const uint32_t nhot = A.bb.nhot[t];
         for (long long h = w0; h < nhot; h += ws) {
             const uint4 hr = A.bb.hot_rec[(size_t)t * g.nh + h];
-            if ((hr.w & 0xFFFFu) != 0) continue;  // segment 0 owns the whole row
-            const uint32_t nseg = hr.w >> 16;
+            if (hr.w != 0) continue;  // segment 0 owns the whole row
+            const uint32_t nseg = hr.z >> HOT_LEN_BITS;
             uint32_t len = 0;
-            for (uint32_t k = 0; k < nseg; k++) len += A.bb.hot_rec[(size_t)t * g.nh + h + k].z;
+            for (uint32_t k = 0; k < nseg; k++) len += A.bb.hot_rec[(size_t)t * g.nh + h + k].z & HOT_LEN_MASK;
             const uint32_t *occ = A.bb.sorted_occ + (size_t)t * g.n + hr.y;
             for (int col = lane; col < D4; col += 32) {
                 Acc4 a{0.0, 0.0, 0.0, 0.0};
@@ -442,25 +443,45 @@ __global__ void __launch_bounds__(256) k_surrogate(const float4 *p, float4 *g, l
 }
 
 // --------------------------------------------------------------- launchers
-static int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+// Per-device caches: a process may hold contexts on several GPUs, and kernel
+// attributes / occupancy are per device.
+static std::mutex g_dev_mu;
+
+int device_sms() {
+    static int sms[256] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (dev < 0 || dev >= 256) return 148;
+    if (!sms[dev]) {
+        int n = 0;
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+        sms[dev] = n > 0 ? n : 148;
     }
-    return n;
+    return sms[dev];
 }
 
 // resident CTAs of a kernel on the whole GPU (a persistent grid never waits
-// for a second wave of a latency-bound kernel)
+// for a second wave of a latency-bound kernel); the carveout hint is applied
+// on first use on each device
 template <typename K>
 static int resident_ctas(K kernel, int threads) {
+    static std::map<std::pair<const void *, int>, int> caps;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        auto it = caps.find({reinterpret_cast<const void *>(kernel), dev});
+        if (it != caps.end()) return it->second;
+    }
+    apply_carveout(kernel);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    return per_sm * num_sms();
+    const int cap = per_sm * device_sms();
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    caps[{reinterpret_cast<const void *>(kernel), dev}] = cap;
+    return cap;
 }
 
 template <typename K, typename... Args>
@@ -484,12 +505,7 @@ static void launch_maybe_pdl(K kernel, int grid, int block, size_t smem, cudaStr
 
 template <int G, int VPL, typename K>
 static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStream_t s, bool pdl = false) {
-    static std::unordered_map<const void *, int> caps;  // per kernel (not per signature)
-    int &cap = caps[reinterpret_cast<const void *>(kernel)];
-    if (!cap) {
-        apply_carveout(kernel);
-        cap = resident_ctas(kernel, 256);
-    }
+    const int cap = resident_ctas(kernel, 256);  // per kernel instance and device
     long long blocks = (groups + (256 / G) - 1) / (256 / G);
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
@@ -533,7 +549,8 @@ int backward_hot_segment(int D) {
     // SP_HOT_SEG overrides (A/B; >= CH so a hot row has >= 2 segments' worth).
     // Measured on Kaggle: 2 and 4 rounds per segment were 16% / 51% slower.
     if (const char *e = getenv("SP_HOT_SEG")) hs = atoi(e) >= CH ? atoi(e) : hs;
-    return hs;
+    // (segment lengths are packed in HOT_LEN_BITS of the hot record)
+    return hs < CH ? CH : (hs > HOT_SEG_MAX ? HOT_SEG_MAX : hs);
 }
 
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
@@ -547,16 +564,17 @@ cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, 
                              float delta, cudaStream_t s) {
     long long n4 = count / 4;
     long long blocks = (n4 + 256 * SU - 1) / (256 * SU);
-    const long long cap = (long long)num_sms() * 8;
+    const long long cap = (long long)device_sms() * 8;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
-    static bool once = false;
-    if (!once) {
-        apply_carveout(k_surrogate);
-        once = true;
-    }
     launch_maybe_pdl(k_surrogate, grid, 256, 0, s, true, reinterpret_cast<const float4 *>(pooled),
                      reinterpret_cast<float4 *>(grad), n4, gamma, delta);
+    return cudaGetLastError();
+}
+
+// attributes of the Train-stage kernels on the current device (sp_create)
+cudaError_t configure_train_kernels() {
+    apply_carveout(k_surrogate);
     return cudaGetLastError();
 }
 

@@ -235,33 +235,27 @@ __global__ void __launch_bounds__(256) k_flush(FlushArgs A) {
     }
 }
 
-static int sm_count() {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 148;
-}
-
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s) {
     const int nb = pullfill_tma_items(a.g.D);
     const size_t smem = (size_t)nb * 2 * a.g.D * 4 * XS;
-    static bool once = false;
-    if (!once) {
-        cudaFuncSetAttribute(k_pullfill, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
-        apply_carveout(k_pullfill);
-        once = true;
-    }
     k_pullfill<<<ctas > 0 ? ctas : 16, 32, smem, s>>>(a, nb);
     return cudaGetLastError();
 }
 
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s) {
     long long blocks = ((long long)a.S_total + 7) / 8;
-    long long cap = (long long)sm_count() * 8;
+    long long cap = (long long)device_sms() * 8;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
     k_flush<<<grid, 256, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+// attributes of the transfer kernel on the current device (sp_create; kernel
+// attributes are per device, so every context sets them on its own GPU)
+cudaError_t configure_xfer_kernels() {
+    apply_carveout(k_pullfill);
+    return cudaFuncSetAttribute(k_pullfill, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
 }
 
 }  // namespace sp

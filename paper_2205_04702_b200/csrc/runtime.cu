@@ -27,6 +27,7 @@
 #include <sys/mman.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -868,8 +869,13 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->g.n = c->n;
     c->g.n1 = c->n + 1;
     c->g.nc = c->n + c->n / CH + 1;
-    c->g.nh = c->n / CH + 1;
     c->g.hs = backward_hot_segment(c->D);
+    // hot-row segment records: rows with > CH occurrences, ceil(len/hs) each
+    c->g.nh = c->n / c->g.hs + c->n / (CH + 1) + 1;
+    if ((long long)c->n / c->g.hs + 1 > HOT_NSEG_MAX) {  // segment count must fit its packing
+        delete c;
+        return SP_ERR_INVALID_ARG;
+    }
     c->rows.resize(c->T);
     c->slots.resize(c->T);
     c->host.resize(c->T);
@@ -981,6 +987,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     if (const char *e = getenv("SP_CARVEOUT")) g_carveout = atoi(e);
     if (const char *e = getenv("SP_PDL")) g_pdl = atoi(e) != 0;
     CKC(configure_push_kernel());
+    CKC(configure_xfer_kernels());
+    CKC(configure_train_kernels());
 
     // device allocations
     const size_t Tn = (size_t)c->T * c->n;
@@ -1539,6 +1547,8 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->wait_list_ms = c->wait_list_ns * 1e-6;
     o->graph_steps = c->graph_steps;
     o->graph_step_host_ms = c->graph_step_ns * 1e-6;
+    o->transfer_mode = c->cpu_gather ? (c->gather_dma ? SP_XFER_GATHER_DMA : SP_XFER_CPU_GATHER) : SP_XFER_GPU_PULL;
+    o->engine_threads = 1 + c->host_threads + (c->cpu_gather ? 1 + c->host_threads : 0);
     if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);
         cudaStreamSynchronize(c->xfer_s2);
@@ -1659,6 +1669,30 @@ sp_status sp_stage_times(sp_ctx *c, double *out_ms, int32_t *n_out) {
         out_ms[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
         n_out[k] = cnt[k];
     }
+    return SP_OK;
+}
+
+sp_status sp_stage_events(sp_ctx *c, double *out_ms) {
+    if (!c || !out_ms) return SP_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    for (int i = 0; i < RING * 8; i++) out_ms[i] = NAN;
+    // reference: the plan-start event that comes first among the timed residues
+    int ref = -1;
+    for (int r = 0; r < RING; r++) {
+        if (!c->sev_used[r][0]) continue;
+        float ms = 0.f;
+        if (ref < 0 || (cudaEventElapsedTime(&ms, c->sev[ref][0], c->sev[r][0]) == cudaSuccess && ms < 0.f)) ref = r;
+        (void)cudaGetLastError();
+    }
+    if (ref < 0) return SP_OK;
+    for (int r = 0; r < RING; r++)
+        for (int k = 0; k < 8; k++) {
+            if (!c->sev_used[r][k < 6 ? 0 : 1]) continue;
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, c->sev[ref][0], c->sev[r][k]) == cudaSuccess) out_ms[r * 8 + k] = ms;
+            (void)cudaGetLastError();
+        }
     return SP_OK;
 }
 

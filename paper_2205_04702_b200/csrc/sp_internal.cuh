@@ -26,6 +26,12 @@ constexpr uint32_t EMPTY = 0xFFFFFFFFu;     // empty Hit-Map entry / vacant slot
 constexpr int32_t VACANT = INT32_MIN;       // last_use of a never-used slot
 constexpr int32_t NEVER = INT32_MIN;        // next_need of a slot with no future use
 constexpr int CH = 16;                      // occurrences per backward chunk
+// hot-row segment record packing: occurrences of the segment (<= hs <= HOT_SEG_MAX)
+// in the low HOT_LEN_BITS of .z, the row's segment count above them (< 2^22)
+constexpr int HOT_LEN_BITS = 10;
+constexpr uint32_t HOT_LEN_MASK = (1u << HOT_LEN_BITS) - 1u;
+constexpr int HOT_SEG_MAX = 512;
+constexpr long long HOT_NSEG_MAX = (1ll << (32 - HOT_LEN_BITS)) - 1;
 #ifndef SP_PUSH_THREADS
 #define SP_PUSH_THREADS 1024
 #endif
@@ -47,11 +53,12 @@ __host__ __device__ inline unsigned long long err_key(long long b, int t, unsign
 //                     fill_*)
 //   n1 = n + 1       (seg_off)
 //   nc = n + n/CH + 1 (chunk_rec)
-//   nh = n/CH + 1     (hot_rec)
+//   nh = n/hs + n/(CH+1) + 1 (hot_rec: a hot row has > CH occurrences and
+//                     ceil(len/hs) <= len/hs + 1 segments)
 // chunk_rec[c]: one unique row with <= CH occurrences, their bag indices inline
 // (ascending occurrence order), so the backward pass needs one record load
 // before the gradient rows.
-// hot_rec[h] = {u -> slot, first sorted occurrence, occurrences, k | nseg<<16}:
+// hot_rec[h] = {u -> slot, first sorted occurrence, occurrences | nseg << 10, k}:
 // segment k of nseg of a row with more than CH occurrences (Zipf head), at most
 // hs occurrences each.  One CTA of k_bwd folds a segment from sorted_occ; a
 // row's segments meet through fp64 partials and hot_cnt (last arriver folds).
@@ -263,5 +270,8 @@ inline void apply_carveout(K kernel) {
     if (g_carveout >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
 }
 cudaError_t configure_push_kernel();
+cudaError_t configure_xfer_kernels();
+cudaError_t configure_train_kernels();
+int device_sms();  // SM count of the current device (cached per device)
 
 }  // namespace sp

@@ -51,20 +51,26 @@ def compare_tables(got: np.ndarray, want: np.ndarray, init: np.ndarray):
 def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init_seed=4702,
                gde=(0.5, 0.01, 0.01), index_dtype="int64", index_on_device=False, log_factor=0,
                check_plans=True, check_slots=True, check_pooled=True, trace=None,
-               register_host=False, profile=False, sample_rows=None, host_alloc=False):
+               register_host=False, profile=False, sample_rows=None, host_alloc=False,
+               tables=None, policy_kw=None):
+    """tables: pre-allocated host tables (HostTable or pinned tensors), already
+    holding init(init_seed) values; policy_kw: extra ScratchPipe / Policy
+    arguments of a replacement-policy variant (policy, policy_seed)."""
     g, d, e = gde
     if trace is None:
         trace = sample_trace(rows, N, L, alpha, nb, trace_seed)
     trace_np = trace.numpy()
-    tables = pinned_tables(rows, D, init_seed, pin=not register_host, host_alloc=host_alloc)
-    views = [t.tensor if host_alloc else t for t in tables]
+    if tables is None:
+        tables = pinned_tables(rows, D, init_seed, pin=not register_host, host_alloc=host_alloc)
+    views = [getattr(t, "tensor", t) for t in tables]
     feed = trace.to(torch.int32 if index_dtype == "int32" else torch.int64)
     if index_on_device:
         feed = feed.cuda()
+    pkw = dict(policy_kw or {})
     sp = ScratchPipe(rows, tables, D, slots, N, L, past=P, future=F, index_dtype=index_dtype,
                      index_on_device=index_on_device, log_factor=log_factor,
-                     register_host=register_host, profile=profile)
-    pol = Policy(rows, slots, P, F) if (check_plans or check_slots) else None
+                     register_host=register_host, profile=profile, **pkw)
+    pol = Policy(rows, slots, P, F, **pkw) if (check_plans or check_slots) else None
     orc = UncachedTrainer(rows, D, N, L, init_seed)
     report = {"plans": 0, "evictions": 0, "pooled": 0}
 

@@ -255,10 +255,12 @@ def test_run_steps_pinned_host_trace_matches_oracle():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("D", [64, 128, 256])
+@pytest.mark.parametrize("D", [64, 128, 256, 512, 1024])
 def test_hot_row_segments_last_arriver_fold(D):
-    """Rows with more occurrences than one k_bwd segment (hs = 128 / 64 / 32
-    for D = 64 / 128 / 256): several CTAs fold segments, write fp64 partials,
+    """Rows with more occurrences than one k_bwd segment (hs = 128 / 64 / 32 /
+    16 / 16 for D = 64 / 128 / 256 / 512 / 1024; at hs = 16 a row with 17-32
+    occurrences already has 2 segments, the worst case of the hot-record
+    sizing): several CTAs fold segments, write fp64 partials,
     and the last to arrive folds them in segment order (plus plain chunk
     records from the large table in the same launch)."""
     rows, N, L, nb = [3, 5, 4000], 512, 4, 8

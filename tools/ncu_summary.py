@@ -69,7 +69,7 @@ def full_raw(path):
 
 def main():
     src, tag = sys.argv[1], sys.argv[2]
-    lines = [f"# {tag}: ncu evidence from {src} (tools/round_measure.sh; bench.py kaggle, steady state)"]
+    lines = [f"# {tag}: ncu evidence from {src} (bench.py, steady state)"]
     ll = launch_list(os.path.join(src, "launches.csv"))
     tot = sum(sum(v) for v in ll.values()) or 1.0
     lines.append("# launch list: ncu --metrics gpu__time_duration.sum --clock-control none "
@@ -95,11 +95,14 @@ def main():
         traffic[st] += statistics.mean(v)
     traffic = {k: int(v) for k, v in traffic.items()}
     traffic["source"] = f"{src}/full.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum, mean per launch)"
-    traffic["config"] = sys.argv[3] if len(sys.argv) > 3 else "kaggle"
-    lines.append("# DRAM bytes per launch by stage: " + json.dumps(traffic))
+    cfg = sys.argv[3] if len(sys.argv) > 3 else "terabyte"
+    lines.append(f"# DRAM bytes per launch by stage ({cfg}): " + json.dumps(traffic))
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w").write("\n".join(lines) + "\n")
-    json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    allt = json.load(open(tp)) if os.path.exists(tp) else {}
+    allt[cfg] = traffic  # bench.py reads the entry of the config it runs
+    json.dump(allt, open(tp, "w"), indent=1)
     print("\n".join(lines))
 
 
