@@ -75,6 +75,11 @@ def lib():
         L.orc_policy_resident.argtypes = [P, ctypes.c_int32, i64p, ctypes.c_int64]
         L.orc_policy_slots.argtypes = [P, ctypes.c_int32, i64p, i64p]
         L.orc_policy_set_full_sort.argtypes = [P, ctypes.c_int32]
+        L.orc_policy_set_kind.argtypes = [P, ctypes.c_int32, ctypes.c_uint64]
+        L.orc_policy_set_padding.argtypes = [P, ctypes.c_int32]
+        L.orc_policy_pin.restype = ctypes.c_int32
+        L.orc_policy_pin.argtypes = [P, ctypes.c_int32, i64p, ctypes.c_int64]
+        L.orc_policy_freq.argtypes = [P, ctypes.c_int32, i64p]
         L.orc_fmaf_array.argtypes = [ctypes.c_int64, f32p, f32p, f32p, f32p]
         _lib = L
     return _lib
@@ -184,11 +189,21 @@ class PlanRecord:
         return e[e >= 0]
 
 
+POLICIES = {"lru": 0, "random": 1, "lfu": 2}
+LFU_FMAX = 8
+
+
 class Policy:
-    """Part B: reference scratchpad policy (IDs only)."""
+    """Part B: reference scratchpad policy (IDs only).
+
+    policy: "lru" (default, P:1273), "random" or "lfu" (P:1270-1278; readings
+    R23-R25); policy_seed: the RANDOM draw seed; allow_padding: -1 entries are
+    not lookups (ragged bags, R27); pinned: per table, rows held in the
+    table's last slots for the whole run (static partition, R26)."""
 
     def __init__(self, rows: Sequence[int], slots: Sequence[int], past: int, future: int,
-                 full_sort: bool = False):
+                 full_sort: bool = False, policy: str = "lru", policy_seed: int = 0,
+                 allow_padding: bool = False, pinned=None):
         self.rows = np.asarray(rows, dtype=np.int64)
         self.slots = np.asarray(slots, dtype=np.int64)
         self.T = len(rows)
@@ -199,6 +214,16 @@ class Policy:
             raise ValueError("bad policy config")
         if full_sort:
             lib().orc_policy_set_full_sort(self._h, 1)
+        lib().orc_policy_set_kind(self._h, POLICIES[policy], policy_seed & ((1 << 64) - 1))
+        if allow_padding:
+            lib().orc_policy_set_padding(self._h, 1)
+        if pinned is not None:
+            for t, ids in enumerate(pinned):
+                if ids is None or len(ids) == 0:
+                    continue
+                a = np.ascontiguousarray(ids, dtype=np.int64)
+                if lib().orc_policy_pin(self._h, t, _p(a, ctypes.c_int64), len(a)) != ORC_OK:
+                    raise ValueError(f"bad pinned rows for table {t}")
 
     def close(self):
         if self._h:
@@ -231,6 +256,11 @@ class Policy:
         n = lib().orc_policy_resident(self._h, t, None, 0)
         out = np.empty(n, np.int64)
         lib().orc_policy_resident(self._h, t, _p(out, ctypes.c_int64), n)
+        return out
+
+    def freq(self, t: int) -> np.ndarray:
+        out = np.empty(int(self.slots[t]), np.int64)
+        lib().orc_policy_freq(self._h, t, _p(out, ctypes.c_int64))
         return out
 
     def slot_state(self, t: int):

@@ -19,7 +19,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-int32_t orc_version(void) { return 3; }
+int32_t orc_version(void) { return 4; }
 
 /* ------------------------------------------------------------------------ */
 /* init generator: identical formula to workload/gen.py                      */
@@ -240,18 +240,42 @@ int64_t orc_train_touched(const orc_train *o, int32_t t, int64_t *out, int64_t c
 /* ------------------------------------------------------------------------ */
 #define ORC_VACANT INT64_MIN
 
+/* Replacement-policy variants ("changing the GPU scratchpad's
+ * replacement policy from our default LRU ... to a random eviction or LFU";
+ * readings R23-R25 in DESIGN.md).  In every variant the CANDIDATES are the
+ * same (past window, future window, not pinned); only their order differs:
+ *   LRU     ascending (last_use, resident ID, slot)                  (R8)
+ *   LFU     ascending (freq, last_use, resident ID, slot); freq = 1 at fill,
+ *           +1 per Plan that hits the slot, saturating at ORC_LFU_FMAX (R24)
+ *   RANDOM  vacant candidates first (ascending slot, R9), then the draw
+ *           sequence s_i = H(seed, t, b, i) mod O, i = 0, 1, ..., where O is
+ *           the number of occupied dynamic slots at the start of Plan(b)
+ *           (occupied slots are [0, O): vacant ones are filled lowest
+ *           first), keeping each occupied candidate the first time it is
+ *           drawn: a uniformly random ordering of the occupied candidates
+ *           (R23).  H = splitmix64 chain sm(sm(sm(sm(seed ^ RAND) ^ t) ^ b) ^ i).
+ * Pinned slots (static top-N partition, reading R26): the
+ * last `count` slots of a table hold rows loaded before the first Plan and
+ * are never candidates. */
 typedef struct {
     int64_t rows, S;
+    int64_t S_dyn;         /* slots [0, S_dyn) are dynamic, [S_dyn, S) pinned */
     int64_t *slot_of_row;  /* Hit-Map: row -> slot or -1 */
     int64_t *resident;     /* slot -> row or -1 */
     int64_t *last_use;     /* slot -> stamp (ORC_VACANT if never used) */
+    int64_t *freq;         /* slot -> LFU use count (0 vacant) */
     uint8_t *future;       /* scratch: slot in future set */
-    int64_t *cand;         /* scratch: candidate (last_use, resident, slot) triples */
+    uint8_t *taken;        /* scratch: slot drawn this Plan (RANDOM) */
+    int64_t *cand;         /* scratch: candidate (key, last_use, resident, slot) tuples */
 } pol_table;
 
 struct orc_policy {
     int32_t T, P, F;
     int32_t full_sort;     /* 1: always sort every candidate (cross-check mode) */
+    int32_t kind;          /* ORC_POL_* */
+    uint64_t seed;         /* RANDOM draw seed */
+    int32_t allow_pad;     /* id == -1 is "no lookup" (ragged bags, R27) */
+    int32_t planned;       /* a Plan has run (pinning no longer allowed) */
     pol_table *tab;
     int64_t *ids;          /* scratch for sorting a batch */
 };
@@ -267,10 +291,13 @@ orc_policy *orc_policy_create(int32_t T, const int64_t *rows, const int64_t *slo
         pt->rows = rows[t]; pt->S = slots[t];
         pt->slot_of_row = (int64_t *)malloc((size_t)rows[t] * sizeof(int64_t));
         for (int64_t r = 0; r < rows[t]; r++) pt->slot_of_row[r] = -1;
+        pt->S_dyn = slots[t];
         pt->resident = (int64_t *)malloc((size_t)slots[t] * sizeof(int64_t));
         pt->last_use = (int64_t *)malloc((size_t)slots[t] * sizeof(int64_t));
+        pt->freq = (int64_t *)calloc((size_t)slots[t], sizeof(int64_t));
         pt->future = (uint8_t *)calloc((size_t)slots[t], 1);
-        pt->cand = (int64_t *)malloc((size_t)slots[t] * 3 * sizeof(int64_t));
+        pt->taken = (uint8_t *)calloc((size_t)slots[t], 1);
+        pt->cand = (int64_t *)malloc((size_t)slots[t] * 4 * sizeof(int64_t));
         for (int64_t s = 0; s < slots[t]; s++) { pt->resident[s] = -1; pt->last_use[s] = ORC_VACANT; }
     }
     return p;
@@ -280,8 +307,8 @@ void orc_policy_destroy(orc_policy *p) {
     if (!p) return;
     for (int32_t t = 0; t < p->T; t++) {
         pol_table *pt = &p->tab[t];
-        free(pt->slot_of_row); free(pt->resident); free(pt->last_use);
-        free(pt->future); free(pt->cand);
+        free(pt->slot_of_row); free(pt->resident); free(pt->last_use); free(pt->freq);
+        free(pt->future); free(pt->taken); free(pt->cand);
     }
     free(p->tab); free(p->ids); free(p);
 }
@@ -291,21 +318,22 @@ static int cmp_i64(const void *a, const void *b) {
     return x < y ? -1 : (x > y ? 1 : 0);
 }
 
+#define CW 4  /* candidate tuple: (policy key, last_use, resident ID, slot) */
 static int cmp_cand(const void *a, const void *b) {
     const int64_t *x = (const int64_t *)a, *y = (const int64_t *)b;
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < CW; i++)
         if (x[i] != y[i]) return x[i] < y[i] ? -1 : 1;
     return 0;
 }
 
-/* move the k smallest triples of c[0..n) to c[0..k), ascending (bounded max-heap) */
+/* move the k smallest tuples of c[0..n) to c[0..k), ascending (bounded max-heap) */
 static void heap_sift(int64_t *h, int64_t k, int64_t i) {
     for (;;) {
         int64_t l = 2 * i + 1, r = l + 1, m = i;
-        if (l < k && cmp_cand(&h[3 * l], &h[3 * m]) > 0) m = l;
-        if (r < k && cmp_cand(&h[3 * r], &h[3 * m]) > 0) m = r;
+        if (l < k && cmp_cand(&h[CW * l], &h[CW * m]) > 0) m = l;
+        if (r < k && cmp_cand(&h[CW * r], &h[CW * m]) > 0) m = r;
         if (m == i) return;
-        for (int j = 0; j < 3; j++) { int64_t x = h[3 * i + j]; h[3 * i + j] = h[3 * m + j]; h[3 * m + j] = x; }
+        for (int j = 0; j < CW; j++) { int64_t x = h[CW * i + j]; h[CW * i + j] = h[CW * m + j]; h[CW * m + j] = x; }
         i = m;
     }
 }
@@ -313,11 +341,38 @@ static void heap_sift(int64_t *h, int64_t k, int64_t i) {
 static void select_smallest(int64_t *c, int64_t n, int64_t k) {
     for (int64_t i = k / 2 - 1; i >= 0; i--) heap_sift(c, k, i);
     for (int64_t i = k; i < n; i++)
-        if (cmp_cand(&c[3 * i], &c[0]) < 0) {
-            for (int j = 0; j < 3; j++) c[j] = c[3 * i + j];
+        if (cmp_cand(&c[CW * i], &c[0]) < 0) {
+            for (int j = 0; j < CW; j++) c[j] = c[CW * i + j];
             heap_sift(c, k, 0);
         }
-    qsort(c, (size_t)k, 3 * sizeof(int64_t), cmp_cand);
+    qsort(c, (size_t)k, CW * sizeof(int64_t), cmp_cand);
+}
+
+/* RANDOM draw H(seed, t, b, i) (reading R23; its own copy of splitmix64) */
+static uint64_t rand_draw(uint64_t seed, int32_t t, int64_t b, int64_t i) {
+    uint64_t h = splitmix64(seed ^ 0x52414E44ull);  /* "RAND" */
+    h = splitmix64(h ^ (uint64_t)(int64_t)t);
+    h = splitmix64(h ^ (uint64_t)b);
+    return splitmix64(h ^ (uint64_t)i);
+}
+
+void orc_policy_set_kind(orc_policy *p, int32_t kind, uint64_t seed) { p->kind = kind; p->seed = seed; }
+void orc_policy_set_padding(orc_policy *p, int32_t allow) { p->allow_pad = allow; }
+
+/* Static partition (R26): rows ids[0..count) (distinct, in range) occupy the
+ * table's last `count` slots, in the given order, before the first Plan. */
+int32_t orc_policy_pin(orc_policy *p, int32_t t, const int64_t *ids, int64_t count) {
+    pol_table *pt = &p->tab[t];
+    if (p->planned || count < 0 || count > pt->S || pt->S_dyn != pt->S) return ORC_ERR_ARG;
+    int64_t base = pt->S - count;
+    for (int64_t k = 0; k < count; k++) {
+        int64_t id = ids[k];
+        if (id < 0 || id >= pt->rows || pt->slot_of_row[id] >= 0) return ORC_ERR_ARG;
+        pt->slot_of_row[id] = base + k;
+        pt->resident[base + k] = id;
+    }
+    pt->S_dyn = base;
+    return ORC_OK;
 }
 
 void orc_policy_set_full_sort(orc_policy *p, int32_t on) { p->full_sort = on; }
@@ -330,17 +385,20 @@ int32_t orc_policy_plan(orc_policy *p, const int64_t *trace, int64_t nb, int32_t
     const int64_t T = p->T;
     if (b < 0 || b >= nb) return ORC_ERR_ARG;
     if (!p->ids) p->ids = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    p->planned = 1;
     for (int32_t t = 0; t < T; t++) {
         pol_table *pt = &p->tab[t];
         const int64_t *bt = trace + ((int64_t)b * T + t) * n;
-        /* 1. U_b */
+        /* 1. U_b (with padding, -1 entries are not lookups) */
+        int64_t nr = 0;
         for (int64_t i = 0; i < n; i++) {
+            if (p->allow_pad && bt[i] == -1) continue;
             if (bt[i] < 0 || bt[i] >= pt->rows) { if (err_table) *err_table = t; return ORC_ERR_INDEX; }
-            p->ids[i] = bt[i];
+            p->ids[nr++] = bt[i];
         }
-        qsort(p->ids, (size_t)n, sizeof(int64_t), cmp_i64);
+        qsort(p->ids, (size_t)nr, sizeof(int64_t), cmp_i64);
         int64_t U = 0;
-        for (int64_t i = 0; i < n; i++)
+        for (int64_t i = 0; i < nr; i++)
             if (i == 0 || p->ids[i] != p->ids[i - 1]) p->ids[U++] = p->ids[i];
         int64_t *ou = uniq + (int64_t)t * n, *os = slot + (int64_t)t * n;
         int64_t *oh = hit + (int64_t)t * n, *oe = evicted + (int64_t)t * n;
@@ -350,7 +408,10 @@ int32_t orc_policy_plan(orc_policy *p, const int64_t *trace, int64_t nb, int32_t
             int64_t id = p->ids[k];
             ou[k] = id; oe[k] = -1;
             int64_t s = pt->slot_of_row[id];
-            if (s >= 0) { oh[k] = 1; os[k] = s; pt->last_use[s] = b; nh++; }
+            if (s >= 0) {
+                oh[k] = 1; os[k] = s; pt->last_use[s] = b; nh++;
+                if (pt->freq[s] < ORC_LFU_FMAX) pt->freq[s]++;
+            }
             else { oh[k] = 0; os[k] = -1; nm++; }
         }
         /* 4. future set */
@@ -358,36 +419,65 @@ int32_t orc_policy_plan(orc_policy *p, const int64_t *trace, int64_t nb, int32_t
         for (int64_t f = 1; f <= p->F && b + f < nb; f++) {
             const int64_t *ft = trace + ((int64_t)(b + f) * T + t) * n;
             for (int64_t i = 0; i < n; i++) {
-                if (ft[i] < 0 || ft[i] >= pt->rows) continue; /* reported when planned */
+                if (ft[i] < 0 || ft[i] >= pt->rows) continue; /* padding, or reported when planned */
                 int64_t s = pt->slot_of_row[ft[i]];
                 if (s >= 0) pt->future[s] = 1;
             }
         }
-        /* 5. candidates in LRU order */
-        int64_t nc = 0;
-        for (int64_t s = 0; s < pt->S; s++) {
+        /* 5. candidates (past window, future window, dynamic slots only), each
+         * with its policy key: LRU 0, LFU freq, RANDOM 0 for vacant / 1 occupied */
+        int64_t nc = 0, nvac = 0, occ = 0;
+        for (int64_t s = 0; s < pt->S_dyn; s++) {
             int64_t lu = pt->last_use[s];
+            if (pt->resident[s] >= 0) occ++;
             if (lu != ORC_VACANT && lu > b - p->P - 1) continue;
             if (pt->future[s]) continue;
-            pt->cand[3 * nc] = lu; pt->cand[3 * nc + 1] = pt->resident[s]; pt->cand[3 * nc + 2] = s;
+            int64_t key = 0;
+            if (p->kind == ORC_POL_LFU) key = pt->freq[s];
+            else if (p->kind == ORC_POL_RANDOM) key = pt->resident[s] >= 0 ? 1 : 0;
+            int64_t *c = &pt->cand[CW * nc];
+            c[0] = key; c[1] = lu; c[2] = pt->resident[s]; c[3] = s;
             nc++;
+            if (pt->resident[s] < 0) nvac++;
         }
         if (nc < nm) { if (err_table) *err_table = t; return ORC_ERR_CAPACITY; }
-        /* the first nm candidates in (last_use, resident, slot) order: the order is
-         * total, so selecting the nm smallest and sorting them equals sorting all */
-        if (!p->full_sort && nm > 0 && nm * 16 < nc) select_smallest(pt->cand, nc, nm);
-        else qsort(pt->cand, (size_t)nc, 3 * sizeof(int64_t), cmp_cand);
+        int64_t *vic = pt->cand;  /* victims in order: slot of the k-th = vic[CW*k + 3] */
+        if (p->kind == ORC_POL_RANDOM) {
+            /* occupied slots are [0, occ): vacant slots are filled lowest first */
+            for (int64_t s = 0; s < pt->S_dyn; s++)
+                if ((s < occ) != (pt->resident[s] >= 0)) return ORC_ERR_ARG;
+            /* vacant candidates first (ascending slot), then draw order */
+            qsort(pt->cand, (size_t)nc, CW * sizeof(int64_t), cmp_cand);  /* vacant ones lead */
+            int64_t got = nvac < nm ? nvac : nm;
+            for (int64_t i = 0; got < nm; i++) {
+                int64_t s = (int64_t)(rand_draw(p->seed, t, b, i) % (uint64_t)occ);
+                int64_t lu = pt->last_use[s];
+                if (lu != ORC_VACANT && lu > b - p->P - 1) continue;
+                if (pt->future[s] || pt->taken[s]) continue;
+                pt->taken[s] = 1;
+                vic[CW * got + 3] = s;  /* (only the slot column is read below) */
+                got++;
+            }
+            for (int64_t k = nvac < nm ? nvac : nm; k < nm; k++) pt->taken[vic[CW * k + 3]] = 0;
+        } else {
+            /* the first nm candidates in (key, last_use, resident, slot) order: the
+             * order is total, so selecting the nm smallest and sorting them equals
+             * sorting all */
+            if (!p->full_sort && nm > 0 && nm * 16 < nc) select_smallest(pt->cand, nc, nm);
+            else qsort(pt->cand, (size_t)nc, CW * sizeof(int64_t), cmp_cand);
+        }
         /* 6. pair k-th miss with k-th victim */
         int64_t ne = 0, v = 0;
         for (int64_t k = 0; k < U; k++) {
             if (oh[k]) continue;
-            int64_t s = pt->cand[3 * v + 2];
+            int64_t s = vic[CW * v + 3];
             v++;
             int64_t old = pt->resident[s];
             if (old >= 0) { pt->slot_of_row[old] = -1; oe[k] = old; ne++; }
             pt->slot_of_row[ou[k]] = s;
             pt->resident[s] = ou[k];
             pt->last_use[s] = b;
+            pt->freq[s] = 1;
             os[k] = s;
         }
         counts[4 * t + 0] = U; counts[4 * t + 1] = nh;
@@ -410,6 +500,11 @@ void orc_policy_slots(const orc_policy *p, int32_t t, int64_t *resident, int64_t
         resident[s] = pt->resident[s];
         last_use[s] = pt->last_use[s];
     }
+}
+
+void orc_policy_freq(const orc_policy *p, int32_t t, int64_t *freq) {
+    const pol_table *pt = &p->tab[t];
+    for (int64_t s = 0; s < pt->S; s++) freq[s] = pt->freq[s];
 }
 
 /* element-wise fp32 fmaf (C99 fmaf: one rounding) for the Python-side Part C */

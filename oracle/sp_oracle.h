@@ -73,6 +73,20 @@ int32_t orc_policy_plan(orc_policy *p, const int64_t *trace, int64_t nb, int32_t
 /* 1 = sort every candidate each Plan (cross-check of the default partial
  * selection of the |misses| smallest, which yields the same victims) */
 void orc_policy_set_full_sort(orc_policy *p, int32_t on);
+/* Replacement-policy variants (R23-R25): the
+ * candidates are the same in every variant, only their order differs. */
+#define ORC_POL_LRU 0
+#define ORC_POL_RANDOM 1
+#define ORC_POL_LFU 2
+#define ORC_LFU_FMAX 8   /* LFU use counts saturate here (R24) */
+void orc_policy_set_kind(orc_policy *p, int32_t kind, uint64_t seed);
+/* id == -1 is "no lookup" (ragged bags as -1 padding, R27) */
+void orc_policy_set_padding(orc_policy *p, int32_t allow);
+/* static partition (R26): ids occupy the last `count` slots of table t,
+ * never evicted; only before the first Plan */
+int32_t orc_policy_pin(orc_policy *p, int32_t t, const int64_t *ids, int64_t count);
+/* LFU use count per slot of table t */
+void orc_policy_freq(const orc_policy *p, int32_t t, int64_t *freq);
 /* sorted resident IDs of table t; returns count */
 int64_t orc_policy_resident(const orc_policy *p, int32_t t, int64_t *out, int64_t cap);
 /* slot-level view: resident id (-1 vacant) and last_use stamp per slot */
