@@ -76,7 +76,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 2
+#define SP_ABI_VERSION 3
 
 typedef struct sp_ctx sp_ctx;
 
@@ -98,6 +98,9 @@ typedef enum {
 #define SP_FLAG_INDEX_DEVICE  (1u << 2) /* batch indices are a device pointer   */
 #define SP_FLAG_PROFILE       (1u << 3) /* CUDA events around every kernel ->   */
                                         /* per-kernel times in sp_get_stats     */
+#define SP_FLAG_PADDING       (1u << 4) /* ragged bags: an ID of -1 is "no      */
+                                        /* lookup" (a bag with none pools to    */
+                                        /* zeros; reading R27); sp_plan_csr     */
 
 /* sp_create(tables, dim, slots, window) of the problem statement. */
 typedef struct {
@@ -121,9 +124,24 @@ typedef struct {
                                  /* log_factor * slots[t] + 4*N*L (0 -> 8)          */
     int32_t host_threads;        /* CPU helper threads that, with the scatter       */
                                  /* thread, copy staged victims into their host     */
-                                 /* rows (0 -> 6)                                   */
-    int32_t reserved;            /* must be 0                                       */
+                                 /* rows (0 -> 3)                                   */
+    int32_t policy;              /* replacement policy among the window-safe        */
+                                 /* candidates: SP_POLICY_*           */
+    uint32_t reserved;           /* must be 0                                       */
+    uint64_t policy_seed;        /* SP_POLICY_RANDOM: seed of the victim draws      */
 } sp_desc;
+
+/* desc.policy (readings R8, R23-R25).  Every policy evicts only
+ * candidates: slots whose row is outside the window B(b-P..b+F) and not pinned.
+ *   LRU     ascending (last Plan that used the slot, resident ID)  [default]
+ *   RANDOM  vacant slots lowest first, then draws s_i = H(seed, t, b, i) mod O
+ *           over the O occupied slots, a candidate taken when first drawn
+ *           (H: splitmix64 chain of seed ^ "RAND", t, b, i)
+ *   LFU     ascending (use count saturating at 8, last use, resident ID); the
+ *           use count is 1 at fill and +1 per Plan that hits the slot */
+#define SP_POLICY_LRU    0
+#define SP_POLICY_RANDOM 1
+#define SP_POLICY_LFU    2
 
 typedef enum {
     SP_K_PLAN = 0,      /* dedup + future probe + Plan (one launch per sp_plan)  */
@@ -192,6 +210,26 @@ sp_status sp_create(const sp_desc *desc, sp_ctx **out);
  * to recycle a pinned staging buffer.  Returns SP_ERR_STATE if the caller is
  * more than 16 batches ahead of sp_train. */
 sp_status sp_plan(sp_ctx *c, const void *batch_indices);
+
+/* Ragged mini-batch B(j) in CSR form (the EmbeddingBag "offsets" layout;
+ * PAPER.md Fig. 2 P:257-263 has bags of 2 and 3 lookups): values int64 [nnz],
+ * offsets int64 [T*N + 1], bag k = t*N + s holds values[offsets[k] ..
+ * offsets[k+1]); offsets[0] == 0; every bag has at most desc.pooling lookups
+ * (so tables may differ in pooling: per-table pooling is bags of different
+ * sizes).  Host pointers, copied before return.  Requires SP_FLAG_PADDING:
+ * the library expands the bags on the GPU (k_csr_pad) into the padded
+ * [T][N][L] layout, -1 in the unused positions, and plans that.
+ * SP_ERR_INVALID_ARG for malformed offsets or a bag longer than pooling. */
+sp_status sp_plan_csr(sp_ctx *c, const int64_t *values, const int64_t *offsets);
+
+/* Static partition (the paper's static top-N cache design
+ * point P:472-495, reading R26): before the first sp_plan, load rows
+ * ids[0..count) of table t (distinct, in range) into the table's LAST `count`
+ * slots, in order, and map them in the Hit-Map.  Pinned rows always hit and
+ * are never victims; the remaining slots are the scratchpad as usual.
+ * SP_ERR_STATE after the first sp_plan or a second call for the table;
+ * SP_ERR_INVALID_ARG for bad IDs or count > slots[t].  Synchronous. */
+sp_status sp_pin_rows(sp_ctx *c, int32_t t, const int64_t *ids, int64_t count);
 
 /* Same as sp_plan with SP_FLAG_INDEX_DEVICE for this one call: dev_indices
  * is a device pointer ([T][N][L], index width per SP_FLAG_INDEX_I32), read

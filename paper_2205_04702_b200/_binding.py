@@ -26,6 +26,8 @@ SP_FLAG_REGISTER_HOST = 1 << 0
 SP_FLAG_INDEX_I32 = 1 << 1
 SP_FLAG_INDEX_DEVICE = 1 << 2
 SP_FLAG_PROFILE = 1 << 3
+SP_FLAG_PADDING = 1 << 4
+POLICIES = {"lru": 0, "random": 1, "lfu": 2}
 KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush", "h2d", "d2h"]
 KERNEL_ONLY = ["plan", "transfer", "forward", "backward", "surrogate", "flush"]
 RING = 16  # batches in flight inside the library (sp_internal.cuh)
@@ -48,7 +50,9 @@ class SpDesc(ctypes.Structure):
         ("flags", ctypes.c_uint32),
         ("log_factor", ctypes.c_int32),
         ("host_threads", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("policy", ctypes.c_int32),
+        ("reserved", ctypes.c_uint32),
+        ("policy_seed", ctypes.c_uint64),
     ]
 
 
@@ -93,6 +97,7 @@ def _load():
                        ("sp_train", [P, P, ctypes.c_float]),
                        ("sp_surrogate_grad", [P, P, P, ctypes.c_int64, ctypes.c_float, ctypes.c_float]),
                        ("sp_flush", [P]), ("sp_destroy", [P]), ("sp_prefill", [P]),
+                       ("sp_plan_csr", [P, P, P]), ("sp_pin_rows", [P, ctypes.c_int32, P, ctypes.c_int64]),
                        ("sp_last_error_batch", [P, i64p, ctypes.POINTER(ctypes.c_int32)]),
                        ("sp_get_stats", [P, ctypes.POINTER(SpStats)]),
                        ("sp_debug_plan", [P, ctypes.c_int64, ctypes.c_int32, i64p, i64p, i64p, i64p, i64p]),
@@ -172,7 +177,8 @@ class ScratchPipe:
                  batch_size: int, pooling: int, window: int = 3, past: int = -1, future: int = -1,
                  device: int = 0, stream=None, index_dtype: str = "int64", index_on_device: bool = False,
                  register_host: bool = False, profile: bool = False, log_factor: int = 0,
-                 host_threads: int = 0):
+                 host_threads: int = 0, policy: str = "lru", policy_seed: int = 0,
+                 padding: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("ScratchPipe needs a CUDA device (no CPU fallback)")
@@ -194,10 +200,12 @@ class ScratchPipe:
             flags |= SP_FLAG_INDEX_DEVICE
         if profile:
             flags |= SP_FLAG_PROFILE
+        if padding:
+            flags |= SP_FLAG_PADDING
         self.index_dtype, self.index_on_device = index_dtype, index_on_device
         d = SpDesc(self.T, _i64(self._rows), self._hp, dim, _i64(self._slots), window, past, future,
                    batch_size, pooling, device, ctypes.c_void_p(stream.cuda_stream), flags, log_factor,
-                   host_threads, 0)
+                   host_threads, POLICIES[policy], 0, policy_seed & ((1 << 64) - 1))
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             st = lib.sp_create(ctypes.byref(d), ctypes.byref(h))
@@ -249,6 +257,23 @@ class ScratchPipe:
             raise TypeError(f"device indices must be contiguous cuda {want}")
         self._keep(idx)
         self._check(lib.sp_plan_device(self._h, ctypes.c_void_p(idx.data_ptr())))
+
+    def plan_csr(self, values, offsets):
+        """Push a ragged batch in CSR form: values int64 [nnz], offsets int64
+        [T*N+1] (bag t*N+s = values[offsets[k]:offsets[k+1]]), host arrays
+        (needs padding=True; sp_plan_csr)."""
+        v = np.ascontiguousarray(values, dtype=np.int64)
+        o = np.ascontiguousarray(offsets, dtype=np.int64)
+        if o.size != self.T * self.N + 1:
+            raise ValueError("offsets must have T*N+1 entries")
+        self._check(lib.sp_plan_csr(self._h, v.ctypes.data_as(ctypes.c_void_p) if v.size else None,
+                                    o.ctypes.data_as(ctypes.c_void_p)))
+
+    def pin_rows(self, t: int, ids):
+        """Static partition: rows `ids` of table t held in its last slots for
+        the whole run (before the first plan; sp_pin_rows)."""
+        a = np.ascontiguousarray(ids, dtype=np.int64)
+        self._check(lib.sp_pin_rows(self._h, t, a.ctypes.data_as(ctypes.c_void_p) if a.size else None, a.size))
 
     def copy_batch_stats(self, b: int, host_out):
         """Async D2H of batch b's per-table (U, hits, misses, evictions) into a

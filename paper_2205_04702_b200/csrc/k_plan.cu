@@ -276,13 +276,16 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
         va = ka + Tn; kb = va + Tn; vb = kb + Tn;
     }
     PhaseClock pc(A.prof, g.T, 1, t);
-    // D1: ingest + range check
-    int bad = 0;
+    // D1: ingest + range check.  With SP_FLAG_PADDING an ID of -1 is "no
+    // lookup" (ragged bags, reading R27): its key R sorts after every real ID
+    // and it joins no unique.
+    int bad = 0, npad = 0;
 #pragma unroll 4
     for (int i = tid; i < n; i += blockDim.x) {
         long long id = A.idx_i32 ? (long long)((const int32_t *)idx)[(size_t)t * n + i]
                                  : ((const long long *)idx)[(size_t)t * n + i];
-        if (id < 0 || id >= R) { bad = 1; id = 0; }
+        if (A.pad && id == -1) { id = R; npad++; }
+        else if (id < 0 || id >= R) { bad = 1; id = 0; }
         ka[i] = (uint32_t)id;
         va[i] = (uint32_t)i;
     }
@@ -290,12 +293,18 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
         if (tid == 0) set_err(A, j, t, DERR_INDEX);
         return;
     }
+    int n_real = n;
+    if (A.pad) {  // real lookups of this table (pads sort last)
+        uint32_t tot;
+        (void)block_scan((uint32_t)npad, &tot);
+        n_real = n - (int)tot;
+    }
     pc.mark(0);
     // D2: sort by id (stable: occurrences stay ascending within an id).  LSD
     // radix over the table's id bits (1-3 passes of 8 bits).  (A shared-memory
     // bitonic sort of packed (id, occurrence) keys was measured slower:
     // 17.8 us for n = 2048, every table paying the full 66 barrier stages.)
-    const int bits = bit_width_u64((unsigned long long)(R - 1));
+    const int bits = bit_width_u64((unsigned long long)(A.pad ? R : R - 1));
     bool sw;
     if (n <= 2 * PUSH_THREADS) sw = radix_sort_smem<2>(ka, va, kb, vb, n, bits);
     else if (n <= 4 * PUSH_THREADS) sw = radix_sort_smem<4>(ka, va, kb, vb, n, bits);
@@ -313,7 +322,7 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
     for (int i0 = 0; i0 < n; i0 += blockDim.x) {
         const int i = i0 + tid;
         uint32_t head = 0, id = 0;
-        if (i < n) {
+        if (i < n_real) {
             id = keys[i];
             head = (i == 0) || (keys[i - 1] != id);
         }
@@ -322,13 +331,13 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
         if (i < n) {
             const uint32_t uid = carry + ex + head - 1;
             sorted_occ[i] = vals[i];
-            sorted_uid[i] = uid;
+            sorted_uid[i] = i < n_real ? uid : EMPTY;  // padding: no unique
             if (head) { uniq_id[uid] = id; seg_off[uid] = (uint32_t)i; }
         }
         carry += tot;
     }
     const uint32_t U = carry;
-    if (tid == 0) { seg_off[U] = (uint32_t)n; nb.U[t] = U; }
+    if (tid == 0) { seg_off[U] = (uint32_t)n_real; nb.U[t] = U; }
     __syncthreads();
     pc.mark(2);
     // D3a: backward work lists.  A unique with <= CH occurrences is one chunk
@@ -388,7 +397,7 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
     pc.mark(3);
     // D3b: inline bag indices of the single-chunk rows, one occurrence per thread
 #pragma unroll 4
-    for (int i = tid; i < n; i += blockDim.x) {
+    for (int i = tid; i < n_real; i += blockDim.x) {
         const uint32_t u = sorted_uid[i];
         const uint32_t c = chunk_first[u];
         if (c != EMPTY) rec[c].bag[(uint32_t)i - seg_off[u]] = vals[i] / (uint32_t)g.L;
@@ -400,13 +409,30 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
 }
 
 // ------------------------------------------------------------------- plan
+// RANDOM eviction draw (reading R23): splitmix64 chain over (seed, t, b, i)
+__device__ __forceinline__ unsigned long long sm64(unsigned long long x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ unsigned long long rand_draw(unsigned long long seed, int t, long long b,
+                                                        unsigned long long i) {
+    unsigned long long h = sm64(seed ^ 0x52414E44ull);  // "RAND"
+    h = sm64(h ^ (unsigned long long)(long long)t);
+    h = sm64(h ^ (unsigned long long)b);
+    return sm64(h ^ i);
+}
+
 __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char *smem_raw) {
     const Geometry &g = A.g;
     const int n = g.n, tid = threadIdx.x;
     __shared__ uint32_t s_fail, s_got;
     __shared__ unsigned long long s_head, s_newhead, s_tail;
+    __shared__ unsigned long long s_chead[LOG_CLASSES_MAX];  // per class log: head after P3
     const unsigned long long roff = A.row_off[t];
     const BatchBufs &pb = A.pb;
+    const int NC = A.log_classes;  // 1 (LRU), LFU_FMAX + 1 (LFU), 0 (RANDOM: no log)
     // working lists of this Plan: in the CTA's dynamic shared memory (the same
     // 16n bytes the dedup role sorts in) when n <= SMEM_SORT_MAX, else global
     const bool small = n <= SMEM_SORT_MAX;
@@ -415,26 +441,34 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
     uint32_t *miss_u = small ? w_uid + 2 * n : A.miss_u + (size_t)t * n;
     uint32_t *victims = small ? w_uid + 3 * n : A.victims + (size_t)t * n;
     uint32_t *slot_u = pb.slot_u + (size_t)t * n;                                    // global copy
+    const uint32_t pin_base = A.pin_base[t];  // slots >= pin_base are pinned (never victims)
 
     PhaseClock pc(A.prof, g.T, 0, t);
-    // P3's first window of the LRU log, loaded now: its entries (slot, stamp)
-    // are not touched before P3, so the loads overlap P1 + P2
-    const unsigned long long cap = A.log_cap[t], lbase = A.log_base[t];
+    // P3's first window of the (class-0) LRU log, loaded now: its entries
+    // (slot, stamp) are not touched before P3, so the loads overlap P1 + P2
     uint32_t *lslot = A.log_slot;
     int32_t *lstamp = A.log_stamp;
-    const unsigned long long head0 = A.log_head[t], tail0 = A.log_tail[t];
-    const bool inr0 = head0 + tid < tail0;
+    const int lid0 = t * (NC > 0 ? NC : 1);
+    unsigned long long head0 = 0, tail0 = 0;
+    bool inr0 = false;
     uint32_t slot0 = 0;
     int32_t stamp0 = 0;
-    if (inr0) {
-        const size_t ix = (size_t)(lbase + (head0 + tid) % cap);
-        slot0 = lslot[ix];
-        stamp0 = lstamp[ix];
+    if (NC > 0) {
+        const unsigned long long cap = A.log_cap[lid0], lbase = A.log_base[lid0];
+        head0 = A.log_head[lid0];
+        tail0 = A.log_tail[lid0];
+        inr0 = head0 + tid < tail0;
+        if (inr0) {
+            const size_t ix = (size_t)(lbase + (head0 + tid) % cap);
+            slot0 = lslot[ix];
+            stamp0 = lstamp[ix];
+        }
     }
     // P1 + P2 in one pass (independent probes of the same Hit-Map):
     // P1 future probe: resident IDs of B(b+F) get next_need = b+F;
     // P2 probe of B(b): hits stamped last_use = b, misses compacted in
-    // ascending ID order (Alg. 1)
+    // ascending ID order (Alg. 1); LFU: a hit adds one use (R24)
+    const bool lfu = A.policy == POL_LFU;
     const uint32_t Ub = pb.U[t];
     const uint32_t Uf = A.has_future ? A.fb.U[t] : 0u;
     const uint32_t *fid = A.fb.uniq_id + (size_t)t * n;
@@ -467,7 +501,10 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
                 if (sf[q] != EMPTY) A.next_need[sf[q]] = fstamp;
                 if (u < Ub) {
                     w_uid[u] = idb[q];
-                    if (sb[q] != EMPTY) A.last_use[sb[q]] = (int32_t)b;
+                    if (sb[q] != EMPTY) {
+                        A.last_use[sb[q]] = (int32_t)b;
+                        if (lfu) A.freq[sb[q]] = (uint8_t)min((int)A.freq[sb[q]] + 1, LFU_FMAX);
+                    }
                     slot_l[u] = sb[q];
                     slot_u[u] = sb[q];
                     hitf[u] = sb[q] != EMPTY;
@@ -493,8 +530,12 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
             if (sf != EMPTY) A.next_need[sf] = fstamp;
             uint32_t miss = 0;
             if (u < Ub) {
-                if (sb != EMPTY) A.last_use[sb] = (int32_t)b;
-                else miss = 1;
+                if (sb != EMPTY) {
+                    A.last_use[sb] = (int32_t)b;
+                    if (lfu) A.freq[sb] = (uint8_t)min((int)A.freq[sb] + 1, LFU_FMAX);
+                } else {
+                    miss = 1;
+                }
                 slot_l[u] = sb;
                 hitf[u] = sb != EMPTY;
             }
@@ -510,61 +551,128 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
 
     pc.mark(0);
     pc.mark(1);
-    // P3: victim selection over the per-table LRU log
+    const long long limit = b - A.P - 1;
     if (tid == 0) {
-        s_head = head0;
-        s_tail = tail0;
         s_got = 0;
         s_fail = 0;
     }
     __syncthreads();
-    const long long limit = b - A.P - 1;
-    bool first = true;
-    while (true) {
-        const unsigned long long head = s_head, tail = s_tail;
-        const uint32_t got = s_got;
-        if (got >= m) break;
-        const unsigned long long pos = head + tid;
-        bool inr;
-        uint32_t slot = 0;
-        int32_t stamp = 0;
-        if (first) {  // head == head0: the prefetched window
-            inr = inr0;
-            slot = slot0;
-            stamp = stamp0;
-            first = false;
-        } else {
-            inr = pos < tail;
-            if (inr) {
-                const size_t ix = (size_t)(lbase + pos % cap);
-                slot = lslot[ix];
-                stamp = lstamp[ix];
+    if (NC > 0) {
+        // P3 (LRU / LFU): walk the class logs in ascending class (LRU: one
+        // log), each from its head.  A slot is a candidate iff its entry is
+        // current (last_use == stamp), last_use <= b-P-1 (past window,
+        // P:840-861), next_need <= b (future window) and it is not pinned; the
+        // first |misses| candidates in (class, last_use, ID) order are taken
+        // (LRU P:1273 reading R8; LFU reading R24).  Eligible entries before
+        // the last one taken are dropped (stale, or future-held: those are hit
+        // again at next_need and re-appended).  Too few -> SP_ERR_CAPACITY
+        // (P:1030-1035).
+        for (int c = 0; c < NC; c++) {
+            const int lid = lid0 + c;
+            const unsigned long long cap = A.log_cap[lid], lbase = A.log_base[lid];
+            if (tid == 0) {
+                s_head = c == 0 ? head0 : A.log_head[lid];
+                s_tail = c == 0 ? tail0 : A.log_tail[lid];
+            }
+            __syncthreads();
+            bool first = c == 0;
+            while (true) {
+                const unsigned long long head = s_head, tail = s_tail;
+                const uint32_t got = s_got;
+                if (got >= m) break;
+                const unsigned long long pos = head + tid;
+                bool inr;
+                uint32_t slot = 0;
+                int32_t stamp = 0;
+                if (first) {  // head == head0: the prefetched window
+                    inr = inr0;
+                    slot = slot0;
+                    stamp = stamp0;
+                    first = false;
+                } else {
+                    inr = pos < tail;
+                    if (inr) {
+                        const size_t ix = (size_t)(lbase + pos % cap);
+                        slot = lslot[ix];
+                        stamp = lstamp[ix];
+                    }
+                }
+                const bool elig = inr && (long long)stamp <= limit;  // stamps are non-decreasing
+                const bool cand = elig && slot < pin_base && A.last_use[slot] == stamp &&
+                                  (long long)A.next_need[slot] <= b;
+                // one scan for both counts (<= blockDim each): eligible in the high half
+                uint32_t tot2;
+                const uint32_t ex2 = block_scan((elig ? 0x10000u : 0u) | (cand ? 1u : 0u), &tot2);
+                const uint32_t n_elig = tot2 >> 16, n_cand = tot2 & 0xFFFFu, r = ex2 & 0xFFFFu;
+                const uint32_t need = m - got;
+                if (cand && r < need) {
+                    victims[got + r] = slot;
+                    if (r == need - 1) s_newhead = pos + 1;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    if (n_cand >= need) {
+                        s_got = m;
+                        s_head = s_newhead;
+                    } else {
+                        s_got = got + n_cand;
+                        s_head = head + n_elig;
+                        if (n_elig < blockDim.x) s_fail = 1;  // reached held entries or the tail
+                    }
+                }
+                __syncthreads();
+                if (s_fail) break;  // this class is exhausted
+            }
+            if (tid == 0) {
+                s_chead[c] = s_head;
+                s_fail = 0;
+            }
+            __syncthreads();
+        }
+        if (tid == 0 && s_got < m) s_fail = 1;  // every class exhausted
+        __syncthreads();
+    } else {
+        // P3 (RANDOM, reading R23): vacant dynamic slots first, lowest first
+        // (they are [nfill, pin_base): slots fill lowest first); then draws
+        // s_i = H(seed, t, b, i) mod O over the O occupied dynamic slots, an
+        // occupied candidate being taken the first time it is drawn.  Draw i
+        // claims its slot with atomicMax of ((b+1) << 32 | ~i): the smallest i
+        // of this Plan wins, claims of older Plans are smaller.
+        const uint32_t sbase = A.slot_base[t];
+        const uint32_t O = A.nfill[t];
+        const uint32_t nvac = pin_base - sbase - O;
+        const uint32_t v = min(m, nvac);
+        for (uint32_t k = tid; k < v; k += blockDim.x) victims[k] = sbase + O + k;
+        uint32_t got = v;
+        bool counted = false;
+        for (unsigned long long i0 = 0; got < m; i0 += blockDim.x) {
+            const unsigned long long i = i0 + tid;
+            const uint32_t s = sbase + (uint32_t)(rand_draw(A.seed, t, b, i) % (unsigned long long)O);
+            const bool cand = (long long)A.last_use[s] <= limit && (long long)A.next_need[s] <= b;
+            const unsigned long long key = ((unsigned long long)(b + 1) << 32) | (0xFFFFFFFFull - (i & 0xFFFFFFFFull));
+            if (cand) atomicMax(&A.claim[s], key);
+            __syncthreads();
+            const bool acc = cand && atomicOr(&A.claim[s], 0ull) == key;  // (L2: every claim of this round landed)
+            uint32_t tot;
+            const uint32_t r = block_scan(acc ? 1u : 0u, &tot);
+            if (acc && got + r < m) victims[got + r] = s;
+            got += min(tot, m - got);
+            if (got < m && !counted && i0 > 8ull * O + 4096) {
+                // many draws without enough candidates: count them (capacity check)
+                uint32_t c = 0;
+                for (uint32_t q = tid; q < O; q += blockDim.x)
+                    c += ((long long)A.last_use[sbase + q] <= limit && (long long)A.next_need[sbase + q] <= b) ? 1u : 0u;
+                uint32_t ctot;
+                (void)block_scan(c, &ctot);
+                counted = true;
+                if (ctot < m - v) {
+                    if (tid == 0) s_fail = 1;
+                    break;
+                }
             }
         }
-        const bool elig = inr && (long long)stamp <= limit;  // stamps are non-decreasing
-        const bool cand = elig && A.last_use[slot] == stamp && (long long)A.next_need[slot] <= b;
-        // one scan for both counts (<= blockDim each): eligible in the high half
-        uint32_t tot2;
-        const uint32_t ex2 = block_scan((elig ? 0x10000u : 0u) | (cand ? 1u : 0u), &tot2);
-        const uint32_t n_elig = tot2 >> 16, n_cand = tot2 & 0xFFFFu, r = ex2 & 0xFFFFu;
-        const uint32_t need = m - got;
-        if (cand && r < need) {
-            victims[got + r] = slot;
-            if (r == need - 1) s_newhead = pos + 1;
-        }
         __syncthreads();
-        if (tid == 0) {
-            if (n_cand >= need) {
-                s_got = m;
-                s_head = s_newhead;
-            } else {
-                s_got = got + n_cand;
-                s_head = head + n_elig;
-                if (n_elig < blockDim.x) s_fail = 1;  // reached held entries or the tail
-            }
-        }
-        __syncthreads();
-        if (s_fail) break;
+        if (tid == 0 && !s_fail) A.nfill[t] = O + v;
     }
     if (s_fail) {
         if (tid == 0) set_err(A, b, t, DERR_CAPACITY);
@@ -588,6 +696,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
         A.resident[s] = id;
         A.last_use[s] = (int32_t)b;
         A.next_need[s] = NEVER;
+        if (lfu) A.freq[s] = 1;
         slot_l[u] = s;
         if (small) slot_u[u] = s;
         fill_slot[k] = s;
@@ -609,42 +718,79 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
     }
 
     pc.mark(3);
-    // P5: LRU log append (after an in-place compaction if it would overflow)
-    const unsigned long long head = s_head;
-    unsigned long long tail = s_tail;
-    if (tail - head + Ub > cap) {
-        unsigned long long w = head;
-        for (unsigned long long c0 = head; c0 < tail; c0 += blockDim.x) {
-            const unsigned long long pos = c0 + tid;
-            const bool inr = pos < tail;
-            uint32_t slot = 0;
-            int32_t stamp = 0;
-            if (inr) {
-                const size_t ix = (size_t)(lbase + pos % cap);
-                slot = lslot[ix];
-                stamp = lstamp[ix];
+    // P5: log append, per class (LRU: every unique of B(b) to the one log;
+    // LFU: each to the log of its use count), after an in-place compaction
+    // of a log that would overflow; stamps b, ascending ID within a batch
+    for (int c = 0; c < NC; c++) {
+        const int lid = lid0 + c;
+        const unsigned long long cap = A.log_cap[lid], lbase = A.log_base[lid];
+        const unsigned long long head = s_chead[c];
+        unsigned long long tail = c == 0 ? tail0 : A.log_tail[lid];
+        // entries going to this class (LFU: freq == c; class 0 only holds the
+        // initial vacant slots, appended to by LRU alone)
+        uint32_t cnt = Ub;
+        if (lfu) {
+            if (c == 0) cnt = 0;
+            else {
+                uint32_t k = 0;
+                for (uint32_t u = tid; u < Ub; u += blockDim.x) k += A.freq[slot_l[u]] == c ? 1u : 0u;
+                (void)block_scan(k, &cnt);
             }
-            const bool keep = inr && A.last_use[slot] == stamp;
-            uint32_t tot;
-            const uint32_t r = block_scan(keep ? 1u : 0u, &tot);  // all reads precede writes
-            if (keep) {
-                const size_t ix = (size_t)(lbase + (w + r) % cap);
-                lslot[ix] = slot;
-                lstamp[ix] = stamp;
-            }
-            w += tot;
-            __syncthreads();
         }
-        tail = w;
-    }
-    for (uint32_t u = tid; u < Ub; u += blockDim.x) {
-        const size_t ix = (size_t)(lbase + (tail + u) % cap);
-        lslot[ix] = slot_l[u];
-        lstamp[ix] = (int32_t)b;
+        if (tail - head + cnt > cap) {
+            unsigned long long w = head;
+            for (unsigned long long c0 = head; c0 < tail; c0 += blockDim.x) {
+                const unsigned long long pos = c0 + tid;
+                const bool inr = pos < tail;
+                uint32_t slot = 0;
+                int32_t stamp = 0;
+                if (inr) {
+                    const size_t ix = (size_t)(lbase + pos % cap);
+                    slot = lslot[ix];
+                    stamp = lstamp[ix];
+                }
+                const bool keep = inr && A.last_use[slot] == stamp;
+                uint32_t tot;
+                const uint32_t r = block_scan(keep ? 1u : 0u, &tot);  // all reads precede writes
+                if (keep) {
+                    const size_t ix = (size_t)(lbase + (w + r) % cap);
+                    lslot[ix] = slot;
+                    lstamp[ix] = stamp;
+                }
+                w += tot;
+                __syncthreads();
+            }
+            tail = w;
+        }
+        if (!lfu) {
+            for (uint32_t u = tid; u < Ub; u += blockDim.x) {
+                const size_t ix = (size_t)(lbase + (tail + u) % cap);
+                lslot[ix] = slot_l[u];
+                lstamp[ix] = (int32_t)b;
+            }
+        } else if (cnt) {
+            uint32_t run = 0;
+            for (uint32_t u0 = 0; u0 < Ub; u0 += blockDim.x) {
+                const uint32_t u = u0 + tid;
+                const uint32_t sl = u < Ub ? slot_l[u] : 0u;
+                const bool mine = u < Ub && A.freq[sl] == c;
+                uint32_t tot;
+                const uint32_t r = block_scan(mine ? 1u : 0u, &tot);
+                if (mine) {
+                    const size_t ix = (size_t)(lbase + (tail + run + r) % cap);
+                    lslot[ix] = sl;
+                    lstamp[ix] = (int32_t)b;
+                }
+                run += tot;
+            }
+        }
+        if (tid == 0) {
+            A.log_head[lid] = head;
+            A.log_tail[lid] = tail + cnt;
+        }
+        __syncthreads();
     }
     if (tid == 0) {
-        A.log_head[t] = head;
-        A.log_tail[t] = tail + Ub;
         uint32_t *st = pb.stats + 4 * t;
         st[0] = Ub; st[1] = nhit; st[2] = m; st[3] = ev_total;
         atomicAdd(&A.cum[0], (unsigned long long)Ub);
@@ -668,7 +814,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
         }
 #pragma unroll
         for (int q = 0; q < 4; q++)
-            if (i0 + q * (int)blockDim.x < n) sl[q] = slot_l[u[q]];
+            if (i0 + q * (int)blockDim.x < n) sl[q] = u[q] == EMPTY ? EMPTY : slot_l[u[q]];  // EMPTY: padding
 #pragma unroll
         for (int q = 0; q < 4; q++)
             if (i0 + q * (int)blockDim.x < n) slot_of_occ[o[q]] = sl[q];

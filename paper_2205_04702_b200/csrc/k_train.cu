@@ -59,6 +59,32 @@ __global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
     const float4 *st = reinterpret_cast<const float4 *>(A.storage) + lane;
     float4 *out = reinterpret_cast<float4 *>(A.pooled) + lane;
     const long long S = (long long)gridDim.x * gpb;
+    if (A.g.pad) {
+        // ragged bags (-1 padding, reading R27): a padded position has slot
+        // EMPTY and is skipped; a bag with no lookup pools to zeros; the fold
+        // starts from the first real row (as the oracle's)
+        for (long long bag = (long long)blockIdx.x * gpb + threadIdx.x / G; bag < nbags; bag += S) {
+            const uint32_t *so = A.bb.slot_of_occ + bag * L;
+            float4 acc[VPL];
+            bool first = true;
+#pragma unroll
+            for (int v = 0; v < VPL; v++) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int p = 0; p < L; p++) {
+                const uint32_t sl = __ldg(so + p);
+                if (sl == EMPTY) continue;
+#pragma unroll
+                for (int v = 0; v < VPL; v++) {
+                    const float4 r = ldg4(st + (size_t)sl * D4 + v * G);
+                    if (first) acc[v] = r;
+                    else add4(acc[v], r);
+                }
+                first = false;
+            }
+#pragma unroll
+            for (int v = 0; v < VPL; v++) __stcs(out + bag * D4 + v * G, acc[v]);
+        }
+        return;
+    }
     for (long long bag0 = (long long)blockIdx.x * gpb + threadIdx.x / G; bag0 < nbags; bag0 += BU * S) {
         const uint32_t *so[BU];
         bool ok[BU];
@@ -109,8 +135,16 @@ __global__ void __launch_bounds__(256) k_fwd_generic(TrainArgs A) {
          bag += (long long)gridDim.x * (blockDim.x / 32)) {
         const uint32_t *so = A.bb.slot_of_occ + bag * L;
         for (int c = lane; c < D4; c += 32) {
-            float4 acc = ldg4(st + (size_t)__ldg(so) * D4 + c);
-            for (int p = 1; p < L; p++) add4(acc, ldg4(st + (size_t)__ldg(so + p) * D4 + c));
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            bool first = true;
+            for (int p = 0; p < L; p++) {
+                const uint32_t sl = __ldg(so + p);
+                if (sl == EMPTY) continue;  // padding (reading R27)
+                const float4 r = ldg4(st + (size_t)sl * D4 + c);
+                if (first) acc = r;
+                else add4(acc, r);
+                first = false;
+            }
             out[bag * D4 + c] = acc;
         }
     }

@@ -22,6 +22,8 @@
 //       Storage[s]  <- smem'     (the freed slot gets the missed row)
 #include "sp_internal.cuh"
 
+#include <algorithm>
+
 namespace sp {
 
 // Completion of Transfer(b) for the scatter thread: every CTA's staging stores
@@ -215,6 +217,55 @@ __global__ void __launch_bounds__(256) k_prefill_map(const uint32_t *slot_base, 
 cudaError_t launch_prefill_map(const uint32_t *slot_base, const unsigned long long *row_off, int T,
                                long long S_total, uint32_t *resident, uint32_t *hitmap, cudaStream_t s) {
     k_prefill_map<<<148 * 8, 256, 0, s>>>(slot_base, row_off, T, S_total, resident, hitmap);
+    return cudaGetLastError();
+}
+
+// initial class-0 log of every table: its slots in ascending order, all
+// vacant (stamp VACANT), at log_base0[t]
+__global__ void __launch_bounds__(256) k_log_init(const uint32_t *slot_base, const unsigned long long *log_base0,
+                                                  int T, long long S_total, uint32_t *log_slot, int32_t *log_stamp) {
+    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < S_total;
+         s += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = T;  // slot_base[lo] <= s < slot_base[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((long long)slot_base[mid] <= s) lo = mid;
+            else hi = mid;
+        }
+        const size_t ix = (size_t)(log_base0[lo] + (unsigned long long)(s - slot_base[lo]));
+        log_slot[ix] = (uint32_t)s;
+        log_stamp[ix] = VACANT;
+    }
+}
+
+cudaError_t launch_log_init(const uint32_t *slot_base, const unsigned long long *log_base0, int T, long long S_total,
+                            uint32_t *log_slot, int32_t *log_stamp, cudaStream_t s) {
+    k_log_init<<<148 * 8, 256, 0, s>>>(slot_base, log_base0, T, S_total, log_slot, log_stamp);
+    return cudaGetLastError();
+}
+
+// Ragged bags (sp_plan_csr, reading R27): CSR (values, offsets [T*N+1]) ->
+// the padded [T][N][L] index layout, -1 in positions past a bag's end.  One
+// thread per (bag, position); offsets were validated on the host.
+__global__ void __launch_bounds__(256) k_csr_pad(const long long *values, const long long *offsets, long long nbags,
+                                                 int L, void *out, int out_i32) {
+    const long long total = nbags * L;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long bag = i / L;
+        const int p = (int)(i - bag * L);
+        const long long o = __ldg(offsets + bag) + p;
+        const long long id = o < __ldg(offsets + bag + 1) ? __ldg(values + o) : -1ll;
+        if (out_i32) static_cast<int32_t *>(out)[i] = (int32_t)id;
+        else static_cast<long long *>(out)[i] = id;
+    }
+}
+
+cudaError_t launch_csr_pad(const long long *values, const long long *offsets, long long nbags, int L, void *out,
+                           int out_i32, cudaStream_t s) {
+    long long blocks = (nbags * L + 255) / 256;
+    const long long cap = (long long)device_sms() * 8;
+    k_csr_pad<<<(int)std::max(1ll, std::min(blocks, cap)), 256, 0, s>>>(values, offsets, nbags, L, out, out_i32);
     return cudaGetLastError();
 }
 

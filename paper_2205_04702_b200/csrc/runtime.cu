@@ -174,7 +174,19 @@ struct sp_ctx {
     uint32_t *d_log_slot = nullptr;
     int32_t *d_log_stamp = nullptr;
     unsigned long long *d_log_base = nullptr, *d_log_cap = nullptr, *d_log_head = nullptr,
-                       *d_log_tail = nullptr;
+                       *d_log_tail = nullptr;  // [T * log_classes]
+    // replacement policy (sp_desc.policy) and its per-slot / per-table state
+    int policy = 0, log_classes = 1;
+    unsigned long long policy_seed = 0;
+    uint32_t *d_pin_base = nullptr;           // [T] first pinned slot (slot_base[t+1]: none)
+    std::vector<uint32_t> pin_base;
+    std::vector<bool> pinned_t;
+    uint32_t *d_nfill = nullptr;              // [T] RANDOM: dynamic slots filled so far
+    unsigned long long *d_claim = nullptr;    // [S] RANDOM: draw claims
+    uint8_t *d_freq = nullptr;                // [S] LFU: use counts
+    // ragged bags in CSR form (sp_plan_csr): pinned host staging + device copies per ring slot
+    int64_t *h_csr = nullptr;                 // pinned [RING][T*n + T*N + 1]
+    int64_t *d_csr = nullptr;                 // device [RING][T*n + T*N + 1]
     unsigned long long *d_err = nullptr, *d_cum = nullptr;
     unsigned long long *d_pprof = nullptr;  // k_push per-CTA timing [2T+2] (profiling only)
     uint32_t *d_miss_u = nullptr, *d_victims = nullptr;
@@ -500,6 +512,14 @@ PushArgs push_args(sp_ctx *c) {
     a.sort_tmp = c->d_sort_tmp;
     a.idx_i32 = (c->flags & SP_FLAG_INDEX_I32) ? 1 : 0;
     a.prof = c->profiling.load() ? c->d_pprof : nullptr;
+    a.policy = c->policy;
+    a.log_classes = c->log_classes;
+    a.seed = c->policy_seed;
+    a.pin_base = c->d_pin_base;
+    a.nfill = c->d_nfill;
+    a.claim = c->d_claim;
+    a.freq = c->d_freq;
+    a.pad = (c->flags & SP_FLAG_PADDING) ? 1 : 0;
     return a;
 }
 
@@ -787,7 +807,7 @@ void destroy_all(sp_ctx *c) {
             if (c->sev[r][k]) cudaEventDestroy(c->sev[r][k]);
     if (c->prof_ref) cudaEventDestroy(c->prof_ref);
     for (void *p : c->allocs) cudaFree(p);
-    for (void *p : {(void *)c->h_stage, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb, (void *)c->h_staged,
+    for (void *p : {(void *)c->h_stage, (void *)c->h_csr, (void *)c->h_err, (void *)c->h_errflag, (void *)c->h_scat, (void *)c->h_wb, (void *)c->h_staged,
                     (void *)c->h_wbdst, (void *)c->h_scnt,
                     (void *)c->hl_ready, (void *)c->hl_m, (void *)c->hl_row, (void *)c->h_in, (void *)c->h_gathered})
         if (p) cudaFreeHost(p);
@@ -849,6 +869,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         F = d->window > 0 ? d->window - 1 : 0;
     }
     if (F > P + 1) return SP_ERR_INVALID_ARG;  // one-shot future probe needs F <= P + 1
+    if (d->policy < SP_POLICY_LRU || d->policy > SP_POLICY_LFU || d->reserved != 0) return SP_ERR_INVALID_ARG;
     if (P + F + 2 > RING) return SP_ERR_INVALID_ARG;
     sp_ctx *c = new sp_ctx();
     c->T = d->num_tables;
@@ -870,6 +891,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->g.n1 = c->n + 1;
     c->g.nc = c->n + c->n / CH + 1;
     c->g.hs = backward_hot_segment(c->D);
+    c->g.pad = (d->flags & SP_FLAG_PADDING) ? 1 : 0;
+    c->policy = d->policy;
+    c->policy_seed = d->policy_seed;
+    c->log_classes = c->policy == SP_POLICY_LFU ? LOG_CLASSES_MAX : (c->policy == SP_POLICY_RANDOM ? 0 : 1);
     // hot-row segment records: rows with > CH occurrences, ceil(len/hs) each
     c->g.nh = c->n / c->g.hs + c->n / (CH + 1) + 1;
     if ((long long)c->n / c->g.hs + 1 > HOT_NSEG_MAX) {  // segment count must fit its packing
@@ -900,7 +925,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     for (int t = 0; t < c->T; t++) c->slot_base[t + 1] = c->slot_base[t] + (uint32_t)c->slots[t];
     c->hit_total = c->row_off[c->T];
     c->XSR = std::max(4, c->F + 2);  // >= F+1: Transfer(b) waits for scatter(b-F-1) >= b-XSR
-    c->host_threads = d->host_threads > 0 ? d->host_threads : 6;
+    c->host_threads = d->host_threads > 0 ? d->host_threads : 3;
     // transfer grid: 16 one-warp CTAs (measured best on Kaggle and Terabyte;
     // 30 / 48 CTAs were 11% / 18% slower on Terabyte: more SMs add interference,
     // not host-link throughput)
@@ -1000,22 +1025,43 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_last_use, (size_t)c->S_total));
     CKC(dalloc(c, &c->d_next_need, (size_t)c->S_total));
     CKC(dalloc(c, &c->d_storage, (size_t)c->S_total * c->D));
-    // LRU log per table: capacity log_factor*S_t + 4n
+    // LRU log per table (LFU: one per use-count class, c = 0 holding the
+    // initial vacant slots; RANDOM: none): capacity log_factor*S_t + 4n
+    // (LFU classes: 2*S_t + 4n each)
     const long long lf = d->log_factor > 0 ? d->log_factor : 8;
-    std::vector<unsigned long long> lbase(c->T), lcap(c->T), lhead(c->T, 0), ltail(c->T);
+    const int NCl = std::max(1, c->log_classes);
+    std::vector<unsigned long long> lbase((size_t)c->T * NCl), lcap((size_t)c->T * NCl), lhead((size_t)c->T * NCl, 0),
+        ltail((size_t)c->T * NCl, 0);
     unsigned long long ltot = 0;
-    for (int t = 0; t < c->T; t++) {
-        lcap[t] = (unsigned long long)(lf * c->slots[t] + 4ll * c->n);
-        lbase[t] = ltot;
-        ltot += lcap[t];
-        ltail[t] = (unsigned long long)c->slots[t];  // initial vacant entries
-    }
+    for (int t = 0; t < c->T; t++)
+        for (int k = 0; k < NCl; k++) {
+            const size_t l = (size_t)t * NCl + k;
+            const long long f = c->log_classes == 0 ? 0 : (c->policy == SP_POLICY_LFU ? (k == 0 ? 0 : 2) : lf);
+            lcap[l] = (unsigned long long)(f * c->slots[t] + (k == 0 ? c->slots[t] : 0) + 4ll * c->n);
+            if (c->log_classes == 0) lcap[l] = 1;
+            lbase[l] = ltot;
+            ltot += lcap[l];
+            ltail[l] = (k == 0 && c->log_classes > 0) ? (unsigned long long)c->slots[t] : 0ull;  // initial vacant entries
+        }
     CKC(dalloc(c, &c->d_log_slot, ltot));
     CKC(dalloc(c, &c->d_log_stamp, ltot));
-    CKC(dalloc(c, &c->d_log_base, c->T));
-    CKC(dalloc(c, &c->d_log_cap, c->T));
-    CKC(dalloc(c, &c->d_log_head, c->T));
-    CKC(dalloc(c, &c->d_log_tail, c->T));
+    CKC(dalloc(c, &c->d_log_base, lbase.size()));
+    CKC(dalloc(c, &c->d_log_cap, lbase.size()));
+    CKC(dalloc(c, &c->d_log_head, lbase.size()));
+    CKC(dalloc(c, &c->d_log_tail, lbase.size()));
+    c->pin_base.assign(c->slot_base.begin() + 1, c->slot_base.end());
+    c->pinned_t.assign(c->T, false);
+    CKC(dalloc(c, &c->d_pin_base, c->T));
+    CKC(dalloc(c, &c->d_nfill, c->T));
+    CKC(cudaMemset(c->d_nfill, 0, c->T * sizeof(uint32_t)));
+    if (c->policy == SP_POLICY_RANDOM) {
+        CKC(dalloc(c, &c->d_claim, (size_t)c->S_total));
+        CKC(cudaMemset(c->d_claim, 0, (size_t)c->S_total * sizeof(unsigned long long)));
+    }
+    if (c->policy == SP_POLICY_LFU) {
+        CKC(dalloc(c, &c->d_freq, (size_t)c->S_total));
+        CKC(cudaMemset(c->d_freq, 0, (size_t)c->S_total));
+    }
     CKC(dalloc(c, &c->d_err, 1));
     CKC(dalloc(c, &c->d_cum, 4));
     CKC(dalloc(c, &c->d_miss_u, Tn));
@@ -1100,18 +1146,21 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         std::vector<int32_t> vac((size_t)c->S_total, VACANT);
         CKC(cudaMemcpy(c->d_last_use, vac.data(), vac.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
         CKC(cudaMemcpy(c->d_next_need, vac.data(), vac.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        // initial LRU log: every slot vacant, ascending slot order
-        std::vector<uint32_t> ls(ltot, 0);
-        std::vector<int32_t> lst(ltot, VACANT);
-        for (int t = 0; t < c->T; t++)
-            for (long long s = 0; s < c->slots[t]; s++) ls[lbase[t] + s] = c->slot_base[t] + (uint32_t)s;
-        CKC(cudaMemcpy(c->d_log_slot, ls.data(), ltot * sizeof(uint32_t), cudaMemcpyHostToDevice));
-        CKC(cudaMemcpy(c->d_log_stamp, lst.data(), ltot * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
-    CKC(cudaMemcpy(c->d_log_base, lbase.data(), c->T * sizeof(unsigned long long), cudaMemcpyHostToDevice));
-    CKC(cudaMemcpy(c->d_log_cap, lcap.data(), c->T * sizeof(unsigned long long), cudaMemcpyHostToDevice));
-    CKC(cudaMemcpy(c->d_log_head, lhead.data(), c->T * sizeof(unsigned long long), cudaMemcpyHostToDevice));
-    CKC(cudaMemcpy(c->d_log_tail, ltail.data(), c->T * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    // initial log (class 0): every slot vacant, ascending slot order
+    if (c->log_classes > 0) {
+        std::vector<unsigned long long> lb0(c->T);
+        for (int t = 0; t < c->T; t++) lb0[t] = lbase[(size_t)t * NCl];
+        unsigned long long *d_lb0 = nullptr;
+        CKC(dalloc(c, &d_lb0, c->T));
+        CKC(cudaMemcpy(d_lb0, lb0.data(), c->T * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+        CKC(launch_log_init(c->d_slot_base, d_lb0, c->T, c->S_total, c->d_log_slot, c->d_log_stamp, nullptr));
+    }
+    CKC(cudaMemcpy(c->d_log_base, lbase.data(), lbase.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    CKC(cudaMemcpy(c->d_log_cap, lcap.data(), lbase.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    CKC(cudaMemcpy(c->d_log_head, lhead.data(), lbase.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    CKC(cudaMemcpy(c->d_log_tail, ltail.data(), lbase.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    CKC(cudaMemcpy(c->d_pin_base, c->pin_base.data(), c->T * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CKC(cudaMemset(c->d_err, 0xFF, sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_cum, 0, 4 * sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_storage, 0, (size_t)c->S_total * c->D * sizeof(float)));
@@ -1128,8 +1177,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     return SP_OK;
 }
 
-static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
-    if (!c || !idx) return SP_ERR_INVALID_ARG;
+// csr != nullptr: a ragged batch {values, offsets} (host), expanded on the
+// GPU into the padded [T][N][L] layout of ring slot r (sp_plan_csr)
+static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device, const int64_t *const *csr = nullptr) {
+    if (!c || (!idx && !csr)) return SP_ERR_INVALID_ARG;
     if (sp_status s = check_async_error(c)) return s;
     if (c->eod) return fail(c, SP_ERR_STATE, "sp_plan after sp_end_of_data (call sp_flush first)");
     const long long j = c->pushed;
@@ -1144,7 +1195,31 @@ static sp_status plan_impl(sp_ctx *c, const void *idx, bool on_device) {
         if (sp_status s = wait_gather_slot(c, b)) return s;
     if (j >= RING) CK(cudaStreamWaitEvent(c->plan_s, c->ev_train[r], 0));  // ring slot r reused
     const void *dev_idx;
-    if (on_device) {
+    if (csr) {
+        const int64_t *vals = csr[0], *offs = csr[1];
+        const long long nbags = (long long)c->T * c->N, nnz = offs[nbags];
+        const size_t per = (size_t)c->T * c->n + (size_t)nbags + 1;
+        if (!c->h_csr) {
+            CK(cudaHostAlloc((void **)&c->h_csr, per * RING * sizeof(int64_t), cudaHostAllocDefault));
+            void *p = nullptr;
+            CK(cudaMalloc(&p, per * RING * sizeof(int64_t)));
+            c->allocs.push_back(p);
+            c->d_csr = static_cast<int64_t *>(p);
+        }
+        int64_t *hs = c->h_csr + (size_t)r * per;
+        if (c->h2d_used[r]) CK(cudaEventSynchronize(c->ev_h2d[r]));
+        std::memcpy(hs, offs, (nbags + 1) * sizeof(int64_t));
+        std::memcpy(hs + nbags + 1, vals, (size_t)nnz * sizeof(int64_t));
+        int64_t *ds = c->d_csr + (size_t)r * per;
+        const size_t bytes = ((size_t)nbags + 1 + (size_t)nnz) * sizeof(int64_t);
+        CK(cudaMemcpyAsync(ds, hs, bytes, cudaMemcpyHostToDevice, c->plan_s));
+        CK(cudaEventRecord(c->ev_h2d[r], c->plan_s));
+        c->h2d_used[r] = true;
+        c->h2d_index_bytes += (long long)bytes;
+        CK(launch_csr_pad(reinterpret_cast<const long long *>(ds + nbags + 1), reinterpret_cast<const long long *>(ds), nbags, c->L, c->d_idx[r], (c->flags & SP_FLAG_INDEX_I32) ? 1 : 0,
+                          c->plan_s));
+        dev_idx = c->d_idx[r];
+    } else if (on_device) {
         // indices produced on the caller's stream
         CK(cudaEventRecord(c->ev_user, c->compute));
         CK(cudaStreamWaitEvent(c->plan_s, c->ev_user, 0));
@@ -1186,6 +1261,58 @@ sp_status sp_plan(sp_ctx *c, const void *idx) {
 }
 
 sp_status sp_plan_device(sp_ctx *c, const void *idx) { return plan_impl(c, idx, true); }
+
+sp_status sp_plan_csr(sp_ctx *c, const int64_t *values, const int64_t *offsets) {
+    if (!c || !offsets) return SP_ERR_INVALID_ARG;
+    if (!(c->flags & SP_FLAG_PADDING)) return fail(c, SP_ERR_INVALID_ARG, "sp_plan_csr needs SP_FLAG_PADDING");
+    const long long nbags = (long long)c->T * c->N;
+    if (offsets[0] != 0) return fail(c, SP_ERR_INVALID_ARG, "sp_plan_csr: offsets[0] must be 0");
+    for (long long k = 0; k < nbags; k++) {
+        const long long len = offsets[k + 1] - offsets[k];
+        if (len < 0 || len > c->L)
+            return fail(c, SP_ERR_INVALID_ARG, "sp_plan_csr: bag " + std::to_string(k) + " has " +
+                                                   std::to_string(len) + " lookups (pooling " + std::to_string(c->L) + ")");
+    }
+    if (offsets[nbags] > 0 && !values) return SP_ERR_INVALID_ARG;
+    const int64_t *csr[2] = {values, offsets};
+    return plan_impl(c, nullptr, false, csr);
+}
+
+sp_status sp_pin_rows(sp_ctx *c, int32_t t, const int64_t *ids, int64_t count) {
+    if (!c || t < 0 || t >= c->T || count < 0 || (count > 0 && !ids)) return SP_ERR_INVALID_ARG;
+    if (sp_status s = check_async_error(c)) return s;
+    if (c->pushed != 0 || c->pinned_t[t]) return fail(c, SP_ERR_STATE, "sp_pin_rows: only once per table, before the first sp_plan");
+    if (count > c->slots[t]) return fail(c, SP_ERR_INVALID_ARG, "sp_pin_rows: more rows than slots");
+    std::vector<int64_t> sorted(ids, ids + count);
+    std::sort(sorted.begin(), sorted.end());
+    for (int64_t k = 0; k < count; k++)
+        if (sorted[k] < 0 || sorted[k] >= c->rows[t] || (k && sorted[k] == sorted[k - 1]))
+            return fail(c, SP_ERR_INVALID_ARG, "sp_pin_rows: IDs must be distinct and in range");
+    CK(cudaSetDevice(c->device));
+    const uint32_t base = c->slot_base[t + 1] - (uint32_t)count;
+    if (count) {
+        // rows -> Storage[base + k] (host gather into pinned staging, one H2D)
+        float *h = nullptr;
+        CK(cudaHostAlloc((void **)&h, (size_t)count * c->D * sizeof(float), cudaHostAllocDefault));
+        std::vector<uint32_t> slot((size_t)count), res((size_t)count);
+        for (int64_t k = 0; k < count; k++) {
+            std::memcpy(h + (size_t)k * c->D, c->host[t] + (size_t)ids[k] * c->D, (size_t)c->D * sizeof(float));
+            res[k] = (uint32_t)ids[k];
+            slot[k] = base + (uint32_t)k;
+        }
+        cudaError_t e = cudaMemcpy(c->d_storage + (size_t)base * c->D, h, (size_t)count * c->D * sizeof(float),
+                                   cudaMemcpyHostToDevice);
+        cudaFreeHost(h);
+        CK(e);
+        CK(cudaMemcpy(c->d_resident + base, res.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        for (int64_t k = 0; k < count; k++)  // Hit-Map entries (count small: one copy each is fine)
+            CK(cudaMemcpy(c->d_hitmap + c->row_off[t] + (size_t)ids[k], &slot[k], sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
+    c->pin_base[t] = base;
+    c->pinned_t[t] = true;
+    CK(cudaMemcpy(c->d_pin_base + t, &base, sizeof(uint32_t), cudaMemcpyHostToDevice));
+    return SP_OK;
+}
 
 sp_status sp_copy_batch_stats(sp_ctx *c, int64_t b, uint32_t *host_out) {
     if (!c || !host_out) return SP_ERR_INVALID_ARG;
@@ -1304,6 +1431,12 @@ sp_status sp_prefill(sp_ctx *c) {
         CK(cudaMemcpyAsync(c->d_storage + (size_t)c->slot_base[t] * c->D, c->host[t],
                            (size_t)c->rows[t] * c->D * sizeof(float), cudaMemcpyHostToDevice, c->plan_s));
     CK(launch_prefill_map(c->d_slot_base, c->d_row_off, c->T, c->S_total, c->d_resident, c->d_hitmap, c->plan_s));
+    {   // RANDOM: every dynamic slot is occupied
+        std::vector<uint32_t> nf(c->T);
+        for (int t = 0; t < c->T; t++) nf[t] = (uint32_t)c->slots[t];
+        CK(cudaMemcpyAsync(c->d_nfill, nf.data(), c->T * sizeof(uint32_t), cudaMemcpyHostToDevice, c->plan_s));
+        CK(cudaStreamSynchronize(c->plan_s));
+    }
     CK(cudaStreamSynchronize(c->plan_s));
     return SP_OK;
 }

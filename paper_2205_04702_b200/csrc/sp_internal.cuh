@@ -88,6 +88,7 @@ struct Geometry {
     int T, N, L, D;
     int n, n1, nc, nh;    // strides
     int hs;               // occurrences per hot-row segment (k_bwd: one CTA round)
+    int pad;              // SP_FLAG_PADDING: slot_of_occ may hold EMPTY (no lookup)
 };
 
 // Missed-row lists of one Plan, mirrored into pinned host memory by the plan
@@ -98,9 +99,24 @@ struct HostList {
     uint32_t *row;              // [T][n] missed row of each fill
 };
 
+// replacement policies (R23-R25)
+enum Policy : int { POL_LRU = 0, POL_RANDOM = 1, POL_LFU = 2 };
+constexpr int LFU_FMAX = 8;                 // LFU use counts saturate here (R24)
+constexpr int LOG_CLASSES_MAX = LFU_FMAX + 1;
+
 struct PushArgs {
     Geometry g;
     int P, F;
+    // policy: LRU walks one log per table; LFU one log per use-count class
+    // (log ids t*log_classes + c); RANDOM keeps no log (log_classes = 0) and
+    // draws from the occupied dynamic slots [slot_base, slot_base + nfill)
+    int policy, log_classes;
+    unsigned long long seed;            // RANDOM draw seed
+    const uint32_t *pin_base;           // [T] first pinned (static) slot of table t
+    uint32_t *nfill;                    // [T] RANDOM: dynamic slots filled so far
+    unsigned long long *claim;          // [S] RANDOM: per-slot draw claims
+    uint8_t *freq;                      // [S] LFU: use count (saturating)
+    int pad;                            // SP_FLAG_PADDING: -1 is "no lookup"
     const unsigned long long *row_off;  // [T+1]
     const long long *rows;              // [T]
     const uint32_t *slot_base;          // [T+1]
@@ -255,6 +271,10 @@ cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
 cudaError_t launch_prefill_map(const uint32_t *slot_base, const unsigned long long *row_off, int T,
                                long long S_total, uint32_t *resident, uint32_t *hitmap, cudaStream_t s);
+cudaError_t launch_log_init(const uint32_t *slot_base, const unsigned long long *log_base0, int T, long long S_total,
+                            uint32_t *log_slot, int32_t *log_stamp, cudaStream_t s);
+cudaError_t launch_csr_pad(const long long *values, const long long *offsets, long long nbags, int L, void *out,
+                           int out_i32, cudaStream_t s);
 size_t push_smem_bytes(int n);
 // shared-memory carveout (percent) requested for every kernel of the library,
 // -1 = driver default; set once at sp_create (SP_CARVEOUT) so consecutive

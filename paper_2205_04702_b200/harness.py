@@ -17,30 +17,35 @@ import torch
 def run_loop(sp, trace, gamma: float, delta: float, eta: float,
              on_plan: Optional[Callable[[int, bool], None]] = None,
              on_pooled: Optional[Callable[[int, torch.Tensor], None]] = None,
-             flush: bool = True, num_batches: Optional[int] = None):
+             flush: bool = True, num_batches: Optional[int] = None,
+             push: Optional[Callable] = None):
     """trace: indexable by batch -> [T][N][L] tensor (CPU or CUDA per the
-    context's index placement).  Returns the number of batches trained."""
+    context's index placement; or anything `push(sp, j)` understands, e.g. a
+    CSR batch list for sp_plan_csr).  Returns the number of batches trained."""
     nb = len(trace) if num_batches is None else num_batches
     ahead = sp.F + sp.P + 1
     pooled = torch.empty((sp.T, sp.N, sp.D), dtype=torch.float32, device=f"cuda:{sp.device}")
     grad = torch.empty_like(pooled)
     planned = 0
 
-    def push(j):
+    def do_push(j):
         nonlocal planned
-        sp.plan(trace[j])
+        if push is None:
+            sp.plan(trace[j])
+        else:
+            push(sp, j)
         while planned <= j - sp.F - 1:  # Plan(b) runs at push(b+F+1)
             if on_plan:  # second argument: this Plan is the newest one enqueued
                 on_plan(planned, planned == j - sp.F - 1)
             planned += 1
 
     for j in range(min(ahead, nb)):
-        push(j)
+        do_push(j)
     eod = False
     for b in range(nb):
         j = b + ahead
         if j < nb:
-            push(j)
+            do_push(j)
         elif not eod:
             sp.end_of_data()
             eod = True

@@ -52,10 +52,13 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
                gde=(0.5, 0.01, 0.01), index_dtype="int64", index_on_device=False, log_factor=0,
                check_plans=True, check_slots=True, check_pooled=True, trace=None,
                register_host=False, profile=False, sample_rows=None, host_alloc=False,
-               tables=None, policy_kw=None):
+               tables=None, policy_kw=None, padding=False, pinned=None, push=None):
     """tables: pre-allocated host tables (HostTable or pinned tensors), already
     holding init(init_seed) values; policy_kw: extra ScratchPipe / Policy
-    arguments of a replacement-policy variant (policy, policy_seed)."""
+    arguments of a replacement-policy variant (policy, policy_seed); padding:
+    -1 entries are "no lookup" on both sides; pinned: per table, rows pinned
+    in the last slots (sp_pin_rows / the oracle's static partition); push:
+    optional push(sp, j) replacing sp.plan(trace[j]) (e.g. sp_plan_csr)."""
     g, d, e = gde
     if trace is None:
         trace = sample_trace(rows, N, L, alpha, nb, trace_seed)
@@ -69,9 +72,14 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
     pkw = dict(policy_kw or {})
     sp = ScratchPipe(rows, tables, D, slots, N, L, past=P, future=F, index_dtype=index_dtype,
                      index_on_device=index_on_device, log_factor=log_factor,
-                     register_host=register_host, profile=profile, **pkw)
-    pol = Policy(rows, slots, P, F, **pkw) if (check_plans or check_slots) else None
-    orc = UncachedTrainer(rows, D, N, L, init_seed)
+                     register_host=register_host, profile=profile, padding=padding, **pkw)
+    if pinned is not None:
+        for t, ids in enumerate(pinned):
+            if ids is not None and len(ids):
+                sp.pin_rows(t, ids)
+    pol = Policy(rows, slots, P, F, allow_padding=padding, pinned=pinned, **pkw) \
+        if (check_plans or check_slots) else None
+    orc = UncachedTrainer(rows, D, N, L, init_seed, allow_padding=padding)
     report = {"plans": 0, "evictions": 0, "pooled": 0}
 
     def on_plan(b, newest=True):
@@ -103,7 +111,7 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
             assert np.array_equal(got, want), (b, float(np.max(np.abs(got - want))))
             report["pooled"] += 1
 
-    run_loop(sp, feed, g, d, e, on_plan=on_plan, on_pooled=on_pooled)
+    run_loop(sp, feed, g, d, e, on_plan=on_plan, on_pooled=on_pooled, push=push)
     # final host tables after sp_flush vs the oracle's uncached training
     worst = {"max_rel": 0.0, "mismatch": 0, "rel_to_update": 0.0, "rows": 0}
     for t, R in enumerate(rows):

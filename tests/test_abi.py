@@ -36,7 +36,8 @@ def test_status_codes_match_header():
 def test_desc_struct_layout():
     # offsets of the C struct under the x86-64 SysV ABI
     assert B.SpDesc.rows.offset == 8 and B.SpDesc.host_tables.offset == 16
-    assert B.SpDesc.stream.offset == 64 and ctypes.sizeof(B.SpDesc) == 88
+    assert B.SpDesc.stream.offset == 64 and B.SpDesc.policy.offset == 84
+    assert B.SpDesc.policy_seed.offset == 96 and ctypes.sizeof(B.SpDesc) == 104
 
 
 def test_invalid_descriptors_rejected_before_touching_a_device():
@@ -49,7 +50,7 @@ def test_invalid_descriptors_rejected_before_touching_a_device():
                 future=-1, batch_size=4, pooling=2, device=0, stream=None, flags=0, log_factor=0,
                 host_threads=0, reserved=0)
     for bad in [dict(dim=6), dict(dim=0), dict(num_tables=0), dict(batch_size=0),
-                dict(past=1, future=3)]:
+                dict(past=1, future=3), dict(policy=3), dict(policy=-1), dict(reserved=1)]:
         d = B.SpDesc(**{**base, **bad})
         assert sp.lib.sp_create(ctypes.byref(d), ctypes.byref(h)) == sp.SP_ERR_INVALID_ARG, bad
     slots[0] = 101  # more slots than rows

@@ -20,16 +20,29 @@ def _k(**us):
     return {k: {"avg_us": v} for k, v in us.items()}
 
 
-def test_overlap_efficiency_bounds(bench):
-    k = _k(plan=30.0, transfer=40.0, forward=10.0, surrogate=10.0, backward=20.0)
-    # fully overlapped: the step costs the slowest stream (compute, 40 = transfer)
-    assert bench._overlap(k, 40.0)["efficiency"] == 1.0
-    # back to back: the step costs the sum of the streams
-    full = bench._overlap(k, 110.0)
-    assert full["efficiency"] == 0.0 and full["serial_sum_us"] == 110.0
-    half = bench._overlap(k, 75.0)
-    assert half["efficiency"] == 0.5
-    assert half["stream_us"] == {"plan": 30.0, "transfer": 40.0, "compute": 40.0}
+def test_union_of_stage_intervals(bench):
+    # overlapping intervals count once; disjoint ones add
+    assert bench._union_us([(0.0, 0.010), (0.005, 0.020), (0.030, 0.040)]) == pytest.approx(30.0)
+    assert bench._union_us([]) == 0.0
+
+
+def test_stream_busy_and_overlap_verdict(bench):
+    import numpy as np
+    ev = np.full((16, 8), np.nan)
+    # 4 steps of 100 us: plan 0-30, compute 40-100 (fwd 40-60, surr 60-70, bwd 70-100),
+    # transfers of 50 us each (disjoint here: the union is their sum)
+    for r in range(4):
+        t0 = r * 0.1
+        ev[r, :6] = [t0, t0 + 0.03, t0 + 0.04, t0 + 0.06, t0 + 0.07, t0 + 0.1]
+        ev[r, 6:8] = [t0 + 0.02, t0 + 0.07]
+    busy = bench._stream_busy(ev)
+    assert busy["plan"] == pytest.approx(30.0) and busy["compute"] == pytest.approx(60.0)
+    assert busy["transfer"] == pytest.approx(50.0) and busy["steps"] == 4
+    ov = bench._overlap({}, 62.0, busy)
+    assert ov["busiest_stream"] == "compute" and ov["full_overlap"] is True
+    assert ov["step_over_busiest"] == pytest.approx(62.0 / 60.0, rel=1e-3)
+    assert bench._overlap({}, 100.0, busy)["full_overlap"] is False
+    assert bench._overlap({}, 62.0, None) is None
 
 
 def test_plan_roles_window_means_and_percentiles(bench):
