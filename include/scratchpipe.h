@@ -51,6 +51,9 @@
  *                         their random host rows itself; 1: CPU threads gather
  *                         them into a contiguous pinned slot first (default:
  *                         1 when T*N*L*dim*4 <= 32 MB, i.e. few rows per batch)
+ *   SP_WRITEBACK=gpu|cpu  victims' write-back: gpu = the transfer kernel stores
+ *                         each victim row straight into its host row (TMA bulk
+ *                         store); cpu = staged contiguously, CPU threads scatter
  *   SP_GATHER_DMA=1       with the CPU gather, copy the gathered slot to HBM by
  *                         copy-engine DMA before the transfer kernel (default 0)
  *   SP_PULL_CTAS=n        transfer-kernel grid (one-warp CTAs, default 16)
@@ -177,9 +180,14 @@ typedef struct {
     int32_t transfer_mode;          /* how missed rows reach HBM: SP_XFER_*        */
     int32_t engine_threads;         /* CPU threads of the transfer engine (workers */
                                     /* + row-copy helpers)                          */
+    int32_t gpu_writeback;          /* 1: k_pullfill writes victims straight into  */
+                                    /* their host rows (SP_WRITEBACK=gpu)           */
+    int32_t reserved_stats;
 } sp_stats;
 
-/* sp_stats.transfer_mode */
+/* sp_stats.transfer_mode (missed rows in); victims out: CPU scatter from
+ * pinned staging, or with sp_stats.gpu_writeback TMA bulk stores from the
+ * transfer kernel straight into the host rows */
 #define SP_XFER_GPU_PULL   0  /* k_pullfill reads each missed row from its host row */
 #define SP_XFER_CPU_GATHER 1  /* CPU threads gather into a contiguous pinned slot   */
 #define SP_XFER_GATHER_DMA 2  /* CPU gather, then copy-engine DMA of the slot       */

@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
     __shared__ __align__(8) uint64_t bar[XS];
     __shared__ uint32_t s_pref[65];
     __shared__ uint32_t s_slot[XS][32], s_stage[XS][32];
+    __shared__ unsigned long long s_dst[XS][32];  // direct write-back: host row of each victim
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
     const uint32_t rowb = (uint32_t)g.D * 4u;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
         auto vbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + i) * rowb; };
         auto nbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + nb + i) * rowb; };
         const bool gathered = A.in_stage != nullptr && !A.diag_nowb;
+        const bool direct = A.wb_direct != 0;  // victims straight to their host rows
         auto issue = [&](uint32_t r) {
             const int s = (int)((phase_ctr + r) % XS);
             const uint32_t k0 = lo + r * nb;
@@ -134,10 +136,13 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 src_host = A.in_stage ? A.in_stage + (size_t)(base_t0 + item) * g.D  // CPU-gathered, contiguous
                                       : A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
                 const uint32_t old = A.bb.evict_row[kk];
-                if (old != EMPTY && !A.diag_nowb) stage = base_t0 + item;
+                if (old != EMPTY && !A.diag_nowb) stage = direct ? (uint32_t)t : base_t0 + item;
                 // the scatter thread's work list: where the staged row goes
-                A.wb_dst[base_t0 + item] =
+                // (direct: the kernel itself stores the row there)
+                const unsigned long long dst =
                     old != EMPTY ? (unsigned long long)(uintptr_t)(A.host[t] + (size_t)old * g.D) : 0ull;
+                if (direct) s_dst[s][lane] = dst;
+                else A.wb_dst[base_t0 + item] = dst;
                 bytes = rowb * (stage != EMPTY ? 2u : 1u);
             }
             s_slot[s][lane] = slot;
@@ -164,7 +169,11 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
             const int s = (int)((phase_ctr + r) % XS);
             mbar_wait(&bar[s], ((phase_ctr + r) / XS) & 1u);
             const uint32_t slot = s_slot[s][lane], stage = s_stage[s][lane];
-            if (gathered) {
+            if (direct) {
+                // victims: one bulk store per row into its host row
+                if (slot != EMPTY && stage != EMPTY)
+                    bulk_s2g(reinterpret_cast<void *>((uintptr_t)s_dst[s][lane]), vbuf(s, lane), rowb);
+            } else if (gathered) {
                 // victims: one contiguous bulk store of the round's staging rows
                 // (rows of fills without a victim carry garbage; their work-list
                 // entry is 0, so the scatter skips them)

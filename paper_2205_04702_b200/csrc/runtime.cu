@@ -208,6 +208,10 @@ struct sp_ctx {
     unsigned long long *h_scnt = nullptr;      // pinned mapped [RING]: staged items of the batch
     unsigned long long *hd_scnt = nullptr;     // device alias
     uint32_t *d_xdone = nullptr;               // [RING] k_pullfill CTA arrival counters
+    // GPU write-back (SP_WRITEBACK=gpu): k_pullfill stores each victim row
+    // straight into its host row (TMA bulk store over the link); no staging,
+    // no scatter thread; RAW-4 is then an event wait on Transfer(b-F-1)
+    bool gpu_wb = false;
     unsigned long long *h_scat = nullptr;      // pinned mapped: batches scattered
     unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
     int pull_ctas = 16;  // k_pullfill grid (one warp per CTA); SP_PULL_CTAS overrides
@@ -638,7 +642,12 @@ void gather_main(sp_ctx *c) {
         for (int t = 0; t < c->T; t++)
             if (((volatile unsigned long long *)c->hl_ready)[(size_t)r * c->T + t] != (unsigned long long)(b + 1))
                 return false;
-        if (c->x_scattered.load(std::memory_order_acquire) < b - c->F) return false;
+        if (c->gpu_wb) {  // the write-backs of Transfer(b-F-1) have landed
+            const long long w = b - c->F - 1;
+            if (w >= 0 && ((volatile unsigned long long *)c->h_staged)[w % RING] < (unsigned long long)(w + 1)) return false;
+        } else if (c->x_scattered.load(std::memory_order_acquire) < b - c->F) {
+            return false;
+        }
         const long long prev = b - c->XSR;
         if (prev >= 0 && ((volatile unsigned long long *)c->h_staged)[prev % RING] < (unsigned long long)(prev + 1))
             return false;
@@ -732,7 +741,10 @@ sp_status pump(sp_ctx *c) {
         if (dep >= 0) CK(cudaStreamWaitEvent(xs, c->ev_train[dep % RING], 0));
         // RAW-4 + staging reuse: the CPU write-back of batch b-F-1 has landed
         const long long need = b - c->F;  // scattered >= b-F
-        if (need > 0) {
+        if (c->gpu_wb) {
+            // the GPU wrote the victims of Transfer(b-F-1) into their host rows
+            if (need > 0) CK(cudaStreamWaitEvent(xs, c->ev_xfer[(need - 1) % RING], 0));
+        } else if (need > 0) {
             wait_value64_fn wv = wait_value64();
             if (!wv) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 unavailable");
             CUresult cr = wv((CUstream)xs, (CUdeviceptr)c->d_scat, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ);
@@ -767,6 +779,7 @@ sp_status pump(sp_ctx *c) {
         a.staged = c->hd_staged + r;
         a.wb_dst = c->hd_wbdst + (size_t)(b % c->XSR) * c->T * c->n;
         a.staged_cnt = c->hd_scnt + r;
+        a.wb_direct = c->gpu_wb ? 1 : 0;
         a.b = b;
         if (c->diag & 1) a.g.T = 0;  // diagnostic: transfer launched, no rows moved
         if (c->diag & 4) a.diag_nowb = 1;  // diagnostic: victims not staged (pull only)
@@ -1105,6 +1118,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     // 54 it/s), where the CPU copy threads become the bound
     c->cpu_gather = (double)c->T * c->n * c->D * sizeof(float) <= 32.0 * (1 << 20);
     if (const char *e = getenv("SP_CPU_GATHER")) c->cpu_gather = atoi(e) != 0;
+    if (const char *e = getenv("SP_WRITEBACK")) c->gpu_wb = std::string(e) == "gpu";
     if (c->cpu_gather) {
         CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
         CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
@@ -1167,8 +1181,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaDeviceSynchronize());
 #undef CKC
     // transfer engine: helpers + worker
-    c->spool.start(c->host_threads);
-    c->scatter_worker = std::thread(scatter_main, c);
+    if (!c->gpu_wb) {
+        c->spool.start(c->host_threads);
+        c->scatter_worker = std::thread(scatter_main, c);
+    }
     if (c->cpu_gather) {
         c->gpool.start(c->host_threads);
         c->gather_worker = std::thread(gather_main, c);
@@ -1448,7 +1464,7 @@ sp_status sp_flush(sp_ctx *c) {
         return fail(c, SP_ERR_STATE, "sp_flush: every pushed batch must be trained first");
     CK(cudaSetDevice(c->device));
     // the transfer engine writes back every victim of every batch
-    if (sp_status s = wait_engine(c, [&] { return c->x_scattered.load(std::memory_order_acquire) >= c->planned; }))
+    if (sp_status s = wait_engine(c, [&] { return c->gpu_wb || c->x_scattered.load(std::memory_order_acquire) >= c->planned; }))
         return s;
     CK(cudaStreamSynchronize(c->plan_s));
     CK(cudaStreamSynchronize(c->xfer_s));
@@ -1681,7 +1697,8 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->graph_steps = c->graph_steps;
     o->graph_step_host_ms = c->graph_step_ns * 1e-6;
     o->transfer_mode = c->cpu_gather ? (c->gather_dma ? SP_XFER_GATHER_DMA : SP_XFER_CPU_GATHER) : SP_XFER_GPU_PULL;
-    o->engine_threads = 1 + c->host_threads + (c->cpu_gather ? 1 + c->host_threads : 0);
+    o->engine_threads = (c->gpu_wb ? 0 : 1 + c->host_threads) + (c->cpu_gather ? 1 + c->host_threads : 0);
+    o->gpu_writeback = c->gpu_wb ? 1 : 0;
     if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);
         cudaStreamSynchronize(c->xfer_s2);

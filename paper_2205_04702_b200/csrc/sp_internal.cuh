@@ -175,6 +175,7 @@ struct XferArgs {
     unsigned long long *wb_dst;  // [sum m] host address of each staged victim's row (0: none)
     unsigned long long *staged_cnt;  // pinned: sum m of this batch (written before `staged`)
     int diag_nowb;                // timing diagnostic: skip the victims' staging stores
+    int wb_direct;                // victims go straight to their host rows (no staging)
     const float *in_dev;          // device copy of the first in_dev_rows rows of in_stage
     uint32_t in_dev_rows;         //   (copy-engine DMA), or nullptr / 0
     const float *in_stage;        // [sum m][D] missed rows gathered by the CPU into pinned

@@ -364,7 +364,10 @@ def test_prefill_all_resident_no_misses_matches_oracle():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"SP_CPU_GATHER": "0"}, {"SP_CPU_GATHER": "1"},
-                                 {"SP_CPU_GATHER": "1", "SP_GATHER_DMA": "1"}])
+                                 {"SP_CPU_GATHER": "1", "SP_GATHER_DMA": "1"},
+                                 {"SP_CPU_GATHER": "0", "SP_WRITEBACK": "gpu"},
+                                 {"SP_CPU_GATHER": "1", "SP_WRITEBACK": "gpu"},
+                                 {"SP_CPU_GATHER": "0", "SP_WRITEBACK": "cpu"}])
 def test_transfer_modes_match_oracle(env, monkeypatch):
     """Every transfer mode (GPU pull of random host rows, CPU gather into a
     pinned slot, CPU gather + copy-engine DMA) gives the oracle's plans,
@@ -377,4 +380,5 @@ def test_transfer_modes_match_oracle(env, monkeypatch):
     slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 4) for t, R in enumerate(rows)]
     rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr, gde=(0.5, 0.01, 0.05))
     assert rep["evictions"] > 200
+    assert rep["stats"]["gpu_writeback"] == (env.get("SP_WRITEBACK") == "gpu")
     _assert_tables(rep)
