@@ -46,11 +46,22 @@ def parse():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="terabyte")
-    ap.add_argument("--variant", default="pipelined", choices=["pipelined", "serial", "resident", "gpuonly"],
+    ap.add_argument("--policy", default="lru", choices=["lru", "random", "lfu"],
+                    help="replacement policy among the window-safe candidates (P:1270-1278)")
+    ap.add_argument("--policy-seed", type=int, default=2205)
+    ap.add_argument("--dim", type=int, default=0, help="sensitivity sweep: override D (P:1248-1258)")
+    ap.add_argument("--pooling", type=int, default=0, help="sensitivity sweep: override L (P:1259-1268)")
+    ap.add_argument("--batch", type=int, default=0, help="sensitivity sweep: override N")
+    ap.add_argument("--slot-frac", type=float, default=0.0, help="sensitivity sweep: slots as a fraction of rows")
+    ap.add_argument("--writeback", default="", choices=["", "gpu", "cpu"],
+                    help="victims' write-back: GPU bulk stores into host rows, or CPU scatter (default: library's)")
+    ap.add_argument("--variant", default="pipelined", choices=["pipelined", "serial", "resident", "gpuonly", "static"],
                     help="design points of PAPER.md Fig. 10 / Table 1 from the same kernels: "
                          "pipelined (ScratchPipe), serial (straw-man: every stage on one stream, "
                          "no overlap), resident (slots = rows, cold start), gpuonly (slots = rows "
-                         "and every row loaded before the first batch: no misses at all)")
+                         "and every row loaded before the first batch: no misses at all), static (the "
+                         "paper's static top-N cache from the same kernels: the hottest rows of a profiling "
+                         "prefix pinned in the slot budget, a window-sized scratchpad for the rest)")
     ap.add_argument("--preroll", type=int, default=-1, help="untimed steady-state fill batches (-1: config)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -355,6 +366,13 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
+    over = {k: v for k, v in (("dim", args.dim), ("pooling", args.pooling), ("batch", args.batch)) if v}
+    if args.slot_frac:
+        over.update(slot_frac=args.slot_frac, slots_fixed=None)
+    if over:
+        cfg = cfg.with_(**over)
+    if args.writeback:
+        os.environ["SP_WRITEBACK"] = args.writeback
     if args.variant in ("resident", "gpuonly"):
         cfg = cfg.with_(slot_frac=1.0, slots_fixed=None)
     if args.variant == "serial":
@@ -397,7 +415,20 @@ def run_ours(args):
 
     stream = torch.cuda.current_stream(dev)
     sp = ScratchPipe(rows, tables, D, slots, N, L, window=cfg.window, device=local, stream=stream,
-                     index_dtype="int32", index_on_device=False)
+                     index_dtype="int32", index_on_device=False, policy=args.policy,
+                     policy_seed=args.policy_seed)
+    pinned_rows = 0
+    if args.variant == "static":
+        # static top-N partition: the hottest rows of the first 200 batches of
+        # the trace fill the slot budget except a window-sized scratchpad
+        # (2w*N*L slots: the minimum the look-forward window needs)
+        prof = trace[:min(200, nb)]
+        for k, t in enumerate(mine):
+            pool = min(slots[k], 2 * cfg.window * N * L)
+            ids, cnt = torch.unique(prof[:, k].reshape(-1), return_counts=True)
+            top = ids[torch.argsort(cnt, descending=True, stable=True)[:slots[k] - pool]]
+            sp.pin_rows(k, top.cpu().numpy())
+            pinned_rows += int(top.numel())
     if args.variant == "gpuonly":
         sp.prefill()
     pooled = torch.empty((len(mine), N, D), dtype=torch.float32, device=dev)
@@ -634,7 +665,8 @@ def run_ours(args):
                          "%.1f GB); every step reads a fresh batch" % (
                              sum(slots_all) * D * 4 / 1e9, sum(cfg.rows) * 4 / 1e6, sum(cfg.rows) * D * 4 / 1e9),
                    "parallelism": f"table-wise x{world}" if world > 1 else "single GPU",
-                   "variant": args.variant},
+                   "variant": args.variant, "policy": args.policy,
+                   **({"pinned_rows": pinned_rows} if args.variant == "static" else {})},
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},

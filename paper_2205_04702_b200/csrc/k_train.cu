@@ -166,54 +166,66 @@ __device__ __forceinline__ float4 sgd(const float4 &w, const Acc4 &a, float lr) 
     return r;
 }
 
-// One launch, two kinds of work item (lists built at dedup, slots at Plan):
-//  H  a hot row (> CH occurrences, the Zipf head): one CTA.  Lane group gi
-//     folds occurrences gi, gi+gpb, gi+2gpb, ... of the row (ascending) in
-//     fp64, RB gradient rows in flight; a fixed binary tree over the groups in
-//     shared memory gives the row sum; group 0 applies the SGD update.  No
-//     partials leave the CTA and no second pass runs; the fold shape depends
-//     only on the occurrence count (deterministic, grid-independent).
-//  N  a chunk record (<= CH occurrences, bag indices inline): one lane group,
-//     one record load, then its gradient rows, the Storage row prefetched
-//     beside them, update in the epilogue.  Groups take records dynamically
-//     (one atomic per CTA per round), so CTAs that folded hot rows take fewer.
-// One owner per unique row: no atomics on Storage.
+__device__ __forceinline__ float4 sgd32(const float4 &w, const float4 &g, float lr) {
+    return make_float4(fmaf(-lr, g.x, w.x), fmaf(-lr, g.y, w.y), fmaf(-lr, g.z, w.z), fmaf(-lr, g.w, w.w));
+}
+
+__device__ __forceinline__ double4 ldcg_d4(const double4 *p) {  // L2 (written by other SMs)
+    const double2 lo = __ldcg(reinterpret_cast<const double2 *>(p));
+    const double2 hi = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
+    return make_double4(lo.x, lo.y, hi.x, hi.y);
+}
+
+__device__ __forceinline__ double4 shfl_xor_d4(const double4 &v, int m) {
+    return make_double4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                        __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+
+// Warp-centric: every work item belongs to one warp (hot-row segment) or one
+// lane group of G lanes (chunk records), so there is no block barrier after
+// the prologue and every warp keeps several rows in flight.
+//  H  hot-row segment (<= hs occurrences of a Zipf-head row): the warp's NG
+//     lane groups take occurrences g, g+NG, ... (RB rows in flight each) and
+//     accumulate in fp64; a fixed xor tree over the groups gives the segment
+//     sum.  A single-segment row is updated at once; otherwise the segment
+//     writes an fp64 partial and the last segment to arrive (counter per row)
+//     folds the partials in segment order and applies SGD.  Every fold order
+//     depends only on the row's occurrence count.
+//  N  chunk records (<= CH occurrences, bag ids inline): BU records per lane
+//     group at once -- headers, Storage rows and the gradient rows of their
+//     first two occurrences all in flight together.  A record of <= 2
+//     occurrences is summed in fp32, which equals the fp32 rounding of the
+//     exact (fp64) sum (reading R7: two fp32 values sum exactly in fp64, or
+//     the smaller is below half an ulp of the larger); longer ones continue
+//     in fp64 in ascending occurrence order.  One owner per unique row: no
+//     atomics on Storage.
 template <int G, int VPL>
-__global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
+__global__ void __launch_bounds__(256, 2) k_bwd(TrainArgs A) {
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
     const int D4 = g.D / 4;
-    __shared__ uint32_t s_pref[65];
-    __shared__ uint32_t s_base;
-    __shared__ double4 s_red[256];
-    const int gpb = blockDim.x / G;
-    const int gi = threadIdx.x / G;
+    constexpr int NG = 32 / G;                                 // lane groups per warp
+    constexpr int RB = VPL >= 4 ? 1 : (VPL == 2 ? 4 : 8);      // hot rows in flight per group
+    constexpr int BU = VPL >= 2 ? 1 : 2;                       // chunk records per group at once
+    __shared__ uint32_t s_ph[65], s_pc[65];
     const int lane = threadIdx.x % G;
+    const int grp = (threadIdx.x & 31) / G;
+    const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const long long W = (long long)gridDim.x * (blockDim.x / 32);
     const float4 *grad = reinterpret_cast<const float4 *>(A.grad);
     float4 *st = reinterpret_cast<float4 *>(A.storage);
-    constexpr int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);   // hot rows: gradient rows in flight per group
-    constexpr int RBN = VPL >= 4 ? 1 : (VPL == 2 ? 2 : 4);  // chunk records (mostly 1-2 occurrences)
-    // ---- H: hot-row segments, one CTA each (RB rows per group: one round)
-    __shared__ uint32_t s_last;
-    __shared__ uint32_t s_pref_n[65];  // chunk-record prefix, computed up front when T <= 64
     const bool one_group = g.T <= 64;
-    if (one_group) table_prefix2(A.bb.nhot, A.bb.nchunks, 0, g.T, s_pref, s_pref_n);
+    if (one_group) table_prefix2(A.bb.nhot, A.bb.nchunks, 0, g.T, s_ph, s_pc);
     griddep_wait();  // (PDL) the surrogate's gradients are complete from here on
-    if (A.diag & 8) {  // timing diagnostic: no hot segments
-        __syncthreads();
-        if (threadIdx.x <= 64) s_pref[threadIdx.x] = 0;
-        __syncthreads();
-    }
-    uint32_t htot = 0;  // hot segments over all tables: CTAs [0, htot) start with one
     for (int t0 = 0; t0 < g.T; t0 += 64) {
         const int tcount = min(64, g.T - t0);
-        if (!one_group) table_prefix(A.bb.nhot, t0, tcount, s_pref);
-        const uint32_t total = s_pref[tcount];
-        htot += total;
-        for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-            const int tl = find_table(s_pref, tcount, item);
+        if (!one_group) table_prefix2(A.bb.nhot, A.bb.nchunks, t0, tcount, s_ph, s_pc);
+        const uint32_t Ht = (A.diag & 8) ? 0u : s_ph[tcount], Ct = (A.diag & 16) ? 0u : s_pc[tcount];
+        // ---- H: one warp per hot-row segment
+        for (long long item = gw; item < Ht; item += W) {
+            const int tl = find_table(s_ph, tcount, (uint32_t)item);
             const int t = t0 + tl;
-            const uint32_t h = item - s_pref[tl];
+            const uint32_t h = (uint32_t)item - s_ph[tl];
             const uint4 hr = A.bb.hot_rec[(size_t)t * g.nh + h];
             const uint32_t slot = hr.x, lo = hr.y, len = hr.z & HOT_LEN_MASK, k = hr.w, nseg = hr.z >> HOT_LEN_BITS;
             const uint32_t *occ = A.bb.sorted_occ + (size_t)t * g.n + lo;
@@ -221,185 +233,162 @@ __global__ void __launch_bounds__(256, (VPL >= 4 ? 2 : 4)) k_bwd(TrainArgs A) {
             Acc4 acc[VPL];
 #pragma unroll
             for (int v = 0; v < VPL; v++) acc[v] = Acc4{0.0, 0.0, 0.0, 0.0};
-            for (uint32_t k0 = gi; k0 < len; k0 += (uint32_t)gpb * RB) {
+            for (uint32_t k0 = grp; k0 < len; k0 += NG * RB) {
                 float4 r[RB][VPL];
 #pragma unroll
                 for (int q = 0; q < RB; q++) {
-                    const uint32_t kq = k0 + (uint32_t)q * gpb;
+                    const uint32_t kq = k0 + (uint32_t)q * NG;
                     if (kq < len) {
                         const uint32_t bag = __ldg(occ + kq) / (uint32_t)g.L;
 #pragma unroll
-                        for (int v = 0; v < VPL; v++) r[q][v] = ldg4(gb + (size_t)bag * D4 + v * G);
+                        for (int v = 0; v < VPL; v++) r[q][v] = __ldg(gb + (size_t)bag * D4 + v * G);
                     }
                 }
 #pragma unroll
                 for (int q = 0; q < RB; q++)
-                    if (k0 + (uint32_t)q * gpb < len)
+                    if (k0 + (uint32_t)q * NG < len)
 #pragma unroll
                         for (int v = 0; v < VPL; v++) acc_add(acc[v], r[q][v]);
             }
-            // fixed tree over the groups, one float4 column block at a time;
-            // group 0 ends with the segment sum
-            double4 *part = reinterpret_cast<double4 *>(A.partial + ((size_t)t * g.nh + h) * g.D) + lane;
+            // fixed xor tree over the warp's lane groups: every group ends
+            // with the segment sum (order fixed by NG only)
 #pragma unroll
             for (int v = 0; v < VPL; v++) {
-                __syncthreads();
-                s_red[threadIdx.x] = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
-                __syncthreads();
-                for (int hh = 1; hh < gpb; hh <<= 1) {
-                    if ((gi % (2 * hh)) == 0 && gi + hh < gpb) {
-                        const double4 o = s_red[threadIdx.x + hh * G];
-                        double4 &m = s_red[threadIdx.x];
-                        m.x += o.x; m.y += o.y; m.z += o.z; m.w += o.w;
-                    }
-                    __syncthreads();
+                double4 m = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
+#pragma unroll
+                for (int o = G; o < 32; o <<= 1) {
+                    const double4 p = shfl_xor_d4(m, o);
+                    m.x += p.x; m.y += p.y; m.z += p.z; m.w += p.w;
                 }
-                if (gi == 0) {
-                    const double4 m = s_red[lane];
-                    if (nseg == 1) {
+                acc[v] = Acc4{m.x, m.y, m.z, m.w};
+            }
+            if (nseg == 1) {
+                if (grp == 0)
+#pragma unroll
+                    for (int v = 0; v < VPL; v++) {
                         float4 *wp = st + (size_t)slot * D4 + lane + v * G;
-                        *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
-                    } else {
-                        part[v * G] = m;
+                        *wp = sgd(*wp, acc[v], A.lr);
                     }
-                }
+                continue;
             }
-            if (nseg > 1) {  // the last segment to arrive folds the row's partials in k order
-                __threadfence();
-                __syncthreads();
-                if (threadIdx.x == 0) s_last = atomicAdd(&A.bb.hot_cnt[(size_t)t * g.nh + (h - k)], 1u) == nseg - 1;
-                __syncthreads();
-                if (s_last) {
-                    // fold the nseg partials: PL lanes per column each sum the
-                    // partials kk = p, p+PL, ... in order, then a fixed tree
-                    // over the lanes (shape depends on nseg only)
-                    __threadfence();
-                    const double2 *p0 = reinterpret_cast<const double2 *>(A.partial + ((size_t)t * g.nh + (h - k)) * g.D);
-                    const int PL = D4 >= 256 ? 1 : 256 / D4;
-                    for (int col0 = 0; col0 < D4; col0 += 256) {
-                        const int col = col0 + (int)threadIdx.x % (D4 < 256 ? D4 : 256);
-                        const int p = (int)threadIdx.x / (D4 < 256 ? D4 : 256);
-                        double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
-                        if (p < PL && col < D4) {
-                            uint32_t kk = (uint32_t)p;
-                            for (; kk + 3u * PL < nseg; kk += 4u * PL) {  // 4 partials in flight
-                                double2 lo[4], hi[4];
+            double4 *part = reinterpret_cast<double4 *>(A.partial + ((size_t)t * g.nh + h) * g.D) + lane;
+            if (grp == 0)
 #pragma unroll
-                                for (int q = 0; q < 4; q++) {
-                                    // L2 loads (__ldcg): the partials were written by other SMs
-                                    lo[q] = __ldcg(p0 + (size_t)(kk + q * PL) * 2 * D4 + 2 * col);
-                                    hi[q] = __ldcg(p0 + (size_t)(kk + q * PL) * 2 * D4 + 2 * col + 1);
-                                }
+                for (int v = 0; v < VPL; v++) part[v * G] = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
+            __threadfence();
+            __syncwarp();
+            uint32_t last = 0;
+            if ((threadIdx.x & 31) == 0) last = atomicAdd(&A.bb.hot_cnt[(size_t)t * g.nh + (h - k)], 1u) == nseg - 1;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (!last) continue;
+            // the last segment folds the row's nseg partials in segment order:
+            // lane l of the warp owns float4 columns l, l+32, ... (4 in flight)
+            __threadfence();
+            const double4 *p0 = reinterpret_cast<const double4 *>(A.partial + ((size_t)t * g.nh + (h - k)) * g.D);
+            for (int col = threadIdx.x & 31; col < D4; col += 32) {
+                double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
+                uint32_t kk = 0;
+                for (; kk + 4 <= nseg; kk += 4) {
+                    double4 q[4];
 #pragma unroll
-                                for (int q = 0; q < 4; q++) { m.x += lo[q].x; m.y += lo[q].y; m.z += hi[q].x; m.w += hi[q].y; }
-                            }
-                            for (; kk < nseg; kk += PL) {
-                                const double2 lo2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col);
-                                const double2 hi2 = __ldcg(p0 + (size_t)kk * 2 * D4 + 2 * col + 1);
-                                m.x += lo2.x; m.y += lo2.y; m.z += hi2.x; m.w += hi2.y;
-                            }
-                        }
-                        __syncthreads();
-                        s_red[threadIdx.x] = m;
-                        __syncthreads();
-                        const int W = D4 < 256 ? D4 : 256;
-                        for (int hh = 1; hh < PL; hh <<= 1) {
-                            if (p < PL && (p % (2 * hh)) == 0 && p + hh < PL) {
-                                const double4 o = s_red[threadIdx.x + hh * W];
-                                double4 &mm = s_red[threadIdx.x];
-                                mm.x += o.x; mm.y += o.y; mm.z += o.z; mm.w += o.w;
-                            }
-                            __syncthreads();
-                        }
-                        if (p == 0 && col < D4) {
-                            const double4 f = s_red[threadIdx.x];
-                            float4 *wp = st + (size_t)slot * D4 + col;
-                            *wp = sgd(*wp, Acc4{f.x, f.y, f.z, f.w}, A.lr);
-                        }
-                    }
+                    for (int u = 0; u < 4; u++) q[u] = ldcg_d4(p0 + (size_t)(kk + u) * D4 + col);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) { m.x += q[u].x; m.y += q[u].y; m.z += q[u].z; m.w += q[u].w; }
                 }
+                for (; kk < nseg; kk++) {
+                    const double4 q = ldcg_d4(p0 + (size_t)kk * D4 + col);
+                    m.x += q.x; m.y += q.y; m.z += q.z; m.w += q.w;
+                }
+                float4 *wp = st + (size_t)slot * D4 + col;
+                *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
             }
         }
-    }
-    // ---- N: single-chunk rows, taken dynamically one record per group
-    for (int t0 = 0; t0 < g.T; t0 += 64) {
-        const int tcount = min(64, g.T - t0);
-        if (one_group) {
-            __syncthreads();
-            if (threadIdx.x < 65) s_pref[threadIdx.x] = s_pref_n[threadIdx.x];
-            __syncthreads();
-        } else {
-            table_prefix(A.bb.nchunks, t0, tcount, s_pref);
-        }
-        const uint32_t total = (A.diag & 16) ? 0u : s_pref[tcount];  // diagnostic: no chunk records
-        uint32_t *ctr = A.bb.work + t0 / 64;
-        // The first round is static (CTA c >= hotc takes records
-        // [(c-hotc)*gpb, (c-hotc+1)*gpb)):
-        // one same-address atomic per CTA at launch cost ~5 us of serialised
-        // L2 atomics for an otherwise empty kernel.  Later rounds are grabbed
-        // from the counter, offset past the static part; the next round's
-        // grab is issued before this round's record is folded, so the
-        // atomic's latency overlaps the gradient loads.
-        // (CTAs that folded a hot segment start on the counter instead)
-        const uint32_t hotc = min(htot, gridDim.x);
-        const uint32_t static_part = (gridDim.x - hotc) * (uint32_t)gpb;
-        uint32_t next;
-        if (blockIdx.x >= hotc) {
-            next = (blockIdx.x - hotc) * (uint32_t)gpb;
-        } else {
-            __syncthreads();
-            if (threadIdx.x == 0) s_base = static_part >= total ? total : static_part + atomicAdd(ctr, (uint32_t)gpb);
-            __syncthreads();
-            next = s_base;
-        }
-        while (true) {
-            const uint32_t base = next;
-            if (base >= total) break;
-            __syncthreads();  // every thread has read s_base
-            uint32_t nx = 0;
-            if (threadIdx.x == 0) nx = static_part >= total ? total : static_part + atomicAdd(ctr, (uint32_t)gpb);
-            const uint32_t item = base + gi;
-            if (item < total) {
-            const int tl = find_table(s_pref, tcount, item);
-            const int t = t0 + tl;
-            const uint32_t c = item - s_pref[tl];
-            const uint4 *rp = reinterpret_cast<const uint4 *>(A.bb.chunk_rec + (size_t)t * g.nc + c);
-            uint4 q4[5];
-            q4[0] = __ldg(rp);
-            const uint32_t slot = q4[0].x, len = q4[0].y;
+        // ---- N: BU chunk records per lane group at once
+        const long long GG = W * NG;
+        const long long gg = gw * NG + grp;
+        for (long long c0 = gg * BU; c0 < Ct; c0 += GG * BU) {
+            uint4 hd[BU];
+            const ChunkRec *rp[BU];
+            int tt[BU];
 #pragma unroll
-            for (int k = 1; k < 5; k++) q4[k] = (uint32_t)(4 * k - 2) < len ? __ldg(rp + k) : make_uint4(0, 0, 0, 0);
-            const uint32_t *bag = reinterpret_cast<const uint32_t *>(q4) + 2;
-            const float4 *gb = grad + (size_t)t * g.N * D4 + lane;
-            float4 *wp = st + (size_t)slot * D4 + lane;
-            float4 w[VPL];
+            for (int u = 0; u < BU; u++) {
+                const long long c = c0 + u;
+                if (c < Ct) {
+                    const int tl = find_table(s_pc, tcount, (uint32_t)c);
+                    tt[u] = t0 + tl;
+                    rp[u] = A.bb.chunk_rec + (size_t)tt[u] * g.nc + ((uint32_t)c - s_pc[tl]);
+                    hd[u] = __ldg(reinterpret_cast<const uint4 *>(rp[u]));  // slot, len, bag0, bag1
+                } else {
+                    tt[u] = 0;
+                    rp[u] = nullptr;
+                    hd[u] = make_uint4(0, 0, 0, 0);
+                }
+            }
+            float4 w[BU][VPL], g0[BU][VPL], g1[BU][VPL];
 #pragma unroll
-            for (int v = 0; v < VPL; v++) w[v] = wp[v * G];
-            Acc4 acc[VPL];
+            for (int u = 0; u < BU; u++) {
+                if (hd[u].y == 0u) continue;
+                const float4 *gb = grad + (size_t)tt[u] * g.N * D4 + lane;
 #pragma unroll
-            for (int v = 0; v < VPL; v++) acc[v] = Acc4{0.0, 0.0, 0.0, 0.0};
+                for (int v = 0; v < VPL; v++) {
+                    w[u][v] = st[(size_t)hd[u].x * D4 + lane + v * G];
+                    g0[u][v] = __ldg(gb + (size_t)hd[u].z * D4 + v * G);
+                    if (hd[u].y >= 2u) g1[u][v] = __ldg(gb + (size_t)hd[u].w * D4 + v * G);
+                }
+            }
+            uint32_t longm = 0;  // records with > 2 occurrences: folded below, from scratch
 #pragma unroll
-            for (int q0 = 0; q0 < CH; q0 += RBN) {
-                if ((uint32_t)q0 < len) {
-                    float4 r[RBN][VPL];
+            for (int u = 0; u < BU; u++) {
+                const uint32_t len = hd[u].y;
+                if (len == 0u) continue;
+                if (len > 2u) {
+                    longm |= 1u << u;
+                    continue;
+                }
+                float4 *wp = st + (size_t)hd[u].x * D4 + lane;
 #pragma unroll
-                    for (int q = 0; q < RBN; q++)
-                        if ((uint32_t)(q0 + q) < len)
+                for (int v = 0; v < VPL; v++) {
+                    float4 s = g0[u][v];
+                    if (len == 2u) { s.x += g1[u][v].x; s.y += g1[u][v].y; s.z += g1[u][v].z; s.w += g1[u][v].w; }
+                    wp[v * G] = sgd32(w[u][v], s, A.lr);
+                }
+            }
+            // > 2 occurrences (rare in the Zipf tail): fp64 in ascending
+            // occurrence order, every gradient row (re)loaded here
+            while (longm) {
+                const int u = __ffs(longm) - 1;
+                longm &= longm - 1;
+                const ChunkRec *rc = A.bb.chunk_rec;
+                int tu = 0;
+                uint32_t slot = 0, len = 0;
+                const uint32_t *bags = nullptr;
 #pragma unroll
-                            for (int v = 0; v < VPL; v++) r[q][v] = ldg4(gb + (size_t)bag[q0 + q] * D4 + v * G);
+                for (int q = 0; q < BU; q++)
+                    if (q == u) { rc = rp[q]; tu = tt[q]; slot = hd[q].x; len = hd[q].y; }
+                bags = rc->bag;
+                const float4 *gb = grad + (size_t)tu * g.N * D4 + lane;
+                float4 *wp = st + (size_t)slot * D4 + lane;
+                Acc4 acc[VPL];
 #pragma unroll
-                    for (int q = 0; q < RBN; q++)
-                        if ((uint32_t)(q0 + q) < len)
+                for (int v = 0; v < VPL; v++) acc[v] = Acc4{0.0, 0.0, 0.0, 0.0};
+                for (uint32_t q0 = 0; q0 < len; q0 += 4) {
+                    float4 r[4][VPL];
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (q0 + q < len) {
+                            const uint32_t bag = __ldg(bags + q0 + q);
+#pragma unroll
+                            for (int v = 0; v < VPL; v++) r[q][v] = __ldg(gb + (size_t)bag * D4 + v * G);
+                        }
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (q0 + q < len)
 #pragma unroll
                             for (int v = 0; v < VPL; v++) acc_add(acc[v], r[q][v]);
                 }
-            }
 #pragma unroll
-            for (int v = 0; v < VPL; v++) wp[v * G] = sgd(w[v], acc[v], A.lr);
+                for (int v = 0; v < VPL; v++) wp[v * G] = sgd(wp[v * G], acc[v], A.lr);
             }
-            if (threadIdx.x == 0) s_base = nx;
-            __syncthreads();
-            next = s_base;
         }
     }
 }
@@ -569,19 +558,11 @@ cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s) {
 // occurrences per hot-row segment: one round of RB rows per lane group of
 // the k_bwd instance that D dispatches to (generic D: 64).  (Half-width lane
 // groups, two float4 per lane, were measured slower: 20.7 vs 16.4 us.)
+// occurrences per hot-row segment (one warp of k_bwd folds a segment;
+// generic D: one warp too).  SP_HOT_SEG overrides (A/B).
 int backward_hot_segment(int D) {
-    int G = 32, VPL = 1;
-    switch (D / 4) {
-        case 1: case 2: case 4: case 8: case 16: case 32: G = D / 4; VPL = 1; break;
-        case 64: VPL = 2; break;
-        case 128: VPL = 4; break;
-        case 256: VPL = 8; break;
-        default: return 64;
-    }
-    const int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);
-    int hs = (256 / G) * RB;  // one round of RB rows per lane group
-    // SP_HOT_SEG overrides (A/B; >= CH so a hot row has >= 2 segments' worth).
-    // Measured on Kaggle: 2 and 4 rounds per segment were 16% / 51% slower.
+    (void)D;
+    int hs = 32;
     if (const char *e = getenv("SP_HOT_SEG")) hs = atoi(e) >= CH ? atoi(e) : hs;
     // (segment lengths are packed in HOT_LEN_BITS of the hot record)
     return hs < CH ? CH : (hs > HOT_SEG_MAX ? HOT_SEG_MAX : hs);
