@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--pooling", type=int, default=0, help="sensitivity sweep: override L (P:1259-1268)")
     ap.add_argument("--batch", type=int, default=0, help="sensitivity sweep: override N")
     ap.add_argument("--slot-frac", type=float, default=0.0, help="sensitivity sweep: slots as a fraction of rows")
+    ap.add_argument("--gather-frac", type=float, default=-1.0,
+                    help="share of each batch's missed rows gathered by CPU threads (hybrid transfer); "
+                         "-1: the library's default")
+    ap.add_argument("--host-threads", type=int, default=0, help="transfer-engine helper threads per pool")
     ap.add_argument("--writeback", default="", choices=["", "gpu", "cpu"],
                     help="victims' write-back: GPU bulk stores into host rows, or CPU scatter (default: library's)")
     ap.add_argument("--variant", default="pipelined", choices=["pipelined", "serial", "resident", "gpuonly", "static"],
@@ -373,6 +377,8 @@ def run_ours(args):
         cfg = cfg.with_(**over)
     if args.writeback:
         os.environ["SP_WRITEBACK"] = args.writeback
+    if args.gather_frac >= 0:
+        os.environ["SP_GATHER_FRAC"] = str(args.gather_frac)
     if args.variant in ("resident", "gpuonly"):
         cfg = cfg.with_(slot_frac=1.0, slots_fixed=None)
     if args.variant == "serial":
@@ -416,6 +422,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     sp = ScratchPipe(rows, tables, D, slots, N, L, window=cfg.window, device=local, stream=stream,
                      index_dtype="int32", index_on_device=False, policy=args.policy,
+                     host_threads=args.host_threads,
                      policy_seed=args.policy_seed)
     pinned_rows = 0
     if args.variant == "static":
@@ -652,7 +659,13 @@ def run_ours(args):
                           "moves it into the freed slots and writes the victims contiguously to pinned "
                           "staging (TMA bulk copies); CPU threads scatter them into their host rows",
             "cpu_gather_dma": "CPU gather into a pinned slot, copy-engine DMA of the slot, k_pullfill "
-                              "fills the slots and stages the victims; CPU scatter"}.get(mode, mode)
+                              "fills the slots and stages the victims; CPU scatter",
+            "hybrid": "CPU threads gather a share (%.2f) of each batch's missed rows into a contiguous "
+                      "pinned slot while k_pullfill pulls the rest from their host rows (TMA bulk "
+                      "copies); the victims are staged contiguously and scattered by CPU threads"
+                      % st2.get("gather_share", 0.0)}.get(mode, mode)
+    if st2.get("gpu_writeback"):
+        path += " [write-back: k_pullfill stores each victim straight into its host row]"
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "iters/s", "n_gpus": world,
@@ -671,6 +684,7 @@ def run_ours(args):
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),
                         "alg_GBs": round(train_bytes / (train_ms * 1e-3) / 1e9, 1) if train_ms else None},
         "host_link": {"path": path, "transfer_mode": mode, "engine_threads": st2.get("engine_threads"),
+                      "gather_share": st2.get("gather_share"), "gpu_writeback": st2.get("gpu_writeback"),
                       "h2d_bytes_per_batch": int(4 * D * m),
                       "h2d_GBs": None if link_GBs is None else round(link_GBs, 2),
                       "d2h_bytes_per_batch": int(4 * D * ev),

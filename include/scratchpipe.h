@@ -54,6 +54,9 @@
  *   SP_WRITEBACK=gpu|cpu  victims' write-back: gpu = the transfer kernel stores
  *                         each victim row straight into its host row (TMA bulk
  *                         store); cpu = staged contiguously, CPU threads scatter
+ *   SP_GATHER_FRAC=f      hybrid: the CPU gathers the share f in (0,1) of each
+ *                         batch's missed rows, the transfer kernel pulls the rest
+ *                         at the same time (1: all gathered, 0: all pulled)
  *   SP_GATHER_DMA=1       with the CPU gather, copy the gathered slot to HBM by
  *                         copy-engine DMA before the transfer kernel (default 0)
  *   SP_PULL_CTAS=n        transfer-kernel grid (one-warp CTAs, default 16)
@@ -183,6 +186,7 @@ typedef struct {
     int32_t gpu_writeback;          /* 1: k_pullfill writes victims straight into  */
                                     /* their host rows (SP_WRITEBACK=gpu)           */
     int32_t reserved_stats;
+    double gather_share;            /* share of the missed rows the CPU gathers    */
 } sp_stats;
 
 /* sp_stats.transfer_mode (missed rows in); victims out: CPU scatter from
@@ -191,6 +195,8 @@ typedef struct {
 #define SP_XFER_GPU_PULL   0  /* k_pullfill reads each missed row from its host row */
 #define SP_XFER_CPU_GATHER 1  /* CPU threads gather into a contiguous pinned slot   */
 #define SP_XFER_GATHER_DMA 2  /* CPU gather, then copy-engine DMA of the slot       */
+#define SP_XFER_HYBRID     3  /* CPU gathers a share (gather_share) into the slot,  */
+                              /* k_pullfill pulls the rest concurrently            */
 
 int32_t sp_abi_version(void);
 

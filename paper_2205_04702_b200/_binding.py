@@ -72,10 +72,11 @@ class SpStats(ctypes.Structure):
         ("graph_steps", ctypes.c_int64), ("graph_step_host_ms", ctypes.c_double),
         ("transfer_mode", ctypes.c_int32), ("engine_threads", ctypes.c_int32),
         ("gpu_writeback", ctypes.c_int32), ("reserved_stats", ctypes.c_int32),
+        ("gather_share", ctypes.c_double),
     ]
 
 
-XFER_MODES = {0: "gpu_pull", 1: "cpu_gather", 2: "cpu_gather_dma"}
+XFER_MODES = {0: "gpu_pull", 1: "cpu_gather", 2: "cpu_gather_dma", 3: "hybrid"}
 
 
 def _load():
@@ -357,7 +358,7 @@ class ScratchPipe:
         out["kernel_timed"] = dict(zip(KERNEL_KINDS, list(s.kernel_timed)))
         for k in ("host_gather_ms", "host_scatter_ms", "host_rows_gathered", "host_rows_scattered",
                   "wait_xfer_ms", "wait_list_ms", "graph_steps", "graph_step_host_ms", "engine_threads",
-                  "gpu_writeback"):
+                  "gpu_writeback", "gather_share"):
             out[k] = getattr(s, k)
         out["transfer_mode"] = XFER_MODES.get(s.transfer_mode, str(s.transfer_mode))
         out["status"] = st

@@ -119,8 +119,24 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
         // round moves as one bulk copy each way)
         auto vbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + i) * rowb; };
         auto nbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + nb + i) * rowb; };
-        const bool gathered = A.in_stage != nullptr && !A.diag_nowb;
         const bool direct = A.wb_direct != 0;  // victims straight to their host rows
+        // items [0, Kg) of this table group were gathered by the CPU into the
+        // contiguous pinned slot, the rest are pulled from their host rows
+        // (hybrid split: the CPU gather and the GPU pull run concurrently)
+        const uint32_t Kg = !A.in_stage ? 0u
+                            : (A.gfrac_q16 >= 65536u ? total : (uint32_t)(((unsigned long long)total * A.gfrac_q16) >> 16));
+        auto round_gathered = [&](uint32_t r) {  // the whole round comes from the gathered slot
+            const uint32_t k0 = lo + r * nb;
+            return A.in_stage != nullptr && !A.diag_nowb && k0 + min((uint32_t)nb, hi - k0) <= Kg;
+        };
+        if (A.gwait && lo < Kg && hi > lo) {
+            // hybrid: this CTA reads gathered rows; wait (in-kernel, on the
+            // pinned progress counter) until the CPU has gathered batch b
+            if (lane == 0)
+                while (*(volatile const unsigned long long *)A.gwait < (unsigned long long)(A.b + 1)) __nanosleep(512);
+            __syncwarp();
+            __threadfence_system();
+        }
         auto issue = [&](uint32_t r) {
             const int s = (int)((phase_ctr + r) % XS);
             const uint32_t k0 = lo + r * nb;
@@ -133,8 +149,8 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 const int t = t0 + tl;
                 const size_t kk = (size_t)t * g.n + (item - s_pref[tl]);
                 slot = A.bb.fill_slot[kk];
-                src_host = A.in_stage ? A.in_stage + (size_t)(base_t0 + item) * g.D  // CPU-gathered, contiguous
-                                      : A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
+                src_host = item < Kg ? A.in_stage + (size_t)(base_t0 + item) * g.D  // CPU-gathered, contiguous
+                                     : A.host[t] + (size_t)A.bb.fill_row[kk] * g.D;
                 const uint32_t old = A.bb.evict_row[kk];
                 if (old != EMPTY && !A.diag_nowb) stage = direct ? (uint32_t)t : base_t0 + item;
                 // the scatter thread's work list: where the staged row goes
@@ -150,7 +166,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
             const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
             if (lane == 0) mbar_expect_tx(&bar[s], tot);
             __syncwarp();
-            if (gathered) {  // the round's new rows: contiguous bulk copies, from the
+            if (round_gathered(r)) {  // the round's new rows: contiguous bulk copies, from the
                              // DMA'd device copy where it reaches, else the pinned slot
                 if (lane == 0 && cnt) {
                     const uint32_t i0 = base_t0 + k0;
@@ -173,7 +189,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 // victims: one bulk store per row into its host row
                 if (slot != EMPTY && stage != EMPTY)
                     bulk_s2g(reinterpret_cast<void *>((uintptr_t)s_dst[s][lane]), vbuf(s, lane), rowb);
-            } else if (gathered) {
+            } else if (round_gathered(r)) {
                 // victims: one contiguous bulk store of the round's staging rows
                 // (rows of fills without a victim carry garbage; their work-list
                 // entry is 0, so the scatter skips them)

@@ -257,6 +257,7 @@ struct sp_ctx {
     // into a contiguous pinned slot, the transfer kernel reads that slot
     // (sequential pages) instead of random host rows
     bool cpu_gather = false;
+    uint32_t gather_q16 = 65536;  // CPU-gathered share of each batch's fills (hybrid < 65536)
     std::thread gather_worker;
     RowPool gpool;  // gather helpers
     unsigned long long *hl_ready = nullptr;    // pinned mapped [RING][T]
@@ -665,14 +666,23 @@ void gather_main(sp_ctx *c) {
             dst.clear();
             float *in = c->h_in + (size_t)(g % c->XSR) * slab;
             size_t k0 = 0;
-            for (int t = 0; t < c->T; t++) {
-                const uint32_t m = c->hl_m[(size_t)r * c->T + t];
-                const uint32_t *rows = c->hl_row + ((size_t)r * c->T + t) * c->n;
-                for (uint32_t k = 0; k < m; k++) {
-                    src.push_back(c->host[t] + (size_t)rows[k] * c->D);
-                    dst.push_back(in + (k0 + k) * c->D);
+            // per group of 64 tables (the transfer kernel's unit), the first
+            // Kg = total * q >> 16 fills in table order (hybrid split)
+            for (int t0 = 0; t0 < c->T; t0 += 64) {
+                const int t1 = std::min(c->T, t0 + 64);
+                unsigned long long total = 0;
+                for (int t = t0; t < t1; t++) total += c->hl_m[(size_t)r * c->T + t];
+                const unsigned long long Kg = c->gather_q16 >= 65536 ? total : (total * c->gather_q16) >> 16;
+                unsigned long long item = 0;
+                for (int t = t0; t < t1 && item < Kg; t++) {
+                    const uint32_t m = c->hl_m[(size_t)r * c->T + t];
+                    const uint32_t *rows = c->hl_row + ((size_t)r * c->T + t) * c->n;
+                    for (uint32_t k = 0; k < m && item < Kg; k++, item++) {
+                        src.push_back(c->host[t] + (size_t)rows[k] * c->D);
+                        dst.push_back(in + (k0 + item) * c->D);
+                    }
                 }
-                k0 += m;
+                k0 += total;
             }
             const auto t0 = std::chrono::steady_clock::now();
             c->gpool.copy(src.data(), dst.data(), (long)src.size(), rowb);
@@ -750,7 +760,8 @@ sp_status pump(sp_ctx *c) {
             CUresult cr = wv((CUstream)xs, (CUdeviceptr)c->d_scat, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ);
             if (cr != CUDA_SUCCESS) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 failed");
         }
-        if (c->cpu_gather) {  // the CPU has gathered batch b's missed rows
+        const bool hybrid = c->cpu_gather && c->gather_q16 < 65536;
+        if (c->cpu_gather && !hybrid) {  // the CPU has gathered batch b's missed rows
             wait_value64_fn wv = wait_value64();
             if (!wv) return fail(c, SP_ERR_CUDA, "cuStreamWaitValue64 unavailable");
             CUresult cr = wv((CUstream)xs, (CUdeviceptr)c->d_gathered, (cuuint64_t)(b + 1), CU_STREAM_WAIT_VALUE_GEQ);
@@ -760,7 +771,9 @@ sp_status pump(sp_ctx *c) {
         a.g = c->g;
         a.bb = c->ring[r];
         if (c->cpu_gather) a.in_stage = c->hd_in + (size_t)(b % c->XSR) * c->T * c->n * c->D;
-        if (c->cpu_gather && c->gather_dma) {
+        a.gfrac_q16 = c->gather_q16;
+        a.gwait = hybrid ? c->d_gathered : nullptr;  // hybrid: gathered rows awaited in-kernel
+        if (c->cpu_gather && c->gather_dma && !hybrid) {
             // rows to DMA: 1.5x the largest of the last 16 gathered batches
             // (+256), at most the slot; rows past them are read zero-copy
             const long long Tn = (long long)c->T * c->n;
@@ -1118,6 +1131,19 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     // 54 it/s), where the CPU copy threads become the bound
     c->cpu_gather = (double)c->T * c->n * c->D * sizeof(float) <= 32.0 * (1 << 20);
     if (const char *e = getenv("SP_CPU_GATHER")) c->cpu_gather = atoi(e) != 0;
+    // hybrid split (SP_GATHER_FRAC in (0, 1)): the CPU gathers that share of
+    // each batch's missed rows while the transfer kernel pulls the rest
+    if (const char *e = getenv("SP_GATHER_FRAC")) {
+        const double f = atof(e);
+        if (f > 0.0 && f < 1.0) {
+            c->cpu_gather = true;
+            c->gather_q16 = (uint32_t)(f * 65536.0);
+        } else if (f >= 1.0) {
+            c->cpu_gather = true;
+        } else {
+            c->cpu_gather = false;
+        }
+    }
     if (const char *e = getenv("SP_WRITEBACK")) c->gpu_wb = std::string(e) == "gpu";
     if (c->cpu_gather) {
         CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
@@ -1696,7 +1722,10 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->wait_list_ms = c->wait_list_ns * 1e-6;
     o->graph_steps = c->graph_steps;
     o->graph_step_host_ms = c->graph_step_ns * 1e-6;
-    o->transfer_mode = c->cpu_gather ? (c->gather_dma ? SP_XFER_GATHER_DMA : SP_XFER_CPU_GATHER) : SP_XFER_GPU_PULL;
+    o->transfer_mode = c->cpu_gather ? (c->gather_q16 < 65536 ? SP_XFER_HYBRID
+                                                              : (c->gather_dma ? SP_XFER_GATHER_DMA : SP_XFER_CPU_GATHER))
+                                     : SP_XFER_GPU_PULL;
+    o->gather_share = c->cpu_gather ? c->gather_q16 / 65536.0 : 0.0;
     o->engine_threads = (c->gpu_wb ? 0 : 1 + c->host_threads) + (c->cpu_gather ? 1 + c->host_threads : 0);
     o->gpu_writeback = c->gpu_wb ? 1 : 0;
     if (!c->prof_pending.empty()) {

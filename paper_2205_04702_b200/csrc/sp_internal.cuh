@@ -178,6 +178,9 @@ struct XferArgs {
     int wb_direct;                // victims go straight to their host rows (no staging)
     const float *in_dev;          // device copy of the first in_dev_rows rows of in_stage
     uint32_t in_dev_rows;         //   (copy-engine DMA), or nullptr / 0
+    uint32_t gfrac_q16;           // share of the fills gathered by the CPU (65536 = all)
+    const unsigned long long *gwait;  // hybrid split: pinned "batches gathered" counter the
+                                      // CTAs reading gathered rows wait on (else nullptr)
     const float *in_stage;        // [sum m][D] missed rows gathered by the CPU into pinned
                                   // host memory (contiguous, flattened over tables), or
                                   // nullptr: pull each row from its host table

@@ -367,7 +367,8 @@ def test_prefill_all_resident_no_misses_matches_oracle():
                                  {"SP_CPU_GATHER": "1", "SP_GATHER_DMA": "1"},
                                  {"SP_CPU_GATHER": "0", "SP_WRITEBACK": "gpu"},
                                  {"SP_CPU_GATHER": "1", "SP_WRITEBACK": "gpu"},
-                                 {"SP_CPU_GATHER": "0", "SP_WRITEBACK": "cpu"}])
+                                 {"SP_CPU_GATHER": "0", "SP_WRITEBACK": "cpu"},
+                                 {"SP_GATHER_FRAC": "0.5"}, {"SP_GATHER_FRAC": "0.3", "SP_WRITEBACK": "gpu"}])
 def test_transfer_modes_match_oracle(env, monkeypatch):
     """Every transfer mode (GPU pull of random host rows, CPU gather into a
     pinned slot, CPU gather + copy-engine DMA) gives the oracle's plans,
