@@ -360,7 +360,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2205_04702_b200 import ScratchPipe
-    from paper_2205_04702_b200.sharding import (exchange_backward, exchange_forward, lpt_assign,
+    from paper_2205_04702_b200.sharding import (lpt_assign,
                                                 table_weights, tables_of)
     from workload import CONFIGS, init_table, sample_trace
 
@@ -387,6 +387,12 @@ def run_ours(args):
     slots_all = cfg.slots
     owner = lpt_assign(table_weights(cfg.rows, slots_all, N * L, D), world)
     mine = tables_of(owner, rank)
+    shard_kw = {}
+    if world > 1:  # table-wise sharding inside the library: NCCL comm from a shared unique id
+        from paper_2205_04702_b200 import nccl_unique_id
+        box = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        shard_kw = dict(world=world, rank=rank, nccl_id=box[0], table_owner=owner, table_ids=mine)
     rows = [cfg.rows[t] for t in mine]
     slots = [slots_all[t] for t in mine]
     g_, d_, e_ = cfg.surrogate()
@@ -423,7 +429,7 @@ def run_ours(args):
     sp = ScratchPipe(rows, tables, D, slots, N, L, window=cfg.window, device=local, stream=stream,
                      index_dtype="int32", index_on_device=False, policy=args.policy,
                      host_threads=args.host_threads,
-                     policy_seed=args.policy_seed)
+                     policy_seed=args.policy_seed, **shard_kw)
     pinned_rows = 0
     if args.variant == "static":
         # static top-N partition: the hottest rows of the first 200 batches of
@@ -438,7 +444,7 @@ def run_ours(args):
             pinned_rows += int(top.numel())
     if args.variant == "gpuonly":
         sp.prefill()
-    pooled = torch.empty((len(mine), N, D), dtype=torch.float32, device=dev)
+    pooled = torch.empty(sp.pooled_shape(), dtype=torch.float32, device=dev)  # [T_all][N/G][D] if sharded
     grad = torch.empty_like(pooled)
     stats_host = torch.zeros((K + max(W, 18) + 8, len(mine), 4), dtype=torch.int32).pin_memory()
     state = {"pushed": 0, "trained": 0}
@@ -455,15 +461,9 @@ def run_ours(args):
 
     def train_step(push, read_stats_slot=None):
         push()
-        sp.forward(pooled)
-        if world > 1:
-            pb = exchange_forward(pooled, owner, rank, world)
-            gb = sp.surrogate(pb, g_, d_)
-            gl = exchange_backward(gb, owner, rank, world, N)
-            sp.train(gl, e_)
-        else:
-            sp.surrogate(pooled, g_, d_, out=grad)
-            sp.train(grad, e_)
+        sp.forward(pooled)          # sharded: NCCL exchange inside the library
+        sp.surrogate(pooled, g_, d_, out=grad)
+        sp.train(grad, e_)
         if read_stats_slot is not None:
             sp.copy_batch_stats(state["trained"], stats_host[read_stats_slot])
         state["trained"] += 1
@@ -496,23 +496,13 @@ def run_ours(args):
     # library's C driver loop (sp_run_steps: plan / forward / surrogate / train)
     dev_trace = trace[:nb_dev + ahead]
     t_pre = time.perf_counter()
-    if world == 1:
-        sp.run_steps(dev_trace, pre + W, pooled, grad, g_, d_, e_)
-    else:
-        for _ in range(ahead):
-            push_dev()
-        for _ in range(pre + W):
-            train_step(push_dev)
+    sp.run_steps(dev_trace, pre + W, pooled, grad, g_, d_, e_)  # sharded: eager steps, NCCL in the library
     torch.cuda.synchronize()
     t_pre = time.perf_counter() - t_pre
     st0 = sp.stats()
 
     def value_loop(n):
-        if world == 1:
-            sp.run_steps(dev_trace, n, pooled, grad, g_, d_, e_)
-        else:
-            for _ in range(n):
-                train_step(push_dev)
+        sp.run_steps(dev_trace, n, pooled, grad, g_, d_, e_)
 
     # ---- timed: value (inputs resident in HBM)
     barrier()
@@ -563,13 +553,11 @@ def run_ours(args):
     h0 = nb_dev + ahead  # host_trace[i] is batch h0 + i
 
     def e2e_one(slot):
-        if world == 1:  # the library's step call: plan kernel reads B(j) over the host link
-            sp.run_steps(host_trace, 1, pooled, grad, g_, d_, e_, first_batch=h0)
-            state["pushed"] += 1
-            sp.copy_batch_stats(state["trained"], stats_host[slot])
-            state["trained"] += 1
-        else:           # per-call API (sp_plan copies B(j) H2D) + NCCL exchange
-            train_step(push_host, read_stats_slot=slot)
+        # the library's step call: the plan kernel reads B(j) over the host link
+        sp.run_steps(host_trace, 1, pooled, grad, g_, d_, e_, first_batch=h0)
+        state["pushed"] += 1
+        sp.copy_batch_stats(state["trained"], stats_host[slot])
+        state["trained"] += 1
         evs[slot % 2].record(stream)
 
     for k in range(WE):
@@ -717,11 +705,10 @@ def run_ours(args):
                 "d2h_bytes_per_step": stats_bytes, "ms_per_step": round(ms_e2e / K, 5),
                 "host_step_us_first5": [round(x, 1) for x in e2e_gaps[:5]],
                 "host_step_us_median": round(statistics.median(e2e_gaps), 1) if e2e_gaps else None,
-                "path": ("sp_run_steps(1 step) on pinned host int32 indices (the plan kernel reads "
-                         "the batch over the host link); sp_copy_batch_stats D2H each step, waited "
-                         "for and read one step later") if world == 1 else
-                        "sp_plan(host int32 indices, pinned) -> H2D on the plan stream; NCCL exchange; "
-                        "sp_copy_batch_stats D2H each step, waited for and read one step later"},
+                "path": "sp_run_steps(1 step) on pinned host int32 indices (the plan kernel reads "
+                        "the batch over the host link); sp_copy_batch_stats D2H each step, waited "
+                        "for and read one step later" + ("; pooled rows and gradients exchanged "
+                                                         "with NCCL inside the library" if world > 1 else "")},
         "preroll_s": round(t_pre, 2),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

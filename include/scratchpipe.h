@@ -82,7 +82,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 3
+#define SP_ABI_VERSION 4
 
 typedef struct sp_ctx sp_ctx;
 
@@ -94,7 +94,7 @@ typedef enum {
     SP_ERR_INDEX_RANGE = 3,  /* a sparse ID < 0 or >= rows[t]                   */
     SP_ERR_STATE = 4,        /* call-order violation (see sp_forward/sp_train)  */
     SP_ERR_CUDA = 5,         /* CUDA runtime error                              */
-    SP_ERR_NCCL = 6,         /* reserved                                        */
+    SP_ERR_NCCL = 6,         /* NCCL library missing or an NCCL call failed     */
     SP_ERR_OOM = 7           /* device or pinned allocation failed              */
 } sp_status;
 
@@ -135,6 +135,24 @@ typedef struct {
                                  /* candidates: SP_POLICY_*           */
     uint32_t reserved;           /* must be 0                                       */
     uint64_t policy_seed;        /* SP_POLICY_RANDOM: seed of the victim draws      */
+    /* Table-wise sharding over G GPUs (one cache manager per
+     * table, "no further inter-GPU RAW hazards"), one context per GPU.  With
+     * world > 1 the context owns num_tables of the num_tables_all global
+     * tables and the library exchanges pooled rows / gradients with NCCL
+     * (send/recv over NVLink, on desc.stream): sp_forward then writes the
+     * batch-sharded [num_tables_all][N/G][D] layout a data-parallel MLP
+     * consumes (rank r holds samples r*N/G .. (r+1)*N/G-1 of every table)
+     * and sp_train takes its gradient in that layout.  world == 1: none of
+     * these fields is read. */
+    int32_t world;               /* G ranks (0 or 1: single GPU)                    */
+    int32_t rank;                /* this context's rank                             */
+    const void *nccl_id;         /* 128-byte ncclUniqueId from sp_nccl_unique_id on */
+                                 /* one rank, the same bytes on every rank          */
+    int32_t num_tables_all;      /* T_all                                           */
+    int32_t reserved2;           /* must be 0                                       */
+    const int32_t *table_owner;  /* [T_all] rank owning each global table           */
+    const int32_t *table_ids;    /* [num_tables] global id of each local table,     */
+                                 /* ascending; rows/slots/host_tables follow it     */
 } sp_desc;
 
 /* desc.policy (readings R8, R23-R25).  Every policy evicts only
@@ -199,6 +217,20 @@ typedef struct {
                               /* k_pullfill pulls the rest concurrently            */
 
 int32_t sp_abi_version(void);
+
+/* A fresh NCCL unique id (128 bytes into out) for sp_desc.nccl_id: created on
+ * one rank and broadcast to the others by the caller.  SP_ERR_NCCL if the
+ * NCCL library cannot be loaded. */
+sp_status sp_nccl_unique_id(void *out);
+
+/* Host-only layout of the sharded exchange (no GPU): for rank `rank` of
+ * `world`, the sends of sp_forward's exchange as (peer, local table,
+ * global table) triples in the order they are posted, and the receives as
+ * (peer, global table) pairs; each message is one table's N/G contiguous
+ * rows.  send[3*k..3*k+2], recv[2*k..2*k+1]; *nsend = T_local * world,
+ * *nrecv = T_all.  sp_train's exchange is the mirror image. */
+sp_status sp_shard_plan(int32_t world, int32_t rank, int32_t num_tables_all, const int32_t *table_owner,
+                        int32_t *send, int64_t *nsend, int32_t *recv, int64_t *nrecv);
 
 /* Host-table allocator: `bytes` of anonymous host memory backed by 2 MB
  * transparent huge pages where the OS allows (the CPU side of the transfer

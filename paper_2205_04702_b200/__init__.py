@@ -20,6 +20,8 @@ from ._binding import (  # noqa: F401
     SpError,
     header_symbols,
     lib,
+    nccl_unique_id,
+    shard_plan,
 )
 from .sizing import slots_for_fraction, window_batches, worst_case_storage_bytes  # noqa: F401
 

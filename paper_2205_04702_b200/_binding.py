@@ -53,6 +53,13 @@ class SpDesc(ctypes.Structure):
         ("policy", ctypes.c_int32),
         ("reserved", ctypes.c_uint32),
         ("policy_seed", ctypes.c_uint64),
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("nccl_id", ctypes.c_void_p),
+        ("num_tables_all", ctypes.c_int32),
+        ("reserved2", ctypes.c_int32),
+        ("table_owner", ctypes.POINTER(ctypes.c_int32)),
+        ("table_ids", ctypes.POINTER(ctypes.c_int32)),
     ]
 
 
@@ -111,6 +118,11 @@ def _load():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = S
+    L.sp_nccl_unique_id.argtypes = [P]
+    L.sp_nccl_unique_id.restype = S
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    L.sp_shard_plan.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, i32p, i32p, i64p, i32p, i64p]
+    L.sp_shard_plan.restype = S
     L.sp_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
     L.sp_host_alloc.restype = S
     L.sp_host_free.argtypes = [P, ctypes.c_size_t]
@@ -128,6 +140,30 @@ def header_symbols() -> List[str]:
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(sp_[a-z_]+)\s*\(", src)))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for a sharded context (sp_nccl_unique_id)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib.sp_nccl_unique_id(buf)
+    if st != SP_OK:
+        raise SpError(st, "sp_nccl_unique_id failed (NCCL library not loadable)")
+    return buf.raw
+
+
+def shard_plan(world: int, rank: int, owner):
+    """Host-only message lists of the sharded exchange (sp_shard_plan):
+    sends [(peer, local table, global table)], recvs [(peer, global table)]."""
+    own = np.ascontiguousarray(owner, dtype=np.int32)
+    ns, nr = ctypes.c_int64(0), ctypes.c_int64(0)
+    i32 = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    st = lib.sp_shard_plan(world, rank, len(own), i32(own), None, ctypes.byref(ns), None, ctypes.byref(nr))
+    if st != SP_OK:
+        raise SpError(st, "sp_shard_plan failed")
+    snd = np.zeros(3 * ns.value, np.int32)
+    rcv = np.zeros(2 * nr.value, np.int32)
+    lib.sp_shard_plan(world, rank, len(own), i32(own), i32(snd), ctypes.byref(ns), i32(rcv), ctypes.byref(nr))
+    return [tuple(x) for x in snd.reshape(-1, 3).tolist()], [tuple(x) for x in rcv.reshape(-1, 2).tolist()]
 
 
 class HostTable:
@@ -180,7 +216,12 @@ class ScratchPipe:
                  device: int = 0, stream=None, index_dtype: str = "int64", index_on_device: bool = False,
                  register_host: bool = False, profile: bool = False, log_factor: int = 0,
                  host_threads: int = 0, policy: str = "lru", policy_seed: int = 0,
-                 padding: bool = False):
+                 padding: bool = False, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
+                 table_owner=None, table_ids=None):
+        """world > 1 (or nccl_id given): table-wise sharding inside the library
+        -- this context owns the global tables `table_ids` (ascending) of the
+        `table_owner` map; forward / train exchange with NCCL and use the
+        batch-sharded [T_all][N/world][D] layout."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("ScratchPipe needs a CUDA device (no CPU fallback)")
@@ -205,9 +246,22 @@ class ScratchPipe:
         if padding:
             flags |= SP_FLAG_PADDING
         self.index_dtype, self.index_on_device = index_dtype, index_on_device
+        self.world, self.rank = world, rank
+        self.T_all = self.T
+        own = ids = None
+        self._nid = None
+        if nccl_id is not None or world > 1:
+            own = np.ascontiguousarray(table_owner, dtype=np.int32)
+            ids = np.ascontiguousarray(table_ids, dtype=np.int32)
+            self.T_all = len(own)
+            self._own, self._ids = own, ids
+            self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        i32 = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)) if a is not None else None
         d = SpDesc(self.T, _i64(self._rows), self._hp, dim, _i64(self._slots), window, past, future,
                    batch_size, pooling, device, ctypes.c_void_p(stream.cuda_stream), flags, log_factor,
-                   host_threads, POLICIES[policy], 0, policy_seed & ((1 << 64) - 1))
+                   host_threads, POLICIES[policy], 0, policy_seed & ((1 << 64) - 1), world, rank,
+                   ctypes.cast(self._nid, ctypes.c_void_p) if self._nid is not None else None,
+                   self.T_all, 0, i32(own), i32(ids))
         h = ctypes.c_void_p()
         with torch.cuda.device(device):
             st = lib.sp_create(ctypes.byref(d), ctypes.byref(h))
@@ -314,10 +368,16 @@ class ScratchPipe:
     def end_of_data(self):
         self._check(lib.sp_end_of_data(self._h))
 
+    def pooled_shape(self):
+        """[T][N][D], or [T_all][N/world][D] when sharded."""
+        if self._nid is not None:
+            return (self.T_all, self.N // self.world, self.D)
+        return (self.T, self.N, self.D)
+
     def forward(self, out=None):
         import torch
         if out is None:
-            out = torch.empty((self.T, self.N, self.D), dtype=torch.float32, device=f"cuda:{self.device}")
+            out = torch.empty(self.pooled_shape(), dtype=torch.float32, device=f"cuda:{self.device}")
         self._check(lib.sp_forward(self._h, ctypes.c_void_p(out.data_ptr())))
         return out
 

@@ -23,10 +23,12 @@
 // No host synchronisation on the caller's thread in the steady state.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <immintrin.h>
 #include <sys/mman.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <atomic>
 #include <chrono>
@@ -140,6 +142,65 @@ struct RowPool {
     }
 };
 
+
+// ---- NCCL, loaded at run time (libnccl.so.2: the copy torch already loaded
+// if any, so a comm created here and torch's share one library)
+struct NcclApi {
+    typedef int (*init_rank_t)(void **, int, std::array<char, 128>, int);
+    typedef int (*uid_t)(std::array<char, 128> *);
+    typedef int (*p2p_t)(const void *, size_t, int, int, void *, cudaStream_t);
+    typedef int (*recv_t)(void *, size_t, int, int, void *, cudaStream_t);
+    typedef int (*void_t)();
+    typedef int (*destroy_t)(void *);
+    typedef const char *(*err_t)(int);
+    init_rank_t init_rank = nullptr;
+    uid_t unique_id = nullptr;
+    p2p_t send = nullptr;
+    recv_t recv = nullptr;
+    void_t group_start = nullptr, group_end = nullptr;
+    destroy_t destroy = nullptr;
+    err_t err = nullptr;
+    bool ok = false;
+};
+
+NcclApi &nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.init_rank = reinterpret_cast<NcclApi::init_rank_t>(dlsym(h, "ncclCommInitRank"));
+        api.unique_id = reinterpret_cast<NcclApi::uid_t>(dlsym(h, "ncclGetUniqueId"));
+        api.send = reinterpret_cast<NcclApi::p2p_t>(dlsym(h, "ncclSend"));
+        api.recv = reinterpret_cast<NcclApi::recv_t>(dlsym(h, "ncclRecv"));
+        api.group_start = reinterpret_cast<NcclApi::void_t>(dlsym(h, "ncclGroupStart"));
+        api.group_end = reinterpret_cast<NcclApi::void_t>(dlsym(h, "ncclGroupEnd"));
+        api.destroy = reinterpret_cast<NcclApi::destroy_t>(dlsym(h, "ncclCommDestroy"));
+        api.err = reinterpret_cast<NcclApi::err_t>(dlsym(h, "ncclGetErrorString"));
+        api.ok = api.init_rank && api.unique_id && api.send && api.recv && api.group_start && api.group_end &&
+                 api.destroy && api.err;
+    });
+    return api;
+}
+constexpr int NCCL_FLOAT32 = 7;
+
+// The sharded exchange's message list (host logic, sp_shard_plan): sends in
+// (peer, local table) order, receives in (peer, global table) order, one
+// message = one table's N/G rows.
+void shard_plan(int world, int rank, int T_all, const int32_t *owner, std::vector<std::array<int, 3>> &send,
+                std::vector<std::array<int, 2>> &recv) {
+    send.clear();
+    recv.clear();
+    std::vector<int> local;
+    for (int t = 0; t < T_all; t++)
+        if (owner[t] == rank) local.push_back(t);
+    for (int g = 0; g < world; g++) {
+        for (int k = 0; k < (int)local.size(); k++) send.push_back({g, k, local[k]});
+        for (int t = 0; t < T_all; t++)
+            if (owner[t] == g) recv.push_back({g, t});
+    }
+}
 
 }  // namespace
 
@@ -276,6 +337,13 @@ struct sp_ctx {
     bool gather_dma = false;
     float *d_in = nullptr;                     // device [XSR][T*n][D]
     std::atomic<long long> x_max_m{0};         // largest of the last 16 gathered batches (rows)
+    // table-wise sharding (world > 1): NCCL comm, local pooled / gradient
+    // buffers [T][N][D], the message lists of the exchange
+    int world = 1, rank = 0, T_all = 0;
+    void *comm = nullptr;
+    float *d_pooled_local = nullptr, *d_grad_local = nullptr;
+    std::vector<std::array<int, 3>> x_send;  // (peer, local table, global table)
+    std::vector<std::array<int, 2>> x_recv;  // (peer, global table)
     // errors
     sp_status poisoned = SP_OK;
     std::string err = "no error";
@@ -810,6 +878,36 @@ sp_status pump(sp_ctx *c) {
 
 void drop_graphs(sp_ctx *c);
 
+// Sharded exchange (world > 1), on the compute stream.  forward: local
+// pooled [T][N][D] -> caller's [T_all][N/G][D] (rank g gets samples
+// g*Ns .. (g+1)*Ns-1 of every table); backward: caller's gradient
+// [T_all][Ns][D] -> local [T][N][D].  Every message is one table's Ns
+// contiguous rows, so no pack / unpack kernel is needed.
+sp_status exchange(sp_ctx *c, bool forward, float *bufA, const float *bufB) {
+    NcclApi &nc = nccl();
+    const size_t Ns = (size_t)c->N / c->world, rowf = (size_t)c->D, msg = Ns * rowf;
+    int r = nc.group_start();
+    for (const auto &m : c->x_send) {  // (peer, local table, global table)
+        if (r) break;
+        if (forward) r = nc.send(c->d_pooled_local + ((size_t)m[1] * c->N + (size_t)m[0] * Ns) * rowf, msg,
+                                 NCCL_FLOAT32, m[0], c->comm, c->compute);
+        else r = nc.recv(c->d_grad_local + ((size_t)m[1] * c->N + (size_t)m[0] * Ns) * rowf, msg, NCCL_FLOAT32,
+                         m[0], c->comm, c->compute);
+    }
+    for (const auto &m : c->x_recv) {  // (peer, global table)
+        if (r) break;
+        if (forward) r = nc.recv(bufA + (size_t)m[1] * msg, msg, NCCL_FLOAT32, m[0], c->comm, c->compute);
+        else r = nc.send(bufB + (size_t)m[1] * msg, msg, NCCL_FLOAT32, m[0], c->comm, c->compute);
+    }
+    const int r2 = nc.group_end();
+    if (r || r2) {
+        c->poisoned = SP_ERR_NCCL;
+        c->err = std::string("NCCL exchange: ") + nc.err(r ? r : r2);
+        return SP_ERR_NCCL;
+    }
+    return SP_OK;
+}
+
 void destroy_all(sp_ctx *c) {
     if (!c) return;
     stop_engine(c);
@@ -844,6 +942,7 @@ void destroy_all(sp_ctx *c) {
     if (c->own_xfer_s2) cudaStreamDestroy(c->own_xfer_s2);
     if (c->cap_s) cudaStreamDestroy(c->cap_s);
     if (c->cap_hi) cudaStreamDestroy(c->cap_hi);
+    if (c->comm && nccl().ok) nccl().destroy(c->comm);
     (void)cudaGetLastError();
     delete c;
 }
@@ -853,6 +952,35 @@ void destroy_all(sp_ctx *c) {
 extern "C" {
 
 int32_t sp_abi_version(void) { return SP_ABI_VERSION; }
+
+sp_status sp_nccl_unique_id(void *out) {
+    if (!out) return SP_ERR_INVALID_ARG;
+    if (!nccl().ok) return SP_ERR_NCCL;
+    std::array<char, 128> id;
+    if (nccl().unique_id(&id) != 0) return SP_ERR_NCCL;
+    std::memcpy(out, id.data(), 128);
+    return SP_OK;
+}
+
+sp_status sp_shard_plan(int32_t world, int32_t rank, int32_t num_tables_all, const int32_t *table_owner,
+                        int32_t *send, int64_t *nsend, int32_t *recv, int64_t *nrecv) {
+    if (world < 1 || rank < 0 || rank >= world || num_tables_all < 1 || !table_owner || !nsend || !nrecv)
+        return SP_ERR_INVALID_ARG;
+    for (int t = 0; t < num_tables_all; t++)
+        if (table_owner[t] < 0 || table_owner[t] >= world) return SP_ERR_INVALID_ARG;
+    std::vector<std::array<int, 3>> sv;
+    std::vector<std::array<int, 2>> rv;
+    shard_plan(world, rank, num_tables_all, table_owner, sv, rv);
+    if (send)
+        for (size_t k = 0; k < sv.size() && (int64_t)k < *nsend; k++)
+            for (int j = 0; j < 3; j++) send[3 * k + j] = sv[k][j];
+    if (recv)
+        for (size_t k = 0; k < rv.size() && (int64_t)k < *nrecv; k++)
+            for (int j = 0; j < 2; j++) recv[2 * k + j] = rv[k][j];
+    *nsend = (int64_t)sv.size();
+    *nrecv = (int64_t)rv.size();
+    return SP_OK;
+}
 
 sp_status sp_host_alloc(size_t bytes, void **out) {
     if (!out || !bytes) return SP_ERR_INVALID_ARG;
@@ -896,6 +1024,22 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     }
     if (F > P + 1) return SP_ERR_INVALID_ARG;  // one-shot future probe needs F <= P + 1
     if (d->policy < SP_POLICY_LRU || d->policy > SP_POLICY_LFU || d->reserved != 0) return SP_ERR_INVALID_ARG;
+    const bool sharded = d->world > 1 || (d->world == 1 && d->nccl_id);
+    if (sharded) {
+        if (!d->nccl_id || d->rank < 0 || d->rank >= d->world || d->num_tables_all < d->num_tables ||
+            !d->table_owner || !d->table_ids || d->batch_size % d->world != 0 || d->reserved2 != 0)
+            return SP_ERR_INVALID_ARG;
+        int mine = 0;
+        for (int t = 0; t < d->num_tables_all; t++) {
+            if (d->table_owner[t] < 0 || d->table_owner[t] >= d->world) return SP_ERR_INVALID_ARG;
+            mine += d->table_owner[t] == d->rank;
+        }
+        if (mine != d->num_tables) return SP_ERR_INVALID_ARG;
+        for (int k = 0; k < d->num_tables; k++)
+            if (d->table_ids[k] < 0 || d->table_ids[k] >= d->num_tables_all ||
+                d->table_owner[d->table_ids[k]] != d->rank || (k && d->table_ids[k] <= d->table_ids[k - 1]))
+                return SP_ERR_INVALID_ARG;
+    }
     if (P + F + 2 > RING) return SP_ERR_INVALID_ARG;
     sp_ctx *c = new sp_ctx();
     c->T = d->num_tables;
@@ -1037,6 +1181,21 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         for (int k = 0; k < 8; k++) CKC(cudaEventCreate(&c->sev[r][k]));
     if (const char *e = getenv("SP_CARVEOUT")) g_carveout = atoi(e);
     if (const char *e = getenv("SP_PDL")) g_pdl = atoi(e) != 0;
+    if (sharded) {  // NCCL communicator of the G contexts (collective: every rank calls sp_create)
+        if (!nccl().ok) return bail(SP_ERR_NCCL);
+        c->world = d->world;
+        c->rank = d->rank;
+        c->T_all = d->num_tables_all;
+        shard_plan(c->world, c->rank, c->T_all, d->table_owner, c->x_send, c->x_recv);
+        std::array<char, 128> id;
+        std::memcpy(id.data(), d->nccl_id, 128);
+        int r = nccl().init_rank(&c->comm, c->world, id, c->rank);
+        if (r != 0) {
+            c->err = std::string("ncclCommInitRank: ") + nccl().err(r);
+            c->comm = nullptr;
+            return bail(SP_ERR_NCCL);
+        }
+    }
     CKC(configure_push_kernel());
     CKC(configure_xfer_kernels());
     CKC(configure_train_kernels());
@@ -1098,6 +1257,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaMemset(c->d_pprof, 0, (18 * (size_t)c->T + 2 + 4096) * sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_pprof + 18 * (size_t)c->T + 2, 0xFF, 1024 * sizeof(unsigned long long)));
     CKC(dalloc(c, &c->d_host, c->T));
+    if (c->comm) {
+        CKC(dalloc(c, &c->d_pooled_local, Tn / c->L * c->D));
+        CKC(dalloc(c, &c->d_grad_local, Tn / c->L * c->D));
+    }
     CKC(dalloc(c, &c->d_ctl, RING));
     CKC(dalloc(c, &c->d_xdone, RING));
     CKC(cudaMemset(c->d_xdone, 0, RING * sizeof(uint32_t)));
@@ -1425,8 +1588,10 @@ sp_status sp_forward(sp_ctx *c, float *pooled) {
     if (c->xfer_enq <= b) return fail(c, SP_ERR_STATE, "sp_forward: transfer not schedulable");
     CK(cudaStreamWaitEvent(c->compute, c->ev_xfer[b % RING], 0));
     TrainArgs a = train_args(c, b);
-    a.pooled = pooled;
+    a.pooled = c->comm ? c->d_pooled_local : pooled;
     CK(launch(c, SP_K_FORWARD, b, c->compute, [&] { return launch_forward(a, c->compute); }));
+    if (c->comm)
+        if (sp_status s = exchange(c, true, pooled, nullptr)) return s;
     c->forwarded = b + 1;
     c->fwd_pending = true;
     return SP_OK;
@@ -1438,8 +1603,10 @@ sp_status sp_train(sp_ctx *c, const float *grad, float lr) {
     if (!c->fwd_pending) return fail(c, SP_ERR_STATE, "sp_train without a preceding sp_forward");
     CK(cudaSetDevice(c->device));
     const long long b = c->trained;
+    if (c->comm)
+        if (sp_status s = exchange(c, false, nullptr, grad)) return s;
     TrainArgs a = train_args(c, b);
-    a.grad = grad;
+    a.grad = c->comm ? c->d_grad_local : grad;
     a.lr = lr;
     CK(launch(c, SP_K_BACKWARD, b, c->compute, [&] {
         return launch_backward(a, c->compute);
@@ -1456,7 +1623,7 @@ sp_status sp_surrogate_grad(sp_ctx *c, const float *pooled, float *grad, int64_t
     if (!c || !pooled || !grad || count < 0 || count % 4) return SP_ERR_INVALID_ARG;
     if (c->poisoned != SP_OK) return c->poisoned;
     CK(cudaSetDevice(c->device));
-    if (count == 0) count = (long long)c->T * c->N * c->D;
+    if (count == 0) count = c->comm ? (long long)c->T_all * (c->N / c->world) * c->D : (long long)c->T * c->N * c->D;
     CK(launch(c, SP_K_SURROGATE, c->trained, c->compute,
               [&] { return launch_surrogate(pooled, grad, count, gamma, delta, c->compute); }));
     return SP_OK;
@@ -1642,7 +1809,7 @@ sp_status sp_run_steps(sp_ctx *c, const void *indices, int64_t num_batches, int6
         drop_graphs(c);
         c->gkey = key;
     }
-    const bool graphs_ok = !stats_out && !getenv("SP_NO_GRAPHS");
+    const bool graphs_ok = !stats_out && !getenv("SP_NO_GRAPHS") && !c->comm;  // sharded: eager steps
     for (int64_t k = 0; k < steps; k++) {
         if (sp_status s = check_async_error(c)) return s;
         // steady state: the look-ahead is full and one push per step keeps it so

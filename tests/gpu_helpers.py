@@ -52,7 +52,7 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
                gde=(0.5, 0.01, 0.01), index_dtype="int64", index_on_device=False, log_factor=0,
                check_plans=True, check_slots=True, check_pooled=True, trace=None,
                register_host=False, profile=False, sample_rows=None, host_alloc=False,
-               tables=None, policy_kw=None, padding=False, pinned=None, push=None):
+               tables=None, policy_kw=None, padding=False, pinned=None, push=None, sp_kw=None):
     """tables: pre-allocated host tables (HostTable or pinned tensors), already
     holding init(init_seed) values; policy_kw: extra ScratchPipe / Policy
     arguments of a replacement-policy variant (policy, policy_seed); padding:
@@ -72,7 +72,8 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
     pkw = dict(policy_kw or {})
     sp = ScratchPipe(rows, tables, D, slots, N, L, past=P, future=F, index_dtype=index_dtype,
                      index_on_device=index_on_device, log_factor=log_factor,
-                     register_host=register_host, profile=profile, padding=padding, **pkw)
+                     register_host=register_host, profile=profile, padding=padding, **pkw,
+                     **(sp_kw or {}))
     if pinned is not None:
         for t, ids in enumerate(pinned):
             if ids is not None and len(ids):

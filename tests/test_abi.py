@@ -37,7 +37,9 @@ def test_desc_struct_layout():
     # offsets of the C struct under the x86-64 SysV ABI
     assert B.SpDesc.rows.offset == 8 and B.SpDesc.host_tables.offset == 16
     assert B.SpDesc.stream.offset == 64 and B.SpDesc.policy.offset == 84
-    assert B.SpDesc.policy_seed.offset == 96 and ctypes.sizeof(B.SpDesc) == 104
+    assert B.SpDesc.policy_seed.offset == 96 and B.SpDesc.world.offset == 104
+    assert B.SpDesc.nccl_id.offset == 112 and B.SpDesc.table_ids.offset == 136
+    assert ctypes.sizeof(B.SpDesc) == 144
 
 
 def test_invalid_descriptors_rejected_before_touching_a_device():

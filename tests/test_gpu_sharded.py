@@ -93,3 +93,22 @@ def test_two_ranks_tablewise_match_oracle():
         assert err is None, err
         assert ntab >= 1
         assert worst <= 1e-5, (rank, worst)
+
+
+@pytest.mark.gpu
+def test_library_nccl_exchange_world1_matches_oracle():
+    """The library's own sharded path (sp_desc.world / nccl_id: NCCL
+    send/recv of every table's rows inside sp_forward / sp_train) at world
+    size 1 -- the only size one GPU allows; every message is a self
+    send/recv -- gives the oracle's pooled values and final tables."""
+    from paper_2205_04702_b200 import nccl_unique_id
+    from tests.gpu_helpers import max_window_union, run_parity
+    from workload import sample_trace
+    rows, D, N, L, nb = [700, 90, 2500], 16, 32, 2, 30
+    tr = sample_trace(rows, N, L, 0.9, nb, 91)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 6) for t, R in enumerate(rows)]
+    kw = dict(world=1, rank=0, nccl_id=nccl_unique_id(), table_owner=[0, 0, 0], table_ids=[0, 1, 2])
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr, gde=(0.5, 0.01, 0.02), policy_kw=None,
+                     sp_kw=kw)
+    assert rep["evictions"] > 50
+    assert rep["tables"]["max_rel"] <= 1e-5 and rep["tables"]["mismatch"] == 0, rep["tables"]

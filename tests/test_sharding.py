@@ -112,3 +112,104 @@ def test_gloo_world2_sharded_training_matches_single_process():
     for p in ps:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+# ---- the library's own sharded exchange (sp_shard_plan: the message lists
+# sp_forward / sp_train post to NCCL), checked on the host
+
+
+def _simulate(world, owner, T_all, N, D, seed):
+    """Run every rank's message list through NCCL's pairing rule (the k-th
+    send from i to j meets the k-th receive on j from i) on host arrays."""
+    from paper_2205_04702_b200 import shard_plan
+    rng = np.random.default_rng(seed)
+    full = rng.standard_normal((T_all, N, D)).astype(np.float32)
+    Ns = N // world
+    plans = [shard_plan(world, r, owner) for r in range(world)]
+    mine = [[t for t in range(T_all) if owner[t] == r] for r in range(world)]
+    local = [full[m] for m in mine]                       # [T_r][N][D] on rank r
+    out = [np.full((T_all, Ns, D), np.nan, np.float32) for _ in range(world)]
+    queues = {}
+    for r, (snd, _) in enumerate(plans):                  # posted sends, per (src, dst) in order
+        for peer, tl, tg in snd:
+            assert mine[r][tl] == tg
+            queues.setdefault((r, peer), []).append(local[r][tl, peer * Ns:(peer + 1) * Ns])
+    for r, (_, rcv) in enumerate(plans):
+        for peer, tg in rcv:
+            out[r][tg] = queues[(peer, r)].pop(0)
+    assert all(len(v) == 0 for v in queues.values())
+    for r in range(world):                                # forward: the batch shard of every table
+        assert np.array_equal(out[r], full[:, r * Ns:(r + 1) * Ns])
+    # backward: the mirror image (receives become sends) rebuilds [T_r][N][D]
+    back = [np.full_like(local[r], np.nan) for r in range(world)]
+    queues = {}
+    for r, (_, rcv) in enumerate(plans):
+        for peer, tg in rcv:
+            queues.setdefault((r, peer), []).append(out[r][tg] * 2 + 1)
+    for r, (snd, _) in enumerate(plans):
+        for peer, tl, tg in snd:
+            back[r][tl, peer * Ns:(peer + 1) * Ns] = queues[(peer, r)].pop(0)
+    for r in range(world):
+        assert np.array_equal(back[r], full[mine[r]] * 2 + 1)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_library_shard_plan_pairs_and_layout(world):
+    T_all = 26
+    for seed in range(3):
+        owner = lpt_assign(list(np.random.default_rng(seed).integers(1, 100, T_all)), world)
+        _simulate(world, owner, T_all, 8 * world, 4, seed)
+
+
+def test_library_shard_plan_rejects_bad_maps():
+    from paper_2205_04702_b200 import SpError, shard_plan
+    with pytest.raises(SpError):
+        shard_plan(2, 0, [0, 2])          # owner out of range
+    with pytest.raises(SpError):
+        shard_plan(2, 2, [0, 1])          # rank out of range
+
+
+def _lib_plan_worker(rank, world, port, q):
+    """Two processes post the library's message lists through gloo P2P in the
+    listed order (as sp_forward / sp_train post them to NCCL)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2205_04702_b200 import shard_plan
+    T_all, N, D = 7, 6, 3
+    owner = lpt_assign([9, 1, 4, 4, 2, 8, 3], world)
+    full = torch.arange(T_all * N * D, dtype=torch.float32).view(T_all, N, D)
+    mine = [t for t in range(T_all) if owner[t] == rank]
+    local = full[mine].contiguous()
+    Ns = N // world
+    snd, rcv = shard_plan(world, rank, owner)
+    out = torch.empty(T_all, Ns, D)
+    reqs = []
+    for peer, tl, tg in snd:
+        buf = local[tl, peer * Ns:(peer + 1) * Ns].contiguous()
+        reqs.append(dist.isend(buf, peer) if peer != rank else None)
+        if peer == rank:
+            out[tg] = buf
+    for peer, tg in rcv:
+        if peer != rank:
+            r = torch.empty(Ns, D)
+            dist.recv(r, peer)
+            out[tg] = r
+    for r in reqs:
+        if r is not None:
+            r.wait()
+    q.put((rank, bool(torch.equal(out, full[:, rank * Ns:(rank + 1) * Ns]))))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_library_message_order():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_lib_plan_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
