@@ -383,3 +383,17 @@ def test_transfer_modes_match_oracle(env, monkeypatch):
     assert rep["evictions"] > 200
     assert rep["stats"]["gpu_writeback"] == (env.get("SP_WRITEBACK") == "gpu")
     _assert_tables(rep)
+
+
+@pytest.mark.gpu
+def test_serial_strawman_schedule_matches_oracle(monkeypatch):
+    """The paper's straw-man design point (Fig. 10: stages back to back, no
+    overlap; bench --variant serial): every stage on the caller's stream
+    (SP_DIAG_SERIAL=1) gives the same plans, pooled values and tables."""
+    monkeypatch.setenv("SP_DIAG_SERIAL", "1")
+    rows, D, N, L, nb = [3000, 250, 40], 16, 48, 2, 40
+    tr = sample_trace(rows, N, L, 0.9, nb, 57)
+    slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 5) for t, R in enumerate(rows)]
+    rep = run_parity(rows, slots, D, N, L, nb, 3, 2, trace=tr, gde=(0.5, 0.01, 0.05))
+    assert rep["evictions"] > 200
+    _assert_tables(rep)
