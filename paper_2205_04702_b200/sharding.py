@@ -98,3 +98,77 @@ def exchange_backward(grad_batch: torch.Tensor, owner: Sequence[int], rank: int,
         out[:, sum(nb[:h]):sum(nb[:h + 1])] = recv[off:off + k].view(len(mine), nb[h], D)
         off += k
     return out
+
+
+# ---------------------------------------------------------------- row split
+# table-wise sharding of Terabyte caps the link-bound
+# speedup near 6x at G = 8 because a few 40M-row tables carry most of the
+# misses.  A table split by row range into k "virtual tables" (each its own
+# cache manager over the rows [lo, hi)) balances them: the
+# seeded Feistel permutation of the trace (reading R16) spreads hot rows
+# evenly over the ID range, so each piece sees ~1/k of the table's lookups
+# and misses.  A lookup of the table becomes a lookup of exactly one piece
+# and -1 (no lookup, SP_FLAG_PADDING) in the others, so with one lookup per
+# bag (L = 1, the Criteo shapes) the table's pooled row is the sum of its
+# pieces' pooled rows with all but one of them zero -- exact -- and each
+# piece's gradient is the table's gradient.
+
+def zipf_miss_weight(rows: Sequence[int], slots: Sequence[int], lookups: int, dim: int,
+                     alpha: float, link_only: bool = False) -> List[float]:
+    """Per-table cost: Train bytes plus host-link bytes (link_only: the
+    host-link bytes alone, the bound of the Criteo shapes), with the miss
+    share estimated as 1 - (Zipf(alpha) mass of the S hottest of R rows)."""
+    import math
+
+    def H(k):  # generalised harmonic number sum_{r<=k} r^-alpha (integral approximation)
+        if abs(alpha - 1.0) < 1e-9:
+            return math.log(k + 1.0) + 0.5772
+        return ((k + 1.0) ** (1.0 - alpha) - 1.0) / (1.0 - alpha) + 1.0
+    out = []
+    for R, S in zip(rows, slots):
+        miss = 0.0 if S >= R else max(0.0, 1.0 - H(S) / H(R))
+        out.append(lookups * dim * ((0.0 if link_only else 1.0) + 2.0 * miss))
+    return out
+
+
+def row_split(rows: Sequence[int], slots: Sequence[int], weights: Sequence[float], world: int,
+              factor: float = 4.0):
+    """Pieces [(table, row_lo, row_hi, slots, weight)]: a table heavier than
+    total / (factor * world) is cut into k equal row ranges so no piece
+    exceeds that; slots are split in proportion to rows (at least 1)."""
+    total = float(sum(weights))
+    cap = total / (factor * max(1, world)) if world > 1 else float("inf")
+    pieces = []
+    for t, (R, S, w) in enumerate(zip(rows, slots, weights)):
+        k = max(1, min(int(R), int(-(-w // cap)) if cap != float("inf") else 1))
+        for i in range(k):
+            lo, hi = R * i // k, R * (i + 1) // k
+            s = min(hi - lo, max(1, -(-S * (hi - lo) // R)))
+            pieces.append((t, lo, hi, s, w / k))
+    return pieces
+
+
+def split_trace(trace: torch.Tensor, pieces) -> torch.Tensor:
+    """[nb][T][N][L] -> [nb][V][N][L]: piece v = (t, lo, hi) sees id - lo for
+    lo <= id < hi and -1 (no lookup) elsewhere.  Input preparation (done once
+    per pre-generated trace, like the data loader's sharding)."""
+    outs = []
+    for t, lo, hi, _, _ in pieces:
+        x = trace[:, t]
+        inr = (x >= lo) & (x < hi)
+        outs.append(torch.where(inr, x - lo, torch.full_like(x, -1)))
+    return torch.stack(outs, dim=1).contiguous()
+
+
+def combine_pooled(pooled_v: torch.Tensor, pieces, num_tables: int) -> torch.Tensor:
+    """[V][N][D] pieces -> [T][N][D]: each table's pieces summed in piece
+    order (exact for one lookup per bag: all but one addend are zero)."""
+    out = torch.zeros((num_tables,) + tuple(pooled_v.shape[1:]), dtype=pooled_v.dtype, device=pooled_v.device)
+    for v, (t, _, _, _, _) in enumerate(pieces):
+        out[t] += pooled_v[v]
+    return out
+
+
+def expand_grad(grad: torch.Tensor, pieces) -> torch.Tensor:
+    """[T][N][D] -> [V][N][D]: every piece receives its table's gradient."""
+    return grad[[p[0] for p in pieces]].contiguous()

@@ -112,3 +112,44 @@ def test_library_nccl_exchange_world1_matches_oracle():
                      sp_kw=kw)
     assert rep["evictions"] > 50
     assert rep["tables"]["max_rel"] <= 1e-5 and rep["tables"]["mismatch"] == 0, rep["tables"]
+
+
+@pytest.mark.gpu
+def test_row_split_virtual_tables_match_unsplit_oracle():
+    """SURVEY §8(f) f1 row split: the 20k-row table is cut into 3 row ranges,
+    each its own context table (host rows = a sub-range view of the table,
+    -1 padding where a lookup falls in another piece).  With one lookup per
+    bag the pieces' pooled rows sum exactly to the table's, and the trained
+    host table equals the unsplit oracle's, bit for bit."""
+    from oracle import UncachedTrainer
+    from paper_2205_04702_b200 import ScratchPipe
+    from paper_2205_04702_b200.harness import run_loop
+    from paper_2205_04702_b200.sharding import combine_pooled, split_trace
+    from tests.gpu_helpers import max_window_union, pinned_tables
+    from workload import sample_trace
+    rows, D, N, L, nb = [20000, 300, 7], 16, 256, 1, 30
+    g, d, e = float(np.float32(0.5 / N)), float(np.float32(0.01 / N)), 1.0
+    tr = sample_trace(rows, N, L, 1.05, nb, 93)
+    tables = pinned_tables(rows, D, 4702)
+    pieces = [(0, 0, 7000, 0, 1.0), (0, 7000, 13000, 0, 1.0), (0, 13000, 20000, 0, 1.0),
+              (1, 0, 300, 0, 1.0), (2, 0, 7, 0, 1.0)]
+    vt = split_trace(tr, pieces)
+    vrows = [hi - lo for _, lo, hi, _, _ in pieces]
+    vslots = [min(R, max_window_union(vt.numpy(), v, 3, 2) + 4) for v, R in enumerate(vrows)]
+    views = [tables[t][lo:hi] for t, lo, hi, _, _ in pieces]
+    sp = ScratchPipe(vrows, views, D, vslots, N, L, padding=True)
+    orc = UncachedTrainer(rows, D, N, L, 4702)
+    bad = []
+
+    def on_pooled(b, pooled):
+        want = orc.step(tr.numpy()[b], g, d, e, want_pooled=True)
+        got = combine_pooled(pooled, pieces, 3).cpu().numpy()
+        if not np.array_equal(got, want):
+            bad.append(b)
+    run_loop(sp, vt, g, d, e, on_pooled=on_pooled)
+    assert not bad, bad
+    for t in range(3):
+        touched = orc.touched(t)
+        got = tables[t][torch.from_numpy(touched)].numpy()
+        assert np.array_equal(got, orc.rows_of(t, touched)), t
+    sp.close()

@@ -213,3 +213,56 @@ def test_gloo_world2_library_message_order():
     for p in ps:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+# ---- row split of the heaviest tables
+from paper_2205_04702_b200.sharding import (combine_pooled, expand_grad, row_split, split_trace,  # noqa: E402
+                                            zipf_miss_weight)
+
+
+def test_row_split_covers_rows_and_balances_terabyte():
+    from workload import CONFIGS
+    c = CONFIGS["terabyte"]
+    w = zipf_miss_weight(c.rows, c.slots, c.batch * c.pooling, c.dim, c.alpha, link_only=True)
+    for G in (2, 4, 8):
+        pieces = row_split(c.rows, c.slots, w, G)
+        for t, R in enumerate(c.rows):   # every row of every table in exactly one piece
+            rng = sorted((lo, hi) for tt, lo, hi, _, _ in pieces if tt == t)
+            assert rng[0][0] == 0 and rng[-1][1] == R
+            assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+        assert sum(p[3] for p in pieces) >= sum(c.slots)
+        whole = lpt_assign(w, G)
+        split = lpt_assign([p[4] for p in pieces], G)
+        lw = [sum(x for x, r in zip(w, whole) if r == k) for k in range(G)]
+        ls = [sum(p[4] for p, r in zip(pieces, split) if r == k) for k in range(G)]
+        # the speedup cap sum/max improves, and is within 30% of the ideal G
+        assert sum(ls) / max(ls) >= sum(lw) / max(lw) - 1e-9
+        assert sum(ls) / max(ls) >= 0.7 * G, (G, sum(ls) / max(ls))
+
+
+def test_split_trace_combine_is_exact_for_one_lookup_per_bag():
+    rows, N, D = [1000, 7], 16, 4
+    gen = torch.Generator().manual_seed(3)
+    trace = torch.stack([torch.randint(0, 1000, (5, N, 1), generator=gen),
+                         torch.randint(0, 7, (5, N, 1), generator=gen)], dim=1)
+    pieces = [(0, 0, 300, 10, 1.0), (0, 300, 1000, 20, 1.0), (1, 0, 7, 7, 1.0)]
+    vt = split_trace(trace, pieces)
+    assert vt.shape == (5, 3, N, 1)
+    # exactly one piece holds each lookup of table 0, shifted by its lo
+    hit = (vt[:, :2] >= 0).sum(dim=1)
+    assert torch.all(hit == 1)
+    back = torch.where(vt[:, 0] >= 0, vt[:, 0], vt[:, 1] + 300)
+    assert torch.equal(back, trace[:, 0])
+    # pooled: a row table E, pooled_v = E[lo + id] or 0 -> combined == E[id]
+    E = torch.randn(1000, D)
+    pv = []
+    for v, (_, lo, _, _, _) in enumerate(pieces[:2]):
+        ids = vt[0, v, :, 0]
+        pv.append(torch.where((ids >= 0).unsqueeze(1), E[(ids + lo).clamp(0, 999)], torch.zeros(N, D)))
+    pv = torch.stack(pv)
+    pv = torch.cat([pv, torch.zeros(1, N, D)])
+    comb = combine_pooled(pv, pieces, 2)
+    assert torch.equal(comb[0], E[trace[0, 0, :, 0]])
+    g = torch.randn(2, N, D)
+    ge = expand_grad(g, pieces)
+    assert torch.equal(ge[0], g[0]) and torch.equal(ge[1], g[0]) and torch.equal(ge[2], g[1])
