@@ -50,7 +50,8 @@
  *   SP_CPU_GATHER=0|1     0: the transfer kernel pulls the missed rows from
  *                         their random host rows itself; 1: CPU threads gather
  *                         them into a contiguous pinned slot first (default:
- *                         1 when T*N*L*dim*4 <= 32 MB, i.e. few rows per batch)
+ *                         all gathered when T*N*L*dim*4 <= 32 MB, i.e. few rows
+ *                         per batch; above, the hybrid split with f = 0.5)
  *   SP_WRITEBACK=gpu|cpu  victims' write-back: gpu = the transfer kernel stores
  *                         each victim row straight into its host row (TMA bulk
  *                         store); cpu = staged contiguously, CPU threads scatter
@@ -128,9 +129,10 @@ typedef struct {
     uint32_t flags;              /* SP_FLAG_*                                       */
     int32_t log_factor;          /* LRU-log ring capacity per table =               */
                                  /* log_factor * slots[t] + 4*N*L (0 -> 8)          */
-    int32_t host_threads;        /* CPU helper threads that, with the scatter       */
-                                 /* thread, copy staged victims into their host     */
-                                 /* rows (0 -> 3)                                   */
+    int32_t host_threads;        /* CPU row-copy helpers per transfer-engine pool   */
+                                 /* (gather, scatter); 0 -> from the node's cores:  */
+                                 /* (ncpu - pools) / pools, pools = 2 * max(1,      */
+                                 /* world) contexts' pools, clamped to [1, 6]       */
     int32_t policy;              /* replacement policy among the window-safe        */
                                  /* candidates: SP_POLICY_*           */
     uint32_t reserved;           /* must be 0                                       */

@@ -26,6 +26,7 @@
 #include <dlfcn.h>
 #include <immintrin.h>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <array>
@@ -1095,7 +1096,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     for (int t = 0; t < c->T; t++) c->slot_base[t + 1] = c->slot_base[t] + (uint32_t)c->slots[t];
     c->hit_total = c->row_off[c->T];
     c->XSR = std::max(4, c->F + 2);  // >= F+1: Transfer(b) waits for scatter(b-F-1) >= b-XSR
-    c->host_threads = d->host_threads > 0 ? d->host_threads : 3;
+    c->host_threads = d->host_threads;  // 0: sized from the node's cores below
     // transfer grid: 16 one-warp CTAs (measured best on Kaggle and Terabyte;
     // 30 / 48 CTAs were 11% / 18% slower on Terabyte: more SMs add interference,
     // not host-link throughput)
@@ -1292,8 +1293,18 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     // dominates): +8-9% on Kaggle (T*n*D*4 = 13.6 MB); the GPU pull wins on
     // Terabyte (54.5 MB: 7.0k vs 6.0k it/s) and high-pooling (671 MB: 96 vs
     // 54 it/s), where the CPU copy threads become the bound
-    c->cpu_gather = (double)c->T * c->n * c->D * sizeof(float) <= 32.0 * (1 << 20);
-    if (const char *e = getenv("SP_CPU_GATHER")) c->cpu_gather = atoi(e) != 0;
+    // Missed rows: all gathered by the CPU when a batch's rows are few
+    // (latency, not copy bandwidth, dominates: Kaggle); above 32 MB of rows
+    // per batch the hybrid split, half gathered by the CPU while the transfer
+    // kernel pulls the other half (Terabyte, measured: 8.0k vs 7.0k it/s for
+    // the pure GPU pull, whose random host reads are bound by host-side
+    // address translation and slow the Train kernels; profiles/r02_a3_sweep)
+    c->cpu_gather = true;
+    if ((double)c->T * c->n * c->D * sizeof(float) > 32.0 * (1 << 20)) c->gather_q16 = 32768;
+    if (const char *e = getenv("SP_CPU_GATHER")) {  // 1: every missed row gathered, 0: every one pulled
+        c->cpu_gather = atoi(e) != 0;
+        c->gather_q16 = 65536;
+    }
     // hybrid split (SP_GATHER_FRAC in (0, 1)): the CPU gathers that share of
     // each batch's missed rows while the transfer kernel pulls the rest
     if (const char *e = getenv("SP_GATHER_FRAC")) {
@@ -1308,6 +1319,14 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         }
     }
     if (const char *e = getenv("SP_WRITEBACK")) c->gpu_wb = std::string(e) == "gpu";
+    if (c->host_threads <= 0) {
+        // row-copy helpers per pool from the node's cores, shared by the
+        // contexts of one node (one per GPU: desc.world of them), at most 6
+        const long ncpu = std::max(1L, sysconf(_SC_NPROCESSORS_ONLN));
+        const long ctx = std::max(1, d->world);
+        const long pools = (c->cpu_gather ? 2 : 1) * ctx;
+        c->host_threads = (int)std::max(1L, std::min(6L, (ncpu - pools) / pools));
+    }
     if (c->cpu_gather) {
         CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
         CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
