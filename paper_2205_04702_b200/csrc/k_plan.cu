@@ -380,9 +380,10 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
         } else if (is_hot) {
             chunk_first[u] = EMPTY;
             const uint32_t h0 = hcarry + hx;
-            for (uint32_t k = 0; k < nseg; k++)
+            for (uint32_t k = 0; k < nseg; k++) {
                 hot[h0 + k] = make_uint4(u, lo + k * hs, min(hs, len - k * hs) | (nseg << HOT_LEN_BITS), k);
-            hcnt[h0] = 0u;
+                hcnt[h0 + k] = 0u;  // row counter at k = 0, group-of-8 counters after it (k_bwd)
+            }
         }
         carry += tot;
         hcarry += htot;

@@ -48,8 +48,8 @@ __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
 // indices, then their rows for lookup position p, are all in flight together,
 // so even L = 1 (one row per bag) keeps BU rows per group outstanding.  Each
 // bag is still a left fold in ascending p (bit-exact with the oracle).
-template <int G, int VPL>
-__global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
+template <int G, int VPL, bool PAD>
+__device__ __forceinline__ void fwd_body(const TrainArgs &A) {
     if (*A.err != NO_ERR) return;
     constexpr int BU = VPL >= 4 ? 1 : (VPL == 2 ? 2 : 4);
     const int L = A.g.L, D4 = A.g.D / 4;
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
     const float4 *st = reinterpret_cast<const float4 *>(A.storage) + lane;
     float4 *out = reinterpret_cast<float4 *>(A.pooled) + lane;
     const long long S = (long long)gridDim.x * gpb;
-    if (A.g.pad) {
+    if constexpr (PAD) {
         // ragged bags (-1 padding, reading R27): a padded position has slot
         // EMPTY and is skipped; a bag with no lookup pools to zeros; the fold
         // starts from the first real row (as the oracle's)
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
             for (int v = 0; v < VPL; v++) __stcs(out + bag * D4 + v * G, acc[v]);
         }
         return;
-    }
+    } else {
     for (long long bag0 = (long long)blockIdx.x * gpb + threadIdx.x / G; bag0 < nbags; bag0 += BU * S) {
         const uint32_t *so[BU];
         bool ok[BU];
@@ -121,10 +121,17 @@ __global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
 #pragma unroll
                 for (int v = 0; v < VPL; v++) __stcs(out + (bag0 + u * S) * D4 + v * G, acc[u][v]);
     }
+    }
 }
 
+template <int G, int VPL>
+__global__ void __launch_bounds__(256) k_fwd(TrainArgs A) { fwd_body<G, VPL, false>(A); }
+// ragged bags (SP_FLAG_PADDING): its own instance keeps the fixed-L kernel lean
+template <int G, int VPL>
+__global__ void __launch_bounds__(256) k_fwd_pad(TrainArgs A) { fwd_body<G, VPL, true>(A); }
+
 // generic D (D/4 not a power-of-two multiple of 32): 32 lanes, strided columns
-__global__ void __launch_bounds__(256) k_fwd_generic(TrainArgs A) {
+__device__ __forceinline__ void fwd_generic_body(const TrainArgs &A) {
     if (*A.err != NO_ERR) return;
     const int L = A.g.L, D4 = A.g.D / 4;
     const long long nbags = (long long)A.g.T * A.g.N;
@@ -149,6 +156,9 @@ __global__ void __launch_bounds__(256) k_fwd_generic(TrainArgs A) {
         }
     }
 }
+
+__global__ void __launch_bounds__(256) k_fwd_generic(TrainArgs A) { fwd_generic_body(A); }
+__global__ void __launch_bounds__(256) k_fwd_pad_generic(TrainArgs A) { fwd_generic_body(A); }
 
 // --------------------------------------------------------------- backward
 struct Acc4 { double x, y, z, w; };
@@ -181,6 +191,17 @@ __device__ __forceinline__ double4 shfl_xor_d4(const double4 &v, int m) {
                         __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
 }
 
+// tuning knobs (measured defaults; -D overrides for A/B builds)
+#ifndef SP_BWD_RB
+#define SP_BWD_RB 4   // D <= 128: gradient rows of a hot segment in flight per lane group
+#endif
+#ifndef SP_BWD_RQ
+#define SP_BWD_RQ 4   // D <= 128: chunk records folded together per lane group
+#endif
+#ifndef SP_BWD_MINB
+#define SP_BWD_MINB 2 // resident CTAs per SM the register budget is sized for
+#endif
+
 // Warp-centric: every work item belongs to one warp (hot-row segment) or one
 // lane group of G lanes (chunk records), so there is no block barrier after
 // the prologue and every warp keeps several rows in flight.
@@ -200,13 +221,12 @@ __device__ __forceinline__ double4 shfl_xor_d4(const double4 &v, int m) {
 //     in fp64 in ascending occurrence order.  One owner per unique row: no
 //     atomics on Storage.
 template <int G, int VPL>
-__global__ void __launch_bounds__(256, 2) k_bwd(TrainArgs A) {
+__global__ void __launch_bounds__(256, SP_BWD_MINB) k_bwd(TrainArgs A) {
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
     const int D4 = g.D / 4;
     constexpr int NG = 32 / G;                                 // lane groups per warp
-    constexpr int RB = VPL >= 4 ? 1 : (VPL == 2 ? 4 : 8);      // hot rows in flight per group
-    constexpr int BU = VPL >= 2 ? 1 : 2;                       // chunk records per group at once
+    constexpr int RB = VPL >= 4 ? 1 : (VPL == 2 ? 2 : SP_BWD_RB);  // hot rows in flight per group
     __shared__ uint32_t s_ph[65], s_pc[65];
     const int lane = threadIdx.x % G;
     const int grp = (threadIdx.x & 31) / G;
@@ -271,101 +291,129 @@ __global__ void __launch_bounds__(256, 2) k_bwd(TrainArgs A) {
                     }
                 continue;
             }
-            double4 *part = reinterpret_cast<double4 *>(A.partial + ((size_t)t * g.nh + h) * g.D) + lane;
+            // several segments: fp64 partials meet in a two-level fixed tree --
+            // the last of each group of 8 consecutive segments folds the
+            // group's partials in order, the last group folds the group sums in
+            // order and applies SGD (the shape depends only on nseg)
+            double *prow = A.partial + ((size_t)t * g.nh + (h - k)) * g.D;  // segment 0 of the row
+            uint32_t *cnt = A.bb.hot_cnt + (size_t)t * g.nh + (h - k);
             if (grp == 0)
 #pragma unroll
-                for (int v = 0; v < VPL; v++) part[v * G] = make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
-            __threadfence();
-            __syncwarp();
-            uint32_t last = 0;
-            if ((threadIdx.x & 31) == 0) last = atomicAdd(&A.bb.hot_cnt[(size_t)t * g.nh + (h - k)], 1u) == nseg - 1;
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (!last) continue;
-            // the last segment folds the row's nseg partials in segment order:
-            // lane l of the warp owns float4 columns l, l+32, ... (4 in flight)
-            __threadfence();
-            const double4 *p0 = reinterpret_cast<const double4 *>(A.partial + ((size_t)t * g.nh + (h - k)) * g.D);
-            for (int col = threadIdx.x & 31; col < D4; col += 32) {
+                for (int v = 0; v < VPL; v++)
+                    reinterpret_cast<double4 *>(prow + (size_t)k * g.D)[lane + v * G] =
+                        make_double4(acc[v].x, acc[v].y, acc[v].z, acc[v].w);
+            const uint32_t ng = (nseg + 7u) / 8u, grpi = k / 8u, gsz = min(8u, nseg - 8u * grpi);
+            auto arrive = [&](uint32_t *ctr, uint32_t total) {
+                __threadfence();
+                __syncwarp();
+                uint32_t last = 0;
+                if ((threadIdx.x & 31) == 0) last = atomicAdd(ctr, 1u) == total - 1u;
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (last) __threadfence();
+                return last != 0;
+            };
+            // fold `count` partials at stride `step` segments from `first` (lane l: float4 columns l, l+32, ...)
+            auto fold = [&](uint32_t first, uint32_t count, uint32_t step, int col) {
+                const double4 *p0 = reinterpret_cast<const double4 *>(prow) + col;
                 double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
-                uint32_t kk = 0;
-                for (; kk + 4 <= nseg; kk += 4) {
-                    double4 q[4];
+                uint32_t q = 0;
+                for (; q + 2 <= count; q += 2) {
+                    double4 x[2];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) q[u] = ldcg_d4(p0 + (size_t)(kk + u) * D4 + col);
+                    for (int u = 0; u < 2; u++) x[u] = ldcg_d4(p0 + (size_t)(first + (q + u) * step) * D4);
 #pragma unroll
-                    for (int u = 0; u < 4; u++) { m.x += q[u].x; m.y += q[u].y; m.z += q[u].z; m.w += q[u].w; }
+                    for (int u = 0; u < 2; u++) { m.x += x[u].x; m.y += x[u].y; m.z += x[u].z; m.w += x[u].w; }
                 }
-                for (; kk < nseg; kk++) {
-                    const double4 q = ldcg_d4(p0 + (size_t)kk * D4 + col);
-                    m.x += q.x; m.y += q.y; m.z += q.z; m.w += q.w;
+                for (; q < count; q++) {
+                    const double4 x = ldcg_d4(p0 + (size_t)(first + q * step) * D4);
+                    m.x += x.x; m.y += x.y; m.z += x.z; m.w += x.w;
                 }
+                return m;
+            };
+            if (ng > 1) {
+                if (!arrive(cnt + 1 + grpi, gsz)) continue;
+                for (int col = threadIdx.x & 31; col < D4; col += 32) {  // group sum -> its first segment's slot
+                    const double4 m = fold(8u * grpi, gsz, 1u, col);
+                    reinterpret_cast<double4 *>(prow + (size_t)(8u * grpi) * g.D)[col] = m;
+                }
+            }
+            if (!arrive(cnt, ng > 1 ? ng : nseg)) continue;
+            for (int col = threadIdx.x & 31; col < D4; col += 32) {
+                const double4 m = ng > 1 ? fold(0u, ng, 8u, col) : fold(0u, nseg, 1u, col);
                 float4 *wp = st + (size_t)slot * D4 + col;
                 *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
             }
         }
-        // ---- N: BU chunk records per lane group at once
-        const long long GG = W * NG;
-        const long long gg = gw * NG + grp;
-        for (long long c0 = gg * BU; c0 < Ct; c0 += GG * BU) {
-            uint4 hd[BU];
-            const ChunkRec *rp[BU];
-            int tt[BU];
-#pragma unroll
-            for (int u = 0; u < BU; u++) {
-                const long long c = c0 + u;
-                if (c < Ct) {
-                    const int tl = find_table(s_pc, tcount, (uint32_t)c);
-                    tt[u] = t0 + tl;
-                    rp[u] = A.bb.chunk_rec + (size_t)tt[u] * g.nc + ((uint32_t)c - s_pc[tl]);
-                    hd[u] = __ldg(reinterpret_cast<const uint4 *>(rp[u]));  // slot, len, bag0, bag1
-                } else {
-                    tt[u] = 0;
-                    rp[u] = nullptr;
-                    hd[u] = make_uint4(0, 0, 0, 0);
-                }
+        // ---- N: chunk records in warp batches of 32: lane i loads the header
+        // (slot, len, bag0, bag1) of record base+i in one coalesced read, then
+        // each lane group folds RQ records per sub-round with every Storage
+        // and gradient row of those records in flight together
+        constexpr int RQ = VPL >= 4 ? 1 : (VPL == 2 ? 2 : SP_BWD_RQ);
+        for (long long base = gw * 32; base < Ct; base += W * 32) {
+            uint4 myhd = make_uint4(0, 0, 0, 0);
+            uint32_t mytt = 0, myci = 0;
+            if (base + (threadIdx.x & 31) < Ct) {
+                const uint32_t c = (uint32_t)(base + (threadIdx.x & 31));
+                const int tl = find_table(s_pc, tcount, c);
+                mytt = (uint32_t)(t0 + tl);
+                myci = c - s_pc[tl];
+                myhd = __ldg(reinterpret_cast<const uint4 *>(A.bb.chunk_rec + (size_t)mytt * g.nc + myci));
             }
-            float4 w[BU][VPL], g0[BU][VPL], g1[BU][VPL];
+            const uint32_t nrec = (uint32_t)min(32ll, Ct - base);
+            uint32_t longm = 0;  // records (warp-batch index) with > 2 occurrences, folded below
+            for (uint32_t j0 = 0; j0 < nrec; j0 += NG * RQ) {
+                uint4 hd[RQ];
+                uint32_t tt[RQ];
 #pragma unroll
-            for (int u = 0; u < BU; u++) {
-                if (hd[u].y == 0u) continue;
-                const float4 *gb = grad + (size_t)tt[u] * g.N * D4 + lane;
-#pragma unroll
-                for (int v = 0; v < VPL; v++) {
-                    w[u][v] = st[(size_t)hd[u].x * D4 + lane + v * G];
-                    g0[u][v] = __ldg(gb + (size_t)hd[u].z * D4 + v * G);
-                    if (hd[u].y >= 2u) g1[u][v] = __ldg(gb + (size_t)hd[u].w * D4 + v * G);
+                for (int q = 0; q < RQ; q++) {
+                    const int src = (int)(j0 + q * NG + grp);  // this group's q-th record of the sub-round
+                    hd[q].x = __shfl_sync(0xffffffffu, myhd.x, src & 31);
+                    hd[q].y = __shfl_sync(0xffffffffu, myhd.y, src & 31);
+                    hd[q].z = __shfl_sync(0xffffffffu, myhd.z, src & 31);
+                    hd[q].w = __shfl_sync(0xffffffffu, myhd.w, src & 31);
+                    tt[q] = __shfl_sync(0xffffffffu, mytt, src & 31);
+                    if (src >= (int)nrec) hd[q].y = 0u;
                 }
-            }
-            uint32_t longm = 0;  // records with > 2 occurrences: folded below, from scratch
+                float4 w[RQ][VPL], g0[RQ][VPL], g1[RQ][VPL];
 #pragma unroll
-            for (int u = 0; u < BU; u++) {
-                const uint32_t len = hd[u].y;
-                if (len == 0u) continue;
-                if (len > 2u) {
-                    longm |= 1u << u;
-                    continue;
+                for (int q = 0; q < RQ; q++) {
+                    if (hd[q].y == 0u || hd[q].y > 2u) continue;
+                    const float4 *gb = grad + (size_t)tt[q] * g.N * D4 + lane;
+#pragma unroll
+                    for (int v = 0; v < VPL; v++) {
+                        w[q][v] = st[(size_t)hd[q].x * D4 + lane + v * G];
+                        g0[q][v] = __ldg(gb + (size_t)hd[q].z * D4 + v * G);
+                        if (hd[q].y == 2u) g1[q][v] = __ldg(gb + (size_t)hd[q].w * D4 + v * G);
+                    }
                 }
-                float4 *wp = st + (size_t)hd[u].x * D4 + lane;
 #pragma unroll
-                for (int v = 0; v < VPL; v++) {
-                    float4 s = g0[u][v];
-                    if (len == 2u) { s.x += g1[u][v].x; s.y += g1[u][v].y; s.z += g1[u][v].z; s.w += g1[u][v].w; }
-                    wp[v * G] = sgd32(w[u][v], s, A.lr);
+                for (int q = 0; q < RQ; q++) {
+                    const uint32_t len = hd[q].y;
+                    if (len == 0u) continue;
+                    if (len > 2u) {
+                        longm |= 1u << (j0 + q * NG + grp);
+                        continue;
+                    }
+                    float4 *wp = st + (size_t)hd[q].x * D4 + lane;
+#pragma unroll
+                    for (int v = 0; v < VPL; v++) {
+                        float4 sg = g0[q][v];
+                        if (len == 2u) { sg.x += g1[q][v].x; sg.y += g1[q][v].y; sg.z += g1[q][v].z; sg.w += g1[q][v].w; }
+                        wp[v * G] = sgd32(w[q][v], sg, A.lr);
+                    }
                 }
             }
             // > 2 occurrences (rare in the Zipf tail): fp64 in ascending
-            // occurrence order, every gradient row (re)loaded here
+            // occurrence order, this group's own records of the batch
             while (longm) {
-                const int u = __ffs(longm) - 1;
+                const int i = __ffs(longm) - 1;
                 longm &= longm - 1;
-                const ChunkRec *rc = A.bb.chunk_rec;
-                int tu = 0;
-                uint32_t slot = 0, len = 0;
-                const uint32_t *bags = nullptr;
-#pragma unroll
-                for (int q = 0; q < BU; q++)
-                    if (q == u) { rc = rp[q]; tu = tt[q]; slot = hd[q].x; len = hd[q].y; }
-                bags = rc->bag;
+                const uint32_t slot = __shfl_sync(0xffffffffu, myhd.x, i);  // (every lane: uniform i)
+                const uint32_t len = __shfl_sync(0xffffffffu, myhd.y, i);
+                const uint32_t tu = __shfl_sync(0xffffffffu, mytt, i);
+                const uint32_t cu = __shfl_sync(0xffffffffu, myci, i);
+                if ((i % NG) != grp) continue;  // owned by another group of the warp
+                const uint32_t *bags = A.bb.chunk_rec[(size_t)tu * g.nc + cu].bag;
                 const float4 *gb = grad + (size_t)tu * g.N * D4 + lane;
                 float4 *wp = st + (size_t)slot * D4 + lane;
                 Acc4 acc[VPL];
@@ -551,7 +599,11 @@ static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStr
 
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
-    SP_DISPATCH_D(D4, k_fwd, (long long)a.g.T * a.g.N, a, s, false);
+    if (a.g.pad) {
+        SP_DISPATCH_D(D4, k_fwd_pad, (long long)a.g.T * a.g.N, a, s, false);
+    } else {
+        SP_DISPATCH_D(D4, k_fwd, (long long)a.g.T * a.g.N, a, s, false);
+    }
     return cudaGetLastError();
 }
 
