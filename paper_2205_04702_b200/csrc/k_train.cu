@@ -404,7 +404,10 @@ __global__ void __launch_bounds__(256, SP_BWD_MINB) k_bwd(TrainArgs A) {
                 }
             }
             // > 2 occurrences (rare in the Zipf tail): fp64 in ascending
-            // occurrence order, this group's own records of the batch
+            // occurrence order, this group's own records of the batch.  Each
+            // group marked only its own records: the union makes the loop
+            // (and its full-warp shuffles) warp-uniform.
+            longm = __reduce_or_sync(0xffffffffu, longm);
             while (longm) {
                 const int i = __ffs(longm) - 1;
                 longm &= longm - 1;
