@@ -340,6 +340,13 @@ __device__ void dedup_table(const PushArgs &A, int t, unsigned char *smem_raw, l
     if (tid == 0) { seg_off[U] = (uint32_t)n_real; nb.U[t] = U; }
     __syncthreads();
     pc.mark(2);
+    if (!A.bwd_recs) {  // the tiled backward reads sorted_occ / sorted_uid / seg_off only
+        if (A.prof) {
+            pc.mark(3);
+            pc.mark(4);
+        }
+        return;
+    }
     // D3a: backward work lists.  A unique with <= CH occurrences is one chunk
     // record (its bag indices inline); a hot unique (> CH occurrences, the
     // Zipf head) is cut into segments of <= hs occurrences, one hot record
@@ -820,11 +827,13 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
         for (int q = 0; q < 4; q++)
             if (i0 + q * (int)blockDim.x < n) slot_of_occ[o[q]] = sl[q];
     }
-    ChunkRec *rec = pb.chunk_rec + (size_t)t * g.nc;
-    uint4 *hot = pb.hot_rec + (size_t)t * g.nh;
-    const uint32_t nch = pb.nchunks[t], nhot = pb.nhot[t];
-    for (uint32_t c = tid; c < nch; c += blockDim.x) rec[c].slot = slot_l[rec[c].slot];
-    for (uint32_t h = tid; h < nhot; h += blockDim.x) hot[h].x = slot_l[hot[h].x];
+    if (A.bwd_recs) {  // (the tiled backward reads slot_u)
+        ChunkRec *rec = pb.chunk_rec + (size_t)t * g.nc;
+        uint4 *hot = pb.hot_rec + (size_t)t * g.nh;
+        const uint32_t nch = pb.nchunks[t], nhot = pb.nhot[t];
+        for (uint32_t c = tid; c < nch; c += blockDim.x) rec[c].slot = slot_l[rec[c].slot];
+        for (uint32_t h = tid; h < nhot; h += blockDim.x) hot[h].x = slot_l[hot[h].x];
+    }
     if (A.prof) {
         __syncthreads();
         pc.mark(5);

@@ -444,6 +444,236 @@ __global__ void __launch_bounds__(256, SP_BWD_MINB) k_bwd(TrainArgs A) {
     }
 }
 
+// ------------------------------------------------ backward, tiled (default)
+// The sorted occurrence list of each table (built at dedup: occurrences
+// grouped by unique row, ascending within a row) is cut into fixed tiles of
+// TR rows; one warp (one CTA) takes a tile at a time:
+//   1. lane r reads sorted occurrence r of the tile and its unique (coalesced)
+//      and issues ONE TMA bulk copy (cp.async.bulk) of that occurrence's
+//      gradient row pooled_grad[t][occ / L] into shared memory; the first lane
+//      of every row that lies wholly inside the tile also bulk-copies the
+//      row's Storage row.  All of the tile's rows are in flight at once on
+//      one mbarrier -- the memory-level parallelism comes from the copy
+//      engine, not from registers.
+//   2. the warp folds the tile's rows in order, lane c owning float4 column
+//      c (+32, ...), in fp64 (reading R7).  At the end of a row wholly inside
+//      the tile: w = fmaf(-lr, (float)sum, w) straight to Storage (the whole
+//      row's sum in ascending occurrence order: the oracle's order).
+//   3. a row spanning several tiles (the Zipf head) leaves one fp64 piece per
+//      tile; the last piece to arrive (counter per row) folds the pieces in
+//      tile order -- through a second level of groups of 8 pieces when there
+//      are more than 8 -- and applies SGD.  The fold shape depends only on the
+//      row's position in the sorted list, never on the grid.
+// Every tile is the same size whatever the skew, so the grid is balanced by
+// construction (no hot/cold work lists, no dynamic work counters); one owner
+// per unique row, so no atomics on Storage.
+namespace {
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool bar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void row_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void dadd4(double4 &a, const double4 &b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+__device__ __forceinline__ double4 ld_piece(const double *p) {  // L2: written by other SMs
+    return ldcg_d4(reinterpret_cast<const double4 *>(p));
+}
+// warp-wide "last of `total` arrivals at *ctr" (release before, acquire after)
+__device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total) {
+    __threadfence();
+    __syncwarp();
+    uint32_t last = 0;
+    if ((threadIdx.x & 31) == 0) last = atomicAdd(ctr, 1u) == total - 1u;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) __threadfence();
+    return last != 0;
+}
+}  // namespace
+
+template <int VPL>
+__global__ void __launch_bounds__(32) k_bwd_tile(TrainArgs A) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t bar;
+    if (*A.err != NO_ERR) return;
+    const Geometry g = A.g;
+    const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
+    const uint32_t rowb = (uint32_t)g.D * 4u;
+    const int lane = threadIdx.x;
+    float4 *sg = reinterpret_cast<float4 *>(sm);  // [TR][D4] gradient rows of the tile
+    float4 *sw = sg + (size_t)TR * D4;            // [TR][D4] Storage rows (at their first row)
+    const float4 *grad = reinterpret_cast<const float4 *>(A.grad);
+    float4 *st = reinterpret_cast<float4 *>(A.storage);
+    if (lane == 0) bar_init(&bar);
+    __syncwarp();
+    griddep_wait();  // (PDL) the surrogate's gradients are complete from here on
+    uint32_t parity = 0;
+    const long long total = (long long)g.T * NT;
+    for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int t = (int)(tile / NT), k = (int)(tile % NT);
+        const int lo = k * TR;
+        const int nrows = min(TR, g.n - lo);
+        const size_t tb = (size_t)t * g.n;
+        // 1. the tile's occurrences, their uniques, the rows' boundaries
+        uint32_t occ = 0, uid = EMPTY;
+        if (lane < nrows) {
+            occ = __ldg(A.bb.sorted_occ + tb + lo + lane);
+            uid = __ldg(A.bb.sorted_uid + tb + lo + lane);  // EMPTY: padding (sorts last)
+        }
+        const bool act = uid != EMPTY;
+        const unsigned amask = __ballot_sync(0xffffffffu, act);
+        if (amask == 0u) continue;  // (warp-uniform)
+        const int nact = 32 - __clz(amask);  // active rows are a prefix
+        const uint32_t up = __shfl_up_sync(0xffffffffu, uid, 1), dn = __shfl_down_sync(0xffffffffu, uid, 1);
+        const bool first = act && (lane == 0 || up != uid);
+        const bool lastr = act && (lane == nact - 1 || dn != uid);
+        // does the row of the tile's first / last active occurrence extend
+        // beyond the tile?  (segment offsets of those two rows only)
+        uint32_t seg_lo = 0, seg_hi = 0;
+        if (lane == 0) seg_lo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + uid);
+        if (lane == nact - 1) seg_hi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + uid + 1);
+        const bool head_open = __shfl_sync(0xffffffffu, seg_lo, 0) < (uint32_t)lo;
+        const bool tail_open = __shfl_sync(0xffffffffu, seg_hi, nact - 1) > (uint32_t)(lo + nact);
+        const uint32_t uid_last = __shfl_sync(0xffffffffu, uid, nact - 1);
+        const bool whole = first && !(lane == 0 && head_open) && !(uid == uid_last && tail_open);
+        uint32_t slot = 0;
+        if (whole) slot = __ldg(A.bb.slot_u + tb + uid);
+        const unsigned wmask = __ballot_sync(0xffffffffu, whole);
+        const unsigned fmask = __ballot_sync(0xffffffffu, first);
+        const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
+        if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
+        __syncwarp();
+        if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + occ / (uint32_t)g.L) * D4, rowb, &bar);
+        if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowb, &bar);
+        while (!bar_try(&bar, parity)) {
+        }
+        parity ^= 1u;
+        // 2. fold in order; 3. pieces of rows spanning tiles
+        double4 acc[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; v++) acc[v] = make_double4(0.0, 0.0, 0.0, 0.0);
+        int r0 = 0;  // first row of the current segment within the tile
+        for (int r = 0; r < nact; r++) {
+#pragma unroll
+            for (int v = 0; v < VPL; v++) {
+                const int c = lane + 32 * v;
+                if (c < D4) {
+                    const float4 x = sg[(size_t)r * D4 + c];
+                    acc[v].x += (double)x.x; acc[v].y += (double)x.y; acc[v].z += (double)x.z; acc[v].w += (double)x.w;
+                }
+            }
+            if (!((lmask >> r) & 1u)) continue;
+            const uint32_t s = __shfl_sync(0xffffffffu, slot, r0);
+            if ((wmask >> r0) & 1u) {  // the whole row is in this tile
+#pragma unroll
+                for (int v = 0; v < VPL; v++) {
+                    const int c = lane + 32 * v;
+                    if (c < D4)
+                        st[(size_t)s * D4 + c] =
+                            sgd(sw[(size_t)r0 * D4 + c], Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr);
+                }
+            } else {
+                // a piece of a row spanning tiles [kf, kl]: slot 0 of tile k if
+                // the row holds the tile's first occurrence, else slot 1 (only
+                // possible in the row's first tile)
+                const uint32_t u = __shfl_sync(0xffffffffu, uid, r0);
+                uint32_t slo = 0, shi = 0;
+                if (lane == 0) {
+                    slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u);
+                    shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
+                }
+                slo = __shfl_sync(0xffffffffu, slo, 0);
+                shi = __shfl_sync(0xffffffffu, shi, 0);
+                const int kf = (int)(slo / (uint32_t)TR), kl = (int)((shi - 1u) / (uint32_t)TR);
+                const int npc = kl - kf + 1;
+                auto pslot = [&](int kk) { return (kk == kf && slo != (uint32_t)(kf * TR)) ? 1 : 0; };
+                auto piece = [&](int kk) { return A.tpart + (((size_t)t * NT + kk) * 2 + pslot(kk)) * g.D; };
+                double *mine = piece(k);
+#pragma unroll
+                for (int v = 0; v < VPL; v++) {
+                    const int c = lane + 32 * v;
+                    if (c < D4) reinterpret_cast<double4 *>(mine)[c] = acc[v];
+                }
+                bool go = true;
+                int step = 1, cnt = npc;
+                if (npc > 8) {  // level 1: groups of 8 consecutive pieces
+                    const int gi = (k - kf) / 8, g0 = kf + 8 * gi, gsz = min(8, kl - g0 + 1);
+                    uint32_t *gc = A.grp_cnt + ((size_t)t * NT + g0) * 2 + pslot(g0);
+                    go = warp_arrive_last(gc, (uint32_t)gsz);
+                    if (go) {
+                        if (lane == 0) *gc = 0u;
+#pragma unroll
+                        for (int v = 0; v < VPL; v++) {
+                            const int c = lane + 32 * v;
+                            if (c >= D4) continue;
+                            double4 x[8], m = make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+                            for (int q = 0; q < 8; q++)
+                                if (q < gsz) x[q] = ld_piece(piece(g0 + q) + 4 * c);
+#pragma unroll
+                            for (int q = 0; q < 8; q++)
+                                if (q < gsz) dadd4(m, x[q]);
+                            reinterpret_cast<double4 *>(piece(g0))[c] = m;
+                        }
+                    }
+                    step = 8;
+                    cnt = (npc + 7) / 8;
+                }
+                if (go) {
+                    uint32_t *rc = A.seg_cnt + tb + u;
+                    if (warp_arrive_last(rc, (uint32_t)cnt)) {
+                        if (lane == 0) *rc = 0u;
+                        uint32_t sl = 0;
+                        if (lane == 0) sl = __ldg(A.bb.slot_u + tb + u);
+                        sl = __shfl_sync(0xffffffffu, sl, 0);
+#pragma unroll
+                        for (int v = 0; v < VPL; v++) {
+                            const int c = lane + 32 * v;
+                            if (c >= D4) continue;
+                            double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
+                            for (int q0 = 0; q0 < cnt; q0 += 8) {
+                                double4 x[8];
+#pragma unroll
+                                for (int q = 0; q < 8; q++)
+                                    if (q0 + q < cnt) x[q] = ld_piece(piece(kf + (q0 + q) * step) + 4 * c);
+#pragma unroll
+                                for (int q = 0; q < 8; q++)
+                                    if (q0 + q < cnt) dadd4(m, x[q]);
+                            }
+                            float4 *wp = st + (size_t)sl * D4 + c;
+                            *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < VPL; v++) acc[v] = make_double4(0.0, 0.0, 0.0, 0.0);
+            r0 = r + 1;
+        }
+        // the tile's shared rows are consumed (generic proxy) before the next
+        // tile's bulk copies (async proxy) overwrite them
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+}
+
 // generic D (D/4 not a power-of-two multiple of 32): one warp per row,
 // strided columns; hot rows and chunk records both folded in ascending
 // occurrence order by that warp (sequential fp64 fold)
@@ -623,8 +853,56 @@ int backward_hot_segment(int D) {
     return hs < CH ? CH : (hs > HOT_SEG_MAX ? HOT_SEG_MAX : hs);
 }
 
+// k_bwd_tile: rows per tile so that a warp's two staging areas (gradient and
+// Storage rows) take 32 KB (at most 32 rows: one per lane).  SP_BWD_TR
+// overrides (A/B).
+int backward_tile_rows(int D) {
+    int tr = 16384 / (D * 4);
+    if (const char *e = getenv("SP_BWD_TR")) tr = atoi(e);
+    return tr < 1 ? 1 : (tr > 32 ? 32 : tr);
+}
+
+bool backward_tiled() {
+    const char *e = getenv("SP_BWD");
+    return !(e && e[0] == 'r');
+}
+
+template <int VPL>
+static void launch_bwd_tile(const TrainArgs &a, cudaStream_t s) {
+    const size_t smem = (size_t)2 * a.tr * a.g.D * sizeof(float);
+    static std::map<std::pair<int, size_t>, int> caps;  // (device, smem) -> resident CTAs
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int cap = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        auto it = caps.find({dev, smem});
+        if (it != caps.end()) cap = it->second;
+    }
+    if (!cap) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_tile<VPL>, 32, smem) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        cap = per_sm * device_sms();
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        caps[{dev, smem}] = cap;
+    }
+    const long long tiles = (long long)a.g.T * a.ntiles;
+    int grid = (int)(tiles < cap ? tiles : cap);
+    if (grid < 1) grid = 1;
+    launch_maybe_pdl(k_bwd_tile<VPL>, grid, 32, smem, s, true, a);
+}
+
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
+    if (a.tpart) {
+        if (D4 <= 32) launch_bwd_tile<1>(a, s);
+        else if (D4 <= 64) launch_bwd_tile<2>(a, s);
+        else if (D4 <= 128) launch_bwd_tile<4>(a, s);
+        else launch_bwd_tile<8>(a, s);
+        return cudaGetLastError();
+    }
     // upper bound of work items: all chunks of all tables
     SP_DISPATCH_D(D4, k_bwd, (long long)a.g.T * a.g.nc, a, s, true);
     return cudaGetLastError();
@@ -645,6 +923,12 @@ cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, 
 // attributes of the Train-stage kernels on the current device (sp_create)
 cudaError_t configure_train_kernels() {
     apply_carveout(k_surrogate);
+    // k_bwd_tile is sized by shared memory (one warp, up to 32 KB each): ask
+    // for the largest carveout so that 6-7 CTAs fit per SM
+    cudaFuncSetAttribute(k_bwd_tile<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_tile<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_tile<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_tile<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return cudaGetLastError();
 }
 

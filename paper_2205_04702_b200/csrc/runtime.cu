@@ -254,6 +254,10 @@ struct sp_ctx {
     uint32_t *d_miss_u = nullptr, *d_victims = nullptr;
     uint32_t *d_sort_tmp = nullptr;
     double *d_partial = nullptr;  // [T][nh][D] hot-row segment partials (k_bwd)
+    // k_bwd_tile: pieces of rows spanning tiles, self-resetting arrival counters
+    double *d_tpart = nullptr;    // [T][ntiles][2][D]
+    uint32_t *d_seg_cnt = nullptr, *d_grp_cnt = nullptr;  // [T][n], [T][ntiles][2]
+    int bwd_tr = 0, bwd_ntiles = 0;
     float **d_host = nullptr;
     void *d_idx[RING] = {};
     BatchBufs ring[RING];
@@ -594,6 +598,7 @@ PushArgs push_args(sp_ctx *c) {
     a.claim = c->d_claim;
     a.freq = c->d_freq;
     a.pad = (c->flags & SP_FLAG_PADDING) ? 1 : 0;
+    a.bwd_recs = c->d_tpart ? 0 : 1;
     return a;
 }
 
@@ -621,6 +626,11 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.bb = c->ring[b % RING];
     a.storage = c->d_storage;
     a.partial = c->d_partial;
+    a.tpart = c->d_tpart;  // null: the record-based k_bwd (SP_BWD=rec)
+    a.seg_cnt = c->d_seg_cnt;
+    a.grp_cnt = c->d_grp_cnt;
+    a.tr = c->bwd_tr;
+    a.ntiles = c->bwd_ntiles;
     a.err = c->d_err;
     if (c->diag & 2) a.g.T = 0;  // diagnostic: Train kernels launched, no work
     a.diag = c->diag;
@@ -1254,6 +1264,16 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_victims, Tn));
     if (c->n > SMEM_SORT_MAX) CKC(dalloc(c, &c->d_sort_tmp, 4 * Tn));
     CKC(dalloc(c, &c->d_partial, (size_t)c->T * c->g.nh * c->D));
+    if (backward_tiled()) {
+        c->bwd_tr = backward_tile_rows(c->D);
+        c->bwd_ntiles = (c->n + c->bwd_tr - 1) / c->bwd_tr;
+        const size_t tiles = (size_t)c->T * c->bwd_ntiles;
+        CKC(dalloc(c, &c->d_tpart, tiles * 2 * c->D));
+        CKC(dalloc(c, &c->d_seg_cnt, Tn));
+        CKC(dalloc(c, &c->d_grp_cnt, tiles * 2));
+        CKC(cudaMemset(c->d_seg_cnt, 0, Tn * sizeof(uint32_t)));
+        CKC(cudaMemset(c->d_grp_cnt, 0, tiles * 2 * sizeof(uint32_t)));
+    }
     CKC(dalloc(c, &c->d_pprof, 18 * (size_t)c->T + 2 + 4096));
     CKC(cudaMemset(c->d_pprof, 0, (18 * (size_t)c->T + 2 + 4096) * sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_pprof + 18 * (size_t)c->T + 2, 0xFF, 1024 * sizeof(unsigned long long)));

@@ -117,6 +117,7 @@ struct PushArgs {
     unsigned long long *claim;          // [S] RANDOM: per-slot draw claims
     uint8_t *freq;                      // [S] LFU: use count (saturating)
     int pad;                            // SP_FLAG_PADDING: -1 is "no lookup"
+    int bwd_recs;                       // build the record-based k_bwd's work lists (SP_BWD=rec)
     const unsigned long long *row_off;  // [T+1]
     const long long *rows;              // [T]
     const uint32_t *slot_base;          // [T+1]
@@ -164,6 +165,12 @@ struct TrainArgs {
     double *partial;     // [T][nh][D] fp64 partial sums of hot-row segments
     const unsigned long long *err;
     int diag;            // timing diagnostic (k_bwd): 8 = skip hot segments, 16 = skip chunk records
+    // k_bwd_tile: the table's sorted occurrence list cut into tiles of `tr`
+    // rows (ntiles per table); a row spanning tiles meets through fp64 pieces
+    double *tpart;       // [T][ntiles][2][D] pieces (slot 0: the tile's first segment, 1: its last)
+    uint32_t *seg_cnt;   // [T][n] arrivals per multi-tile row (self-resetting)
+    uint32_t *grp_cnt;   // [T][ntiles][2] arrivals per group of 8 pieces (self-resetting)
+    int tr, ntiles;
 };
 
 struct XferArgs {
@@ -269,6 +276,8 @@ cudaError_t launch_push(const PushArgs &a, cudaStream_t s);
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s);
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s);
 int backward_hot_segment(int D);
+int backward_tile_rows(int D);   // k_bwd_tile rows per tile
+bool backward_tiled();           // k_bwd_tile (default) vs the record-based k_bwd (SP_BWD=rec)
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
                              float delta, cudaStream_t s);
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
