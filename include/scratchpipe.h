@@ -128,7 +128,7 @@ typedef struct {
                                  /* sp_surrogate_grad (NULL = legacy default)       */
     uint32_t flags;              /* SP_FLAG_*                                       */
     int32_t log_factor;          /* LRU-log ring capacity per table =               */
-                                 /* log_factor * slots[t] + 4*N*L (0 -> 8)          */
+                                 /* log_factor * slots[t] + 4*N*L (0 -> 32)         */
     int32_t host_threads;        /* CPU row-copy helpers per transfer-engine pool   */
                                  /* (gather, scatter); 0 -> from the node's cores:  */
                                  /* (ncpu - pools) / pools, pools = 2 * max(1,      */

@@ -735,9 +735,13 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
         const unsigned long long head = s_chead[c];
         unsigned long long tail = c == 0 ? tail0 : A.log_tail[lid];
         // entries going to this class (LFU: freq == c; class 0 only holds the
-        // initial vacant slots, appended to by LRU alone)
-        uint32_t cnt = Ub;
-        if (lfu) {
+        // initial vacant slots, appended to by LRU alone).  A table with at
+        // least as many dynamic slots as rows never evicts: its misses always
+        // find the next initial vacant entry, so nothing is appended (and its
+        // log never needs compaction).
+        const bool no_append = A.log_skip != nullptr && A.log_skip[t] != 0;
+        uint32_t cnt = no_append ? 0u : Ub;
+        if (lfu && !no_append) {
             if (c == 0) cnt = 0;
             else {
                 uint32_t k = 0;
@@ -770,7 +774,8 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
             }
             tail = w;
         }
-        if (!lfu) {
+        if (no_append) {
+        } else if (!lfu) {
             for (uint32_t u = tid; u < Ub; u += blockDim.x) {
                 const size_t ix = (size_t)(lbase + (tail + u) % cap);
                 lslot[ix] = slot_l[u];
@@ -811,6 +816,7 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
     const uint32_t *sorted_occ = pb.sorted_occ + (size_t)t * n;
     const uint32_t *sorted_uid = pb.sorted_uid + (size_t)t * n;
     uint32_t *slot_of_occ = pb.slot_of_occ + (size_t)t * n;
+    uint32_t *sorted_slot = pb.sorted_slot + (size_t)t * n;  // same map in sorted order (backward)
     // (4 elements per thread per round: their independent loads are in flight
     // together instead of one dependent pair per loop trip)
     for (int i0 = tid; i0 < n; i0 += 4 * (int)blockDim.x) {
@@ -824,8 +830,13 @@ __device__ void plan_table(const PushArgs &A, int t, long long b, unsigned char 
         for (int q = 0; q < 4; q++)
             if (i0 + q * (int)blockDim.x < n) sl[q] = u[q] == EMPTY ? EMPTY : slot_l[u[q]];  // EMPTY: padding
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-            if (i0 + q * (int)blockDim.x < n) slot_of_occ[o[q]] = sl[q];
+        for (int q = 0; q < 4; q++) {
+            const int i = i0 + q * (int)blockDim.x;
+            if (i < n) {
+                slot_of_occ[o[q]] = sl[q];
+                sorted_slot[i] = sl[q];
+            }
+        }
     }
     if (A.bwd_recs) {  // (the tiled backward reads slot_u)
         ChunkRec *rec = pb.chunk_rec + (size_t)t * g.nc;

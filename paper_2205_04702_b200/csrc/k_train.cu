@@ -508,8 +508,11 @@ __device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total) 
 }
 }  // namespace
 
+#ifndef SP_BWD_TILE_MINB
+#define SP_BWD_TILE_MINB 16  // resident warps per SM the registers are sized for (<= 128 regs)
+#endif
 template <int VPL>
-__global__ void __launch_bounds__(32) k_bwd_tile(TrainArgs A) {
+__global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_TILE_MINB) k_bwd_tile(TrainArgs A) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t bar;
     if (*A.err != NO_ERR) return;
@@ -523,65 +526,101 @@ __global__ void __launch_bounds__(32) k_bwd_tile(TrainArgs A) {
     float4 *st = reinterpret_cast<float4 *>(A.storage);
     if (lane == 0) bar_init(&bar);
     __syncwarp();
+    // a tile's metadata, one load wave: lane r holds sorted occurrence r, its
+    // unique and its Storage slot (frozen at Plan); lane 0 also the unique
+    // before the tile, lane nrows-1 the one after it (does a row cross the
+    // tile's edges?)
+    struct Meta { uint32_t occ, uid, slot, prev, next; };
+    const long long total = (long long)g.T * NT;
+    auto load_meta = [&](long long tile, Meta &m) {
+        m = Meta{0u, EMPTY, 0u, EMPTY, EMPTY};
+        if (tile >= total) return;
+        const int t = (int)(tile / NT), k = (int)(tile % NT);
+        const int lo = k * TR, nrows = min(TR, g.n - lo);
+        const size_t base = (size_t)t * g.n + lo;
+        if (lane < nrows) {
+            m.occ = __ldg(A.bb.sorted_occ + base + lane);
+            m.uid = __ldg(A.bb.sorted_uid + base + lane);  // EMPTY: padding (sorts last)
+            m.slot = __ldg(A.bb.sorted_slot + base + lane);
+        }
+        if (lane == 0 && lo > 0) m.prev = __ldg(A.bb.sorted_uid + base - 1);
+        if (lane == nrows - 1 && lo + nrows < g.n) m.next = __ldg(A.bb.sorted_uid + base + nrows);
+    };
+    Meta nxt;
+    load_meta(blockIdx.x, nxt);  // (Plan's output: complete before the forward ran)
     griddep_wait();  // (PDL) the surrogate's gradients are complete from here on
     uint32_t parity = 0;
-    const long long total = (long long)g.T * NT;
     for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const Meta m = nxt;
         const int t = (int)(tile / NT), k = (int)(tile % NT);
         const int lo = k * TR;
         const int nrows = min(TR, g.n - lo);
         const size_t tb = (size_t)t * g.n;
-        // 1. the tile's occurrences, their uniques, the rows' boundaries
-        uint32_t occ = 0, uid = EMPTY;
-        if (lane < nrows) {
-            occ = __ldg(A.bb.sorted_occ + tb + lo + lane);
-            uid = __ldg(A.bb.sorted_uid + tb + lo + lane);  // EMPTY: padding (sorts last)
-        }
+        const uint32_t uid = m.uid, slot = m.slot;
         const bool act = uid != EMPTY;
         const unsigned amask = __ballot_sync(0xffffffffu, act);
-        if (amask == 0u) continue;  // (warp-uniform)
+        if (amask == 0u) {  // (warp-uniform) all padding
+            load_meta(tile + gridDim.x, nxt);
+            continue;
+        }
         const int nact = 32 - __clz(amask);  // active rows are a prefix
         const uint32_t up = __shfl_up_sync(0xffffffffu, uid, 1), dn = __shfl_down_sync(0xffffffffu, uid, 1);
-        const bool first = act && (lane == 0 || up != uid);
-        const bool lastr = act && (lane == nact - 1 || dn != uid);
-        // does the row of the tile's first / last active occurrence extend
-        // beyond the tile?  (segment offsets of those two rows only)
-        uint32_t seg_lo = 0, seg_hi = 0;
-        if (lane == 0) seg_lo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + uid);
-        if (lane == nact - 1) seg_hi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + uid + 1);
-        const bool head_open = __shfl_sync(0xffffffffu, seg_lo, 0) < (uint32_t)lo;
-        const bool tail_open = __shfl_sync(0xffffffffu, seg_hi, nact - 1) > (uint32_t)(lo + nact);
+        const uint32_t prevu = lane == 0 ? m.prev : up;
+        const uint32_t nextu = lane == nrows - 1 ? m.next : dn;  // (padding: EMPTY)
+        const bool first = act && prevu != uid;
+        const bool lastr = act && (lane == nact - 1 || nextu != uid);  // (a segment ends at the tile's edge)
         const uint32_t uid_last = __shfl_sync(0xffffffffu, uid, nact - 1);
-        const bool whole = first && !(lane == 0 && head_open) && !(uid == uid_last && tail_open);
-        uint32_t slot = 0;
-        if (whole) slot = __ldg(A.bb.slot_u + tb + uid);
+        const bool tail_open = __shfl_sync(0xffffffffu, nextu == uid, nact - 1);
+        const bool whole = first && !(uid == uid_last && tail_open);  // (lane 0 of an open head is not `first`)
         const unsigned wmask = __ballot_sync(0xffffffffu, whole);
-        const unsigned fmask = __ballot_sync(0xffffffffu, first);
         const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
         if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
         __syncwarp();
-        if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + occ / (uint32_t)g.L) * D4, rowb, &bar);
+        if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + m.occ / (uint32_t)g.L) * D4, rowb, &bar);
         if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowb, &bar);
+        load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
         while (!bar_try(&bar, parity)) {
         }
         parity ^= 1u;
-        // 2. fold in order; 3. pieces of rows spanning tiles
-        double4 acc[VPL];
+        // 2. fold segment by segment (a segment = one row's occurrences in
+        // this tile).  A whole row of 1 or 2 occurrences is summed in fp32:
+        // that is the fp32 rounding of the exact sum, i.e. the oracle's
+        // (float)(fp64 sum) (reading R7); longer rows and pieces of rows
+        // spanning tiles accumulate in fp64 in ascending occurrence order.
+        unsigned ends = lmask;
+        int r0 = 0;  // first row of the current segment
+        while (ends) {
+            const int r1 = __ffs(ends) - 1;  // its last row
+            ends &= ends - 1;
+            const int len = r1 - r0 + 1;
+            const uint32_t s = __shfl_sync(0xffffffffu, slot, r0);
+            const bool wh = (wmask >> r0) & 1u;
+            if (wh && len <= 2 && !(A.diag & 32)) {  // (SP_DIAG=32: every row through fp64, A/B)
 #pragma unroll
-        for (int v = 0; v < VPL; v++) acc[v] = make_double4(0.0, 0.0, 0.0, 0.0);
-        int r0 = 0;  // first row of the current segment within the tile
-        for (int r = 0; r < nact; r++) {
+                for (int v = 0; v < VPL; v++) {
+                    const int c = lane + 32 * v;
+                    if (c < D4) {
+                        float4 gs = sg[(size_t)r0 * D4 + c];
+                        if (len == 2) add4(gs, sg[(size_t)(r0 + 1) * D4 + c]);
+                        st[(size_t)s * D4 + c] = sgd32(sw[(size_t)r0 * D4 + c], gs, A.lr);
+                    }
+                }
+                r0 = r1 + 1;
+                continue;
+            }
+            double4 acc[VPL];
 #pragma unroll
             for (int v = 0; v < VPL; v++) {
+                acc[v] = make_double4(0.0, 0.0, 0.0, 0.0);
                 const int c = lane + 32 * v;
-                if (c < D4) {
-                    const float4 x = sg[(size_t)r * D4 + c];
-                    acc[v].x += (double)x.x; acc[v].y += (double)x.y; acc[v].z += (double)x.z; acc[v].w += (double)x.w;
-                }
+                if (c < D4)
+                    for (int r = r0; r <= r1; r++) {
+                        const float4 x = sg[(size_t)r * D4 + c];
+                        acc[v].x += (double)x.x; acc[v].y += (double)x.y;
+                        acc[v].z += (double)x.z; acc[v].w += (double)x.w;
+                    }
             }
-            if (!((lmask >> r) & 1u)) continue;
-            const uint32_t s = __shfl_sync(0xffffffffu, slot, r0);
-            if ((wmask >> r0) & 1u) {  // the whole row is in this tile
+            if (wh) {  // the whole row is in this tile
 #pragma unroll
                 for (int v = 0; v < VPL; v++) {
                     const int c = lane + 32 * v;
@@ -590,9 +629,9 @@ __global__ void __launch_bounds__(32) k_bwd_tile(TrainArgs A) {
                             sgd(sw[(size_t)r0 * D4 + c], Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr);
                 }
             } else {
-                // a piece of a row spanning tiles [kf, kl]: slot 0 of tile k if
-                // the row holds the tile's first occurrence, else slot 1 (only
-                // possible in the row's first tile)
+                // 3. a piece of a row spanning tiles [kf, kl]: slot 0 of tile k
+                // if the row holds the tile's first occurrence, else slot 1
+                // (only possible in the row's first tile)
                 const uint32_t u = __shfl_sync(0xffffffffu, uid, r0);
                 uint32_t slo = 0, shi = 0;
                 if (lane == 0) {
@@ -623,13 +662,16 @@ __global__ void __launch_bounds__(32) k_bwd_tile(TrainArgs A) {
                         for (int v = 0; v < VPL; v++) {
                             const int c = lane + 32 * v;
                             if (c >= D4) continue;
-                            double4 x[8], m = make_double4(0.0, 0.0, 0.0, 0.0);
+                            double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
+                            for (int q0 = 0; q0 < gsz; q0 += 4) {
+                                double4 x[4];
 #pragma unroll
-                            for (int q = 0; q < 8; q++)
-                                if (q < gsz) x[q] = ld_piece(piece(g0 + q) + 4 * c);
+                                for (int q = 0; q < 4; q++)
+                                    if (q0 + q < gsz) x[q] = ld_piece(piece(g0 + q0 + q) + 4 * c);
 #pragma unroll
-                            for (int q = 0; q < 8; q++)
-                                if (q < gsz) dadd4(m, x[q]);
+                                for (int q = 0; q < 4; q++)
+                                    if (q0 + q < gsz) dadd4(m, x[q]);
+                            }
                             reinterpret_cast<double4 *>(piece(g0))[c] = m;
                         }
                     }
@@ -640,32 +682,27 @@ __global__ void __launch_bounds__(32) k_bwd_tile(TrainArgs A) {
                     uint32_t *rc = A.seg_cnt + tb + u;
                     if (warp_arrive_last(rc, (uint32_t)cnt)) {
                         if (lane == 0) *rc = 0u;
-                        uint32_t sl = 0;
-                        if (lane == 0) sl = __ldg(A.bb.slot_u + tb + u);
-                        sl = __shfl_sync(0xffffffffu, sl, 0);
 #pragma unroll
                         for (int v = 0; v < VPL; v++) {
                             const int c = lane + 32 * v;
                             if (c >= D4) continue;
                             double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
-                            for (int q0 = 0; q0 < cnt; q0 += 8) {
-                                double4 x[8];
+                            for (int q0 = 0; q0 < cnt; q0 += 4) {
+                                double4 x[4];
 #pragma unroll
-                                for (int q = 0; q < 8; q++)
+                                for (int q = 0; q < 4; q++)
                                     if (q0 + q < cnt) x[q] = ld_piece(piece(kf + (q0 + q) * step) + 4 * c);
 #pragma unroll
-                                for (int q = 0; q < 8; q++)
+                                for (int q = 0; q < 4; q++)
                                     if (q0 + q < cnt) dadd4(m, x[q]);
                             }
-                            float4 *wp = st + (size_t)sl * D4 + c;
+                            float4 *wp = st + (size_t)s * D4 + c;
                             *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
                         }
                     }
                 }
             }
-#pragma unroll
-            for (int v = 0; v < VPL; v++) acc[v] = make_double4(0.0, 0.0, 0.0, 0.0);
-            r0 = r + 1;
+            r0 = r1 + 1;
         }
         // the tile's shared rows are consumed (generic proxy) before the next
         // tile's bulk copies (async proxy) overwrite them
@@ -854,10 +891,10 @@ int backward_hot_segment(int D) {
 }
 
 // k_bwd_tile: rows per tile so that a warp's two staging areas (gradient and
-// Storage rows) take 32 KB (at most 32 rows: one per lane).  SP_BWD_TR
-// overrides (A/B).
+// Storage rows) take 16 KB (at most 32 rows: one per lane), i.e. 13 warps
+// per SM.  SP_BWD_TR overrides (A/B).
 int backward_tile_rows(int D) {
-    int tr = 16384 / (D * 4);
+    int tr = 8192 / (D * 4);
     if (const char *e = getenv("SP_BWD_TR")) tr = atoi(e);
     return tr < 1 ? 1 : (tr > 32 ? 32 : tr);
 }

@@ -215,6 +215,92 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
     publish_staged(A, base_t0);  // base_t0 = sum over tables of m[t]
 }
 
+// k_xfer_warp: the same Collect / Exchange / Insert work as k_pullfill with
+// plain 16-B loads and stores from many warps instead of TMA bulk copies from
+// a few.  Measured on this platform (profiles/r02_host_xlat_microbench.txt,
+// r02_host_mix_microbench.txt): random 512-B host rows cost ~16 ns each on
+// the GPU side whatever the page size, once >= ~600 warps have a row in
+// flight (26 ns from 128 warps), and pulls and write-backs share that one
+// limit; the CPU's row copies do not touch it.  So the kernel keeps one or
+// two rows in flight per warp over a grid of ~600 warps, and the victims it
+// does not write back itself go contiguously to pinned staging for the CPU
+// scatter threads.  Per fill k (slot s, missed row x, previous resident o):
+//     v = Storage[s] (if o valid);  r = host[t][x] (or the CPU-gathered row)
+//     victim v -> its host row (share wbq of the valid victims, direct) or
+//                 staging[k] + its host address in the scatter work list
+//     Storage[s] = r
+// Items run pulled-first; a warp reaching CPU-gathered items (hybrid) waits
+// on the gather counter there.  Completion: publish_staged (last CTA).
+template <int VPL>
+__global__ void __launch_bounds__(128) k_xfer_warp(XferArgs A) {
+    __shared__ uint32_t s_pref[65];
+    if (*A.err != NO_ERR) return;
+    const Geometry g = A.g;
+    const int D4 = g.D / 4;
+    const int lane = threadIdx.x & 31;
+    const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const long long W = (long long)gridDim.x * (blockDim.x / 32);
+    float4 *st = reinterpret_cast<float4 *>(A.storage);
+    uint32_t base_t0 = 0;
+    for (int t0 = 0; t0 < g.T; t0 += 64) {
+        const int tcount = min(64, g.T - t0);
+        table_prefix(A.bb.m, t0, tcount, s_pref);
+        const uint32_t total = s_pref[tcount];
+        const uint32_t Kg = !A.in_stage ? 0u
+                            : (A.gfrac_q16 >= 65536u ? total : (uint32_t)(((unsigned long long)total * A.gfrac_q16) >> 16));
+        bool waited = A.gwait == nullptr;
+        // pulled items [Kg, total) first, then the CPU-gathered [0, Kg)
+        for (long long j = gw; j < total; j += W) {
+            const uint32_t item = (uint32_t)((j + Kg) % total);
+            const bool gathered = item < Kg;
+            if (gathered && !waited) {
+                if (lane == 0)
+                    while (*(volatile const unsigned long long *)A.gwait < (unsigned long long)(A.b + 1)) __nanosleep(256);
+                __syncwarp();
+                __threadfence_system();
+                waited = true;
+            }
+            const int tl = find_table(s_pref, tcount, item);
+            const int t = t0 + tl;
+            const size_t kk = (size_t)t * g.n + (item - s_pref[tl]);
+            const uint32_t slot = A.bb.fill_slot[kk], row = A.bb.fill_row[kk], old = A.bb.evict_row[kk];
+            const bool victim = old != EMPTY && !A.diag_nowb;
+            const float4 *src = reinterpret_cast<const float4 *>(
+                gathered ? A.in_stage + (size_t)(base_t0 + item) * g.D : A.host[t] + (size_t)row * g.D);
+            float4 v[VPL], r[VPL];
+#pragma unroll
+            for (int q = 0; q < VPL; q++) {
+                const int c = lane + 32 * q;
+                if (c < D4) {
+                    if (victim) v[q] = st[(size_t)slot * D4 + c];
+                    r[q] = __ldcv(src + c);  // (host memory: no stale L2 lines)
+                }
+            }
+            // direct write-back for a share of the victims (a fixed hash of
+            // the item index, so the CPU and GPU shares are spread evenly)
+            const bool direct = victim && ((item * 2654435761u) >> 16) < A.wb_q16;
+            float4 *dst = victim ? reinterpret_cast<float4 *>(A.host[t] + (size_t)old * g.D) : nullptr;
+            float4 *stg = reinterpret_cast<float4 *>(A.wb_stage + (size_t)(base_t0 + item) * g.D);
+#pragma unroll
+            for (int q = 0; q < VPL; q++) {
+                const int c = lane + 32 * q;
+                if (c < D4) {
+                    if (victim) {
+                        if (direct) dst[c] = v[q];
+                        else stg[c] = v[q];
+                    }
+                    st[(size_t)slot * D4 + c] = r[q];
+                }
+            }
+            if (lane == 0)
+                A.wb_dst[base_t0 + item] = (victim && !direct) ? (unsigned long long)(uintptr_t)dst : 0ull;
+        }
+        base_t0 += total;
+        __syncthreads();  // (s_pref is reloaded for the next group)
+    }
+    publish_staged(A, base_t0);
+}
+
 int pullfill_tma_items(int D) {
     const size_t budget = 192 * 1024, per_item = (size_t)2 * D * 4 * XS;
     size_t nb = budget / per_item;
@@ -309,6 +395,15 @@ __global__ void __launch_bounds__(256) k_flush(FlushArgs A) {
         const float4 *src = reinterpret_cast<const float4 *>(A.storage) + (size_t)s * D4;
         for (int c = lane; c < D4; c += 32) dst[c] = src[c];
     }
+}
+
+cudaError_t launch_xfer_warp(const XferArgs &a, int ctas, cudaStream_t s) {
+    const int D4 = a.g.D / 4, g = ctas > 0 ? ctas : device_sms();
+    if (D4 <= 32) k_xfer_warp<1><<<g, 128, 0, s>>>(a);
+    else if (D4 <= 64) k_xfer_warp<2><<<g, 128, 0, s>>>(a);
+    else if (D4 <= 128) k_xfer_warp<4><<<g, 128, 0, s>>>(a);
+    else k_xfer_warp<8><<<g, 128, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s) {

@@ -241,6 +241,8 @@ struct sp_ctx {
     int policy = 0, log_classes = 1;
     unsigned long long policy_seed = 0;
     uint32_t *d_pin_base = nullptr;           // [T] first pinned slot (slot_base[t+1]: none)
+    uint8_t *d_log_skip = nullptr;            // [T] dynamic slots >= unpinned rows: no log appends
+    std::vector<uint8_t> log_skip;
     std::vector<uint32_t> pin_base;
     std::vector<bool> pinned_t;
     uint32_t *d_nfill = nullptr;              // [T] RANDOM: dynamic slots filled so far
@@ -281,6 +283,13 @@ struct sp_ctx {
     unsigned long long *h_scat = nullptr;      // pinned mapped: batches scattered
     unsigned long long *d_scat = nullptr;      // its device alias (stream wait-value)
     int pull_ctas = 16;  // k_pullfill grid (one warp per CTA); SP_PULL_CTAS overrides
+    // transfer kernel: k_pullfill (TMA bulk copies from 16 one-warp CTAs,
+    // default) or k_xfer_warp (plain loads from ~1,200 warps, SP_XFER=warp:
+    // measured slower in the pipeline, its sysmem loads slow the Train
+    // kernels 1.3-1.8x; profiles/r02_xs1_sweep.txt)
+    bool xfer_warp = false;
+    int xfer_ctas = 0;          // k_xfer_warp grid (0: 2 x SMs); SP_XFER_CTAS overrides
+    uint32_t wb_q16 = 0;        // k_xfer_warp: victims written back by the GPU (SP_WB_GPU_FRAC)
     // timing diagnostics (SP_DIAG bit mask; results are then WRONG): 1 = the
     // transfer kernel moves nothing, 2 = the Train kernels do nothing, 4 = the
     // transfer kernel pulls but does not stage the victims
@@ -500,6 +509,7 @@ BatchBufs carve(sp_ctx *c, cudaError_t *st) {
     A(&b.hot_cnt, (size_t)c->T * c->g.nh);
     A(&b.slot_u, Tn);
     A(&b.slot_of_occ, Tn);
+    A(&b.sorted_slot, Tn);
     A(&b.hit, Tn);
     A(&b.fill_slot, Tn);
     A(&b.fill_row, Tn);
@@ -594,6 +604,7 @@ PushArgs push_args(sp_ctx *c) {
     a.log_classes = c->log_classes;
     a.seed = c->policy_seed;
     a.pin_base = c->d_pin_base;
+    a.log_skip = c->d_log_skip;
     a.nfill = c->d_nfill;
     a.claim = c->d_claim;
     a.freq = c->d_freq;
@@ -872,12 +883,16 @@ sp_status pump(sp_ctx *c) {
         a.wb_dst = c->hd_wbdst + (size_t)(b % c->XSR) * c->T * c->n;
         a.staged_cnt = c->hd_scnt + r;
         a.wb_direct = c->gpu_wb ? 1 : 0;
+        a.wb_q16 = c->gpu_wb ? 65536u : c->wb_q16;
         a.b = b;
         if (c->diag & 1) a.g.T = 0;  // diagnostic: transfer launched, no rows moved
         if (c->diag & 4) a.diag_nowb = 1;  // diagnostic: victims not staged (pull only)
         a.err = c->d_err;
         if (c->stage_timing) CK(cudaEventRecord(c->sev[r][6], xs));
-        CK(launch(c, SP_K_TRANSFER, b, xs, [&] { return launch_pullfill(a, c->pull_ctas, xs); }));
+        CK(launch(c, SP_K_TRANSFER, b, xs, [&] {
+            return c->xfer_warp ? launch_xfer_warp(a, c->xfer_ctas ? c->xfer_ctas : 2 * device_sms(), xs)
+                                : launch_pullfill(a, c->pull_ctas, xs);
+        }));
         if (c->stage_timing) CK(cudaEventRecord(c->sev[r][7], xs));
         c->sev_used[r][1] = c->stage_timing;
         CK(cudaEventRecord(c->ev_xfer[r], xs));
@@ -1111,6 +1126,12 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     // 30 / 48 CTAs were 11% / 18% slower on Terabyte: more SMs add interference,
     // not host-link throughput)
     if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
+    if (const char *e = getenv("SP_XFER")) c->xfer_warp = std::string(e) == "warp";
+    if (const char *e = getenv("SP_XFER_CTAS")) c->xfer_ctas = std::max(1, atoi(e));
+    if (const char *e = getenv("SP_WB_GPU_FRAC")) {
+        const double f = atof(e);
+        c->wb_q16 = f <= 0.0 ? 0u : (f >= 1.0 ? 65536u : (uint32_t)(f * 65536.0));
+    }
     if (const char *e = getenv("SP_DIAG")) c->diag = atoi(e);
 
     cudaError_t e = cudaSetDevice(c->device);
@@ -1224,7 +1245,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     // LRU log per table (LFU: one per use-count class, c = 0 holding the
     // initial vacant slots; RANDOM: none): capacity log_factor*S_t + 4n
     // (LFU classes: 2*S_t + 4n each)
-    const long long lf = d->log_factor > 0 ? d->log_factor : 8;
+    const long long lf = d->log_factor > 0 ? d->log_factor : 32;  // HBM is plentiful: compaction rare
     const int NCl = std::max(1, c->log_classes);
     std::vector<unsigned long long> lbase((size_t)c->T * NCl), lcap((size_t)c->T * NCl), lhead((size_t)c->T * NCl, 0),
         ltail((size_t)c->T * NCl, 0);
@@ -1403,6 +1424,10 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaMemcpy(c->d_log_head, lhead.data(), lbase.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
     CKC(cudaMemcpy(c->d_log_tail, ltail.data(), lbase.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
     CKC(cudaMemcpy(c->d_pin_base, c->pin_base.data(), c->T * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    c->log_skip.assign(c->T, 0);
+    for (int t = 0; t < c->T; t++) c->log_skip[t] = c->slots[t] >= c->rows[t] ? 1 : 0;
+    CKC(dalloc(c, &c->d_log_skip, c->T));
+    CKC(cudaMemcpy(c->d_log_skip, c->log_skip.data(), c->T, cudaMemcpyHostToDevice));
     CKC(cudaMemset(c->d_err, 0xFF, sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_cum, 0, 4 * sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_storage, 0, (size_t)c->S_total * c->D * sizeof(float)));
@@ -1555,6 +1580,9 @@ sp_status sp_pin_rows(sp_ctx *c, int32_t t, const int64_t *ids, int64_t count) {
     c->pin_base[t] = base;
     c->pinned_t[t] = true;
     CK(cudaMemcpy(c->d_pin_base + t, &base, sizeof(uint32_t), cudaMemcpyHostToDevice));
+    // never evicts iff the dynamic slots can hold every unpinned row
+    c->log_skip[t] = (long long)(base - c->slot_base[t]) >= c->rows[t] - count ? 1 : 0;
+    CK(cudaMemcpy(c->d_log_skip + t, &c->log_skip[t], 1, cudaMemcpyHostToDevice));
     return SP_OK;
 }
 

@@ -78,6 +78,7 @@ struct BatchBufs {
     uint32_t *nhot;
     uint32_t *hot_cnt;  // [T][nh] arrivals per hot row (at its segment-0 index)
     uint32_t *slot_u, *slot_of_occ;
+    uint32_t *sorted_slot;  // [T][n] Storage slot of each sorted occurrence (k_bwd_tile)
     uint8_t *hit;
     uint32_t *fill_slot, *fill_row, *evict_row, *m;
     uint32_t *stats;  // [T][4] U, hits, misses, evictions
@@ -113,6 +114,7 @@ struct PushArgs {
     int policy, log_classes;
     unsigned long long seed;            // RANDOM draw seed
     const uint32_t *pin_base;           // [T] first pinned (static) slot of table t
+    const uint8_t *log_skip;            // [T] 1: dynamic slots >= rows (never evicts): no log appends
     uint32_t *nfill;                    // [T] RANDOM: dynamic slots filled so far
     unsigned long long *claim;          // [S] RANDOM: per-slot draw claims
     uint8_t *freq;                      // [S] LFU: use count (saturating)
@@ -183,6 +185,8 @@ struct XferArgs {
     unsigned long long *staged_cnt;  // pinned: sum m of this batch (written before `staged`)
     int diag_nowb;                // timing diagnostic: skip the victims' staging stores
     int wb_direct;                // victims go straight to their host rows (no staging)
+    uint32_t wb_q16;              // k_xfer_warp: share of the valid victims written back by the
+                                  // kernel itself (65536 = all), the rest staged for the CPU
     const float *in_dev;          // device copy of the first in_dev_rows rows of in_stage
     uint32_t in_dev_rows;         //   (copy-engine DMA), or nullptr / 0
     uint32_t gfrac_q16;           // share of the fills gathered by the CPU (65536 = all)
@@ -281,6 +285,7 @@ bool backward_tiled();           // k_bwd_tile (default) vs the record-based k_b
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
                              float delta, cudaStream_t s);
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
+cudaError_t launch_xfer_warp(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);
 cudaError_t launch_prefill_map(const uint32_t *slot_base, const unsigned long long *row_off, int T,
                                long long S_total, uint32_t *resident, uint32_t *hitmap, cudaStream_t s);

@@ -38,10 +38,21 @@ def test_stream_busy_and_overlap_verdict(bench):
     busy = bench._stream_busy(ev)
     assert busy["plan"] == pytest.approx(30.0) and busy["compute"] == pytest.approx(60.0)
     assert busy["transfer"] == pytest.approx(50.0) and busy["steps"] == 4
+    assert busy["step_us"] == pytest.approx(100.0)
+    # the verdict compares against the timing pass's own step (100 us here),
+    # not the timed region's (62 us)
     ov = bench._overlap({}, 62.0, busy)
-    assert ov["busiest_stream"] == "compute" and ov["full_overlap"] is True
-    assert ov["step_over_busiest"] == pytest.approx(62.0 / 60.0, rel=1e-3)
-    assert bench._overlap({}, 100.0, busy)["full_overlap"] is False
+    assert ov["busiest_stream"] == "compute" and ov["full_overlap"] is False
+    assert ov["timing_pass_step_us"] == pytest.approx(100.0)
+    assert ov["step_over_busiest"] == pytest.approx(100.0 / 60.0, rel=1e-3)
+    # stages packed back to back: step 62 us, compute busy 60 us -> full overlap
+    ev2 = np.full((16, 8), np.nan)
+    for r in range(4):
+        t0 = r * 0.062
+        ev2[r, :6] = [t0, t0 + 0.03, t0 + 0.002, t0 + 0.02, t0 + 0.03, t0 + 0.062]
+        ev2[r, 6:8] = [t0, t0 + 0.05]
+    ov2 = bench._overlap({}, 62.0, bench._stream_busy(ev2))
+    assert ov2["full_overlap"] is True and ov2["busiest_over_step"] <= 1.0
     assert bench._overlap({}, 62.0, None) is None
 
 
