@@ -342,6 +342,28 @@ def _overlap(kernels, step_us, busy=None):
                       "union of intervals per stream over the last %d steps" % busy["steps"]}
 
 
+def _span_summary(sp_ms):
+    """In-kernel span stamps of the last 16 steps (sp_span_times: [kind][slot]
+    [start, end] ms): per stage the median in-situ duration (first CTA start to
+    last CTA end), per stream the busy time per step (union of its intervals /
+    steps), and the step period from consecutive backward ends."""
+    import numpy as np
+    kinds = ["plan", "transfer", "forward", "surrogate", "backward"]
+    iv = {k: [(a, b) for a, b in sp_ms[i] if a == a and b == b] for i, k in enumerate(kinds)}
+    dur = {k: float(np.median([(b - a) * 1e3 for a, b in v])) if v else None for k, v in iv.items()}
+    ends = sorted(b for _, b in iv["backward"])
+    step = (ends[-1] - ends[0]) * 1e3 / (len(ends) - 1) if len(ends) > 1 else float("nan")
+    nst = max(1, len(iv["backward"]))
+    busy = {"plan": _union_us(iv["plan"]) / max(1, len(iv["plan"])),
+            "transfer": _union_us(iv["transfer"]) / max(1, len(iv["transfer"])),
+            "compute": _union_us(iv["forward"] + iv["surrogate"] + iv["backward"]) / nst}
+    return {"duration_us": {k: (round(v, 2) if v is not None else None) for k, v in dur.items()},
+            "stream_busy_us_per_step": {k: round(v, 2) for k, v in busy.items()},
+            "step_us": round(step, 2), "steps": nst,
+            "source": "%globaltimer stamps of every CTA of the five stage kernels in the graph-mode "
+                      "steady state (sp_set_span_timing; no events in the graphs), last 16 steps"}
+
+
 def _plan_roles(p0, p1):
     """k_push critical chain: mean per-launch wall time of each table's Plan
     CTA and dedup CTA over the profiling window (globaltimer, in-kernel)."""
@@ -531,13 +553,17 @@ def run_ours(args):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     st1 = sp.stats()
-    stage_t = stage_busy = None
+    stage_t = stage_busy = spans = None
     if world == 1:  # same graph-mode steady state, step graphs recaptured with event nodes
         sp.set_stage_timing(True)
         value_loop(KS)
         stage_t = sp.stage_times()   # events of the last 16 steps, on each stage's own stream
         stage_busy = _stream_busy(sp.stage_events())
         sp.set_stage_timing(False)
+        sp.set_span_timing(True)    # the same steady state, kernels stamping their own spans
+        value_loop(KS)
+        spans = _span_summary(sp.span_times())
+        sp.set_span_timing(False)
     st1p = sp.stats()  # baseline of the (eager) profiling pass
     value = K / (ms / 1e3)   # iterations of the global batch per second (max over ranks)
     ms_per_step = ms / K
@@ -623,7 +649,9 @@ def run_ours(args):
     for k in ["plan", "transfer", "forward", "backward", "surrogate"]:
         us = stage_t[k]["ms"] * 1e3 if timed_src and stage_t[k]["n"] else avg_ms[k] * 1e3
         gbs = alg_bytes[k] / (us * 1e-6) / 1e9 if us else None
-        kernels[k] = {"avg_us": round(us, 3), "share_profiling_pass": round(kms[k] / total_ms, 4),
+        kernels[k] = {"avg_us": round(us, 3),
+                      "span_us": spans["duration_us"][k] if spans else None,
+                      "share_profiling_pass": round(kms[k] / total_ms, 4),
                       "profiling_pass_us": round(avg_ms[k] * 1e3, 3),
                       "alg_bytes_per_launch": int(alg_bytes[k]), "alg_GBs": None if gbs is None else round(gbs, 1)}
     # dominant HBM-bound kernel (the Train stage: forward or backward)
@@ -641,6 +669,12 @@ def run_ours(args):
                 "bytes_per_launch": int(alg_bytes[dom]),
                 "bytes_formula": ("4*T*n + 4*D*T*n + 4*D*T*N" if dom == "forward"
                                   else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
+    if spans and spans["duration_us"].get(dom):
+        # cross-check: the same bytes over the kernel's own first-CTA-start to
+        # last-CTA-end span in the same steady state
+        sa = alg_bytes[dom] / (spans["duration_us"][dom] * 1e-6) / 1e9
+        roofline["span_achieved"] = round(sa, 1)
+        roofline["span_frac"] = round(sa / peak, 4)
     train_ms = (kernels["forward"]["avg_us"] + kernels["backward"]["avg_us"]) * 1e-3
     train_bytes = alg_bytes["forward"] + alg_bytes["backward"]
     # host link: the transfer stream's busy time per step (union of its event
@@ -697,6 +731,7 @@ def run_ours(args):
         # stage overlap in the graph-mode steady state: 1.0 = the step costs
         # only its slowest stream, 0.0 = the stages run back to back
         "overlap": _overlap(kernels, ms_per_step * 1e3, stage_busy) if timed_src else None,
+        "spans": spans,
         "kernels": kernels,
         "plan_ctas": _plan_roles(pp0, pp1),
         "host_engine": {"scatter_us_per_batch": round(1e3 * (st2["host_scatter_ms"] - st1p["host_scatter_ms"]) / KP, 2),

@@ -402,6 +402,18 @@ sp_status sp_stage_times(sp_ctx *c, double *out_ms, int32_t *n_out);
  * busy intervals instead of summing spans.  Synchronises the device. */
 sp_status sp_stage_events(sp_ctx *c, double *out_ms);
 
+/* Span timing of the steady state as it runs (diagnostic).  on != 0: every
+ * CTA of the five stage kernels (k_push Plan, the transfer kernel, k_fwd,
+ * k_surrogate, k_bwd) stamps %globaltimer when it starts its work and when it
+ * is done; the step graphs are recaptured with the stamp buffer (no event
+ * nodes).  Turning it on clears the stamps.  sp_span_times then returns, per
+ * kind k (0 plan, 1 transfer, 2 forward, 3 surrogate, 4 backward) and ring
+ * slot r (batch % 16), out_ms[(k*16 + r)*2 + {0,1}] = the earliest CTA start
+ * and latest CTA end of the last launch for that slot, in ms from the
+ * earliest recorded start (NaN: not recorded).  Synchronises the device. */
+sp_status sp_set_span_timing(sp_ctx *c, int32_t on);
+sp_status sp_span_times(sp_ctx *c, double *out_ms);
+
 /* k_push per-CTA wall time while profiling is on (sp_set_profiling / SP_FLAG_PROFILE),
  * from %globaltimer at CTA entry and exit.  out[18T+2+4096] (caller-owned host array):
  * out[t] = summed ns of the Plan CTA of table t, out[T+t] = summed ns of the

@@ -114,7 +114,8 @@ def _load():
                        ("sp_debug_slots", [P, ctypes.c_int32, i64p, i64p]),
                        ("sp_debug_storage", [P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, P]),
                        ("sp_debug_plan_profile", [P, P]), ("sp_stage_times", [P, P, P]),
-                       ("sp_set_stage_timing", [P, ctypes.c_int32]), ("sp_stage_events", [P, P])]:
+                       ("sp_set_stage_timing", [P, ctypes.c_int32]), ("sp_stage_events", [P, P]),
+                       ("sp_set_span_timing", [P, ctypes.c_int32]), ("sp_span_times", [P, P])]:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = S
@@ -466,6 +467,17 @@ class ScratchPipe:
         out = np.zeros(RING * 8, np.float64)
         self._check(lib.sp_stage_events(self._h, out.ctypes.data_as(ctypes.c_void_p)))
         return out.reshape(RING, 8)
+
+    def set_span_timing(self, on: bool):
+        self._check(lib.sp_set_span_timing(self._h, 1 if on else 0))
+
+    def span_times(self) -> np.ndarray:
+        """[5 kinds][16 ring slots][start, end] ms (plan, transfer, forward,
+        surrogate, backward) of the last launch per slot, from the kernels'
+        own %globaltimer stamps (NaN: not recorded); sp_span_times."""
+        out = np.zeros(5 * RING * 2, np.float64)
+        self._check(lib.sp_span_times(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out.reshape(5, RING, 2)
 
     def debug_plan_profile(self) -> dict:
         """k_push per-CTA wall time while profiling: mean us per launch of the

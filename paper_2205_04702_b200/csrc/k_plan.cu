@@ -867,11 +867,17 @@ __global__ void __launch_bounds__(PUSH_THREADS, SP_PUSH_MIN_BLOCKS) k_push(PushA
     }
     unsigned long long t_start = 0;
     if (A.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    unsigned long long *spn = A.do_plan ? span_base(A.span, SPK_PLAN, b) : nullptr;
+    span_mark(spn, 0);
     const bool role_plan = (int)blockIdx.x < T;
     if (role_plan) {
         if (A.do_plan) plan_table(A, blockIdx.x, b, smem_raw);
     } else if (A.has_new) {
         dedup_table(A, blockIdx.x - T, smem_raw, j, idx);
+    }
+    if (spn) {
+        __syncthreads();
+        span_mark(spn, 1);
     }
     if (A.prof && (role_plan ? A.do_plan : A.has_new)) {  // per-CTA wall time, by role and table
         __syncthreads();

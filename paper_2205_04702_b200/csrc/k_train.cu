@@ -125,10 +125,26 @@ __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
 }
 
 template <int G, int VPL>
-__global__ void __launch_bounds__(256) k_fwd(TrainArgs A) { fwd_body<G, VPL, false>(A); }
+__global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
+    unsigned long long *sp = span_base(A.span, SPK_FWD, A.span_b);
+    span_mark(sp, 0);
+    fwd_body<G, VPL, false>(A);
+    if (sp) {
+        __syncthreads();
+        span_mark(sp, 1);
+    }
+}
 // ragged bags (SP_FLAG_PADDING): its own instance keeps the fixed-L kernel lean
 template <int G, int VPL>
-__global__ void __launch_bounds__(256) k_fwd_pad(TrainArgs A) { fwd_body<G, VPL, true>(A); }
+__global__ void __launch_bounds__(256) k_fwd_pad(TrainArgs A) {
+    unsigned long long *sp = span_base(A.span, SPK_FWD, A.span_b);
+    span_mark(sp, 0);
+    fwd_body<G, VPL, true>(A);
+    if (sp) {
+        __syncthreads();
+        span_mark(sp, 1);
+    }
+}
 
 // generic D (D/4 not a power-of-two multiple of 32): 32 lanes, strided columns
 __device__ __forceinline__ void fwd_generic_body(const TrainArgs &A) {
@@ -549,6 +565,8 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     Meta nxt;
     load_meta(blockIdx.x, nxt);  // (Plan's output: complete before the forward ran)
     griddep_wait();  // (PDL) the surrogate's gradients are complete from here on
+    unsigned long long *spn = span_base(A.span, SPK_BWD, A.span_b);
+    span_mark(spn, 0);
     uint32_t parity = 0;
     for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
         const Meta m = nxt;
@@ -709,6 +727,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         __syncwarp();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    span_mark(spn, 1);
 }
 
 // generic D (D/4 not a power-of-two multiple of 32): one warp per row,
@@ -758,8 +777,9 @@ __global__ void __launch_bounds__(256) k_bwd_generic(TrainArgs A) {
 // result does not depend on the grid.
 constexpr int SU = 4;
 __global__ void __launch_bounds__(256) k_surrogate(const float4 *p, float4 *g, long long n4,
-                                                   float gamma, float delta) {
+                                                   float gamma, float delta, unsigned long long *span) {
     griddep_wait();  // (PDL) pooled is complete from here on
+    span_mark(span, 0);
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += SU * stride) {
         float4 x[SU];
@@ -780,6 +800,10 @@ __global__ void __launch_bounds__(256) k_surrogate(const float4 *p, float4 *g, l
                 g[i] = y;
             }
         }
+    }
+    if (span) {
+        __syncthreads();
+        span_mark(span, 1);
     }
 }
 
@@ -946,14 +970,15 @@ cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
-                             float delta, cudaStream_t s) {
+                             float delta, cudaStream_t s, unsigned long long *span, long long span_b) {
     long long n4 = count / 4;
     long long blocks = (n4 + 256 * SU - 1) / (256 * SU);
     const long long cap = (long long)device_sms() * 8;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
     launch_maybe_pdl(k_surrogate, grid, 256, 0, s, true, reinterpret_cast<const float4 *>(pooled),
-                     reinterpret_cast<float4 *>(grad), n4, gamma, delta);
+                     reinterpret_cast<float4 *>(grad), n4, gamma, delta,
+                     span ? span + (((size_t)SPK_SURR * RING + (size_t)(span_b % RING)) * SPAN_MAXCTA) * 2 : nullptr);
     return cudaGetLastError();
 }
 

@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
     __shared__ uint32_t s_slot[XS][32], s_stage[XS][32];
     __shared__ unsigned long long s_dst[XS][32];  // direct write-back: host row of each victim
     if (*A.err != NO_ERR) return;
+    unsigned long long *spn = span_base(A.span, SPK_XFER, A.b);
+    span_mark(spn, 0);
     const Geometry g = A.g;
     const uint32_t rowb = (uint32_t)g.D * 4u;
     const int lane = threadIdx.x;
@@ -154,13 +156,17 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 const uint32_t old = A.bb.evict_row[kk];
                 if (old != EMPTY && !A.diag_nowb) stage = direct ? (uint32_t)t : base_t0 + item;
                 // the scatter thread's work list: where the staged row goes
-                // (direct: the kernel itself stores the row there)
+                // (direct: the kernel itself stores the row there -- every
+                // victim, or the share wb_q16 of them picked by a fixed hash
+                // of the item index; the CPU scatters the rest)
                 const unsigned long long dst =
                     old != EMPTY ? (unsigned long long)(uintptr_t)(A.host[t] + (size_t)old * g.D) : 0ull;
-                if (direct) s_dst[s][lane] = dst;
-                else A.wb_dst[base_t0 + item] = dst;
+                const bool dir = direct || ((item * 2654435761u) >> 16) < A.wb_q16;
+                s_dst[s][lane] = dir ? dst : 0ull;
+                if (!direct) A.wb_dst[base_t0 + item] = dir ? 0ull : dst;
                 bytes = rowb * (stage != EMPTY ? 2u : 1u);
             }
+            if ((uint32_t)lane >= cnt) s_dst[s][lane] = 0ull;
             s_slot[s][lane] = slot;
             s_stage[s][lane] = stage;
             const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
@@ -185,17 +191,18 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
             const int s = (int)((phase_ctr + r) % XS);
             mbar_wait(&bar[s], ((phase_ctr + r) / XS) & 1u);
             const uint32_t slot = s_slot[s][lane], stage = s_stage[s][lane];
+            const unsigned long long dd = s_dst[s][lane];
+            // victims written back by the kernel: one bulk store per row into
+            // its host row
+            if (slot != EMPTY && stage != EMPTY && dd) bulk_s2g(reinterpret_cast<void *>((uintptr_t)dd), vbuf(s, lane), rowb);
             if (direct) {
-                // victims: one bulk store per row into its host row
-                if (slot != EMPTY && stage != EMPTY)
-                    bulk_s2g(reinterpret_cast<void *>((uintptr_t)s_dst[s][lane]), vbuf(s, lane), rowb);
             } else if (round_gathered(r)) {
                 // victims: one contiguous bulk store of the round's staging rows
                 // (rows of fills without a victim carry garbage; their work-list
                 // entry is 0, so the scatter skips them)
                 const uint32_t k0 = lo + r * nb, cnt = min((uint32_t)nb, hi - k0);
                 if (lane == 0 && cnt) bulk_s2g(A.wb_stage + (size_t)(base_t0 + k0) * g.D, vbuf(s, 0), cnt * rowb);
-            } else if (slot != EMPTY && stage != EMPTY) {
+            } else if (slot != EMPTY && stage != EMPTY && !dd) {
                 bulk_s2g(A.wb_stage + (size_t)stage * g.D, vbuf(s, lane), rowb);
             }
             if (slot != EMPTY) bulk_s2g(A.storage + (size_t)slot * g.D, nbuf(s, lane), rowb);
@@ -213,6 +220,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
     }
     bulk_wait0();
     publish_staged(A, base_t0);  // base_t0 = sum over tables of m[t]
+    span_mark(spn, 1);
 }
 
 // k_xfer_warp: the same Collect / Exchange / Insert work as k_pullfill with
@@ -235,6 +243,8 @@ template <int VPL>
 __global__ void __launch_bounds__(128) k_xfer_warp(XferArgs A) {
     __shared__ uint32_t s_pref[65];
     if (*A.err != NO_ERR) return;
+    unsigned long long *spn = span_base(A.span, SPK_XFER, A.b);
+    span_mark(spn, 0);
     const Geometry g = A.g;
     const int D4 = g.D / 4;
     const int lane = threadIdx.x & 31;
@@ -299,6 +309,7 @@ __global__ void __launch_bounds__(128) k_xfer_warp(XferArgs A) {
         __syncthreads();  // (s_pref is reloaded for the next group)
     }
     publish_staged(A, base_t0);
+    span_mark(spn, 1);
 }
 
 int pullfill_tma_items(int D) {

@@ -312,6 +312,8 @@ struct sp_ctx {
     cudaEvent_t sev[RING][8] = {};
     bool sev_used[RING][2] = {};
     bool stage_timing = false;  // sp_set_stage_timing: record sev in new graphs
+    bool span_on = false;       // sp_set_span_timing: kernels stamp their CTA spans
+    unsigned long long *d_span = nullptr;  // [SPAN_KINDS][RING][SPAN_MAXCTA][2] %globaltimer ns
     bool h2d_used[RING] = {};
     // schedule state (caller's thread)
     long long pushed = 0, planned = 0, forwarded = 0, trained = 0;
@@ -576,6 +578,7 @@ sp_status wait_engine(sp_ctx *c, Pred pred) {
 
 PushArgs push_args(sp_ctx *c) {
     PushArgs a{};
+    a.span = c->span_on ? c->d_span : nullptr;
     a.g = c->g;
     a.P = c->P;
     a.F = c->F;
@@ -642,6 +645,8 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.grp_cnt = c->d_grp_cnt;
     a.tr = c->bwd_tr;
     a.ntiles = c->bwd_ntiles;
+    a.span = c->span_on ? c->d_span : nullptr;
+    a.span_b = b;
     a.err = c->d_err;
     if (c->diag & 2) a.g.T = 0;  // diagnostic: Train kernels launched, no work
     a.diag = c->diag;
@@ -884,6 +889,7 @@ sp_status pump(sp_ctx *c) {
         a.staged_cnt = c->hd_scnt + r;
         a.wb_direct = c->gpu_wb ? 1 : 0;
         a.wb_q16 = c->gpu_wb ? 65536u : c->wb_q16;
+        a.span = c->span_on ? c->d_span : nullptr;
         a.b = b;
         if (c->diag & 1) a.g.T = 0;  // diagnostic: transfer launched, no rows moved
         if (c->diag & 4) a.diag_nowb = 1;  // diagnostic: victims not staged (pull only)
@@ -1692,7 +1698,10 @@ sp_status sp_surrogate_grad(sp_ctx *c, const float *pooled, float *grad, int64_t
     CK(cudaSetDevice(c->device));
     if (count == 0) count = c->comm ? (long long)c->T_all * (c->N / c->world) * c->D : (long long)c->T * c->N * c->D;
     CK(launch(c, SP_K_SURROGATE, c->trained, c->compute,
-              [&] { return launch_surrogate(pooled, grad, count, gamma, delta, c->compute); }));
+              [&] {
+                  return launch_surrogate(pooled, grad, count, gamma, delta, c->compute,
+                                          c->span_on ? c->d_span : nullptr, c->trained);
+              }));
     return SP_OK;
 }
 
@@ -1799,7 +1808,8 @@ sp_status capture_step(sp_ctx *c, int r) {
     if (st) cudaEventRecordWithFlags(c->sev[r][2], c->cap_s, cudaEventRecordExternal);
     launch_forward(ta, c->cap_s);
     if (st) cudaEventRecordWithFlags(c->sev[r][3], c->cap_s, cudaEventRecordExternal);
-    launch_surrogate(k.pooled, k.grad, (long long)c->T * c->N * c->D, k.gamma, k.delta, c->cap_s);
+    launch_surrogate(k.pooled, k.grad, (long long)c->T * c->N * c->D, k.gamma, k.delta, c->cap_s,
+                     c->span_on ? c->d_span : nullptr, r);
     if (st) cudaEventRecordWithFlags(c->sev[r][4], c->cap_s, cudaEventRecordExternal);
     launch_backward(tb, c->cap_s);
     if (st) cudaEventRecordWithFlags(c->sev[r][5], c->cap_s, cudaEventRecordExternal);
@@ -2052,6 +2062,49 @@ sp_status sp_set_stage_timing(sp_ctx *c, int32_t on) {
         drop_graphs(c);  // recaptured with / without the timing event nodes
         for (int r = 0; r < RING; r++) c->sev_used[r][0] = c->sev_used[r][1] = false;
     }
+    return SP_OK;
+}
+
+sp_status sp_set_span_timing(sp_ctx *c, int32_t on) {
+    if (!c) return SP_ERR_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    if (on && !c->d_span)
+        CK(dalloc(c, &c->d_span, (size_t)SPAN_KINDS * RING * SPAN_MAXCTA * 2));
+    if ((on != 0) != c->span_on) {
+        CK(cudaDeviceSynchronize());
+        c->span_on = on != 0;
+        drop_graphs(c);  // recaptured with / without the span pointers
+    }
+    if (on) CK(cudaMemset(c->d_span, 0, (size_t)SPAN_KINDS * RING * SPAN_MAXCTA * 2 * sizeof(unsigned long long)));
+    return SP_OK;
+}
+
+sp_status sp_span_times(sp_ctx *c, double *out_ms) {
+    if (!c || !out_ms) return SP_ERR_INVALID_ARG;
+    const size_t per = (size_t)SPAN_MAXCTA * 2, total = (size_t)SPAN_KINDS * RING * per;
+    for (size_t i = 0; i < (size_t)SPAN_KINDS * RING * 2; i++) out_ms[i] = std::nan("");
+    if (!c->d_span) return SP_OK;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(total);
+    CK(cudaMemcpy(h.data(), c->d_span, total * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    std::vector<unsigned long long> lo((size_t)SPAN_KINDS * RING, ~0ull), hi((size_t)SPAN_KINDS * RING, 0);
+    for (size_t q = 0; q < (size_t)SPAN_KINDS * RING; q++) {
+        for (size_t k = 0; k < (size_t)SPAN_MAXCTA; k++) {
+            const unsigned long long a = h[q * per + 2 * k], b = h[q * per + 2 * k + 1];
+            if (a && b >= a) {
+                lo[q] = std::min(lo[q], a);
+                hi[q] = std::max(hi[q], b);
+            }
+        }
+        if (hi[q]) t0 = std::min(t0, lo[q]);
+    }
+    for (size_t q = 0; q < (size_t)SPAN_KINDS * RING; q++)
+        if (hi[q]) {
+            out_ms[2 * q] = (double)(lo[q] - t0) * 1e-6;
+            out_ms[2 * q + 1] = (double)(hi[q] - t0) * 1e-6;
+        }
     return SP_OK;
 }
 

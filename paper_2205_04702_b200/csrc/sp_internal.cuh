@@ -155,6 +155,7 @@ struct PushArgs {
     // profiling (nullable): [0,T) plan-CTA ns, [T,2T) dedup-CTA ns summed over
     // launches, [2T] plan launches, [2T+1] dedup launches
     unsigned long long *prof;
+    unsigned long long *span;  // span timing (nullable): Plan(b) at slot b % RING
 };
 
 struct TrainArgs {
@@ -173,6 +174,8 @@ struct TrainArgs {
     uint32_t *seg_cnt;   // [T][n] arrivals per multi-tile row (self-resetting)
     uint32_t *grp_cnt;   // [T][ntiles][2] arrivals per group of 8 pieces (self-resetting)
     int tr, ntiles;
+    unsigned long long *span;  // span timing (nullable), slot = batch % RING
+    long long span_b;
 };
 
 struct XferArgs {
@@ -199,6 +202,7 @@ struct XferArgs {
     unsigned long long *staged;  // pinned host flag: = b + 1 once every victim is staged
     long long b;
     const unsigned long long *err;
+    unsigned long long *span;  // span timing (nullable)
 };
 
 
@@ -275,6 +279,24 @@ __device__ __forceinline__ int find_table(const uint32_t *s_pref, int tcount, ui
     return lo;
 }
 
+// Span timing (sp_set_span_timing): every CTA of the five stage kernels
+// stamps %globaltimer when it starts its work and when it is done, into
+// span[kind][ring slot][cta][start, end]; the host takes min / max per
+// (kind, slot).  No atomics, no events in the graphs: the steady state is
+// timed as it runs (bench.py's per-stage durations and overlap).
+enum SpanKind : int { SPK_PLAN = 0, SPK_XFER = 1, SPK_FWD = 2, SPK_SURR = 3, SPK_BWD = 4, SPAN_KINDS = 5 };
+constexpr int SPAN_MAXCTA = 4096;
+__device__ __forceinline__ unsigned long long *span_base(unsigned long long *span, int kind, long long b) {
+    return span ? span + (((size_t)kind * RING + (size_t)(b % RING)) * SPAN_MAXCTA) * 2 : nullptr;
+}
+__device__ __forceinline__ void span_mark(unsigned long long *base, int which) {
+    if (base && threadIdx.x == 0 && blockIdx.x < (unsigned)SPAN_MAXCTA) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        base[(size_t)blockIdx.x * 2 + which] = t;
+    }
+}
+
 // launchers (return cudaGetLastError())
 cudaError_t launch_push(const PushArgs &a, cudaStream_t s);
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s);
@@ -283,7 +305,7 @@ int backward_hot_segment(int D);
 int backward_tile_rows(int D);   // k_bwd_tile rows per tile
 bool backward_tiled();           // k_bwd_tile (default) vs the record-based k_bwd (SP_BWD=rec)
 cudaError_t launch_surrogate(const float *pooled, float *grad, long long count, float gamma,
-                             float delta, cudaStream_t s);
+                             float delta, cudaStream_t s, unsigned long long *span = nullptr, long long span_b = 0);
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_xfer_warp(const XferArgs &a, int ctas, cudaStream_t s);
 cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s);

@@ -72,3 +72,24 @@ def test_plan_roles_window_means_and_percentiles(bench):
     assert len(r["plan"]["phases_us_of_argmax"]) == 6 and len(r["dedup"]["phases_us_of_argmax"]) == 5
     pl = r["per_launch_p50_p90_p99_us"]
     assert pl["launches"] == 3 and pl["kernel_span"][0] == pytest.approx(20.0)
+
+
+def test_span_summary_durations_busy_and_step(bench):
+    import numpy as np
+    sp = np.full((5, 16, 2), np.nan)
+    # 4 steps of 50 us: plan 0-20, transfer 10-60 (overlapping the next step's),
+    # fwd 20-30, surrogate 30-35, backward 35-50
+    for r in range(4):
+        t0 = r * 0.05
+        sp[0, r] = [t0, t0 + 0.02]
+        sp[1, r] = [t0 + 0.01, t0 + 0.06]
+        sp[2, r] = [t0 + 0.02, t0 + 0.03]
+        sp[3, r] = [t0 + 0.03, t0 + 0.035]
+        sp[4, r] = [t0 + 0.035, t0 + 0.05]
+    s = bench._span_summary(sp)
+    assert s["duration_us"]["backward"] == pytest.approx(15.0)
+    assert s["duration_us"]["transfer"] == pytest.approx(50.0)
+    assert s["step_us"] == pytest.approx(50.0)
+    assert s["stream_busy_us_per_step"]["compute"] == pytest.approx(30.0)
+    # transfers back to back (each 50 us, one per step): busy the whole step
+    assert s["stream_busy_us_per_step"]["transfer"] == pytest.approx(50.0)
