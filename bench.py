@@ -433,8 +433,8 @@ def run_ours(args):
     pre = cfg.preroll if args.preroll < 0 else args.preroll
     P, F = cfg.window, max(cfg.window - 1, 0)
     ahead = P + F + 1
-    KS = 48 if world == 1 else 0       # graph-mode stage-timing pass (16 recaptures + 32 timed)
-    nb_dev = pre + W + K + KS + KP     # device-index phase (incl. the `ahead` pushed first)
+    KS = 48 if world == 1 else 0       # graph-mode stage-timing pass (16 recaptures + 32 timed), and again for spans
+    nb_dev = pre + W + K + 2 * KS + KP  # device-index phase (incl. the `ahead` pushed first)
     WE = max(W, 18)                    # e2e warm-up: also (re)captures the 16 step graphs
     nb_host = WE + K                   # host-index (e2e) phase
     nb = nb_dev + ahead + nb_host

@@ -508,6 +508,10 @@ __device__ __forceinline__ void row_g2s(void *dst, const void *src, uint32_t byt
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
 }
+// 16-B async copy global -> shared (LDGSTS), L2 only
+__device__ __forceinline__ void cp16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void dadd4(double4 &a, const double4 &b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
 __device__ __forceinline__ double4 ld_piece(const double *p) {  // L2: written by other SMs
     return ldcg_d4(reinterpret_cast<const double4 *>(p));
@@ -592,14 +596,34 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const bool whole = first && !(uid == uid_last && tail_open);  // (lane 0 of an open head is not `first`)
         const unsigned wmask = __ballot_sync(0xffffffffu, whole);
         const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
-        if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
-        __syncwarp();
-        if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + m.occ / (uint32_t)g.L) * D4, rowb, &bar);
-        if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowb, &bar);
-        load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
-        while (!bar_try(&bar, parity)) {
+        if (A.bwd_tma) {  // (A/B) one TMA bulk copy per row, completion on the mbarrier
+            if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
+            __syncwarp();
+            if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + m.occ / (uint32_t)g.L) * D4, rowb, &bar);
+            if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowb, &bar);
+            load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
+            while (!bar_try(&bar, parity)) {
+            }
+            parity ^= 1u;
+        } else {
+            // 16-B async copies (LDGSTS), one warp-wide instruction per 512 B
+            // of row: small bulk copies are bound by the per-SM TMA request
+            // rate, these by the memory system
+            for (int r = 0; r < nact; r++) {
+                const uint32_t o = __shfl_sync(0xffffffffu, m.occ, r);
+                const float4 *src = grad + ((size_t)t * g.N + o / (uint32_t)g.L) * D4;
+                for (int c = lane; c < D4; c += 32) cp16(sg + (size_t)r * D4 + c, src + c);
+            }
+            for (unsigned wm = wmask; wm; wm &= wm - 1) {
+                const int r = __ffs(wm) - 1;
+                const uint32_t sl = __shfl_sync(0xffffffffu, slot, r);
+                for (int c = lane; c < D4; c += 32) cp16(sw + (size_t)r * D4 + c, st + (size_t)sl * D4 + c);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
         }
-        parity ^= 1u;
         // 2. fold segment by segment (a segment = one row's occurrences in
         // this tile).  A whole row of 1 or 2 occurrences is summed in fp32:
         // that is the fp32 rounding of the exact sum, i.e. the oracle's
@@ -725,7 +749,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         // the tile's shared rows are consumed (generic proxy) before the next
         // tile's bulk copies (async proxy) overwrite them
         __syncwarp();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (A.bwd_tma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     span_mark(spn, 1);
 }

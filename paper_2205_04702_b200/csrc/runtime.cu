@@ -260,6 +260,7 @@ struct sp_ctx {
     double *d_tpart = nullptr;    // [T][ntiles][2][D]
     uint32_t *d_seg_cnt = nullptr, *d_grp_cnt = nullptr;  // [T][n], [T][ntiles][2]
     int bwd_tr = 0, bwd_ntiles = 0;
+    int bwd_tma = 0;  // SP_BWD_TMA=1: k_bwd_tile stages rows with TMA bulk copies (A/B)
     float **d_host = nullptr;
     void *d_idx[RING] = {};
     BatchBufs ring[RING];
@@ -645,6 +646,7 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.grp_cnt = c->d_grp_cnt;
     a.tr = c->bwd_tr;
     a.ntiles = c->bwd_ntiles;
+    a.bwd_tma = c->bwd_tma;
     a.span = c->span_on ? c->d_span : nullptr;
     a.span_b = b;
     a.err = c->d_err;
@@ -1133,6 +1135,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     // not host-link throughput)
     if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_XFER")) c->xfer_warp = std::string(e) == "warp";
+    if (const char *e = getenv("SP_BWD_TMA")) c->bwd_tma = atoi(e) != 0;
     if (const char *e = getenv("SP_XFER_CTAS")) c->xfer_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_WB_GPU_FRAC")) {
         const double f = atof(e);

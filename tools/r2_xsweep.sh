@@ -12,8 +12,10 @@ for spec in "$@"; do
 import json, sys
 try:
     d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-    print("   busy", d["overlap"]["stream_busy_us_per_step"], "pass step", d["overlap"].get("timing_pass_step_us"),
-          "| eng", d["host_engine"], "| link h2d %.1f d2h %.1f GB/s" % (d["host_link"]["h2d_GBs"], d["host_link"]["d2h_GBs"]))
+    sp = d.get("spans") or {}
+    print("   spans", sp.get("duration_us"), "busy", sp.get("stream_busy_us_per_step"), "step", sp.get("step_us"),
+          "| eng", {k: v for k, v in d["host_engine"].items() if k != "threads"},
+          "| link h2d %.1f d2h %.1f GB/s" % (d["host_link"]["h2d_GBs"], d["host_link"]["d2h_GBs"]))
 except Exception as e:
     print("   parse error", e)
 PY
