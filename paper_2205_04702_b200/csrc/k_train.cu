@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const bool whole = first && !(uid == uid_last && tail_open);  // (lane 0 of an open head is not `first`)
         const unsigned wmask = __ballot_sync(0xffffffffu, whole);
         const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
-        if (A.bwd_tma) {  // (A/B) one TMA bulk copy per row, completion on the mbarrier
+        if (A.bwd_tma) {  // one TMA bulk copy per row, completion on the mbarrier
             if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
             __syncwarp();
             if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + m.occ / (uint32_t)g.L) * D4, rowb, &bar);
@@ -606,9 +606,9 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             }
             parity ^= 1u;
         } else {
-            // 16-B async copies (LDGSTS), one warp-wide instruction per 512 B
-            // of row: small bulk copies are bound by the per-SM TMA request
-            // rate, these by the memory system
+            // (A/B) 16-B async copies (LDGSTS), one warp-wide instruction per
+            // 512 B of row: measured slower than the bulk copies (TB pipelined
+            // 54 vs 38 us in-situ span; profiles/r02_xs3_sweep.txt)
             for (int r = 0; r < nact; r++) {
                 const uint32_t o = __shfl_sync(0xffffffffu, m.occ, r);
                 const float4 *src = grad + ((size_t)t * g.N + o / (uint32_t)g.L) * D4;

@@ -260,7 +260,7 @@ struct sp_ctx {
     double *d_tpart = nullptr;    // [T][ntiles][2][D]
     uint32_t *d_seg_cnt = nullptr, *d_grp_cnt = nullptr;  // [T][n], [T][ntiles][2]
     int bwd_tr = 0, bwd_ntiles = 0;
-    int bwd_tma = 0;  // SP_BWD_TMA=1: k_bwd_tile stages rows with TMA bulk copies (A/B)
+    int bwd_tma = 1;  // k_bwd_tile stages rows with TMA bulk copies; SP_BWD_TMA=0: LDGSTS (A/B, slower)
     float **d_host = nullptr;
     void *d_idx[RING] = {};
     BatchBufs ring[RING];

@@ -174,7 +174,7 @@ struct TrainArgs {
     uint32_t *seg_cnt;   // [T][n] arrivals per multi-tile row (self-resetting)
     uint32_t *grp_cnt;   // [T][ntiles][2] arrivals per group of 8 pieces (self-resetting)
     int tr, ntiles;
-    int bwd_tma;         // k_bwd_tile stages rows by TMA bulk copies (SP_BWD_TMA=1) instead of LDGSTS
+    int bwd_tma;         // k_bwd_tile stages rows by TMA bulk copies (default) or LDGSTS (SP_BWD_TMA=0)
     unsigned long long *span;  // span timing (nullable), slot = batch % RING
     long long span_b;
 };
