@@ -163,6 +163,17 @@ def host_cpu_info():
     return info
 
 
+def host_mem_available():
+    """MemAvailable of this node in bytes (None if unknown)."""
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
 def link_peaks(dev, mib=256, reps=5):
     """Host-link peaks measured in this run: pinned cudaMemcpyAsync of `mib`
     MiB, best of `reps`, H2D, D2H and both directions at once (two streams),
@@ -357,7 +368,8 @@ def _span_summary(sp_ms):
     busy = {"plan": _union_us(iv["plan"]) / max(1, len(iv["plan"])),
             "transfer": _union_us(iv["transfer"]) / max(1, len(iv["transfer"])),
             "compute": _union_us(iv["forward"] + iv["surrogate"] + iv["backward"]) / nst}
-    return {"duration_us": {k: (round(v, 2) if v is not None else None) for k, v in dur.items()},
+    return {"raw_ms": [[[round(x, 4) if x == x else None for x in ab] for ab in sp_ms[i]] for i in range(5)],
+            "duration_us": {k: (round(v, 2) if v is not None else None) for k, v in dur.items()},
             "stream_busy_us_per_step": {k: round(v, 2) for k, v in busy.items()},
             "step_us": round(step, 2), "steps": nst,
             "source": "%globaltimer stamps of every CTA of the five stage kernels in the graph-mode "
@@ -441,6 +453,11 @@ def run_ours(args):
 
     # ---- inputs: host tables (pinned), trace (device int32; host int32 part pinned)
     from paper_2205_04702_b200 import HostTable
+    need = sum(cfg.rows[t] for t in mine) * D * 4
+    avail = host_mem_available()
+    if avail is not None and need > 0.9 * avail:
+        raise SystemExit(f"host RAM: this rank's tables need {need / 1e9:.1f} GB of pinned memory, the node has "
+                         f"{avail / 1e9:.1f} GB available (MemAvailable): run {args.config} on more GPUs or a larger node")
     tables = []   # THP-backed, CUDA-registered host tables (sp_host_alloc)
     for t in mine:
         h = HostTable(cfg.rows[t], D)

@@ -89,7 +89,10 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 // request instead of sixteen 16-B loads.  The flattened fill list is split
 // into contiguous shares, one per CTA, moved in rounds of nb items (one per
 // lane) through XS shared-memory stages.
-constexpr int XS = 4;
+#ifndef SP_XS
+#define SP_XS 4  // shared-memory stages per transfer CTA (compile-time A/B)
+#endif
+constexpr int XS = SP_XS;
 
 __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
     extern __shared__ __align__(128) unsigned char sm[];
@@ -114,35 +117,49 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
         const int tcount = min(64, g.T - t0);
         table_prefix(A.bb.m, t0, tcount, s_pref);  // (32 threads: one warp)
         const uint32_t total = s_pref[tcount];
-        const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
-        const uint32_t lo = min(total, blockIdx.x * per), hi = min(total, lo + per);
-        const uint32_t nround = hi > lo ? (hi - lo + nb - 1) / nb : 0;
         // per stage: nb victim rows, then nb new rows (contiguous, so a gathered
         // round moves as one bulk copy each way)
         auto vbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + i) * rowb; };
         auto nbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + nb + i) * rowb; };
         const bool direct = A.wb_direct != 0;  // victims straight to their host rows
         // items [0, Kg) of this table group were gathered by the CPU into the
-        // contiguous pinned slot, the rest are pulled from their host rows
-        // (hybrid split: the CPU gather and the GPU pull run concurrently)
+        // contiguous pinned slot, the rest [Kg, total) are pulled from their
+        // host rows (hybrid split: the CPU gather and the GPU pull run
+        // concurrently).  Every CTA takes a contiguous share of BOTH ranges and
+        // runs its pulled rounds first, so all CTAs pull while the CPU gathers
+        // and reach the gathered rows last.
         const uint32_t Kg = !A.in_stage ? 0u
                             : (A.gfrac_q16 >= 65536u ? total : (uint32_t)(((unsigned long long)total * A.gfrac_q16) >> 16));
-        auto round_gathered = [&](uint32_t r) {  // the whole round comes from the gathered slot
-            const uint32_t k0 = lo + r * nb;
-            return A.in_stage != nullptr && !A.diag_nowb && k0 + min((uint32_t)nb, hi - k0) <= Kg;
+        const uint32_t G = gridDim.x, Pn = total - Kg;
+        const uint32_t pper = (Pn + G - 1) / G, gper = (Kg + G - 1) / G;
+        const uint32_t plo = Kg + min(Pn, blockIdx.x * pper), phi = Kg + min(Pn, blockIdx.x * pper + pper);
+        const uint32_t glo = min(Kg, blockIdx.x * gper), ghi = min(Kg, blockIdx.x * gper + gper);
+        const uint32_t npr = phi > plo ? (phi - plo + nb - 1) / nb : 0u;
+        const uint32_t nround = npr + (ghi > glo ? (ghi - glo + nb - 1) / nb : 0u);
+        auto round_k0 = [&](uint32_t r) { return r < npr ? plo + r * nb : glo + (r - npr) * nb; };
+        auto round_cnt = [&](uint32_t r) {
+            const uint32_t k0 = round_k0(r);
+            return min((uint32_t)nb, (r < npr ? phi : ghi) - k0);
         };
-        if (A.gwait && lo < Kg && hi > lo) {
+        auto round_gathered = [&](uint32_t r) {  // the whole round comes from the gathered slot
+            return A.in_stage != nullptr && !A.diag_nowb && r >= npr;
+        };
+        bool waited = !(A.gwait && ghi > glo);
+        auto wait_gathered = [&]() {
             // hybrid: this CTA reads gathered rows; wait (in-kernel, on the
             // pinned progress counter) until the CPU has gathered batch b
+            if (waited) return;
             if (lane == 0)
                 while (*(volatile const unsigned long long *)A.gwait < (unsigned long long)(A.b + 1)) __nanosleep(512);
             __syncwarp();
             __threadfence_system();
-        }
+            waited = true;
+        };
         auto issue = [&](uint32_t r) {
             const int s = (int)((phase_ctr + r) % XS);
-            const uint32_t k0 = lo + r * nb;
-            const uint32_t cnt = min((uint32_t)nb, hi - k0);
+            const uint32_t k0 = round_k0(r);
+            const uint32_t cnt = round_cnt(r);
+            if (round_gathered(r)) wait_gathered();
             uint32_t bytes = 0, slot = EMPTY, stage = EMPTY;
             const float *src_host = nullptr;
             if ((uint32_t)lane < cnt) {
@@ -200,7 +217,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 // victims: one contiguous bulk store of the round's staging rows
                 // (rows of fills without a victim carry garbage; their work-list
                 // entry is 0, so the scatter skips them)
-                const uint32_t k0 = lo + r * nb, cnt = min((uint32_t)nb, hi - k0);
+                const uint32_t k0 = round_k0(r), cnt = round_cnt(r);
                 if (lane == 0 && cnt) bulk_s2g(A.wb_stage + (size_t)(base_t0 + k0) * g.D, vbuf(s, 0), cnt * rowb);
             } else if (slot != EMPTY && stage != EMPTY && !dd) {
                 bulk_s2g(A.wb_stage + (size_t)stage * g.D, vbuf(s, lane), rowb);
