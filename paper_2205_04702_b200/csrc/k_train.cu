@@ -16,7 +16,10 @@
 //   k_surrogate  the harness's MLP stand-in g = fmaf(gamma, pooled, delta).
 #include "sp_internal.cuh"
 
+#include <cuda.h>  // CUtensorMap (tile::gather4)
+
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 
@@ -508,6 +511,16 @@ __device__ __forceinline__ void row_g2s(void *dst, const void *src, uint32_t byt
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
 }
+// TMA tile::gather4: rows r0..r3 (all D columns) of the 2-D tensor of `tm`
+// into consecutive rows of shared memory at dst, completion on bar
+__device__ __forceinline__ void rows4_g2s(void *dst, const CUtensorMap *tm, uint32_t r0, uint32_t r1, uint32_t r2,
+                                          uint32_t r3, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5, %6}], [%7];" ::"r"(smem_addr(dst)),
+        "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_addr(bar))
+        : "memory");
+}
 // 16-B async copy global -> shared (LDGSTS), L2 only
 __device__ __forceinline__ void cp16(void *dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
@@ -532,7 +545,8 @@ __device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total) 
 #define SP_BWD_TILE_MINB 16  // resident warps per SM the registers are sized for (<= 128 regs)
 #endif
 template <int VPL>
-__global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_TILE_MINB) k_bwd_tile(TrainArgs A) {
+__global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_TILE_MINB)
+    k_bwd_tile(TrainArgs A, const __grid_constant__ CUtensorMap tmg, const __grid_constant__ CUtensorMap tms) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t bar;
     if (*A.err != NO_ERR) return;
@@ -596,7 +610,30 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const bool whole = first && !(uid == uid_last && tail_open);  // (lane 0 of an open head is not `first`)
         const unsigned wmask = __ballot_sync(0xffffffffu, whole);
         const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
-        if (A.bwd_tma) {  // one TMA bulk copy per row, completion on the mbarrier
+        if (A.g4) {
+            // TMA tile::gather4: lane q fetches tile rows 4q..4q+3 (the last
+            // group padded with the last row) and lane q the Storage rows of
+            // whole segments 4q..4q+3 (compacted: the k-th whole segment's row
+            // at sw[k]); one request per 4 rows
+            const int ng = (nact + 3) >> 2, nw = __popc(wmask), nsg = (nw + 3) >> 2;
+            if (lane == 0) bar_expect(&bar, (uint32_t)(4 * ng + 4 * nsg) * rowb);
+            __syncwarp();
+            const uint32_t grow = (uint32_t)t * (uint32_t)g.N + m.occ / (uint32_t)g.L;
+            uint32_t gr[4], sr[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                gr[i] = __shfl_sync(0xffffffffu, grow, min(4 * lane + i, nact - 1));
+                const int j = min(4 * lane + i, max(nw - 1, 0));
+                const int pos = nw ? (int)__fns(wmask, 0, j + 1) : 0;
+                sr[i] = __shfl_sync(0xffffffffu, slot, pos & 31);
+            }
+            if (lane < ng) rows4_g2s(sg + (size_t)4 * lane * D4, &tmg, gr[0], gr[1], gr[2], gr[3], &bar);
+            if (lane < nsg) rows4_g2s(sw + (size_t)4 * lane * D4, &tms, sr[0], sr[1], sr[2], sr[3], &bar);
+            load_meta(tile + gridDim.x, nxt);
+            while (!bar_try(&bar, parity)) {
+            }
+            parity ^= 1u;
+        } else if (A.bwd_tma) {  // one TMA bulk copy per row, completion on the mbarrier
             if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
             __syncwarp();
             if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + m.occ / (uint32_t)g.L) * D4, rowb, &bar);
@@ -637,6 +674,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             const int len = r1 - r0 + 1;
             const uint32_t s = __shfl_sync(0xffffffffu, slot, r0);
             const bool wh = (wmask >> r0) & 1u;
+            const int wr = A.g4 ? __popc(wmask & ((1u << r0) - 1u)) : r0;  // its staged Storage row
             if (wh && len <= 2 && !(A.diag & 32)) {  // (SP_DIAG=32: every row through fp64, A/B)
 #pragma unroll
                 for (int v = 0; v < VPL; v++) {
@@ -644,7 +682,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
                     if (c < D4) {
                         float4 gs = sg[(size_t)r0 * D4 + c];
                         if (len == 2) add4(gs, sg[(size_t)(r0 + 1) * D4 + c]);
-                        st[(size_t)s * D4 + c] = sgd32(sw[(size_t)r0 * D4 + c], gs, A.lr);
+                        st[(size_t)s * D4 + c] = sgd32(sw[(size_t)wr * D4 + c], gs, A.lr);
                     }
                 }
                 r0 = r1 + 1;
@@ -668,7 +706,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
                     const int c = lane + 32 * v;
                     if (c < D4)
                         st[(size_t)s * D4 + c] =
-                            sgd(sw[(size_t)r0 * D4 + c], Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr);
+                            sgd(sw[(size_t)wr * D4 + c], Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr);
                 }
             } else {
                 // 3. a piece of a row spanning tiles [kf, kl]: slot 0 of tile k
@@ -749,7 +787,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         // the tile's shared rows are consumed (generic proxy) before the next
         // tile's bulk copies (async proxy) overwrite them
         __syncwarp();
-        if (A.bwd_tma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (A.bwd_tma || A.g4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     span_mark(spn, 1);
 }
@@ -952,8 +990,52 @@ bool backward_tiled() {
     return !(e && e[0] == 'r');
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda)
+typedef CUresult (*tmap_encode_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static tmap_encode_fn tmap_encode() {
+    static tmap_encode_fn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<tmap_encode_fn>(p);
+        (void)cudaGetLastError();
+    });
+    return fn;
+}
+
+// a [rows][D] fp32 matrix as a 2-D tensor map with a one-row box (the form
+// tile::gather4 takes: tools/gather4_probe.cu)
+static bool rows_map(CUtensorMap *m, const void *base, unsigned long long rows, int D) {
+    tmap_encode_fn enc = tmap_encode();
+    if (!enc || !base || rows == 0 || D > 256 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t gdim[2] = {(cuuint64_t)D, (cuuint64_t)rows}, gstr[1] = {(cuuint64_t)D * 4};
+    cuuint32_t box[2] = {(cuuint32_t)D, 1}, es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), gdim, gstr, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int g_bwd_g4 = -1;  // SP_BWD_G4: 0 disables tile::gather4 (A/B)
+
 template <int VPL>
-static void launch_bwd_tile(const TrainArgs &a, cudaStream_t s) {
+static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
+    TrainArgs a = a0;
+    CUtensorMap tmg, tms;
+    std::memset(&tmg, 0, sizeof tmg);
+    std::memset(&tms, 0, sizeof tms);
+    if (g_bwd_g4 < 0) {
+        const char *e = getenv("SP_BWD_G4");
+        g_bwd_g4 = e ? (atoi(e) != 0) : 1;
+    }
+    a.g4 = g_bwd_g4 && a.bwd_tma && a.tr % 4 == 0 && a.tr <= 32 &&
+           rows_map(&tmg, a.grad, (unsigned long long)a.g.T * a.g.N, a.g.D) &&
+           rows_map(&tms, a.storage, (unsigned long long)a.srows, a.g.D);
     const size_t smem = (size_t)2 * a.tr * a.g.D * sizeof(float);
     static std::map<std::pair<int, size_t>, int> caps;  // (device, smem) -> resident CTAs
     int dev = 0;
@@ -976,7 +1058,7 @@ static void launch_bwd_tile(const TrainArgs &a, cudaStream_t s) {
     const long long tiles = (long long)a.g.T * a.ntiles;
     int grid = (int)(tiles < cap ? tiles : cap);
     if (grid < 1) grid = 1;
-    launch_maybe_pdl(k_bwd_tile<VPL>, grid, 32, smem, s, true, a);
+    launch_maybe_pdl(k_bwd_tile<VPL>, grid, 32, smem, s, true, a, tmg, tms);
 }
 
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {

@@ -329,6 +329,7 @@ struct sp_ctx {
     std::atomic<bool> stop{false};
     RowPool spool;  // scatter helpers
     int host_threads = 6;
+    int scatter_helpers = 0, gather_helpers = 0;  // per pool (0: host_threads); SP_SCATTER_THREADS / SP_GATHER_THREADS
     // CPU gather of the missed rows (default; SP_CPU_GATHER=0 lets the transfer
     // kernel pull random host rows itself): Plan mirrors its
     // missed-row lists to pinned memory, the gather thread copies the rows
@@ -647,6 +648,7 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.tr = c->bwd_tr;
     a.ntiles = c->bwd_ntiles;
     a.bwd_tma = c->bwd_tma;
+    a.srows = c->S_total;
     a.span = c->span_on ? c->d_span : nullptr;
     a.span_b = b;
     a.err = c->d_err;
@@ -1377,6 +1379,9 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         const long pools = (c->cpu_gather ? 2 : 1) * ctx;
         c->host_threads = (int)std::max(1L, std::min(6L, (ncpu - pools) / pools));
     }
+    c->scatter_helpers = c->gather_helpers = c->host_threads;
+    if (const char *e = getenv("SP_SCATTER_THREADS")) c->scatter_helpers = std::max(1, atoi(e) - 1);
+    if (const char *e = getenv("SP_GATHER_THREADS")) c->gather_helpers = std::max(1, atoi(e) - 1);
     if (c->cpu_gather) {
         CKC(cudaHostAlloc((void **)&c->hl_ready, (size_t)RING * c->T * sizeof(unsigned long long), cudaHostAllocMapped));
         CKC(cudaHostAlloc((void **)&c->hl_m, (size_t)RING * c->T * sizeof(uint32_t), cudaHostAllocMapped));
@@ -1444,11 +1449,11 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
 #undef CKC
     // transfer engine: helpers + worker
     if (!c->gpu_wb) {
-        c->spool.start(c->host_threads);
+        c->spool.start(c->scatter_helpers);
         c->scatter_worker = std::thread(scatter_main, c);
     }
     if (c->cpu_gather) {
-        c->gpool.start(c->host_threads);
+        c->gpool.start(c->gather_helpers);
         c->gather_worker = std::thread(gather_main, c);
     }
     *out = c;
@@ -1973,7 +1978,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
                                                               : (c->gather_dma ? SP_XFER_GATHER_DMA : SP_XFER_CPU_GATHER))
                                      : SP_XFER_GPU_PULL;
     o->gather_share = c->cpu_gather ? c->gather_q16 / 65536.0 : 0.0;
-    o->engine_threads = (c->gpu_wb ? 0 : 1 + c->host_threads) + (c->cpu_gather ? 1 + c->host_threads : 0);
+    o->engine_threads = (c->gpu_wb ? 0 : 1 + c->scatter_helpers) + (c->cpu_gather ? 1 + c->gather_helpers : 0);
     o->gpu_writeback = c->gpu_wb ? 1 : 0;
     if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);

@@ -175,6 +175,8 @@ struct TrainArgs {
     uint32_t *grp_cnt;   // [T][ntiles][2] arrivals per group of 8 pieces (self-resetting)
     int tr, ntiles;
     int bwd_tma;         // k_bwd_tile stages rows by TMA bulk copies (default) or LDGSTS (SP_BWD_TMA=0)
+    int g4;              // (set by the launcher) TMA tile::gather4, 4 rows per request, via tensor maps
+    long long srows;     // Storage rows (tensor map of Storage)
     unsigned long long *span;  // span timing (nullable), slot = batch % RING
     long long span_b;
 };
