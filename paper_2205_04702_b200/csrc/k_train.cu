@@ -1033,7 +1033,9 @@ static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
         const char *e = getenv("SP_BWD_G4");
         g_bwd_g4 = e ? (atoi(e) != 0) : 1;
     }
-    a.g4 = g_bwd_g4 && a.bwd_tma && a.tr % 4 == 0 && a.tr <= 32 &&
+    // a tensor copy's shared-memory destination must be 128-B aligned: a
+    // group of 4 rows (16*D bytes) is when D % 8 == 0
+    a.g4 = g_bwd_g4 && a.bwd_tma && a.tr % 4 == 0 && a.tr <= 32 && a.g.D % 8 == 0 &&
            rows_map(&tmg, a.grad, (unsigned long long)a.g.T * a.g.N, a.g.D) &&
            rows_map(&tms, a.storage, (unsigned long long)a.srows, a.g.D);
     const size_t smem = (size_t)2 * a.tr * a.g.D * sizeof(float);

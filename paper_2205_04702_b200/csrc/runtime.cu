@@ -85,6 +85,7 @@ struct RowPool {
             for (long i = i0; i < i1; i++) {
                 const char *p = reinterpret_cast<const char *>(src[i]);
                 for (size_t o = 0; o < bytes; o += 64) __builtin_prefetch(p + o, 0, 2);
+                __builtin_prefetch(dst[i], 1, 2);  // the destination's translation, walked early
             }
             // non-temporal stores: a random destination row costs no
             // read-for-ownership, and staging never pollutes the caches
@@ -123,8 +124,11 @@ struct RowPool {
         for (int i = 0; i < nthreads; i++) th.emplace_back([this] { helper(); });
     }
 
+    std::mutex job_mu;  // one copy job at a time (a pool shared by the gather and scatter threads)
+
     void copy(const float *const *s, float *const *d, long count, size_t row_bytes) {
         if (count <= 0) return;
+        std::lock_guard<std::mutex> lk(job_mu);
         src = s;
         dst = d;
         n = count;
@@ -339,6 +343,7 @@ struct sp_ctx {
     uint32_t gather_q16 = 65536;  // CPU-gathered share of each batch's fills (hybrid < 65536)
     std::thread gather_worker;
     RowPool gpool;  // gather helpers
+    bool shared_pool = false;  // SP_SHARED_POOL=1: gather and scatter jobs take turns on one pool of both sizes
     unsigned long long *hl_ready = nullptr;    // pinned mapped [RING][T]
     uint32_t *hl_m = nullptr;                  // pinned mapped [RING][T]
     uint32_t *hl_row = nullptr;                // pinned mapped [RING][T][n]
@@ -784,7 +789,7 @@ void gather_main(sp_ctx *c) {
                 k0 += total;
             }
             const auto t0 = std::chrono::steady_clock::now();
-            c->gpool.copy(src.data(), dst.data(), (long)src.size(), rowb);
+            (c->shared_pool ? c->spool : c->gpool).copy(src.data(), dst.data(), (long)src.size(), rowb);
             c->x_gather_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
                                   std::chrono::steady_clock::now() - t0).count();
             c->x_rows_g += (long long)src.size();
@@ -1449,11 +1454,12 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
 #undef CKC
     // transfer engine: helpers + worker
     if (!c->gpu_wb) {
-        c->spool.start(c->scatter_helpers);
+        if (const char *e = getenv("SP_SHARED_POOL")) c->shared_pool = atoi(e) != 0 && c->cpu_gather;
+        c->spool.start(c->shared_pool ? c->scatter_helpers + c->gather_helpers : c->scatter_helpers);
         c->scatter_worker = std::thread(scatter_main, c);
     }
     if (c->cpu_gather) {
-        c->gpool.start(c->gather_helpers);
+        if (!c->shared_pool) c->gpool.start(c->gather_helpers);
         c->gather_worker = std::thread(gather_main, c);
     }
     *out = c;
