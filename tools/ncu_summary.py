@@ -71,7 +71,8 @@ def full_raw(path):
 def main():
     src, tag = sys.argv[1], sys.argv[2]
     lines = [f"# {tag}: ncu evidence from {src} (bench.py, steady state)"]
-    ll = launch_list(os.path.join(src, "launches.csv"))
+    lp = os.path.join(src, "launches.csv")
+    ll = launch_list(lp) if os.path.exists(lp) else {}
     tot = sum(sum(v) for v in ll.values()) or 1.0
     lines.append("# launch list: ncu --metrics gpu__time_duration.sum --clock-control none "
                  "(serialised, cold cache: compare SHARES, not absolute times)")
