@@ -541,6 +541,144 @@ __device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total) 
 }
 }  // namespace
 
+// 2.-3. of a tile (shared by k_bwd_tile and the warp-specialised k_bwd_ws):
+// fold the staged rows segment by segment and update Storage, or leave the
+// pieces of rows spanning tiles and fold them at the last arrival.  Lane
+// masks: lmask = last row of each segment in the tile, wmask = first row of
+// each row wholly inside it; per lane (row r): slot, uid.
+template <int VPL>
+__device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, unsigned lmask, unsigned wmask,
+                                              uint32_t slot, uint32_t uid, const float4 *sg, const float4 *sw) {
+    const Geometry &g = A.g;
+    const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
+    const int lane = threadIdx.x & 31;
+    float4 *st = reinterpret_cast<float4 *>(A.storage);
+    const size_t tb = (size_t)t * g.n;
+    // 2. fold segment by segment (a segment = one row's occurrences in
+    // this tile).  A whole row of 1 or 2 occurrences is summed in fp32:
+    // that is the fp32 rounding of the exact sum, i.e. the oracle's
+    // (float)(fp64 sum) (reading R7); longer rows and pieces of rows
+    // spanning tiles accumulate in fp64 in ascending occurrence order.
+    unsigned ends = lmask;
+    int r0 = 0;  // first row of the current segment
+    while (ends) {
+        const int r1 = __ffs(ends) - 1;  // its last row
+        ends &= ends - 1;
+        const int len = r1 - r0 + 1;
+        const uint32_t s = __shfl_sync(0xffffffffu, slot, r0);
+        const bool wh = (wmask >> r0) & 1u;
+        const int wr = A.g4 ? __popc(wmask & ((1u << r0) - 1u)) : r0;  // its staged Storage row
+        if (wh && len <= 2 && !(A.diag & 32)) {  // (SP_DIAG=32: every row through fp64, A/B)
+#pragma unroll
+            for (int v = 0; v < VPL; v++) {
+                const int c = lane + 32 * v;
+                if (c < D4) {
+                    float4 gs = sg[(size_t)r0 * D4 + c];
+                    if (len == 2) add4(gs, sg[(size_t)(r0 + 1) * D4 + c]);
+                    st[(size_t)s * D4 + c] = sgd32(sw[(size_t)wr * D4 + c], gs, A.lr);
+                }
+            }
+            r0 = r1 + 1;
+            continue;
+        }
+        double4 acc[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; v++) {
+            acc[v] = make_double4(0.0, 0.0, 0.0, 0.0);
+            const int c = lane + 32 * v;
+            if (c < D4)
+                for (int r = r0; r <= r1; r++) {
+                    const float4 x = sg[(size_t)r * D4 + c];
+                    acc[v].x += (double)x.x; acc[v].y += (double)x.y;
+                    acc[v].z += (double)x.z; acc[v].w += (double)x.w;
+                }
+        }
+        if (wh) {  // the whole row is in this tile
+#pragma unroll
+            for (int v = 0; v < VPL; v++) {
+                const int c = lane + 32 * v;
+                if (c < D4)
+                    st[(size_t)s * D4 + c] =
+                        sgd(sw[(size_t)wr * D4 + c], Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr);
+            }
+        } else {
+            // 3. a piece of a row spanning tiles [kf, kl]: slot 0 of tile k
+            // if the row holds the tile's first occurrence, else slot 1
+            // (only possible in the row's first tile)
+            const uint32_t u = __shfl_sync(0xffffffffu, uid, r0);
+            uint32_t slo = 0, shi = 0;
+            if (lane == 0) {
+                slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u);
+                shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
+            }
+            slo = __shfl_sync(0xffffffffu, slo, 0);
+            shi = __shfl_sync(0xffffffffu, shi, 0);
+            const int kf = (int)(slo / (uint32_t)TR), kl = (int)((shi - 1u) / (uint32_t)TR);
+            const int npc = kl - kf + 1;
+            auto pslot = [&](int kk) { return (kk == kf && slo != (uint32_t)(kf * TR)) ? 1 : 0; };
+            auto piece = [&](int kk) { return A.tpart + (((size_t)t * NT + kk) * 2 + pslot(kk)) * g.D; };
+            double *mine = piece(k);
+#pragma unroll
+            for (int v = 0; v < VPL; v++) {
+                const int c = lane + 32 * v;
+                if (c < D4) reinterpret_cast<double4 *>(mine)[c] = acc[v];
+            }
+            bool go = true;
+            int step = 1, cnt = npc;
+            if (npc > 8) {  // level 1: groups of 8 consecutive pieces
+                const int gi = (k - kf) / 8, g0 = kf + 8 * gi, gsz = min(8, kl - g0 + 1);
+                uint32_t *gc = A.grp_cnt + ((size_t)t * NT + g0) * 2 + pslot(g0);
+                go = warp_arrive_last(gc, (uint32_t)gsz);
+                if (go) {
+                    if (lane == 0) *gc = 0u;
+#pragma unroll
+                    for (int v = 0; v < VPL; v++) {
+                        const int c = lane + 32 * v;
+                        if (c >= D4) continue;
+                        double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
+                        for (int q0 = 0; q0 < gsz; q0 += 4) {
+                            double4 x[4];
+#pragma unroll
+                            for (int q = 0; q < 4; q++)
+                                if (q0 + q < gsz) x[q] = ld_piece(piece(g0 + q0 + q) + 4 * c);
+#pragma unroll
+                            for (int q = 0; q < 4; q++)
+                                if (q0 + q < gsz) dadd4(m, x[q]);
+                        }
+                        reinterpret_cast<double4 *>(piece(g0))[c] = m;
+                    }
+                }
+                step = 8;
+                cnt = (npc + 7) / 8;
+            }
+            if (go) {
+                uint32_t *rc = A.seg_cnt + tb + u;
+                if (warp_arrive_last(rc, (uint32_t)cnt)) {
+                    if (lane == 0) *rc = 0u;
+#pragma unroll
+                    for (int v = 0; v < VPL; v++) {
+                        const int c = lane + 32 * v;
+                        if (c >= D4) continue;
+                        double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
+                        for (int q0 = 0; q0 < cnt; q0 += 4) {
+                            double4 x[4];
+#pragma unroll
+                            for (int q = 0; q < 4; q++)
+                                if (q0 + q < cnt) x[q] = ld_piece(piece(kf + (q0 + q) * step) + 4 * c);
+#pragma unroll
+                            for (int q = 0; q < 4; q++)
+                                if (q0 + q < cnt) dadd4(m, x[q]);
+                        }
+                        float4 *wp = st + (size_t)s * D4 + c;
+                        *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
+                    }
+                }
+            }
+        }
+        r0 = r1 + 1;
+    }
+}
+
 #ifndef SP_BWD_TILE_MINB
 #define SP_BWD_TILE_MINB 16  // resident warps per SM the registers are sized for (<= 128 regs)
 #endif
@@ -591,7 +729,6 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const int t = (int)(tile / NT), k = (int)(tile % NT);
         const int lo = k * TR;
         const int nrows = min(TR, g.n - lo);
-        const size_t tb = (size_t)t * g.n;
         const uint32_t uid = m.uid, slot = m.slot;
         const bool act = uid != EMPTY;
         const unsigned amask = __ballot_sync(0xffffffffu, act);
@@ -661,134 +798,148 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         }
-        // 2. fold segment by segment (a segment = one row's occurrences in
-        // this tile).  A whole row of 1 or 2 occurrences is summed in fp32:
-        // that is the fp32 rounding of the exact sum, i.e. the oracle's
-        // (float)(fp64 sum) (reading R7); longer rows and pieces of rows
-        // spanning tiles accumulate in fp64 in ascending occurrence order.
-        unsigned ends = lmask;
-        int r0 = 0;  // first row of the current segment
-        while (ends) {
-            const int r1 = __ffs(ends) - 1;  // its last row
-            ends &= ends - 1;
-            const int len = r1 - r0 + 1;
-            const uint32_t s = __shfl_sync(0xffffffffu, slot, r0);
-            const bool wh = (wmask >> r0) & 1u;
-            const int wr = A.g4 ? __popc(wmask & ((1u << r0) - 1u)) : r0;  // its staged Storage row
-            if (wh && len <= 2 && !(A.diag & 32)) {  // (SP_DIAG=32: every row through fp64, A/B)
-#pragma unroll
-                for (int v = 0; v < VPL; v++) {
-                    const int c = lane + 32 * v;
-                    if (c < D4) {
-                        float4 gs = sg[(size_t)r0 * D4 + c];
-                        if (len == 2) add4(gs, sg[(size_t)(r0 + 1) * D4 + c]);
-                        st[(size_t)s * D4 + c] = sgd32(sw[(size_t)wr * D4 + c], gs, A.lr);
-                    }
-                }
-                r0 = r1 + 1;
-                continue;
-            }
-            double4 acc[VPL];
-#pragma unroll
-            for (int v = 0; v < VPL; v++) {
-                acc[v] = make_double4(0.0, 0.0, 0.0, 0.0);
-                const int c = lane + 32 * v;
-                if (c < D4)
-                    for (int r = r0; r <= r1; r++) {
-                        const float4 x = sg[(size_t)r * D4 + c];
-                        acc[v].x += (double)x.x; acc[v].y += (double)x.y;
-                        acc[v].z += (double)x.z; acc[v].w += (double)x.w;
-                    }
-            }
-            if (wh) {  // the whole row is in this tile
-#pragma unroll
-                for (int v = 0; v < VPL; v++) {
-                    const int c = lane + 32 * v;
-                    if (c < D4)
-                        st[(size_t)s * D4 + c] =
-                            sgd(sw[(size_t)wr * D4 + c], Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr);
-                }
-            } else {
-                // 3. a piece of a row spanning tiles [kf, kl]: slot 0 of tile k
-                // if the row holds the tile's first occurrence, else slot 1
-                // (only possible in the row's first tile)
-                const uint32_t u = __shfl_sync(0xffffffffu, uid, r0);
-                uint32_t slo = 0, shi = 0;
-                if (lane == 0) {
-                    slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u);
-                    shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
-                }
-                slo = __shfl_sync(0xffffffffu, slo, 0);
-                shi = __shfl_sync(0xffffffffu, shi, 0);
-                const int kf = (int)(slo / (uint32_t)TR), kl = (int)((shi - 1u) / (uint32_t)TR);
-                const int npc = kl - kf + 1;
-                auto pslot = [&](int kk) { return (kk == kf && slo != (uint32_t)(kf * TR)) ? 1 : 0; };
-                auto piece = [&](int kk) { return A.tpart + (((size_t)t * NT + kk) * 2 + pslot(kk)) * g.D; };
-                double *mine = piece(k);
-#pragma unroll
-                for (int v = 0; v < VPL; v++) {
-                    const int c = lane + 32 * v;
-                    if (c < D4) reinterpret_cast<double4 *>(mine)[c] = acc[v];
-                }
-                bool go = true;
-                int step = 1, cnt = npc;
-                if (npc > 8) {  // level 1: groups of 8 consecutive pieces
-                    const int gi = (k - kf) / 8, g0 = kf + 8 * gi, gsz = min(8, kl - g0 + 1);
-                    uint32_t *gc = A.grp_cnt + ((size_t)t * NT + g0) * 2 + pslot(g0);
-                    go = warp_arrive_last(gc, (uint32_t)gsz);
-                    if (go) {
-                        if (lane == 0) *gc = 0u;
-#pragma unroll
-                        for (int v = 0; v < VPL; v++) {
-                            const int c = lane + 32 * v;
-                            if (c >= D4) continue;
-                            double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
-                            for (int q0 = 0; q0 < gsz; q0 += 4) {
-                                double4 x[4];
-#pragma unroll
-                                for (int q = 0; q < 4; q++)
-                                    if (q0 + q < gsz) x[q] = ld_piece(piece(g0 + q0 + q) + 4 * c);
-#pragma unroll
-                                for (int q = 0; q < 4; q++)
-                                    if (q0 + q < gsz) dadd4(m, x[q]);
-                            }
-                            reinterpret_cast<double4 *>(piece(g0))[c] = m;
-                        }
-                    }
-                    step = 8;
-                    cnt = (npc + 7) / 8;
-                }
-                if (go) {
-                    uint32_t *rc = A.seg_cnt + tb + u;
-                    if (warp_arrive_last(rc, (uint32_t)cnt)) {
-                        if (lane == 0) *rc = 0u;
-#pragma unroll
-                        for (int v = 0; v < VPL; v++) {
-                            const int c = lane + 32 * v;
-                            if (c >= D4) continue;
-                            double4 m = make_double4(0.0, 0.0, 0.0, 0.0);
-                            for (int q0 = 0; q0 < cnt; q0 += 4) {
-                                double4 x[4];
-#pragma unroll
-                                for (int q = 0; q < 4; q++)
-                                    if (q0 + q < cnt) x[q] = ld_piece(piece(kf + (q0 + q) * step) + 4 * c);
-#pragma unroll
-                                for (int q = 0; q < 4; q++)
-                                    if (q0 + q < cnt) dadd4(m, x[q]);
-                            }
-                            float4 *wp = st + (size_t)s * D4 + c;
-                            *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
-                        }
-                    }
-                }
-            }
-            r0 = r1 + 1;
-        }
+        bwd_fold_tile<VPL>(A, t, k, lmask, wmask, slot, uid, sg, sw);
         // the tile's shared rows are consumed (generic proxy) before the next
         // tile's bulk copies (async proxy) overwrite them
         __syncwarp();
         if (A.bwd_tma || A.g4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    span_mark(spn, 1);
+}
+
+// Warp-specialised variant (default): a CTA of two warps and two staging
+// buffers.  Warp 0 (producer) reads a tile's metadata, derives the segment
+// masks, hands them over in shared memory and issues the TMA copies of the
+// tile's rows into a free buffer (mbarrier `full`, with the byte count);
+// warp 1 (consumer) folds the previous buffer and releases it (mbarrier
+// `empty`).  The copies of tile i+1 and the per-tile bookkeeping run while
+// tile i is folded.  Same tiles, same fold (bwd_fold_tile), same results as
+// k_bwd_tile.
+template <int VPL>
+__global__ void __launch_bounds__(64, VPL >= 2 ? 4 : 8)
+    k_bwd_ws(TrainArgs A, const __grid_constant__ CUtensorMap tmg, const __grid_constant__ CUtensorMap tms) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t full[2], empty[2];
+    __shared__ uint32_t s_slot[2][32], s_uid[2][32], s_lm[2], s_wm[2];
+    if (*A.err != NO_ERR) return;
+    const Geometry g = A.g;
+    const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
+    const uint32_t rowb = (uint32_t)g.D * 4u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float4 *stage0 = reinterpret_cast<float4 *>(sm);
+    auto gbuf = [&](int b) { return stage0 + (size_t)b * 2 * TR * D4; };  // [TR][D4] gradient rows
+    auto wbuf = [&](int b) { return gbuf(b) + (size_t)TR * D4; };         // [TR][D4] Storage rows
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; b++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[b])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&empty[b])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long total = (long long)g.T * NT;
+    unsigned long long *spn = span_base(A.span, SPK_BWD, A.span_b);
+    if (warp == 0) {
+        // ---------------- producer
+        const float4 *grad = reinterpret_cast<const float4 *>(A.grad);
+        const float4 *st = reinterpret_cast<const float4 *>(A.storage);
+        uint32_t occ = 0, uid = EMPTY, slot = 0, prev = EMPTY, next = EMPTY;
+        auto load_meta = [&](long long tile) {
+            occ = 0; uid = EMPTY; slot = 0; prev = EMPTY; next = EMPTY;
+            if (tile >= total) return;
+            const int t = (int)(tile / NT), k = (int)(tile % NT);
+            const int lo = k * TR, nrows = min(TR, g.n - lo);
+            const size_t base = (size_t)t * g.n + lo;
+            if (lane < nrows) {
+                occ = __ldg(A.bb.sorted_occ + base + lane);
+                uid = __ldg(A.bb.sorted_uid + base + lane);
+                slot = __ldg(A.bb.sorted_slot + base + lane);
+            }
+            if (lane == 0 && lo > 0) prev = __ldg(A.bb.sorted_uid + base - 1);
+            if (lane == nrows - 1 && lo + nrows < g.n) next = __ldg(A.bb.sorted_uid + base + nrows);
+        };
+        load_meta(blockIdx.x);
+        griddep_wait();  // (PDL) the surrogate's gradients are complete from here on
+        span_mark(spn, 0);
+        uint32_t i = 0;
+        for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, i++) {
+            const int b = (int)(i & 1u);
+            const uint32_t ph = (i >> 1) & 1u;
+            const uint32_t m_occ = occ, m_uid = uid, m_slot = slot, m_prev = prev, m_next = next;
+            const int t = (int)(tile / NT), k = (int)(tile % NT);
+            const int nrows = min(TR, g.n - k * TR);
+            const bool act = m_uid != EMPTY;
+            const unsigned amask = __ballot_sync(0xffffffffu, act);
+            unsigned lmask = 0u, wmask = 0u;
+            int nact = 0;
+            if (amask) {
+                nact = 32 - __clz(amask);
+                const uint32_t up = __shfl_up_sync(0xffffffffu, m_uid, 1), dn = __shfl_down_sync(0xffffffffu, m_uid, 1);
+                const uint32_t prevu = lane == 0 ? m_prev : up;
+                const uint32_t nextu = lane == nrows - 1 ? m_next : dn;
+                const bool first = act && prevu != m_uid;
+                const bool lastr = act && (lane == nact - 1 || nextu != m_uid);
+                const uint32_t uid_last = __shfl_sync(0xffffffffu, m_uid, nact - 1);
+                const bool tail_open = __shfl_sync(0xffffffffu, nextu == m_uid, nact - 1);
+                const bool whole = first && !(m_uid == uid_last && tail_open);
+                wmask = __ballot_sync(0xffffffffu, whole);
+                lmask = __ballot_sync(0xffffffffu, lastr);
+            }
+            // the consumer has released buffer b (its use two tiles ago)
+            while (!bar_try(&empty[b], ph ^ 1u)) {
+            }
+            s_slot[b][lane] = m_slot;
+            s_uid[b][lane] = m_uid;
+            if (lane == 0) {
+                s_lm[b] = lmask;
+                s_wm[b] = wmask;
+            }
+            __syncwarp();
+            float4 *sg = gbuf(b), *sw = wbuf(b);
+            if (A.g4 && amask) {
+                const int ng = (nact + 3) >> 2, nw = __popc(wmask), nsg = (nw + 3) >> 2;
+                if (lane == 0) bar_expect(&full[b], (uint32_t)(4 * ng + 4 * nsg) * rowb);
+                __syncwarp();
+                const uint32_t grow = (uint32_t)t * (uint32_t)g.N + m_occ / (uint32_t)g.L;
+                uint32_t gr[4], sr[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    gr[q] = __shfl_sync(0xffffffffu, grow, min(4 * lane + q, nact - 1));
+                    const int j = min(4 * lane + q, max(nw - 1, 0));
+                    const int pos = nw ? (int)__fns(wmask, 0, j + 1) : 0;
+                    sr[q] = __shfl_sync(0xffffffffu, m_slot, pos & 31);
+                }
+                if (lane < ng) rows4_g2s(sg + (size_t)4 * lane * D4, &tmg, gr[0], gr[1], gr[2], gr[3], &full[b]);
+                if (lane < nsg) rows4_g2s(sw + (size_t)4 * lane * D4, &tms, sr[0], sr[1], sr[2], sr[3], &full[b]);
+            } else {
+                if (lane == 0) bar_expect(&full[b], (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
+                __syncwarp();
+                if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + m_occ / (uint32_t)g.L) * D4, rowb, &full[b]);
+                if ((wmask >> lane) & 1u) row_g2s(sw + (size_t)lane * D4, st + (size_t)m_slot * D4, rowb, &full[b]);
+            }
+            load_meta(tile + gridDim.x);
+        }
+    } else {
+        // ---------------- consumer
+        griddep_wait();
+        uint32_t i = 0;
+        for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, i++) {
+            const int b = (int)(i & 1u);
+            const uint32_t ph = (i >> 1) & 1u;
+            while (!bar_try(&full[b], ph)) {
+            }
+            const unsigned lmask = s_lm[b], wmask = s_wm[b];
+            const uint32_t slot = s_slot[b][lane], uid = s_uid[b][lane];
+            const int t = (int)(tile / NT), k = (int)(tile % NT);
+            if (lmask) bwd_fold_tile<VPL>(A, t, k, lmask, wmask, slot, uid, gbuf(b), wbuf(b));
+            // buffer b consumed (generic proxy) before the producer's next
+            // copies (async proxy) into it
+            __syncwarp();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[b])) : "memory");
+        }
+    }
+    __syncthreads();
     span_mark(spn, 1);
 }
 
@@ -1022,6 +1173,7 @@ static bool rows_map(CUtensorMap *m, const void *base, unsigned long long rows, 
 }
 
 static int g_bwd_g4 = -1;  // SP_BWD_G4: 0 disables tile::gather4 (A/B)
+static int g_bwd_ws = -1;  // SP_BWD_WS: 0 runs the one-warp k_bwd_tile instead of k_bwd_ws (A/B)
 
 template <int VPL>
 static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
@@ -1058,6 +1210,33 @@ static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
         caps[{dev, smem}] = cap;
     }
     const long long tiles = (long long)a.g.T * a.ntiles;
+    if (g_bwd_ws < 0) {
+        const char *e = getenv("SP_BWD_WS");
+        g_bwd_ws = e ? (atoi(e) != 0) : 1;
+    }
+    if (g_bwd_ws && a.bwd_tma) {  // two warps, two staging buffers per CTA
+        const size_t smem2 = 2 * smem;
+        static std::map<std::pair<int, size_t>, int> caps2;
+        int cap2 = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_dev_mu);
+            auto it = caps2.find({dev, smem2});
+            if (it != caps2.end()) cap2 = it->second;
+        }
+        if (!cap2) {
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_ws<VPL>, 64, smem2) != cudaSuccess ||
+                per_sm < 1)
+                per_sm = 1;
+            cap2 = per_sm * device_sms();
+            std::lock_guard<std::mutex> lk(g_dev_mu);
+            caps2[{dev, smem2}] = cap2;
+        }
+        int grid2 = (int)(tiles < cap2 ? tiles : cap2);
+        if (grid2 < 1) grid2 = 1;
+        launch_maybe_pdl(k_bwd_ws<VPL>, grid2, 64, smem2, s, true, a, tmg, tms);
+        return;
+    }
     int grid = (int)(tiles < cap ? tiles : cap);
     if (grid < 1) grid = 1;
     launch_maybe_pdl(k_bwd_tile<VPL>, grid, 32, smem, s, true, a, tmg, tms);
@@ -1099,6 +1278,10 @@ cudaError_t configure_train_kernels() {
     cudaFuncSetAttribute(k_bwd_tile<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_tile<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_tile<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_ws<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_ws<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_ws<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_ws<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return cudaGetLastError();
 }
 
