@@ -559,28 +559,57 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
     // that is the fp32 rounding of the exact sum, i.e. the oracle's
     // (float)(fp64 sum) (reading R7); longer rows and pieces of rows
     // spanning tiles accumulate in fp64 in ascending occurrence order.
-    unsigned ends = lmask;
-    int r0 = 0;  // first row of the current segment
+    // whole rows of one occurrence (the segment starts and ends on row r) and
+    // of two (starts at r, ends at r+1) first, in straight loops: two
+    // rows of each per trip, loads before stores (SP_DIAG=32 sends every row
+    // through the fp64 path, A/B)
+    const unsigned lone1 = (A.diag & 32) ? 0u : (wmask & lmask);
+    const unsigned lone2 = (A.diag & 32) ? 0u : (wmask & (lmask >> 1) & ~lmask);
+    auto wrow = [&](int r) { return A.g4 ? __popc(wmask & ((1u << r) - 1u)) : r; };  // its staged Storage row
+    for (unsigned m1 = lone1; m1;) {
+        const int ra = __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        const int rb = m1 ? __ffs(m1) - 1 : -1;
+        if (rb >= 0) m1 &= m1 - 1;
+        const uint32_t sa = __shfl_sync(0xffffffffu, slot, ra), sb = __shfl_sync(0xffffffffu, slot, rb & 31);
+        const int wa = wrow(ra), wb = rb >= 0 ? wrow(rb) : 0;
+#pragma unroll
+        for (int v = 0; v < VPL; v++) {
+            const int c = lane + 32 * v;
+            if (c < D4) {
+                const float4 ga = sg[(size_t)ra * D4 + c], xa = sw[(size_t)wa * D4 + c];
+                float4 gb, xb;
+                if (rb >= 0) { gb = sg[(size_t)rb * D4 + c]; xb = sw[(size_t)wb * D4 + c]; }
+                st[(size_t)sa * D4 + c] = sgd32(xa, ga, A.lr);
+                if (rb >= 0) st[(size_t)sb * D4 + c] = sgd32(xb, gb, A.lr);
+            }
+        }
+    }
+    for (unsigned m2 = lone2; m2; m2 &= m2 - 1) {
+        const int r = __ffs(m2) - 1;
+        const uint32_t s2 = __shfl_sync(0xffffffffu, slot, r);
+        const int w2 = wrow(r);
+#pragma unroll
+        for (int v = 0; v < VPL; v++) {
+            const int c = lane + 32 * v;
+            if (c < D4) {
+                float4 gs = sg[(size_t)r * D4 + c];
+                add4(gs, sg[(size_t)(r + 1) * D4 + c]);
+                st[(size_t)s2 * D4 + c] = sgd32(sw[(size_t)w2 * D4 + c], gs, A.lr);
+            }
+        }
+    }
+    // the other segments: each ends at a bit of `ends`, starts after the
+    // previous bit of lmask
+    unsigned ends = lmask & ~(lone1 | (lone2 << 1));
     while (ends) {
         const int r1 = __ffs(ends) - 1;  // its last row
         ends &= ends - 1;
-        const int len = r1 - r0 + 1;
+        const unsigned below = lmask & ((1u << r1) - 1u);
+        const int r0 = below ? 32 - __clz(below) : 0;  // its first row
         const uint32_t s = __shfl_sync(0xffffffffu, slot, r0);
         const bool wh = (wmask >> r0) & 1u;
-        const int wr = A.g4 ? __popc(wmask & ((1u << r0) - 1u)) : r0;  // its staged Storage row
-        if (wh && len <= 2 && !(A.diag & 32)) {  // (SP_DIAG=32: every row through fp64, A/B)
-#pragma unroll
-            for (int v = 0; v < VPL; v++) {
-                const int c = lane + 32 * v;
-                if (c < D4) {
-                    float4 gs = sg[(size_t)r0 * D4 + c];
-                    if (len == 2) add4(gs, sg[(size_t)(r0 + 1) * D4 + c]);
-                    st[(size_t)s * D4 + c] = sgd32(sw[(size_t)wr * D4 + c], gs, A.lr);
-                }
-            }
-            r0 = r1 + 1;
-            continue;
-        }
+        const int wr = wrow(r0);
         double4 acc[VPL];
 #pragma unroll
         for (int v = 0; v < VPL; v++) {
@@ -675,7 +704,6 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
                 }
             }
         }
-        r0 = r1 + 1;
     }
 }
 
@@ -807,7 +835,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     span_mark(spn, 1);
 }
 
-// Warp-specialised variant (default): a CTA of two warps and two staging
+// Warp-specialised variant (A/B, SP_BWD_WS=1): a CTA of two warps and two staging
 // buffers.  Warp 0 (producer) reads a tile's metadata, derives the segment
 // masks, hands them over in shared memory and issues the TMA copies of the
 // tile's rows into a free buffer (mbarrier `full`, with the byte count);
@@ -1173,7 +1201,8 @@ static bool rows_map(CUtensorMap *m, const void *base, unsigned long long rows, 
 }
 
 static int g_bwd_g4 = -1;  // SP_BWD_G4: 0 disables tile::gather4 (A/B)
-static int g_bwd_ws = -1;  // SP_BWD_WS: 0 runs the one-warp k_bwd_tile instead of k_bwd_ws (A/B)
+static int g_bwd_ws = -1;  // SP_BWD_WS=1: the warp-specialised k_bwd_ws (A/B: measured slower, 52 vs 36 us isolated
+                           // on Terabyte: 6 consumer warps per SM fold less than 13 one-warp CTAs)
 
 template <int VPL>
 static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
@@ -1212,7 +1241,7 @@ static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
     const long long tiles = (long long)a.g.T * a.ntiles;
     if (g_bwd_ws < 0) {
         const char *e = getenv("SP_BWD_WS");
-        g_bwd_ws = e ? (atoi(e) != 0) : 1;
+        g_bwd_ws = e ? (atoi(e) != 0) : 0;
     }
     if (g_bwd_ws && a.bwd_tma) {  // two warps, two staging buffers per CTA
         const size_t smem2 = 2 * smem;
