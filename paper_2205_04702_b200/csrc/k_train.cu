@@ -731,11 +731,13 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     // before the tile, lane nrows-1 the one after it (does a row cross the
     // tile's edges?)
     struct Meta { uint32_t occ, uid, slot, prev, next; };
-    const long long total = (long long)g.T * NT;
-    auto load_meta = [&](long long tile, Meta &m) {
+    const uint32_t L = (uint32_t)g.L;
+    auto bagof = [&](uint32_t occ) { return L == 1u ? occ : occ / L; };  // (no division for L = 1)
+    const int total = g.T * NT;  // (< 2^31: T < 2^16 tables, NT <= n)
+    auto load_meta = [&](int tile, Meta &m) {
         m = Meta{0u, EMPTY, 0u, EMPTY, EMPTY};
         if (tile >= total) return;
-        const int t = (int)(tile / NT), k = (int)(tile % NT);
+        const int t = tile / NT, k = tile - t * NT;
         const int lo = k * TR, nrows = min(TR, g.n - lo);
         const size_t base = (size_t)t * g.n + lo;
         if (lane < nrows) {
@@ -752,9 +754,9 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     unsigned long long *spn = span_base(A.span, SPK_BWD, A.span_b);
     span_mark(spn, 0);
     uint32_t parity = 0;
-    for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         const Meta m = nxt;
-        const int t = (int)(tile / NT), k = (int)(tile % NT);
+        const int t = tile / NT, k = tile - t * NT;
         const int lo = k * TR;
         const int nrows = min(TR, g.n - lo);
         const uint32_t uid = m.uid, slot = m.slot;
@@ -783,7 +785,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             const int ng = (nact + 3) >> 2, nw = __popc(wmask), nsg = (nw + 3) >> 2;
             if (lane == 0) bar_expect(&bar, (uint32_t)(4 * ng + 4 * nsg) * rowb);
             __syncwarp();
-            const uint32_t grow = (uint32_t)t * (uint32_t)g.N + m.occ / (uint32_t)g.L;
+            const uint32_t grow = (uint32_t)t * (uint32_t)g.N + bagof(m.occ);
             uint32_t gr[4], sr[4];
 #pragma unroll
             for (int i = 0; i < 4; i++) {
@@ -801,7 +803,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         } else if (A.bwd_tma) {  // one TMA bulk copy per row, completion on the mbarrier
             if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
             __syncwarp();
-            if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + m.occ / (uint32_t)g.L) * D4, rowb, &bar);
+            if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + bagof(m.occ)) * D4, rowb, &bar);
             if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowb, &bar);
             load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
             while (!bar_try(&bar, parity)) {
