@@ -777,7 +777,9 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const bool whole = first && !(uid == uid_last && tail_open);  // (lane 0 of an open head is not `first`)
         const unsigned wmask = __ballot_sync(0xffffffffu, whole);
         const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
-        if (A.g4) {
+        if (A.diag & 128) {  // timing diagnostic: no staging (the fold reads stale shared memory)
+            load_meta(tile + gridDim.x, nxt);
+        } else if (A.g4) {
             // TMA tile::gather4: lane q fetches tile rows 4q..4q+3 (the last
             // group padded with the last row) and lane q the Storage rows of
             // whole segments 4q..4q+3 (compacted: the k-th whole segment's row
@@ -828,7 +830,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         }
-        bwd_fold_tile<VPL>(A, t, k, lmask, wmask, slot, uid, sg, sw);
+        if (!(A.diag & 64)) bwd_fold_tile<VPL>(A, t, k, lmask, wmask, slot, uid, sg, sw);  // (64: no fold, timing)
         // the tile's shared rows are consumed (generic proxy) before the next
         // tile's bulk copies (async proxy) overwrite them
         __syncwarp();

@@ -297,7 +297,8 @@ struct sp_ctx {
     uint32_t wb_q16 = 0;        // k_xfer_warp: victims written back by the GPU (SP_WB_GPU_FRAC)
     // timing diagnostics (SP_DIAG bit mask; results are then WRONG): 1 = the
     // transfer kernel moves nothing, 2 = the Train kernels do nothing, 4 = the
-    // transfer kernel pulls but does not stage the victims
+    // transfer kernel pulls but does not stage the victims; k_bwd_tile: 32 =
+    // every row through the fp64 fold, 64 = no fold, 128 = no staging
     int diag = 0;
     long long xfer_enq = 0;                    // transfers enqueued (caller's thread)
     // pinned index staging
