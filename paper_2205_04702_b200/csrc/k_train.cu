@@ -529,14 +529,23 @@ __device__ __forceinline__ void dadd4(double4 &a, const double4 &b) { a.x += b.x
 __device__ __forceinline__ double4 ld_piece(const double *p) {  // L2: written by other SMs
     return ldcg_d4(reinterpret_cast<const double4 *>(p));
 }
-// warp-wide "last of `total` arrivals at *ctr" (release before, acquire after)
-__device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total) {
-    __threadfence();
+// warp-wide "last of `total` arrivals at *ctr": the warp's writes are
+// ordered before lane 0's acq_rel atomic by the warp barrier (release), and
+// the winner's later reads after it (acquire) -- the semaphore pattern of
+// CUTLASS's barrier, without a full fence (__threadfence costs MEMBAR +
+// ERRBAR + CCTL: ~20% of k_bwd_tile's stall samples; SP_DIAG=256 restores it)
+__device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total, bool full_fence) {
+    if (full_fence) __threadfence();
     __syncwarp();
     uint32_t last = 0;
-    if ((threadIdx.x & 31) == 0) last = atomicAdd(ctr, 1u) == total - 1u;
+    if ((threadIdx.x & 31) == 0) {
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
+        last = prev == total - 1u;
+    }
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) __threadfence();
+    __syncwarp();
+    if (last && full_fence) __threadfence();
     return last != 0;
 }
 }  // namespace
@@ -657,7 +666,7 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
             if (npc > 8) {  // level 1: groups of 8 consecutive pieces
                 const int gi = (k - kf) / 8, g0 = kf + 8 * gi, gsz = min(8, kl - g0 + 1);
                 uint32_t *gc = A.grp_cnt + ((size_t)t * NT + g0) * 2 + pslot(g0);
-                go = warp_arrive_last(gc, (uint32_t)gsz);
+                go = warp_arrive_last(gc, (uint32_t)gsz, (A.diag & 256) != 0);
                 if (go) {
                     if (lane == 0) *gc = 0u;
 #pragma unroll
@@ -682,7 +691,7 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
             }
             if (go) {
                 uint32_t *rc = A.seg_cnt + tb + u;
-                if (warp_arrive_last(rc, (uint32_t)cnt)) {
+                if (warp_arrive_last(rc, (uint32_t)cnt, (A.diag & 256) != 0)) {
                     if (lane == 0) *rc = 0u;
 #pragma unroll
                     for (int v = 0; v < VPL; v++) {
