@@ -557,7 +557,10 @@ __device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total, 
 // each row wholly inside it; per lane (row r): slot, uid.
 template <int VPL>
 __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, unsigned lmask, unsigned wmask,
-                                              uint32_t slot, uint32_t uid, const float4 *sg, const float4 *sw) {
+                                              uint32_t slot, uint32_t uid, const float4 *sg, const float4 *sw,
+                                              uint32_t eslo = EMPTY, uint32_t eshi = EMPTY) {
+    // eslo / eshi: segment offsets of the row of lane 0 (and of the last
+    // row, on its lane), prefetched with the tile's metadata; EMPTY = load here
     const Geometry &g = A.g;
     const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
     const int lane = threadIdx.x & 31;
@@ -644,13 +647,17 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
             // if the row holds the tile's first occurrence, else slot 1
             // (only possible in the row's first tile)
             const uint32_t u = __shfl_sync(0xffffffffu, uid, r0);
-            uint32_t slo = 0, shi = 0;
-            if (lane == 0) {
-                slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u);
-                shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
+            // a piece is the tile's head row (r0 = 0) or its tail row (r1 = the last row)
+            const int src = r0 == 0 ? 0 : r1;
+            uint32_t slo = __shfl_sync(0xffffffffu, eslo, src), shi = __shfl_sync(0xffffffffu, eshi, src);
+            if (slo == EMPTY) {
+                if (lane == 0) {
+                    slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u);
+                    shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
+                }
+                slo = __shfl_sync(0xffffffffu, slo, 0);
+                shi = __shfl_sync(0xffffffffu, shi, 0);
             }
-            slo = __shfl_sync(0xffffffffu, slo, 0);
-            shi = __shfl_sync(0xffffffffu, shi, 0);
             const int kf = (int)(slo / (uint32_t)TR), kl = (int)((shi - 1u) / (uint32_t)TR);
             const int npc = kl - kf + 1;
             auto pslot = [&](int kk) { return (kk == kf && slo != (uint32_t)(kf * TR)) ? 1 : 0; };
@@ -739,12 +746,12 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     // unique and its Storage slot (frozen at Plan); lane 0 also the unique
     // before the tile, lane nrows-1 the one after it (does a row cross the
     // tile's edges?)
-    struct Meta { uint32_t occ, uid, slot, prev, next; };
+    struct Meta { uint32_t occ, uid, slot, prev, next, slo, shi; };
     const uint32_t L = (uint32_t)g.L;
     auto bagof = [&](uint32_t occ) { return L == 1u ? occ : occ / L; };  // (no division for L = 1)
     const int total = g.T * NT;  // (< 2^31: T < 2^16 tables, NT <= n)
     auto load_meta = [&](int tile, Meta &m) {
-        m = Meta{0u, EMPTY, 0u, EMPTY, EMPTY};
+        m = Meta{0u, EMPTY, 0u, EMPTY, EMPTY, EMPTY, EMPTY};
         if (tile >= total) return;
         const int t = tile / NT, k = tile - t * NT;
         const int lo = k * TR, nrows = min(TR, g.n - lo);
@@ -756,6 +763,11 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         }
         if (lane == 0 && lo > 0) m.prev = __ldg(A.bb.sorted_uid + base - 1);
         if (lane == nrows - 1 && lo + nrows < g.n) m.next = __ldg(A.bb.sorted_uid + base + nrows);
+        // the edge rows' segment offsets (a row crossing the tile's edge is a piece)
+        if ((lane == 0 || lane == nrows - 1) && m.uid != EMPTY) {
+            m.slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + m.uid);
+            m.shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + m.uid + 1);
+        }
     };
     Meta nxt;
     load_meta(blockIdx.x, nxt);  // (Plan's output: complete before the forward ran)
@@ -839,7 +851,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         }
-        if (!(A.diag & 64)) bwd_fold_tile<VPL>(A, t, k, lmask, wmask, slot, uid, sg, sw);  // (64: no fold, timing)
+        if (!(A.diag & 64)) bwd_fold_tile<VPL>(A, t, k, lmask, wmask, slot, uid, sg, sw, m.slo, m.shi);  // (64: no fold, timing)
         // the tile's shared rows are consumed (generic proxy) before the next
         // tile's bulk copies (async proxy) overwrite them
         __syncwarp();

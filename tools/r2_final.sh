@@ -1,0 +1,25 @@
+#!/bin/bash
+# Round-2 measurement pass on one B200 (run via gpurun from the repo root):
+#   r2_final.sh TAG
+# box facts, build, the GPU suite, smoke(), the driver-shaped bench (--steps 20
+# --warmup 5, with cpu_baseline), a 1000-step bench, the reference arm, the ncu
+# launch list and one ncu --set full capture of the stage kernels.
+TAG=${1:-final}
+O=gpurun_out/$TAG
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
+nproc > $O/nproc.txt; lscpu > $O/lscpu.txt; free -g > $O/free.txt
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench20.json 2> $O/bench20.err
+timeout 900 python bench.py --steps 1000 --warmup 50 --no-cpu-baseline > $O/bench1000.json 2> $O/bench1000.err
+timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $O/ref.json 2> $O/ref.err
+KR='regex:^(k_push|k_pullfill|k_fwd|k_bwd|k_surrogate)'
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KR" -s 2000 -c 500 --csv \
+  --log-file $O/launches.csv python bench.py --preroll 1000 --steps 200 --warmup 5 --no-cpu-baseline --profile-steps 5 > $O/ncu_list.log 2>&1
+SP_CPU_GATHER=0 timeout 1200 ncu --set full --import-source on --clock-control none -k "$KR" -s 2000 -c 10 \
+  -o $O/full python bench.py --preroll 1000 --steps 40 --warmup 5 --no-cpu-baseline --profile-steps 5 > $O/ncu_full.log 2>&1
+tail -3 $O/pytest_gpu.log; tail -2 $O/smoke.log
+python tools/bench_brief.py $O/bench20.json $O/bench1000.json
+ls -la $O
