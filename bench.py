@@ -460,7 +460,7 @@ def run_ours(args):
                          f"{avail / 1e9:.1f} GB available (MemAvailable): run {args.config} on more GPUs or a larger node")
     tables = []   # THP-backed, CUDA-registered host tables (sp_host_alloc)
     for t in mine:
-        h = HostTable(cfg.rows[t], D)
+        h = HostTable(cfg.rows[t], D, device=local)  # NUMA-local to this rank's GPU
         init_table(cfg.init_seed, t, cfg.rows[t], D, device=dev, out=h.tensor)
         tables.append(h)
     trace = torch.empty((nb, len(mine), N, L), dtype=torch.int32, device=dev)

@@ -236,10 +236,20 @@ sp_status sp_shard_plan(int32_t world, int32_t rank, int32_t num_tables_all, con
 
 /* Host-table allocator: `bytes` of anonymous host memory backed by 2 MB
  * transparent huge pages where the OS allows (the CPU side of the transfer
- * engine gathers / scatters random rows: 4 KB pages cost a TLB walk per row),
- * registered with CUDA as mapped + portable.  Pass the pointer in
- * desc.host_tables WITHOUT SP_FLAG_REGISTER_HOST.  Free with sp_host_free. */
+ * engine gathers / scatters random rows), registered with CUDA as mapped +
+ * portable.  Pass the pointer in desc.host_tables WITHOUT
+ * SP_FLAG_REGISTER_HOST.  Free with sp_host_free.  Returns SP_ERR_OOM when
+ * the pages cannot be mapped or pinned. */
 sp_status sp_host_alloc(size_t bytes, void **out);
+
+/* The same, with the pages placed on the host NUMA node closest to CUDA
+ * device `device` (cudaDevAttrHostNumaId; mbind MPOL_PREFERRED before the
+ * pages are first touched), so each GPU's tables sit behind its own memory
+ * controllers on a multi-socket node ("pinned host rows, placed
+ * NUMA-local to that GPU").  On a single-node host, or when the device
+ * reports no NUMA id, it is sp_host_alloc.  *numa_node_out (nullable) gets
+ * the node used, -1 for none. */
+sp_status sp_host_alloc_near(size_t bytes, int32_t device, void **out, int32_t *numa_node_out);
 sp_status sp_host_free(void *ptr, size_t bytes);
 
 /* Create a context: validates the descriptor, allocates Storage

@@ -126,6 +126,9 @@ def _load():
     L.sp_shard_plan.restype = S
     L.sp_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
     L.sp_host_alloc.restype = S
+    L.sp_host_alloc_near.argtypes = [ctypes.c_size_t, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p),
+                                     ctypes.POINTER(ctypes.c_int32)]
+    L.sp_host_alloc_near.restype = S
     L.sp_host_free.argtypes = [P, ctypes.c_size_t]
     L.sp_host_free.restype = S
     L.sp_error_string.argtypes = [P]
@@ -169,13 +172,21 @@ def shard_plan(world: int, rank: int, owner):
 
 class HostTable:
     """A host embedding table from sp_host_alloc (THP-backed, CUDA-registered);
-    `.tensor` is a float32 CPU torch view [rows][dim]."""
+    `.tensor` is a float32 CPU torch view [rows][dim].  With `device`, the
+    pages go to the host NUMA node closest to that GPU (sp_host_alloc_near;
+    `.numa_node` is the node used, -1 for none)."""
 
-    def __init__(self, rows: int, dim: int):
+    def __init__(self, rows: int, dim: int, device: int | None = None):
         import torch
         self.bytes = int(rows) * int(dim) * 4
         p = ctypes.c_void_p()
-        st = lib.sp_host_alloc(self.bytes, ctypes.byref(p))
+        self.numa_node = -1
+        if device is None:
+            st = lib.sp_host_alloc(self.bytes, ctypes.byref(p))
+        else:
+            nn = ctypes.c_int32(-1)
+            st = lib.sp_host_alloc_near(self.bytes, int(device), ctypes.byref(p), ctypes.byref(nn))
+            self.numa_node = nn.value
         if st != SP_OK:
             raise SpError(st, "sp_host_alloc failed")
         self.ptr = p.value

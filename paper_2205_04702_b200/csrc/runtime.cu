@@ -26,6 +26,7 @@
 #include <dlfcn.h>
 #include <immintrin.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -1031,6 +1032,33 @@ sp_status sp_host_alloc(size_t bytes, void **out) {
     if (p == MAP_FAILED) return SP_ERR_OOM;
     madvise(p, bytes, MADV_HUGEPAGE);  // best effort (THP "madvise" mode)
     // pinning faults the pages in, so they come up as 2 MB pages when possible
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        munmap(p, bytes);
+        return e == cudaErrorMemoryAllocation ? SP_ERR_OOM : SP_ERR_CUDA;
+    }
+    *out = p;
+    return SP_OK;
+}
+
+sp_status sp_host_alloc_near(size_t bytes, int32_t device, void **out, int32_t *numa_node_out) {
+    if (!out || !bytes) return SP_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (numa_node_out) *numa_node_out = -1;
+    int node = -1;
+    if (cudaDeviceGetAttribute(&node, cudaDevAttrHostNumaId, device) != cudaSuccess) {
+        (void)cudaGetLastError();
+        node = -1;
+    }
+    void *p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return SP_ERR_OOM;
+    madvise(p, bytes, MADV_HUGEPAGE);
+    if (node >= 0 && node < 64) {
+        // MPOL_PREFERRED (1): the node's pages first, others if it is full
+        const unsigned long mask = 1ul << node;
+        if (syscall(SYS_mbind, p, bytes, 1, &mask, 64ul, 0u) == 0 && numa_node_out) *numa_node_out = node;
+    }
     cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();

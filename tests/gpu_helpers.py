@@ -15,7 +15,7 @@ def pinned_tables(rows, D, seed, device="cuda", pin=True, host_alloc=False):
     for t, R in enumerate(rows):
         if host_alloc:  # sp_host_alloc: THP-backed, registered by the library allocator
             from paper_2205_04702_b200 import HostTable
-            ht = HostTable(R, D)
+            ht = HostTable(R, D, device=0 if host_alloc == "near" else None)  # "near": sp_host_alloc_near
             init_table(seed, t, R, D, device=device, out=ht.tensor)
             out.append(ht)
             continue

@@ -111,6 +111,21 @@ def test_host_alloc_tables():
     _assert_tables(rep)
 
 
+def test_host_alloc_near_numa_tables():
+    """sp_host_alloc_near: the tables on the host NUMA node closest to the GPU
+    (the node id is reported; -1 when the host has no NUMA information)."""
+    from paper_2205_04702_b200 import HostTable
+    h = HostTable(1000, 16, device=0)
+    assert h.numa_node == -1 or 0 <= h.numa_node < 64
+    h.tensor[7].fill_(3.0)
+    assert float(h.tensor[7].sum()) == 48.0
+    h.free()
+    c = CONFIGS["tiny"]
+    rep = run_parity(c.rows, c.slots, c.dim, c.batch, c.pooling, c.num_batches, 3, 2,
+                     alpha=c.alpha, host_alloc="near")
+    _assert_tables(rep)
+
+
 def test_capacity_error_at_oracle_batch_and_table():
     rows, D, N, L, nb = [400, 400], 8, 8, 2, 40
     tr = sample_trace(rows, N, L, 0.5, nb, 3)
