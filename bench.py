@@ -679,7 +679,9 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "duration_source": ("CUDA events around the kernel on its stream inside the step graphs "
-                                    "of a graph-mode pass right after the timed region (mean of 16 steps)")
+                                    "of a graph-mode pass right after the timed region (mean of 16 steps; that "
+                                    "pass launches without programmatic dependent launch so each event pair "
+                                    "brackets one kernel)")
                                    if timed_src else
                                    "CUDA events around each launch in a separate profiling pass",
                 "traffic": tr_bytes,

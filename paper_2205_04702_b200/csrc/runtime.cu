@@ -1848,6 +1848,11 @@ sp_status capture_step(sp_ctx *c, int r) {
     CK(cudaStreamBeginCapture(c->cap_s, cudaStreamCaptureModeThreadLocal));
     cudaStreamWaitEvent(c->cap_s, c->ev_xfer[r], cudaEventWaitExternal);
     const bool st = c->stage_timing;
+    // the event pass captures without programmatic dependent launch: an event
+    // node between PDL-launched kernels would otherwise also time the early
+    // launch's wait, and the events are to bracket each kernel alone
+    const int pdl_saved = g_pdl;
+    if (st) g_pdl = 0;
     if (st) cudaEventRecordWithFlags(c->sev[r][2], c->cap_s, cudaEventRecordExternal);
     launch_forward(ta, c->cap_s);
     if (st) cudaEventRecordWithFlags(c->sev[r][3], c->cap_s, cudaEventRecordExternal);
@@ -1856,6 +1861,7 @@ sp_status capture_step(sp_ctx *c, int r) {
     if (st) cudaEventRecordWithFlags(c->sev[r][4], c->cap_s, cudaEventRecordExternal);
     launch_backward(tb, c->cap_s);
     if (st) cudaEventRecordWithFlags(c->sev[r][5], c->cap_s, cudaEventRecordExternal);
+    g_pdl = pdl_saved;
     cudaEventRecordWithFlags(c->ev_train[r], c->cap_s, cudaEventRecordExternal);
     CK(cudaStreamEndCapture(c->cap_s, &gr));
     CK(cudaGraphInstantiate(&c->gcomp[r], gr, 0));
