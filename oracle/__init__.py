@@ -63,6 +63,8 @@ def lib():
         L.orc_train_get_row.argtypes = [P, ctypes.c_int32, ctypes.c_int64, f32p]
         L.orc_train_set_padding.argtypes = [P, ctypes.c_int32]
         L.orc_train_set_table_ids.argtypes = [P, P]
+        L.orc_train_set_bf16.argtypes = [P, ctypes.c_int32]
+        L.orc_bf16_round_array.argtypes = [ctypes.c_int64, P, P]
         L.orc_train_touched.restype = ctypes.c_int64
         L.orc_train_touched.argtypes = [P, ctypes.c_int32, i64p, ctypes.c_int64]
         L.orc_policy_create.restype = P
@@ -100,6 +102,14 @@ def fmaf32(a, b, c) -> np.ndarray:
     return out
 
 
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """The oracle's bf16 round-to-nearest-even (reading R28), widened to fp32."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    lib().orc_bf16_round_array(x.size, _p(x, ctypes.c_float), _p(out, ctypes.c_float))
+    return out
+
+
 def init_value(seed: int, t: int, row: int, col: int) -> float:
     return float(lib().orc_init_value(seed, t, row, col))
 
@@ -114,7 +124,8 @@ class UncachedTrainer:
     """Part A: uncached EmbeddingBag training with sparse SGD (ground truth)."""
 
     def __init__(self, rows: Sequence[int], dim: int, batch: int, pooling: int, init_seed: int,
-                 allow_padding: bool = False, table_ids: Optional[Sequence[int]] = None):
+                 allow_padding: bool = False, table_ids: Optional[Sequence[int]] = None,
+                 bf16: bool = False):
         self.rows = np.asarray(rows, dtype=np.int64)
         self.T, self.D, self.N, self.L = len(rows), dim, batch, pooling
         self._h = lib().orc_train_create(self.T, _p(self.rows, ctypes.c_int64), dim, batch,
@@ -123,6 +134,8 @@ class UncachedTrainer:
             raise ValueError("bad oracle config")
         if allow_padding:
             lib().orc_train_set_padding(self._h, 1)
+        if bf16:  # bf16 Storage (reading R28)
+            lib().orc_train_set_bf16(self._h, 1)
         if table_ids is not None:  # global table ids (table-wise sharding)
             self._gid = np.ascontiguousarray(table_ids, dtype=np.int32)
             lib().orc_train_set_table_ids(self._h, _p(self._gid, ctypes.c_int32))

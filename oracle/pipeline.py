@@ -31,19 +31,22 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import Policy, fmaf32, init_value
+from . import Policy, bf16_round, fmaf32, init_value
 
 
 class PipelineSim:
     STAGES = "PCEIT"
 
     def __init__(self, rows, slots, dim, batch, pooling, past, future, init_seed,
-                 gamma, delta, eta, order="TICEP", init_tables=None):
+                 gamma, delta, eta, order="TICEP", init_tables=None, bf16=False):
         assert sorted(order) == sorted(self.STAGES)
         self.rows, self.slots = list(rows), list(slots)
         self.T, self.D, self.N, self.L = len(rows), dim, batch, pooling
         self.P, self.F = past, future
         self.order = order
+        # bf16 Storage (reading R28): the scratchpad holds rows rounded to bf16,
+        # on Insert and after every update; the CPU tables stay fp32
+        self.rnd = bf16_round if bf16 else (lambda v: v)
         self.gamma, self.delta, self.eta = np.float32(gamma), np.float32(delta), np.float32(eta)
         if init_tables is None:
             init_tables = [np.array([[init_value(init_seed, t, r, j) for j in range(dim)]
@@ -102,7 +105,7 @@ class PipelineSim:
                     self.cpu[t][o] = ev
                     if self.pending_wb[t].get(o) == b:
                         del self.pending_wb[t][o]
-                self.storage[t][s] = fv
+                self.storage[t][s] = self.rnd(fv)
                 self.tag[t][s] = x
                 self.pending_slot_writes[t][s].discard((b, "I"))
 
@@ -128,7 +131,7 @@ class PipelineSim:
                 for occ in np.nonzero(ids.reshape(-1) == x)[0]:
                     acc += g[occ // self.L].astype(np.float64)
                 s = slot_of[x]
-                st[s] = fmaf32(-self.eta, acc.astype(np.float32), st[s])
+                st[s] = self.rnd(fmaf32(-self.eta, acc.astype(np.float32), st[s]))
             for s in set(slot_of.values()):
                 self.pending_slot_writes[t][s].discard((b, "T"))
 

@@ -61,6 +61,7 @@ typedef struct {
 struct orc_train {
     int32_t T, D, N, L;
     int32_t allow_pad;   /* id == -1 means "no lookup" (only for the Fig. 2 pin) */
+    int32_t bf16;        /* bf16 Storage (reading R28): values rounded at first touch and after each update */
     uint64_t seed;
     lazy_table *tab;
     /* scratch */
@@ -70,6 +71,27 @@ struct orc_train {
     float *upd;
     int64_t *upd_row;
 };
+
+/* bf16 round-to-nearest-even of an fp32 value, returned widened to fp32
+ * (reading R28; the bf16 format is fp32's top 16 bits: sign, 8-bit exponent,
+ * 7-bit mantissa).  Ties go to the even mantissa; NaN stays NaN. */
+float orc_bf16_round(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) {         /* inf or NaN: keep, quiet a NaN */
+        if (u & 0x007fffffu) u |= 0x00400000u;
+        u &= 0xffff0000u;
+    } else {
+        u += 0x7fffu + ((u >> 16) & 1u);            /* round half to even on bit 16 */
+        u &= 0xffff0000u;
+    }
+    memcpy(&x, &u, 4);
+    return x;
+}
+
+void orc_bf16_round_array(int64_t n, const float *in, float *out) {
+    for (int64_t i = 0; i < n; i++) out[i] = orc_bf16_round(in[i]);
+}
 
 static float *lazy_row(orc_train *o, int32_t t, int64_t row) {
     lazy_table *lt = &o->tab[t];
@@ -82,8 +104,11 @@ static float *lazy_row(orc_train *o, int32_t t, int64_t row) {
         }
         k = lt->used++;
         lt->pool_of_row[row] = k;
-        for (int32_t j = 0; j < o->D; j++)
-            lt->pool[k * o->D + j] = orc_init_value(o->seed, lt->gid, row, j);
+        for (int32_t j = 0; j < o->D; j++) {
+            const float v = orc_init_value(o->seed, lt->gid, row, j);
+            /* bf16 Storage: a row enters the scratchpad rounded (R28) */
+            lt->pool[k * o->D + j] = o->bf16 ? orc_bf16_round(v) : v;
+        }
     }
     return &lt->pool[k * o->D];
 }
@@ -186,13 +211,17 @@ int32_t orc_train_step(orc_train *o, const int64_t *ids, const float *grad_in,
         /* scatter update after all reads of this batch (RAW-1 honoured) */
         for (int64_t u = 0; u < nu; u++) {
             float *e = lazy_row(o, t, o->upd_row[u]);
-            for (int32_t j = 0; j < D; j++) e[j] = fmaf(-eta, o->upd[u * D + j], e[j]);
+            for (int32_t j = 0; j < D; j++) {
+                const float w = fmaf(-eta, o->upd[u * D + j], e[j]);
+                e[j] = o->bf16 ? orc_bf16_round(w) : w;   /* bf16 Storage: the update is stored rounded (R28) */
+            }
         }
     }
     return ORC_OK;
 }
 
 void orc_train_set_padding(orc_train *o, int32_t allow) { o->allow_pad = allow; }
+void orc_train_set_bf16(orc_train *o, int32_t on) { o->bf16 = on; }
 
 /* Table-wise sharding (one cache-manager instance per table):
  * a trainer holding a subset of the tables keys their initial values by the

@@ -48,6 +48,12 @@ int32_t orc_train_step(orc_train *o, const int64_t *ids, const float *grad_in,
 void orc_train_get_row(const orc_train *o, int32_t t, int64_t row, float *out);
 /* allow id == -1 as "no lookup" (ragged bags; used only to pin Fig. 2) */
 void orc_train_set_padding(orc_train *o, int32_t allow);
+/* bf16 Storage (reading R28): every value rounded to bf16 (round to nearest
+ * even) when its row is first touched and after every update; the forward and
+ * the coalescing stay fp32 / fp64.  Set before the first step. */
+void orc_train_set_bf16(orc_train *o, int32_t on);
+float orc_bf16_round(float x);
+void orc_bf16_round_array(int64_t n, const float *in, float *out);
 /* init values of local table t keyed by global table id gid[t] (sharding) */
 void orc_train_set_table_ids(orc_train *o, const int32_t *gid);
 /* sorted list of rows ever touched in table t; returns count (writes <= cap) */
