@@ -108,6 +108,13 @@ typedef enum {
 #define SP_FLAG_PADDING       (1u << 4) /* ragged bags: an ID of -1 is "no      */
                                         /* lookup" (a bag with none pools to    */
                                         /* zeros; reading R27); sp_plan_csr     */
+#define SP_FLAG_BF16          (1u << 5) /* bf16 Storage (reading */
+                                        /* R28): the scratchpad holds each row  */
+                                        /* rounded to bf16 (nearest even) on    */
+                                        /* fill and after every update; pooled, */
+                                        /* gradients and host tables stay fp32  */
+                                        /* (a write-back widens exactly).       */
+                                        /* Requires dim % 8 == 0.               */
 
 /* sp_create(tables, dim, slots, window) of the problem statement. */
 typedef struct {
@@ -436,6 +443,9 @@ sp_status sp_span_times(sp_ctx *c, double *out_ms);
  * Synchronises the plan stream.  Diagnostics only. */
 sp_status sp_debug_plan_profile(sp_ctx *c, uint64_t *out);
 
+/* Storage rows [first, first+count) of table t's slots into out (fp32; with
+ * SP_FLAG_BF16 the bf16 rows widened exactly).  Synchronises the device.
+ * Diagnostics only. */
 sp_status sp_debug_storage(sp_ctx *c, int32_t t, int64_t first, int64_t count, float *out);
 
 #ifdef __cplusplus

@@ -27,6 +27,7 @@ SP_FLAG_INDEX_I32 = 1 << 1
 SP_FLAG_INDEX_DEVICE = 1 << 2
 SP_FLAG_PROFILE = 1 << 3
 SP_FLAG_PADDING = 1 << 4
+SP_FLAG_BF16 = 1 << 5
 POLICIES = {"lru": 0, "random": 1, "lfu": 2}
 KERNEL_KINDS = ["plan", "transfer", "forward", "backward", "surrogate", "flush", "h2d", "d2h"]
 KERNEL_ONLY = ["plan", "transfer", "forward", "backward", "surrogate", "flush"]
@@ -229,11 +230,12 @@ class ScratchPipe:
                  register_host: bool = False, profile: bool = False, log_factor: int = 0,
                  host_threads: int = 0, policy: str = "lru", policy_seed: int = 0,
                  padding: bool = False, world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
-                 table_owner=None, table_ids=None):
+                 table_owner=None, table_ids=None, bf16: bool = False):
         """world > 1 (or nccl_id given): table-wise sharding inside the library
         -- this context owns the global tables `table_ids` (ascending) of the
         `table_owner` map; forward / train exchange with NCCL and use the
-        batch-sharded [T_all][N/world][D] layout."""
+        batch-sharded [T_all][N/world][D] layout.  bf16=True: bf16 Storage
+        (SP_FLAG_BF16, reading R28)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("ScratchPipe needs a CUDA device (no CPU fallback)")
@@ -257,6 +259,8 @@ class ScratchPipe:
             flags |= SP_FLAG_PROFILE
         if padding:
             flags |= SP_FLAG_PADDING
+        if bf16:
+            flags |= SP_FLAG_BF16
         self.index_dtype, self.index_on_device = index_dtype, index_on_device
         self.world, self.rank = world, rank
         self.T_all = self.T

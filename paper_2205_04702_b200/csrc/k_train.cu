@@ -37,7 +37,6 @@ __device__ __forceinline__ unsigned group_mask() {
     }
 }
 
-__device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
 
 __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
     a.x = a.x + b.x; a.y = a.y + b.y; a.z = a.z + b.z; a.w = a.w + b.w;
@@ -51,15 +50,16 @@ __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
 // indices, then their rows for lookup position p, are all in flight together,
 // so even L = 1 (one row per bag) keeps BU rows per group outstanding.  Each
 // bag is still a left fold in ascending p (bit-exact with the oracle).
-template <int G, int VPL, bool PAD>
+template <int G, int VPL, bool PAD, bool BF>
 __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
+    using SR = SRow<BF>;  // fp32 or bf16 Storage rows (R28: widened, folded in fp32)
     if (*A.err != NO_ERR) return;
     constexpr int BU = VPL >= 4 ? 1 : (VPL == 2 ? 2 : 4);
     const int L = A.g.L, D4 = A.g.D / 4;
     const long long nbags = (long long)A.g.T * A.g.N;
     const int gpb = blockDim.x / G;
     const int lane = threadIdx.x % G;
-    const float4 *st = reinterpret_cast<const float4 *>(A.storage) + lane;
+    const typename SR::V *st = reinterpret_cast<const typename SR::V *>(A.storage) + lane;
     float4 *out = reinterpret_cast<float4 *>(A.pooled) + lane;
     const long long S = (long long)gridDim.x * gpb;
     if constexpr (PAD) {
@@ -77,7 +77,7 @@ __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
                 if (sl == EMPTY) continue;
 #pragma unroll
                 for (int v = 0; v < VPL; v++) {
-                    const float4 r = ldg4(st + (size_t)sl * D4 + v * G);
+                    const float4 r = SR::wid(__ldg(st + (size_t)sl * D4 + v * G));
                     if (first) acc[v] = r;
                     else add4(acc[v], r);
                 }
@@ -104,7 +104,7 @@ __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
 #pragma unroll
         for (int u = 0; u < BU; u++)
 #pragma unroll
-            for (int v = 0; v < VPL; v++) acc[u][v] = ldg4(st + (size_t)s[u] * D4 + v * G);
+            for (int v = 0; v < VPL; v++) acc[u][v] = SR::wid(__ldg(st + (size_t)s[u] * D4 + v * G));
         for (int p = 1; p < L; p++) {
 #pragma unroll
             for (int u = 0; u < BU; u++) s[u] = __ldg(so[u] + p);
@@ -112,7 +112,7 @@ __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
 #pragma unroll
             for (int u = 0; u < BU; u++)
 #pragma unroll
-                for (int v = 0; v < VPL; v++) r[u][v] = ldg4(st + (size_t)s[u] * D4 + v * G);
+                for (int v = 0; v < VPL; v++) r[u][v] = SR::wid(__ldg(st + (size_t)s[u] * D4 + v * G));
 #pragma unroll
             for (int u = 0; u < BU; u++)
 #pragma unroll
@@ -131,7 +131,7 @@ template <int G, int VPL>
 __global__ void __launch_bounds__(256) k_fwd(TrainArgs A) {
     unsigned long long *sp = span_base(A.span, SPK_FWD, A.span_b);
     span_mark(sp, 0);
-    fwd_body<G, VPL, false>(A);
+    fwd_body<G, VPL, false, false>(A);
     if (sp) {
         __syncthreads();
         span_mark(sp, 1);
@@ -142,7 +142,7 @@ template <int G, int VPL>
 __global__ void __launch_bounds__(256) k_fwd_pad(TrainArgs A) {
     unsigned long long *sp = span_base(A.span, SPK_FWD, A.span_b);
     span_mark(sp, 0);
-    fwd_body<G, VPL, true>(A);
+    fwd_body<G, VPL, true, false>(A);
     if (sp) {
         __syncthreads();
         span_mark(sp, 1);
@@ -150,12 +150,14 @@ __global__ void __launch_bounds__(256) k_fwd_pad(TrainArgs A) {
 }
 
 // generic D (D/4 not a power-of-two multiple of 32): 32 lanes, strided columns
+template <bool BF>
 __device__ __forceinline__ void fwd_generic_body(const TrainArgs &A) {
+    using SR = SRow<BF>;
     if (*A.err != NO_ERR) return;
     const int L = A.g.L, D4 = A.g.D / 4;
     const long long nbags = (long long)A.g.T * A.g.N;
     const int lane = threadIdx.x & 31;
-    const float4 *st = reinterpret_cast<const float4 *>(A.storage);
+    const typename SR::V *st = reinterpret_cast<const typename SR::V *>(A.storage);
     float4 *out = reinterpret_cast<float4 *>(A.pooled);
     for (long long bag = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; bag < nbags;
          bag += (long long)gridDim.x * (blockDim.x / 32)) {
@@ -166,7 +168,7 @@ __device__ __forceinline__ void fwd_generic_body(const TrainArgs &A) {
             for (int p = 0; p < L; p++) {
                 const uint32_t sl = __ldg(so + p);
                 if (sl == EMPTY) continue;  // padding (reading R27)
-                const float4 r = ldg4(st + (size_t)sl * D4 + c);
+                const float4 r = SR::wid(__ldg(st + (size_t)sl * D4 + c));
                 if (first) acc = r;
                 else add4(acc, r);
                 first = false;
@@ -176,8 +178,31 @@ __device__ __forceinline__ void fwd_generic_body(const TrainArgs &A) {
     }
 }
 
-__global__ void __launch_bounds__(256) k_fwd_generic(TrainArgs A) { fwd_generic_body(A); }
-__global__ void __launch_bounds__(256) k_fwd_pad_generic(TrainArgs A) { fwd_generic_body(A); }
+__global__ void __launch_bounds__(256) k_fwd_generic(TrainArgs A) { fwd_generic_body<false>(A); }
+__global__ void __launch_bounds__(256) k_fwd_pad_generic(TrainArgs A) { fwd_generic_body<false>(A); }
+__global__ void __launch_bounds__(256) k_fwd_bf_generic(TrainArgs A) { fwd_generic_body<true>(A); }
+__global__ void __launch_bounds__(256) k_fwd_pad_bf_generic(TrainArgs A) { fwd_generic_body<true>(A); }
+// bf16 Storage instances (SP_FLAG_BF16)
+template <int G, int VPL>
+__global__ void __launch_bounds__(256) k_fwd_bf(TrainArgs A) {
+    unsigned long long *sp = span_base(A.span, SPK_FWD, A.span_b);
+    span_mark(sp, 0);
+    fwd_body<G, VPL, false, true>(A);
+    if (sp) {
+        __syncthreads();
+        span_mark(sp, 1);
+    }
+}
+template <int G, int VPL>
+__global__ void __launch_bounds__(256) k_fwd_pad_bf(TrainArgs A) {
+    unsigned long long *sp = span_base(A.span, SPK_FWD, A.span_b);
+    span_mark(sp, 0);
+    fwd_body<G, VPL, true, true>(A);
+    if (sp) {
+        __syncthreads();
+        span_mark(sp, 1);
+    }
+}
 
 // --------------------------------------------------------------- backward
 struct Acc4 { double x, y, z, w; };
@@ -555,16 +580,20 @@ __device__ __forceinline__ bool warp_arrive_last(uint32_t *ctr, uint32_t total, 
 // pieces of rows spanning tiles and fold them at the last arrival.  Lane
 // masks: lmask = last row of each segment in the tile, wmask = first row of
 // each row wholly inside it; per lane (row r): slot, uid.
-template <int VPL>
+template <int VPL, bool BF = false>
 __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, unsigned lmask, unsigned wmask,
-                                              uint32_t slot, uint32_t uid, const float4 *sg, const float4 *sw,
-                                              uint32_t eslo = EMPTY, uint32_t eshi = EMPTY) {
+                                              uint32_t slot, uint32_t uid, const float4 *sg,
+                                              const typename SRow<BF>::V *sw, uint32_t eslo = EMPTY,
+                                              uint32_t eshi = EMPTY) {
+    // BF: Storage rows are bf16 (reading R28): widened on read, the update
+    // rounded to nearest even on write; the sums are the same as for fp32
+    using SR = SRow<BF>;
     // eslo / eshi: segment offsets of the row of lane 0 (and of the last
     // row, on its lane), prefetched with the tile's metadata; EMPTY = load here
     const Geometry &g = A.g;
     const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
     const int lane = threadIdx.x & 31;
-    float4 *st = reinterpret_cast<float4 *>(A.storage);
+    typename SR::V *st = reinterpret_cast<typename SR::V *>(A.storage);
     const size_t tb = (size_t)t * g.n;
     // 2. fold segment by segment (a segment = one row's occurrences in
     // this tile).  A whole row of 1 or 2 occurrences is summed in fp32:
@@ -589,11 +618,11 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
         for (int v = 0; v < VPL; v++) {
             const int c = lane + 32 * v;
             if (c < D4) {
-                const float4 ga = sg[(size_t)ra * D4 + c], xa = sw[(size_t)wa * D4 + c];
+                const float4 ga = sg[(size_t)ra * D4 + c], xa = SR::wid(sw[(size_t)wa * D4 + c]);
                 float4 gb, xb;
-                if (rb >= 0) { gb = sg[(size_t)rb * D4 + c]; xb = sw[(size_t)wb * D4 + c]; }
-                st[(size_t)sa * D4 + c] = sgd32(xa, ga, A.lr);
-                if (rb >= 0) st[(size_t)sb * D4 + c] = sgd32(xb, gb, A.lr);
+                if (rb >= 0) { gb = sg[(size_t)rb * D4 + c]; xb = SR::wid(sw[(size_t)wb * D4 + c]); }
+                st[(size_t)sa * D4 + c] = SR::nar(sgd32(xa, ga, A.lr));
+                if (rb >= 0) st[(size_t)sb * D4 + c] = SR::nar(sgd32(xb, gb, A.lr));
             }
         }
     }
@@ -607,7 +636,7 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
             if (c < D4) {
                 float4 gs = sg[(size_t)r * D4 + c];
                 add4(gs, sg[(size_t)(r + 1) * D4 + c]);
-                st[(size_t)s2 * D4 + c] = sgd32(sw[(size_t)w2 * D4 + c], gs, A.lr);
+                st[(size_t)s2 * D4 + c] = SR::nar(sgd32(SR::wid(sw[(size_t)w2 * D4 + c]), gs, A.lr));
             }
         }
     }
@@ -639,8 +668,8 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
             for (int v = 0; v < VPL; v++) {
                 const int c = lane + 32 * v;
                 if (c < D4)
-                    st[(size_t)s * D4 + c] =
-                        sgd(sw[(size_t)wr * D4 + c], Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr);
+                    st[(size_t)s * D4 + c] = SR::nar(
+                        sgd(SR::wid(sw[(size_t)wr * D4 + c]), Acc4{acc[v].x, acc[v].y, acc[v].z, acc[v].w}, A.lr));
             }
         } else {
             // 3. a piece of a row spanning tiles [kf, kl]: slot 0 of tile k
@@ -714,8 +743,8 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
                             for (int q = 0; q < 4; q++)
                                 if (q0 + q < cnt) dadd4(m, x[q]);
                         }
-                        float4 *wp = st + (size_t)s * D4 + c;
-                        *wp = sgd(*wp, Acc4{m.x, m.y, m.z, m.w}, A.lr);
+                        typename SR::V *wp = st + (size_t)s * D4 + c;
+                        *wp = SR::nar(sgd(SR::wid(*wp), Acc4{m.x, m.y, m.z, m.w}, A.lr));
                     }
                 }
             }
@@ -726,20 +755,21 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
 #ifndef SP_BWD_TILE_MINB
 #define SP_BWD_TILE_MINB 16  // resident warps per SM the registers are sized for (<= 128 regs)
 #endif
-template <int VPL>
+template <int VPL, bool BF = false>
 __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_TILE_MINB)
     k_bwd_tile(TrainArgs A, const __grid_constant__ CUtensorMap tmg, const __grid_constant__ CUtensorMap tms) {
+    using SR = SRow<BF>;  // fp32 or bf16 Storage rows (R28)
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t bar;
     if (*A.err != NO_ERR) return;
     const Geometry g = A.g;
     const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
-    const uint32_t rowb = (uint32_t)g.D * 4u;
+    const uint32_t rowb = (uint32_t)g.D * 4u, rowsb = (uint32_t)D4 * SR::bytes;  // gradient / Storage row bytes
     const int lane = threadIdx.x;
     float4 *sg = reinterpret_cast<float4 *>(sm);  // [TR][D4] gradient rows of the tile
-    float4 *sw = sg + (size_t)TR * D4;            // [TR][D4] Storage rows (at their first row)
+    typename SR::V *sw = reinterpret_cast<typename SR::V *>(sg + (size_t)TR * D4);  // [TR][D4] Storage rows
     const float4 *grad = reinterpret_cast<const float4 *>(A.grad);
-    float4 *st = reinterpret_cast<float4 *>(A.storage);
+    typename SR::V *st = reinterpret_cast<typename SR::V *>(A.storage);
     if (lane == 0) bar_init(&bar);
     __syncwarp();
     // a tile's metadata, one load wave: lane r holds sorted occurrence r, its
@@ -806,7 +836,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             // whole segments 4q..4q+3 (compacted: the k-th whole segment's row
             // at sw[k]); one request per 4 rows
             const int ng = (nact + 3) >> 2, nw = __popc(wmask), nsg = (nw + 3) >> 2;
-            if (lane == 0) bar_expect(&bar, (uint32_t)(4 * ng + 4 * nsg) * rowb);
+            if (lane == 0) bar_expect(&bar, (uint32_t)(4 * ng) * rowb + (uint32_t)(4 * nsg) * rowsb);
             __syncwarp();
             const uint32_t grow = (uint32_t)t * (uint32_t)g.N + bagof(m.occ);
             uint32_t gr[4], sr[4];
@@ -824,10 +854,10 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             }
             parity ^= 1u;
         } else if (A.bwd_tma) {  // one TMA bulk copy per row, completion on the mbarrier
-            if (lane == 0) bar_expect(&bar, (uint32_t)(__popc(amask) + __popc(wmask)) * rowb);
+            if (lane == 0) bar_expect(&bar, (uint32_t)__popc(amask) * rowb + (uint32_t)__popc(wmask) * rowsb);
             __syncwarp();
             if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + bagof(m.occ)) * D4, rowb, &bar);
-            if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowb, &bar);
+            if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowsb, &bar);
             load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
             while (!bar_try(&bar, parity)) {
             }
@@ -844,14 +874,16 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             for (unsigned wm = wmask; wm; wm &= wm - 1) {
                 const int r = __ffs(wm) - 1;
                 const uint32_t sl = __shfl_sync(0xffffffffu, slot, r);
-                for (int c = lane; c < D4; c += 32) cp16(sw + (size_t)r * D4 + c, st + (size_t)sl * D4 + c);
+                const char *src = reinterpret_cast<const char *>(st + (size_t)sl * D4);
+                char *dst = reinterpret_cast<char *>(sw + (size_t)r * D4);
+                for (uint32_t c = lane; c < rowsb / 16u; c += 32) cp16(dst + 16 * c, src + 16 * c);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
             load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         }
-        if (!(A.diag & 64)) bwd_fold_tile<VPL>(A, t, k, lmask, wmask, slot, uid, sg, sw, m.slo, m.shi);  // (64: no fold, timing)
+        if (!(A.diag & 64)) bwd_fold_tile<VPL, BF>(A, t, k, lmask, wmask, slot, uid, sg, sw, m.slo, m.shi);  // (64: no fold, timing)
         // the tile's shared rows are consumed (generic proxy) before the next
         // tile's bulk copies (async proxy) overwrite them
         __syncwarp();
@@ -1159,7 +1191,11 @@ static void launch_sized(K kernel, long long groups, const TrainArgs &a, cudaStr
 
 cudaError_t launch_forward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
-    if (a.g.pad) {
+    if (a.g.bf16 && a.g.pad) {
+        SP_DISPATCH_D(D4, k_fwd_pad_bf, (long long)a.g.T * a.g.N, a, s, false);
+    } else if (a.g.bf16) {
+        SP_DISPATCH_D(D4, k_fwd_bf, (long long)a.g.T * a.g.N, a, s, false);
+    } else if (a.g.pad) {
         SP_DISPATCH_D(D4, k_fwd_pad, (long long)a.g.T * a.g.N, a, s, false);
     } else {
         SP_DISPATCH_D(D4, k_fwd, (long long)a.g.T * a.g.N, a, s, false);
@@ -1215,12 +1251,15 @@ static tmap_encode_fn tmap_encode() {
 
 // a [rows][D] fp32 matrix as a 2-D tensor map with a one-row box (the form
 // tile::gather4 takes: tools/gather4_probe.cu)
-static bool rows_map(CUtensorMap *m, const void *base, unsigned long long rows, int D) {
+static bool rows_map(CUtensorMap *m, const void *base, unsigned long long rows, int D, bool bf16 = false) {
     tmap_encode_fn enc = tmap_encode();
     if (!enc || !base || rows == 0 || D > 256 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
-    cuuint64_t gdim[2] = {(cuuint64_t)D, (cuuint64_t)rows}, gstr[1] = {(cuuint64_t)D * 4};
+    const int esz = bf16 ? 2 : 4;
+    if ((D * esz) % 16) return false;  // row stride: a multiple of 16 B
+    cuuint64_t gdim[2] = {(cuuint64_t)D, (cuuint64_t)rows}, gstr[1] = {(cuuint64_t)D * esz};
     cuuint32_t box[2] = {(cuuint32_t)D, 1}, es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), gdim, gstr, box, es,
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+               const_cast<void *>(base), gdim, gstr, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1229,7 +1268,7 @@ static int g_bwd_g4 = -1;  // SP_BWD_G4: 0 disables tile::gather4 (A/B)
 static int g_bwd_ws = -1;  // SP_BWD_WS=1: the warp-specialised k_bwd_ws (A/B: measured slower, 52 vs 36 us isolated
                            // on Terabyte: 6 consumer warps per SM fold less than 13 one-warp CTAs)
 
-template <int VPL>
+template <int VPL, bool BF>
 static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
     TrainArgs a = a0;
     CUtensorMap tmg, tms;
@@ -1240,35 +1279,38 @@ static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
         g_bwd_g4 = e ? (atoi(e) != 0) : 1;
     }
     // a tensor copy's shared-memory destination must be 128-B aligned: a
-    // group of 4 rows (16*D bytes) is when D % 8 == 0
-    a.g4 = g_bwd_g4 && a.bwd_tma && a.tr % 4 == 0 && a.tr <= 32 && a.g.D % 8 == 0 &&
+    // group of 4 gradient rows (16*D bytes) is when D % 8 == 0, of 4 bf16
+    // Storage rows (8*D bytes) when D % 16 == 0
+    a.g4 = g_bwd_g4 && a.bwd_tma && a.tr % 4 == 0 && a.tr <= 32 && a.g.D % (BF ? 16 : 8) == 0 &&
            rows_map(&tmg, a.grad, (unsigned long long)a.g.T * a.g.N, a.g.D) &&
-           rows_map(&tms, a.storage, (unsigned long long)a.srows, a.g.D);
-    const size_t smem = (size_t)2 * a.tr * a.g.D * sizeof(float);
-    static std::map<std::pair<int, size_t>, int> caps;  // (device, smem) -> resident CTAs
+           rows_map(&tms, a.storage, (unsigned long long)a.srows, a.g.D, BF);
+    const size_t smem = (size_t)a.tr * a.g.D * (sizeof(float) + (BF ? 2 : sizeof(float)));
+    // (device, kernel) -> resident CTAs
+    static std::map<std::pair<int, const void *>, int> caps;
+    const void *kid = reinterpret_cast<const void *>(k_bwd_tile<VPL, BF>);
     int dev = 0;
     cudaGetDevice(&dev);
     int cap = 0;
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        auto it = caps.find({dev, smem});
+        auto it = caps.find({dev, kid});
         if (it != caps.end()) cap = it->second;
     }
     if (!cap) {
         int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_tile<VPL>, 32, smem) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_tile<VPL, BF>, 32, smem) != cudaSuccess ||
             per_sm < 1)
             per_sm = 1;
         cap = per_sm * device_sms();
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        caps[{dev, smem}] = cap;
+        caps[{dev, kid}] = cap;
     }
     const long long tiles = (long long)a.g.T * a.ntiles;
     if (g_bwd_ws < 0) {
         const char *e = getenv("SP_BWD_WS");
         g_bwd_ws = e ? (atoi(e) != 0) : 0;
     }
-    if (g_bwd_ws && a.bwd_tma) {  // two warps, two staging buffers per CTA
+    if (!BF && g_bwd_ws && a.bwd_tma) {  // two warps, two staging buffers per CTA (fp32 Storage only)
         const size_t smem2 = 2 * smem;
         static std::map<std::pair<int, size_t>, int> caps2;
         int cap2 = 0;
@@ -1293,18 +1335,26 @@ static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
     }
     int grid = (int)(tiles < cap ? tiles : cap);
     if (grid < 1) grid = 1;
-    launch_maybe_pdl(k_bwd_tile<VPL>, grid, 32, smem, s, true, a, tmg, tms);
+    launch_maybe_pdl(k_bwd_tile<VPL, BF>, grid, 32, smem, s, true, a, tmg, tms);
 }
 
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
     const int D4 = a.g.D / 4;
-    if (a.tpart) {
-        if (D4 <= 32) launch_bwd_tile<1>(a, s);
-        else if (D4 <= 64) launch_bwd_tile<2>(a, s);
-        else if (D4 <= 128) launch_bwd_tile<4>(a, s);
-        else launch_bwd_tile<8>(a, s);
+    if (a.tpart && a.g.bf16) {  // bf16 Storage: the tiled backward only
+        if (D4 <= 32) launch_bwd_tile<1, true>(a, s);
+        else if (D4 <= 64) launch_bwd_tile<2, true>(a, s);
+        else if (D4 <= 128) launch_bwd_tile<4, true>(a, s);
+        else launch_bwd_tile<8, true>(a, s);
         return cudaGetLastError();
     }
+    if (a.tpart) {
+        if (D4 <= 32) launch_bwd_tile<1, false>(a, s);
+        else if (D4 <= 64) launch_bwd_tile<2, false>(a, s);
+        else if (D4 <= 128) launch_bwd_tile<4, false>(a, s);
+        else launch_bwd_tile<8, false>(a, s);
+        return cudaGetLastError();
+    }
+    if (a.g.bf16) return cudaErrorInvalidValue;  // (the record-based k_bwd is fp32 only)
     // upper bound of work items: all chunks of all tables
     SP_DISPATCH_D(D4, k_bwd, (long long)a.g.T * a.g.nc, a, s, true);
     return cudaGetLastError();
@@ -1332,6 +1382,10 @@ cudaError_t configure_train_kernels() {
     cudaFuncSetAttribute(k_bwd_tile<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_tile<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_tile<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_tile<1, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_tile<2, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_tile<4, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_bwd_tile<8, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_ws<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_ws<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_ws<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

@@ -94,6 +94,11 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 #endif
 constexpr int XS = SP_XS;
 
+// BF (SP_FLAG_BF16, reading R28): Storage rows are bf16.  A stage then also
+// holds the victims as loaded (bf16) and the new rows narrowed (bf16): after
+// a round lands the warp widens the victims (exact) and rounds the new rows
+// to nearest even, and the bulk stores take the converted copies.
+template <bool BF>
 __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t bar[XS];
@@ -104,7 +109,8 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
     unsigned long long *spn = span_base(A.span, SPK_XFER, A.b);
     span_mark(spn, 0);
     const Geometry g = A.g;
-    const uint32_t rowb = (uint32_t)g.D * 4u;
+    const uint32_t rowb = (uint32_t)g.D * 4u;        // fp32 row (host side)
+    const uint32_t srowb = BF ? rowb / 2u : rowb;     // Storage row
     const int lane = threadIdx.x;
     if (lane == 0) {
         for (int s = 0; s < XS; s++) mbar_init(&bar[s], 1);
@@ -119,8 +125,15 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
         const uint32_t total = s_pref[tcount];
         // per stage: nb victim rows, then nb new rows (contiguous, so a gathered
         // round moves as one bulk copy each way)
-        auto vbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + i) * rowb; };
-        auto nbuf = [&](int s, int i) { return sm + ((size_t)s * 2 * nb + nb + i) * rowb; };
+        // stage s: [nb] victims (fp32), [nb] new rows (fp32); BF adds [nb]
+        // victims as loaded and [nb] new rows narrowed (bf16 each)
+        const size_t sstride = (size_t)nb * (BF ? 3 : 2) * rowb;
+        auto vbuf = [&](int s, int i) { return sm + s * sstride + (size_t)i * rowb; };
+        auto nbuf = [&](int s, int i) { return sm + s * sstride + ((size_t)nb + i) * rowb; };
+        auto v16 = [&](int s, int i) { return sm + s * sstride + (size_t)2 * nb * rowb + (size_t)i * srowb; };
+        auto n16 = [&](int s, int i) { return sm + s * sstride + (size_t)2 * nb * rowb + ((size_t)nb + i) * srowb; };
+        auto vload = [&](int s, int i) { return BF ? v16(s, i) : vbuf(s, i); };  // victim as loaded from Storage
+        auto nstore = [&](int s, int i) { return BF ? n16(s, i) : nbuf(s, i); };  // new row as stored
         const bool direct = A.wb_direct != 0;  // victims straight to their host rows
         // items [0, Kg) of this table group were gathered by the CPU into the
         // contiguous pinned slot, the rest [Kg, total) are pulled from their
@@ -181,7 +194,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 const bool dir = direct || ((item * 2654435761u) >> 16) < A.wb_q16;
                 s_dst[s][lane] = dir ? dst : 0ull;
                 if (!direct) A.wb_dst[base_t0 + item] = dir ? 0ull : dst;
-                bytes = rowb * (stage != EMPTY ? 2u : 1u);
+                bytes = rowb + (stage != EMPTY ? srowb : 0u);
             }
             if ((uint32_t)lane >= cnt) s_dst[s][lane] = 0ull;
             s_slot[s][lane] = slot;
@@ -201,12 +214,28 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
             } else if (slot != EMPTY) {
                 bulk_g2s(nbuf(s, lane), src_host, rowb, &bar[s]);
             }
-            if (slot != EMPTY && stage != EMPTY) bulk_g2s(vbuf(s, lane), A.storage + (size_t)slot * g.D, rowb, &bar[s]);
+            if (slot != EMPTY && stage != EMPTY)
+                bulk_g2s(vload(s, lane), reinterpret_cast<const char *>(A.storage) + (size_t)slot * srowb, srowb, &bar[s]);
         };
         for (uint32_t r = 0; r < min((uint32_t)XS, nround); r++) issue(r);
         for (uint32_t r = 0; r < nround; r++) {
             const int s = (int)((phase_ctr + r) % XS);
             mbar_wait(&bar[s], ((phase_ctr + r) / XS) & 1u);
+            if constexpr (BF) {
+                // widen the victims, round the new rows (lanes stride over the
+                // round's rows, four columns at a time); the bulk stores below
+                // read the results through the async proxy
+                const uint32_t cnt = round_cnt(r), D4 = (uint32_t)g.D / 4u;
+                for (uint32_t i = lane; i < cnt * D4; i += 32) {
+                    const uint32_t row = i / D4, c = i - row * D4;
+                    reinterpret_cast<float4 *>(vbuf(s, row))[c] =
+                        SRow<true>::wid(reinterpret_cast<const uint2 *>(v16(s, row))[c]);
+                    reinterpret_cast<uint2 *>(n16(s, row))[c] =
+                        SRow<true>::nar(reinterpret_cast<const float4 *>(nbuf(s, row))[c]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+            }
             const uint32_t slot = s_slot[s][lane], stage = s_stage[s][lane];
             const unsigned long long dd = s_dst[s][lane];
             // victims written back by the kernel: one bulk store per row into
@@ -222,7 +251,7 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
             } else if (slot != EMPTY && stage != EMPTY && !dd) {
                 bulk_s2g(A.wb_stage + (size_t)stage * g.D, vbuf(s, lane), rowb);
             }
-            if (slot != EMPTY) bulk_s2g(A.storage + (size_t)slot * g.D, nbuf(s, lane), rowb);
+            if (slot != EMPTY) bulk_s2g(reinterpret_cast<char *>(A.storage) + (size_t)slot * srowb, nstore(s, lane), srowb);
             bulk_commit();
             if (r + XS < nround) {
                 bulk_wait_read0();  // stage s has been read out: refill it
@@ -329,8 +358,8 @@ __global__ void __launch_bounds__(128) k_xfer_warp(XferArgs A) {
     span_mark(spn, 1);
 }
 
-int pullfill_tma_items(int D) {
-    const size_t budget = 192 * 1024, per_item = (size_t)2 * D * 4 * XS;
+int pullfill_tma_items(int D, bool bf16) {
+    const size_t budget = 192 * 1024, per_item = (size_t)(bf16 ? 3 : 2) * D * 4 * XS;
     size_t nb = budget / per_item;
     return (int)(nb > 32 ? 32 : (nb < 1 ? 1 : nb));
 }
@@ -408,8 +437,10 @@ cudaError_t launch_csr_pad(const long long *values, const long long *offsets, lo
     return cudaGetLastError();
 }
 
-// write back every resident slot (sp_flush)
+// write back every resident slot (sp_flush); BF: bf16 rows widened (exact)
+template <bool BF>
 __global__ void __launch_bounds__(256) k_flush(FlushArgs A) {
+    using SR = SRow<BF>;
     const int D4 = A.g.D / 4;
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x / 32;
@@ -420,8 +451,8 @@ __global__ void __launch_bounds__(256) k_flush(FlushArgs A) {
         int t = 0;
         while ((long long)A.slot_base[t + 1] <= s) t++;
         float4 *dst = reinterpret_cast<float4 *>(A.host[t] + (size_t)id * A.g.D);
-        const float4 *src = reinterpret_cast<const float4 *>(A.storage) + (size_t)s * D4;
-        for (int c = lane; c < D4; c += 32) dst[c] = src[c];
+        const typename SR::V *src = reinterpret_cast<const typename SR::V *>(A.storage) + (size_t)s * D4;
+        for (int c = lane; c < D4; c += 32) dst[c] = SR::wid(src[c]);
     }
 }
 
@@ -435,9 +466,27 @@ cudaError_t launch_xfer_warp(const XferArgs &a, int ctas, cudaStream_t s) {
 }
 
 cudaError_t launch_pullfill(const XferArgs &a, int ctas, cudaStream_t s) {
-    const int nb = pullfill_tma_items(a.g.D);
-    const size_t smem = (size_t)nb * 2 * a.g.D * 4 * XS;
-    k_pullfill<<<ctas > 0 ? ctas : 16, 32, smem, s>>>(a, nb);
+    const bool bf = a.g.bf16 != 0;
+    const int nb = pullfill_tma_items(a.g.D, bf);
+    const size_t smem = (size_t)nb * (bf ? 3 : 2) * a.g.D * 4 * XS;
+    if (bf) k_pullfill<true><<<ctas > 0 ? ctas : 16, 32, smem, s>>>(a, nb);
+    else k_pullfill<false><<<ctas > 0 ? ctas : 16, 32, smem, s>>>(a, nb);
+    return cudaGetLastError();
+}
+
+// fp32 rows (device or mapped host memory) -> bf16 Storage rows, rounded to
+// nearest even (SP_FLAG_BF16: sp_prefill, sp_pin_rows)
+__global__ void __launch_bounds__(256) k_rows_to_bf16(const float4 *src, uint2 *dst, long long n4) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = SRow<true>::nar(src[i]);
+}
+
+cudaError_t launch_rows_to_bf16(const float *src, void *dst, long long count, int D, cudaStream_t s) {
+    const long long n4 = count * (D / 4);
+    if (n4 <= 0) return cudaSuccess;
+    const long long blocks = (n4 + 255) / 256, cap = (long long)device_sms() * 8;
+    k_rows_to_bf16<<<(int)std::min(blocks, cap), 256, 0, s>>>(reinterpret_cast<const float4 *>(src),
+                                                               static_cast<uint2 *>(dst), n4);
     return cudaGetLastError();
 }
 
@@ -446,15 +495,18 @@ cudaError_t launch_flush(const FlushArgs &a, cudaStream_t s) {
     long long cap = (long long)device_sms() * 8;
     int grid = (int)(blocks < cap ? blocks : cap);
     if (grid < 1) grid = 1;
-    k_flush<<<grid, 256, 0, s>>>(a);
+    if (a.g.bf16) k_flush<true><<<grid, 256, 0, s>>>(a);
+    else k_flush<false><<<grid, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 
 // attributes of the transfer kernel on the current device (sp_create; kernel
 // attributes are per device, so every context sets them on its own GPU)
 cudaError_t configure_xfer_kernels() {
-    apply_carveout(k_pullfill);
-    return cudaFuncSetAttribute(k_pullfill, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
+    apply_carveout(k_pullfill<false>);
+    apply_carveout(k_pullfill<true>);
+    cudaFuncSetAttribute(k_pullfill<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
+    return cudaFuncSetAttribute(k_pullfill<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
 }
 
 }  // namespace sp

@@ -267,6 +267,7 @@ struct sp_ctx {
     int bwd_tr = 0, bwd_ntiles = 0;
     int bwd_tma = 1;  // k_bwd_tile stages rows with TMA bulk copies; SP_BWD_TMA=0: LDGSTS (A/B, slower)
     float **d_host = nullptr;
+    std::vector<float *> host_dev;  // [T] device-visible (mapped) host table pointers
     void *d_idx[RING] = {};
     BatchBufs ring[RING];
     // victim staging: XSR slots of sum(m) rows (<= T*n) in pinned host memory,
@@ -1083,6 +1084,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     if (!d || d->num_tables < 1 || d->num_tables > 65535 || !d->rows || !d->slots || !d->host_tables)
         return SP_ERR_INVALID_ARG;
     if (d->dim < 4 || d->dim > 1024 || d->dim % 4) return SP_ERR_INVALID_ARG;
+    // bf16 Storage rows move by bulk copies: 2*D bytes, a multiple of 16
+    if ((d->flags & SP_FLAG_BF16) && d->dim % 8) return SP_ERR_INVALID_ARG;
     if (d->batch_size < 1 || d->pooling < 1) return SP_ERR_INVALID_ARG;
     const long long n = (long long)d->batch_size * d->pooling;
     if (n > (1ll << 26)) return SP_ERR_INVALID_ARG;
@@ -1132,6 +1135,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->g.nc = c->n + c->n / CH + 1;
     c->g.hs = backward_hot_segment(c->D);
     c->g.pad = (d->flags & SP_FLAG_PADDING) ? 1 : 0;
+    c->g.bf16 = (d->flags & SP_FLAG_BF16) ? 1 : 0;
     c->policy = d->policy;
     c->policy_seed = d->policy_seed;
     c->log_classes = c->policy == SP_POLICY_LFU ? LOG_CLASSES_MAX : (c->policy == SP_POLICY_RANDOM ? 0 : 1);
@@ -1144,6 +1148,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     c->rows.resize(c->T);
     c->slots.resize(c->T);
     c->host.resize(c->T);
+    c->host_dev.resize(c->T);
     c->row_off.assign(c->T + 1, 0);
     c->slot_base.assign(c->T + 1, 0);
     for (int t = 0; t < c->T; t++) {
@@ -1178,6 +1183,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         c->wb_q16 = f <= 0.0 ? 0u : (f >= 1.0 ? 65536u : (uint32_t)(f * 65536.0));
     }
     if (const char *e = getenv("SP_DIAG")) c->diag = atoi(e);
+    if (c->g.bf16) c->xfer_warp = false;  // bf16 Storage: k_pullfill converts rows, k_xfer_warp does not
 
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) {
@@ -1219,6 +1225,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
             return bail(SP_ERR_INVALID_ARG);  // not pinned / registered
         }
         hdev[t] = static_cast<float *>(p);
+        c->host_dev[t] = hdev[t];
         // the transfer kernel moves whole rows with cp.async.bulk: 16-B aligned
         if ((reinterpret_cast<uintptr_t>(p) & 15) != 0) return bail(SP_ERR_INVALID_ARG);
     }
@@ -1286,7 +1293,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_resident, (size_t)c->S_total));
     CKC(dalloc(c, &c->d_last_use, (size_t)c->S_total));
     CKC(dalloc(c, &c->d_next_need, (size_t)c->S_total));
-    CKC(dalloc(c, &c->d_storage, (size_t)c->S_total * c->D));
+    // Storage: S rows of D fp32, or of D bf16 (SP_FLAG_BF16: half the bytes)
+    CKC(dalloc(c, &c->d_storage, (size_t)c->S_total * c->D / (c->g.bf16 ? 2 : 1)));
     // LRU log per table (LFU: one per use-count class, c = 0 holding the
     // initial vacant slots; RANDOM: none): capacity log_factor*S_t + 4n
     // (LFU classes: 2*S_t + 4n each)
@@ -1330,7 +1338,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_victims, Tn));
     if (c->n > SMEM_SORT_MAX) CKC(dalloc(c, &c->d_sort_tmp, 4 * Tn));
     CKC(dalloc(c, &c->d_partial, (size_t)c->T * c->g.nh * c->D));
-    if (backward_tiled()) {
+    if (backward_tiled() || c->g.bf16) {  // (bf16 Storage: the tiled backward only)
         c->bwd_tr = backward_tile_rows(c->D);
         c->bwd_ntiles = (c->n + c->bwd_tr - 1) / c->bwd_tr;
         const size_t tiles = (size_t)c->T * c->bwd_ntiles;
@@ -1478,7 +1486,7 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(cudaMemcpy(c->d_log_skip, c->log_skip.data(), c->T, cudaMemcpyHostToDevice));
     CKC(cudaMemset(c->d_err, 0xFF, sizeof(unsigned long long)));
     CKC(cudaMemset(c->d_cum, 0, 4 * sizeof(unsigned long long)));
-    CKC(cudaMemset(c->d_storage, 0, (size_t)c->S_total * c->D * sizeof(float)));
+    CKC(cudaMemset(c->d_storage, 0, (size_t)c->S_total * c->D * (c->g.bf16 ? 2 : sizeof(float))));
     CKC(cudaDeviceSynchronize());
 #undef CKC
     // transfer engine: helpers + worker
@@ -1618,8 +1626,12 @@ sp_status sp_pin_rows(sp_ctx *c, int32_t t, const int64_t *ids, int64_t count) {
             res[k] = (uint32_t)ids[k];
             slot[k] = base + (uint32_t)k;
         }
-        cudaError_t e = cudaMemcpy(c->d_storage + (size_t)base * c->D, h, (size_t)count * c->D * sizeof(float),
-                                   cudaMemcpyHostToDevice);
+        cudaError_t e = c->g.bf16  // bf16 Storage: rows rounded on the GPU (R28)
+                            ? launch_rows_to_bf16(h, reinterpret_cast<char *>(c->d_storage) + (size_t)base * c->D * 2,
+                                                  count, c->D, nullptr)
+                            : cudaMemcpy(c->d_storage + (size_t)base * c->D, h, (size_t)count * c->D * sizeof(float),
+                                         cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && c->g.bf16) e = cudaDeviceSynchronize();
         cudaFreeHost(h);
         CK(e);
         CK(cudaMemcpy(c->d_resident + base, res.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice));
@@ -1755,9 +1767,14 @@ sp_status sp_prefill(sp_ctx *c) {
     for (int t = 0; t < c->T; t++)
         if (c->slots[t] != c->rows[t]) return fail(c, SP_ERR_INVALID_ARG, "sp_prefill: needs slots == rows for every table");
     CK(cudaSetDevice(c->device));
-    for (int t = 0; t < c->T; t++)
-        CK(cudaMemcpyAsync(c->d_storage + (size_t)c->slot_base[t] * c->D, c->host[t],
-                           (size_t)c->rows[t] * c->D * sizeof(float), cudaMemcpyHostToDevice, c->plan_s));
+    for (int t = 0; t < c->T; t++) {
+        if (c->g.bf16)  // bf16 Storage: every row rounded on the GPU as it is read (R28)
+            CK(launch_rows_to_bf16(c->host_dev[t], reinterpret_cast<char *>(c->d_storage) + (size_t)c->slot_base[t] * c->D * 2,
+                                   c->rows[t], c->D, c->plan_s));
+        else
+            CK(cudaMemcpyAsync(c->d_storage + (size_t)c->slot_base[t] * c->D, c->host[t],
+                               (size_t)c->rows[t] * c->D * sizeof(float), cudaMemcpyHostToDevice, c->plan_s));
+    }
     CK(launch_prefill_map(c->d_slot_base, c->d_row_off, c->T, c->S_total, c->d_resident, c->d_hitmap, c->plan_s));
     {   // RANDOM: every dynamic slot is occupied
         std::vector<uint32_t> nf(c->T);
@@ -2224,6 +2241,16 @@ sp_status sp_debug_storage(sp_ctx *c, int32_t t, int64_t first, int64_t count, f
         return SP_ERR_INVALID_ARG;
     CK(cudaSetDevice(c->device));
     CK(cudaDeviceSynchronize());
+    if (c->g.bf16) {  // bf16 rows, widened here (exact: the top 16 bits of an fp32)
+        std::vector<uint16_t> tmp((size_t)count * c->D);
+        CK(cudaMemcpy(tmp.data(), reinterpret_cast<const char *>(c->d_storage) + ((size_t)c->slot_base[t] + first) * c->D * 2,
+                      tmp.size() * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < tmp.size(); i++) {
+            const uint32_t u = (uint32_t)tmp[i] << 16;
+            std::memcpy(out + i, &u, 4);
+        }
+        return SP_OK;
+    }
     CK(cudaMemcpy(out, c->d_storage + ((size_t)c->slot_base[t] + first) * c->D,
                   (size_t)count * c->D * sizeof(float), cudaMemcpyDeviceToHost));
     return SP_OK;

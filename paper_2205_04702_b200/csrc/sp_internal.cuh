@@ -16,6 +16,7 @@
 //                                   last_use[slot] == stamp)
 //   ring of 16 per-batch buffers, per table region of n = N*L entries.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -90,6 +91,32 @@ struct Geometry {
     int n, n1, nc, nh;    // strides
     int hs;               // occurrences per hot-row segment (k_bwd: one CTA round)
     int pad;              // SP_FLAG_PADDING: slot_of_occ may hold EMPTY (no lookup)
+    int bf16;             // SP_FLAG_BF16: Storage rows are bf16 (reading R28)
+};
+
+// A Storage row seen four columns at a time: fp32 rows hold a float4, bf16
+// rows (SP_FLAG_BF16, reading R28) a uint2 of four bf16 (column 4c+0 in the
+// low half of .x).  wid widens exactly; nar rounds to nearest even
+// (cvt.rn.bf16x2.f32), the rounding the oracle's orc_bf16_round writes out.
+template <bool BF>
+struct SRow {
+    using V = float4;
+    static constexpr uint32_t bytes = 16;
+    __device__ __forceinline__ static float4 wid(const V &v) { return v; }
+    __device__ __forceinline__ static V nar(const float4 &x) { return x; }
+};
+template <>
+struct SRow<true> {
+    using V = uint2;
+    static constexpr uint32_t bytes = 8;
+    __device__ __forceinline__ static float4 wid(const V &v) {
+        return make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u),
+                           __uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
+    }
+    __device__ __forceinline__ static V nar(const float4 &x) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+        return make_uint2(*reinterpret_cast<const uint32_t *>(&lo), *reinterpret_cast<const uint32_t *>(&hi));
+    }
 };
 
 // Missed-row lists of one Plan, mirrored into pinned host memory by the plan
@@ -210,13 +237,17 @@ struct XferArgs {
 
 
 struct FlushArgs {
-    Geometry g;
+    Geometry g;             // (g.bf16: Storage rows widened to fp32 on the way out)
     int S_total;
     const uint32_t *slot_base;
     const uint32_t *resident;
     const float *storage;
     float *const *host;
 };
+
+// fp32 rows -> bf16 Storage rows (SP_FLAG_BF16: sp_prefill, sp_pin_rows);
+// src may be a mapped host pointer; count rows of D columns
+cudaError_t launch_rows_to_bf16(const float *src, void *dst, long long count, int D, cudaStream_t s);
 
 // Exclusive prefix of per-table counts[t0 .. t0+tcount) into s_pref[0..tcount]
 // (tcount <= 64).  Loads are issued in parallel (one per thread) and scanned

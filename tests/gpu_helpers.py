@@ -52,13 +52,16 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
                gde=(0.5, 0.01, 0.01), index_dtype="int64", index_on_device=False, log_factor=0,
                check_plans=True, check_slots=True, check_pooled=True, trace=None,
                register_host=False, profile=False, sample_rows=None, host_alloc=False,
-               tables=None, policy_kw=None, padding=False, pinned=None, push=None, sp_kw=None):
+               tables=None, policy_kw=None, padding=False, pinned=None, push=None, sp_kw=None,
+               bf16=False):
     """tables: pre-allocated host tables (HostTable or pinned tensors), already
     holding init(init_seed) values; policy_kw: extra ScratchPipe / Policy
     arguments of a replacement-policy variant (policy, policy_seed); padding:
     -1 entries are "no lookup" on both sides; pinned: per table, rows pinned
     in the last slots (sp_pin_rows / the oracle's static partition); push:
-    optional push(sp, j) replacing sp.plan(trace[j]) (e.g. sp_plan_csr)."""
+    optional push(sp, j) replacing sp.plan(trace[j]) (e.g. sp_plan_csr);
+    bf16: bf16 Storage on both sides (SP_FLAG_BF16 / the oracle's bf16 mode,
+    reading R28)."""
     g, d, e = gde
     if trace is None:
         trace = sample_trace(rows, N, L, alpha, nb, trace_seed)
@@ -72,7 +75,7 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
     pkw = dict(policy_kw or {})
     sp = ScratchPipe(rows, tables, D, slots, N, L, past=P, future=F, index_dtype=index_dtype,
                      index_on_device=index_on_device, log_factor=log_factor,
-                     register_host=register_host, profile=profile, padding=padding, **pkw,
+                     register_host=register_host, profile=profile, padding=padding, bf16=bf16, **pkw,
                      **(sp_kw or {}))
     if pinned is not None:
         for t, ids in enumerate(pinned):
@@ -80,7 +83,7 @@ def run_parity(rows, slots, D, N, L, nb, P, F, alpha=1.05, trace_seed=2205, init
                 sp.pin_rows(t, ids)
     pol = Policy(rows, slots, P, F, allow_padding=padding, pinned=pinned, **pkw) \
         if (check_plans or check_slots) else None
-    orc = UncachedTrainer(rows, D, N, L, init_seed, allow_padding=padding)
+    orc = UncachedTrainer(rows, D, N, L, init_seed, allow_padding=padding, bf16=bf16)
     report = {"plans": 0, "evictions": 0, "pooled": 0}
 
     def on_plan(b, newest=True):
