@@ -66,6 +66,9 @@ def parse():
                          "and every row loaded before the first batch: no misses at all), static (the "
                          "paper's static top-N cache from the same kernels: the hottest rows of a profiling "
                          "prefix pinned in the slot budget, a window-sized scratchpad for the rest)")
+    ap.add_argument("--storage", default="f32", choices=["f32", "bf16"],
+                    help="Storage row format (SURVEY 8(f) f4): f32 (the paper's), or bf16 (SP_FLAG_BF16, "
+                         "reading R28: rows rounded to bf16 in HBM, host tables, pooled and gradients fp32)")
     ap.add_argument("--preroll", type=int, default=-1, help="untimed steady-state fill batches (-1: config)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -478,7 +481,7 @@ def run_ours(args):
     sp = ScratchPipe(rows, tables, D, slots, N, L, window=cfg.window, device=local, stream=stream,
                      index_dtype="int32", index_on_device=False, policy=args.policy,
                      host_threads=args.host_threads,
-                     policy_seed=args.policy_seed, **shard_kw)
+                     policy_seed=args.policy_seed, bf16=args.storage == "bf16", **shard_kw)
     pinned_rows = 0
     if args.variant == "static":
         # static top-N partition: the hottest rows of the first 200 batches of
@@ -572,10 +575,17 @@ def run_ours(args):
     st1 = sp.stats()
     stage_t = stage_busy = spans = None
     if world == 1:  # same graph-mode steady state, step graphs recaptured with event nodes
+        evspan = os.environ.get("SP_BENCH_EVSPAN") == "1"  # diagnostic: spans stamped in the event pass too
         sp.set_stage_timing(True)
+        if evspan:
+            sp.set_span_timing(True)
         value_loop(KS)
         stage_t = sp.stage_times()   # events of the last 16 steps, on each stage's own stream
         stage_busy = _stream_busy(sp.stage_events())
+        if evspan:
+            print("evspan events", {k: round(v["ms"] * 1e3, 2) for k, v in stage_t.items()},
+                  "spans", _span_summary(sp.span_times())["duration_us"], file=sys.stderr)
+            sp.set_span_timing(False)
         sp.set_stage_timing(False)
         sp.set_span_timing(True)    # the same steady state, kernels stamping their own spans
         value_loop(KS)
@@ -645,11 +655,12 @@ def run_ours(args):
     kms = {k: st2["kernel_ms"][k] - st1p["kernel_ms"][k] for k in st2["kernel_ms"]}
     kcount = {k: st2["kernel_timed"][k] - st1p["kernel_timed"][k] for k in st2["kernel_timed"]}
     avg_ms = {k: (kms[k] / kcount[k] if kcount[k] else 0.0) for k in kms}
+    es = 2 if args.storage == "bf16" else 4  # bytes per Storage element
     alg_bytes = {
         # slot map + gathered rows + pooled out (nominal TBE bytes)
-        "forward": 4 * Tg * n + 4 * D * Tg * n + 4 * D * Tg * N,
+        "forward": 4 * Tg * n + es * D * Tg * n + 4 * D * Tg * N,
         # pooled grad in + occurrence list + per-unique segment/slot words + SGD read+write
-        "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 8 * D * U,
+        "backward": 4 * D * Tg * N + 4 * Tg * n + 16 * U + 2 * es * D * U,
         "surrogate": 8 * D * Tg * N,
         # k_pullfill, host-link bytes: missed rows pulled (H2D) + victims written
         # to the pinned staging slot (D2H); HBM: the same rows written / read
@@ -675,7 +686,8 @@ def run_ours(args):
     dom = max(["forward", "backward"], key=lambda k: kernels[k]["avg_us"])
     ach = kernels[dom]["alg_GBs"] or 0.0
     # ncu DRAM traffic applies to the configuration it was captured on
-    tr_bytes = traffic.get(args.config, {}).get(dom)  # per config (captured on that workload)
+    tkey = args.config if args.storage == "f32" else f"{args.config}:{args.storage}"
+    tr_bytes = traffic.get(tkey, {}).get(dom)  # per config (captured on that workload)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "duration_source": ("CUDA events around the kernel on its stream inside the step graphs "
@@ -686,8 +698,8 @@ def run_ours(args):
                                    "CUDA events around each launch in a separate profiling pass",
                 "traffic": tr_bytes,
                 "bytes_per_launch": int(alg_bytes[dom]),
-                "bytes_formula": ("4*T*n + 4*D*T*n + 4*D*T*N" if dom == "forward"
-                                  else "4*D*T*N + 4*T*n + 16*U + 8*D*U")}
+                "bytes_formula": (("4*T*n + %d*D*T*n + 4*D*T*N" % es) if dom == "forward"
+                                  else ("4*D*T*N + 4*T*n + 16*U + %d*D*U" % (2 * es)))}
     if spans and spans["duration_us"].get(dom):
         # cross-check: the same bytes over the kernel's own first-CTA-start to
         # last-CTA-end span in the same steady state
@@ -727,9 +739,9 @@ def run_ours(args):
                    "window": cfg.window, "preroll_batches": pre, "index_input": "device int32 (value)",
                    "l2": "no flush: inputs larger than L2 (Storage %.2f GB, Hit-Map %.0f MB, host tables "
                          "%.1f GB); every step reads a fresh batch" % (
-                             sum(slots_all) * D * 4 / 1e9, sum(cfg.rows) * 4 / 1e6, sum(cfg.rows) * D * 4 / 1e9),
+                             sum(slots_all) * D * es / 1e9, sum(cfg.rows) * 4 / 1e6, sum(cfg.rows) * D * 4 / 1e9),
                    "parallelism": f"table-wise x{world}" if world > 1 else "single GPU",
-                   "variant": args.variant, "policy": args.policy,
+                   "variant": args.variant, "policy": args.policy, "storage": args.storage,
                    **({"pinned_rows": pinned_rows} if args.variant == "static" else {})},
         "roofline": roofline,
         "train_stage": {"avg_us": round(train_ms * 1e3, 3), "alg_bytes": int(train_bytes),

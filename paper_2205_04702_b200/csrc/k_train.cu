@@ -697,6 +697,7 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
                 const int c = lane + 32 * v;
                 if (c < D4) reinterpret_cast<double4 *>(mine)[c] = acc[v];
             }
+            if (A.tp2) continue;  // two-phase: k_bwd_rows folds the pieces
             bool go = true;
             int step = 1, cnt = npc;
             if (npc > 8) {  // level 1: groups of 8 consecutive pieces
@@ -761,7 +762,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     using SR = SRow<BF>;  // fp32 or bf16 Storage rows (R28)
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ __align__(8) uint64_t bar;
-    if (*A.err != NO_ERR) return;
+    const bool dead = *A.err != NO_ERR;  // (no work, but still counted out: the tile counters reset)
     const Geometry g = A.g;
     const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
     const uint32_t rowb = (uint32_t)g.D * 4u, rowsb = (uint32_t)D4 * SR::bytes;  // gradient / Storage row bytes
@@ -779,7 +780,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     struct Meta { uint32_t occ, uid, slot, prev, next, slo, shi; };
     const uint32_t L = (uint32_t)g.L;
     auto bagof = [&](uint32_t occ) { return L == 1u ? occ : occ / L; };  // (no division for L = 1)
-    const int total = g.T * NT;  // (< 2^31: T < 2^16 tables, NT <= n)
+    const int total = dead ? 0 : g.T * NT;  // (< 2^31: T < 2^16 tables, NT <= n)
     auto load_meta = [&](int tile, Meta &m) {
         m = Meta{0u, EMPTY, 0u, EMPTY, EMPTY, EMPTY, EMPTY};
         if (tile >= total) return;
@@ -805,8 +806,22 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     unsigned long long *spn = span_base(A.span, SPK_BWD, A.span_b);
     span_mark(spn, 0);
     uint32_t parity = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    // tile order: blockIdx.x, blockIdx.x + G, then claimed (2G + claim) when
+    // A.tctr is set, else blockIdx.x + 2G, + 3G, ... (static)
+    uint32_t *ctr = A.tctr ? A.tctr + 2 * (A.span_b % RING) : nullptr;
+    const int G = (int)gridDim.x;
+    int after = blockIdx.x + G;  // the tile after the current one (its metadata is loaded during this tile)
+    for (int tile = blockIdx.x; tile < total;) {
         const Meta m = nxt;
+        // claim the tile after `after` now; its index is needed only at the end of this tile
+        uint32_t claim = 0;
+        if (ctr && lane == 0 && after < total) claim = atomicAdd(ctr, 1u);
+        auto advance = [&]() {
+            tile = after;
+            if (after >= total) return;
+            after = ctr ? 2 * G + (int)__shfl_sync(0xffffffffu, claim, 0) : after + G;
+            if (after > total) after = total;
+        };
         const int t = tile / NT, k = tile - t * NT;
         const int lo = k * TR;
         const int nrows = min(TR, g.n - lo);
@@ -814,7 +829,8 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const bool act = uid != EMPTY;
         const unsigned amask = __ballot_sync(0xffffffffu, act);
         if (amask == 0u) {  // (warp-uniform) all padding
-            load_meta(tile + gridDim.x, nxt);
+            load_meta(after, nxt);
+            advance();
             continue;
         }
         const int nact = 32 - __clz(amask);  // active rows are a prefix
@@ -829,7 +845,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const unsigned wmask = __ballot_sync(0xffffffffu, whole);
         const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
         if (A.diag & 128) {  // timing diagnostic: no staging (the fold reads stale shared memory)
-            load_meta(tile + gridDim.x, nxt);
+            load_meta(after, nxt);
         } else if (A.g4) {
             // TMA tile::gather4: lane q fetches tile rows 4q..4q+3 (the last
             // group padded with the last row) and lane q the Storage rows of
@@ -849,7 +865,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             }
             if (lane < ng) rows4_g2s(sg + (size_t)4 * lane * D4, &tmg, gr[0], gr[1], gr[2], gr[3], &bar);
             if (lane < nsg) rows4_g2s(sw + (size_t)4 * lane * D4, &tms, sr[0], sr[1], sr[2], sr[3], &bar);
-            load_meta(tile + gridDim.x, nxt);
+            load_meta(after, nxt);
             while (!bar_try(&bar, parity)) {
             }
             parity ^= 1u;
@@ -858,7 +874,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             __syncwarp();
             if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + bagof(m.occ)) * D4, rowb, &bar);
             if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowsb, &bar);
-            load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
+            load_meta(after, nxt);  // the next tile's metadata, in flight with the copies
             while (!bar_try(&bar, parity)) {
             }
             parity ^= 1u;
@@ -879,7 +895,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
                 for (uint32_t c = lane; c < rowsb / 16u; c += 32) cp16(dst + 16 * c, src + 16 * c);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
-            load_meta(tile + gridDim.x, nxt);  // the next tile's metadata, in flight with the copies
+            load_meta(after, nxt);  // the next tile's metadata, in flight with the copies
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         }
@@ -888,8 +904,166 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         // tile's bulk copies (async proxy) overwrite them
         __syncwarp();
         if (A.bwd_tma || A.g4) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        advance();
     }
     span_mark(spn, 1);
+    if (ctr && lane == 0) {  // every claim of every CTA precedes its exit: the last one out resets
+        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+            ctr[0] = 0u;
+            ctr[1] = 0u;
+        }
+    }
+}
+
+// Second phase of the two-phase backward: every row spanning tiles [kf, kl]
+// left one fp64 piece per tile (k_bwd_tile); here the pieces are folded and
+// SGD applied.  The owner of such a row is its first tile kf (the row starts
+// inside it and runs past its end).  A CTA takes 32 tiles at a time: warp 0
+// checks them (one lane per tile, one load wave) and lists the owners in
+// shared memory; a row of <= BWD2_SMALL pieces is then folded by one warp,
+// in tile order (all its pieces in flight at once); a longer one (the Zipf
+// head: up to n/TR pieces) by all 8 warps -- warp w sums pieces kf+w, kf+w+8,
+// ... in order, then warp 0 adds the 8 partials in warp order.  The fold
+// shape depends only on the batch.
+constexpr int BWD2_SMALL = 8;
+template <int VPL, bool BF>
+__global__ void __launch_bounds__(256, 2) k_bwd_rows(TrainArgs A) {
+    using SR = SRow<BF>;
+    extern __shared__ __align__(16) unsigned char sm2[];
+    double4 *spart = reinterpret_cast<double4 *>(sm2);  // [8][D4] partials of a long row
+    __shared__ uint4 s_item[32];                         // (t, u, kf, kl) of each owner found
+    __shared__ uint32_t s_slo[32], s_slot[32];
+    __shared__ uint32_t s_small, s_big;                  // ballots of short / long owners
+    const bool dead = *A.err != NO_ERR;
+    const Geometry g = A.g;
+    const int D4 = g.D / 4, TR = A.tr, NT = A.ntiles;
+    const int total = dead ? 0 : g.T * NT;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    typename SR::V *st = reinterpret_cast<typename SR::V *>(A.storage);
+    unsigned long long *spn = span_base(A.span, SPK_BWD, A.span_b);
+    span_mark(spn, 0, SPAN_BWD2_OFF);
+    auto piece = [&](int t, int kk, int kf, uint32_t slo) {
+        const int ps = (kk == kf && slo != (uint32_t)(kf * TR)) ? 1 : 0;
+        return reinterpret_cast<const double4 *>(A.tpart + (((size_t)t * NT + kk) * 2 + ps) * g.D);
+    };
+    auto apply = [&](uint32_t slot, int c, const double4 &m) {
+        typename SR::V *wp = st + (size_t)slot * D4 + c;
+        *wp = SR::nar(sgd(SR::wid(*wp), Acc4{m.x, m.y, m.z, m.w}, A.lr));
+    };
+    bool waited = false;
+    for (int base = blockIdx.x * 32; base < total; base += gridDim.x * 32) {
+        // 1. owners among tiles base..base+31 (Plan's output: readable before the wait)
+        if (warp == 0) {
+            const int tile = base + lane;
+            uint4 it = make_uint4(EMPTY, 0u, 0u, 0u);
+            uint32_t slo = 0, slot = 0;
+            if (tile < total) {
+                const int t = tile / NT, k = tile - t * NT;
+                const int lo = k * TR, nrows = min(TR, g.n - lo);
+                if (lo + nrows < g.n) {
+                    const size_t tb = (size_t)t * g.n;
+                    const uint32_t u = __ldg(A.bb.sorted_uid + tb + lo + nrows - 1);
+                    const uint32_t un = __ldg(A.bb.sorted_uid + tb + lo + nrows);
+                    if (u != EMPTY && u == un) {
+                        slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u);
+                        if (slo >= (uint32_t)lo) {
+                            const uint32_t shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
+                            slot = __ldg(A.bb.sorted_slot + tb + slo);
+                            it = make_uint4((uint32_t)t, u, (uint32_t)k, (shi - 1u) / (uint32_t)TR);
+                        }
+                    }
+                }
+            }
+            const bool own = it.x != EMPTY;
+            const bool big = own && (int)(it.w - it.z) + 1 > BWD2_SMALL;
+            s_item[lane] = it;
+            s_slo[lane] = slo;
+            s_slot[lane] = slot;
+            const unsigned bs = __ballot_sync(0xffffffffu, own && !big), bb = __ballot_sync(0xffffffffu, big);
+            if (lane == 0) { s_small = bs; s_big = bb; }
+        }
+        __syncthreads();
+        const unsigned small = s_small, bigm = s_big;
+        if (!(small | bigm)) continue;  // (CTA-uniform; the next chunk's writes follow this barrier)
+        if (!waited) {  // (PDL) the pieces of k_bwd_tile are complete from here on
+            griddep_wait();
+            waited = true;
+        }
+        // 2. short rows: owner i of the chunk goes to warp (rank of i) % 8
+        {
+            unsigned m = small;
+            for (int r = 0; m; r++, m &= m - 1) {
+                if ((r & 7) != warp) continue;
+                const int i = __ffs(m) - 1;
+                const uint4 it = s_item[i];
+                const int t = (int)it.x, kf = (int)it.z, npc = (int)(it.w - it.z) + 1;
+                const uint32_t slo = s_slo[i], slot = s_slot[i];
+#pragma unroll 1
+                for (int v = 0; v < VPL; v++) {
+                    const int c = lane + 32 * v;
+                    if (c >= D4) continue;
+                    // (npc >= 2) all pieces in flight, then added in tile order
+                    const double4 *p0 = piece(t, kf, kf, slo) + c;
+                    const size_t stp = (size_t)2 * g.D / 4;  // double4 from one tile's slot 0 to the next's
+                    const double4 *p1 = reinterpret_cast<const double4 *>(A.tpart + (((size_t)t * NT + kf + 1) * 2) * g.D) + c;
+                    double4 x0 = ldcg_d4(p0), x1 = ldcg_d4(p1), x2, x3, x4, x5, x6, x7;
+                    if (npc > 2) x2 = ldcg_d4(p1 + stp);
+                    if (npc > 3) x3 = ldcg_d4(p1 + 2 * stp);
+                    if (npc > 4) x4 = ldcg_d4(p1 + 3 * stp);
+                    if (npc > 5) x5 = ldcg_d4(p1 + 4 * stp);
+                    if (npc > 6) x6 = ldcg_d4(p1 + 5 * stp);
+                    if (npc > 7) x7 = ldcg_d4(p1 + 6 * stp);
+                    dadd4(x0, x1);
+                    if (npc > 2) dadd4(x0, x2);
+                    if (npc > 3) dadd4(x0, x3);
+                    if (npc > 4) dadd4(x0, x4);
+                    if (npc > 5) dadd4(x0, x5);
+                    if (npc > 6) dadd4(x0, x6);
+                    if (npc > 7) dadd4(x0, x7);
+                    apply(slot, c, x0);
+                }
+            }
+        }
+        // 3. long rows: all 8 warps, then warp 0 in warp order
+        for (unsigned m = bigm; m; m &= m - 1) {
+            const int i = __ffs(m) - 1;
+            const uint4 it = s_item[i];
+            const int t = (int)it.x, kf = (int)it.z, np = (int)(it.w - it.z) + 1;
+            const uint32_t slo = s_slo[i];
+#pragma unroll 1
+            for (int v = 0; v < VPL; v++) {
+                const int c = lane + 32 * v;
+                if (c >= D4) continue;
+                double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
+                for (int q0 = warp; q0 < np; q0 += 32) {  // pieces q0, q0+8, q0+16, q0+24 in flight
+                    double4 x0, x1, x2, x3;
+                    x0 = ldcg_d4(piece(t, kf + q0, kf, slo) + c);
+                    if (q0 + 8 < np) x1 = ldcg_d4(piece(t, kf + q0 + 8, kf, slo) + c);
+                    if (q0 + 16 < np) x2 = ldcg_d4(piece(t, kf + q0 + 16, kf, slo) + c);
+                    if (q0 + 24 < np) x3 = ldcg_d4(piece(t, kf + q0 + 24, kf, slo) + c);
+                    dadd4(acc, x0);
+                    if (q0 + 8 < np) dadd4(acc, x1);
+                    if (q0 + 16 < np) dadd4(acc, x2);
+                    if (q0 + 24 < np) dadd4(acc, x3);
+                }
+                spart[(size_t)warp * D4 + c] = acc;
+            }
+            __syncthreads();
+            if (warp == 0) {
+#pragma unroll
+                for (int v = 0; v < VPL; v++) {
+                    const int c = lane + 32 * v;
+                    if (c >= D4) continue;
+                    double4 acc = spart[c];
+                    for (int ww = 1; ww < 8; ww++) dadd4(acc, spart[(size_t)ww * D4 + c]);
+                    apply(s_slot[i], c, acc);
+                }
+            }
+            __syncthreads();
+        }
+        __syncthreads();  // s_item is rewritten by the next chunk
+    }
+    span_mark(spn, 1, SPAN_BWD2_OFF);
 }
 
 // Warp-specialised variant (A/B, SP_BWD_WS=1): a CTA of two warps and two staging
@@ -1311,6 +1485,7 @@ static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
         g_bwd_ws = e ? (atoi(e) != 0) : 0;
     }
     if (!BF && g_bwd_ws && a.bwd_tma) {  // two warps, two staging buffers per CTA (fp32 Storage only)
+        a.tp2 = 0;  // (one phase: last-arriver counters)
         const size_t smem2 = 2 * smem;
         static std::map<std::pair<int, size_t>, int> caps2;
         int cap2 = 0;
@@ -1336,6 +1511,12 @@ static void launch_bwd_tile(const TrainArgs &a0, cudaStream_t s) {
     int grid = (int)(tiles < cap ? tiles : cap);
     if (grid < 1) grid = 1;
     launch_maybe_pdl(k_bwd_tile<VPL, BF>, grid, 32, smem, s, true, a, tmg, tms);
+    if (a.tp2) {  // second phase: rows spanning tiles (32 tiles checked per CTA)
+        long long g2 = (tiles + 31) / 32;
+        if (g2 > SPAN_MAXCTA - SPAN_BWD2_OFF) g2 = SPAN_MAXCTA - SPAN_BWD2_OFF;
+        if (g2 < 1) g2 = 1;
+        launch_maybe_pdl(k_bwd_rows<VPL, BF>, (int)g2, 256, (size_t)64 * a.g.D, s, true, a);
+    }
 }
 
 cudaError_t launch_backward(const TrainArgs &a, cudaStream_t s) {
@@ -1386,6 +1567,15 @@ cudaError_t configure_train_kernels() {
     cudaFuncSetAttribute(k_bwd_tile<2, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_tile<4, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_tile<8, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    // k_bwd_rows: 8 fp64 partial rows of D (64 KB at D = 1024)
+    cudaFuncSetAttribute(k_bwd_rows<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_bwd_rows<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_bwd_rows<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_bwd_rows<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_bwd_rows<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_bwd_rows<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_bwd_rows<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_bwd_rows<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     cudaFuncSetAttribute(k_bwd_ws<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_ws<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_bwd_ws<4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

@@ -265,6 +265,9 @@ struct sp_ctx {
     double *d_tpart = nullptr;    // [T][ntiles][2][D]
     uint32_t *d_seg_cnt = nullptr, *d_grp_cnt = nullptr;  // [T][n], [T][ntiles][2]
     int bwd_tr = 0, bwd_ntiles = 0;
+    uint32_t *d_tctr = nullptr;   // [RING][2] k_bwd_tile tile claims / exits per batch slot
+    bool bwd_dyn = true;
+    bool bwd_2p = true;           // two-phase backward (SP_BWD_2P=0: last-arriver counters in k_bwd_tile)          // k_bwd_tile claims tiles dynamically (SP_BWD_DYN=0: static round robin)
     int bwd_tma = 1;  // k_bwd_tile stages rows with TMA bulk copies; SP_BWD_TMA=0: LDGSTS (A/B, slower)
     float **d_host = nullptr;
     std::vector<float *> host_dev;  // [T] device-visible (mapped) host table pointers
@@ -655,6 +658,8 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.grp_cnt = c->d_grp_cnt;
     a.tr = c->bwd_tr;
     a.ntiles = c->bwd_ntiles;
+    a.tctr = c->bwd_dyn ? c->d_tctr : nullptr;
+    a.tp2 = c->bwd_2p ? 1 : 0;
     a.bwd_tma = c->bwd_tma;
     a.srows = c->S_total;
     a.span = c->span_on ? c->d_span : nullptr;
@@ -1177,6 +1182,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     if (const char *e = getenv("SP_PULL_CTAS")) c->pull_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_XFER")) c->xfer_warp = std::string(e) == "warp";
     if (const char *e = getenv("SP_BWD_TMA")) c->bwd_tma = atoi(e) != 0;
+    if (const char *e = getenv("SP_BWD_DYN")) c->bwd_dyn = atoi(e) != 0;
+    if (const char *e = getenv("SP_BWD_2P")) c->bwd_2p = atoi(e) != 0;
     if (const char *e = getenv("SP_XFER_CTAS")) c->xfer_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_WB_GPU_FRAC")) {
         const double f = atof(e);
@@ -1347,6 +1354,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         CKC(dalloc(c, &c->d_grp_cnt, tiles * 2));
         CKC(cudaMemset(c->d_seg_cnt, 0, Tn * sizeof(uint32_t)));
         CKC(cudaMemset(c->d_grp_cnt, 0, tiles * 2 * sizeof(uint32_t)));
+        CKC(dalloc(c, &c->d_tctr, (size_t)RING * 2));
+        CKC(cudaMemset(c->d_tctr, 0, (size_t)RING * 2 * sizeof(uint32_t)));
     }
     CKC(dalloc(c, &c->d_pprof, 18 * (size_t)c->T + 2 + 4096));
     CKC(cudaMemset(c->d_pprof, 0, (18 * (size_t)c->T + 2 + 4096) * sizeof(unsigned long long)));

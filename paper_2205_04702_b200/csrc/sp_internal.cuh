@@ -201,6 +201,16 @@ struct TrainArgs {
     uint32_t *seg_cnt;   // [T][n] arrivals per multi-tile row (self-resetting)
     uint32_t *grp_cnt;   // [T][ntiles][2] arrivals per group of 8 pieces (self-resetting)
     int tr, ntiles;
+    // k_bwd_tile dynamic tiles (nullable: static round robin): [RING][2]
+    // {claims, exits} per batch slot; a CTA's first two tiles are static
+    // (blockIdx.x, + gridDim.x), later ones claimed, so a CTA that becomes
+    // resident late (its SM shared with the transfer / plan kernels) takes
+    // fewer tiles; the last CTA to exit resets the pair
+    uint32_t *tctr;
+    // two-phase backward (default; SP_BWD_2P=0: one phase with last-arriver
+    // counters): k_bwd_tile only writes the fp64 pieces of rows spanning
+    // tiles, k_bwd_rows then folds each such row's pieces and applies SGD
+    int tp2;
     int bwd_tma;         // k_bwd_tile stages rows by TMA bulk copies (default) or LDGSTS (SP_BWD_TMA=0)
     int g4;              // (set by the launcher) TMA tile::gather4, 4 rows per request, via tensor maps
     long long srows;     // Storage rows (tensor map of Storage)
@@ -319,15 +329,16 @@ __device__ __forceinline__ int find_table(const uint32_t *s_pref, int tcount, ui
 // (kind, slot).  No atomics, no events in the graphs: the steady state is
 // timed as it runs (bench.py's per-stage durations and overlap).
 enum SpanKind : int { SPK_PLAN = 0, SPK_XFER = 1, SPK_FWD = 2, SPK_SURR = 3, SPK_BWD = 4, SPAN_KINDS = 5 };
-constexpr int SPAN_MAXCTA = 4096;
+constexpr int SPAN_MAXCTA = 8192;
+constexpr int SPAN_BWD2_OFF = 7168;  // k_bwd_rows (the backward's second phase) stamps CTAs from here
 __device__ __forceinline__ unsigned long long *span_base(unsigned long long *span, int kind, long long b) {
     return span ? span + (((size_t)kind * RING + (size_t)(b % RING)) * SPAN_MAXCTA) * 2 : nullptr;
 }
-__device__ __forceinline__ void span_mark(unsigned long long *base, int which) {
-    if (base && threadIdx.x == 0 && blockIdx.x < (unsigned)SPAN_MAXCTA) {
+__device__ __forceinline__ void span_mark(unsigned long long *base, int which, unsigned off = 0) {
+    if (base && threadIdx.x == 0 && off + blockIdx.x < (unsigned)SPAN_MAXCTA) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        base[(size_t)blockIdx.x * 2 + which] = t;
+        base[(size_t)(off + blockIdx.x) * 2 + which] = t;
     }
 }
 

@@ -82,3 +82,47 @@ def test_every_occurrence_once_and_pieces_disjoint(n, R, alpha, TR):
         finished[row] += 1
     assert not pieces                     # no orphan piece
     assert (seen == 1).all() and (finished == 1).all()
+
+
+def _owners(uid, TR):
+    """k_bwd_rows' owner rule: tile k owns the row at its tail iff that row
+    continues past the tile's end and starts inside the tile (seg_off >= lo)."""
+    n = len(uid)
+    seg_off = np.searchsorted(uid, np.arange(int(uid.max()) + 2))
+    NT = (n + TR - 1) // TR
+    own = {}
+    for k in range(NT):
+        lo, nrows = k * TR, min(TR, n - k * TR)
+        if lo + nrows >= n:
+            continue
+        u, un = uid[lo + nrows - 1], uid[lo + nrows]
+        if u == un and seg_off[u] >= lo:
+            assert u not in own
+            own[int(u)] = (k, (seg_off[u + 1] - 1) // TR)
+    return seg_off, own
+
+
+@pytest.mark.parametrize("n,R,alpha,TR", [(4096, 3, 1.05, 16), (4096, 40_000_000, 1.05, 16),
+                                          (20_000, 2000, 0.8, 32), (5000, 1000, 1.2, 7),
+                                          (1000, 1, 1.0, 32), (33, 5, 1.0, 32), (64, 64, 0.0, 32)])
+def test_two_phase_owner_finishes_every_spanning_row_once(n, R, alpha, TR):
+    """Two-phase backward: every row spanning tiles [kf, kl] has exactly one
+    owner, its first tile kf, which folds the pieces of kf..kl; rows inside
+    one tile have none (k_bwd_tile finishes them)."""
+    rng = np.random.default_rng(n * 7 + R)
+    p = 1.0 / np.arange(1, R + 1) ** alpha
+    p /= p.sum()
+    ids = np.sort(rng.choice(R, size=n, p=p))
+    _, uid = np.unique(ids, return_inverse=True)
+    seg_off, own = _owners(uid, TR)
+    _, _, pieces = _partition(uid, TR)
+    for row in range(len(seg_off) - 1):
+        kf, kl = seg_off[row] // TR, (seg_off[row + 1] - 1) // TR
+        if kf == kl:
+            assert row not in own
+        else:
+            assert own[row] == (kf, kl)
+            for kk in range(kf, kl + 1):   # the pieces it folds exist and are this row's
+                ps = 1 if (kk == kf and seg_off[row] != kf * TR) else 0
+                assert pieces.pop((kk, ps))[0] == row
+    assert not pieces
