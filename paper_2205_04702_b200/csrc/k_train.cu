@@ -806,21 +806,36 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     unsigned long long *spn = span_base(A.span, SPK_BWD, A.span_b);
     span_mark(spn, 0);
     uint32_t parity = 0;
-    // tile order: blockIdx.x, blockIdx.x + G, then claimed (2G + claim) when
-    // A.tctr is set, else blockIdx.x + 2G, + 3G, ... (static)
-    uint32_t *ctr = A.tctr ? A.tctr + 2 * (A.span_b % RING) : nullptr;
+    // tile order: blockIdx.x, + G, + 2G, then claimed (3G + claim) when
+    // A.tctr is set, else + 3G, + 4G, ... (static).  A claim is issued two
+    // tiles before its index is needed (its latency hides behind two tiles).
+    // Claims are spread over TCTR_GROUPS counters (one 128-B line each; one
+    // same-address counter serialised ~7k claims at the L2): CTA c claims
+    // from group j = c % TCTR_GROUPS, whose i-th claim is tile 3G + j + i*TCTR_GROUPS
+    uint32_t *ctrs = A.tctr ? A.tctr + (size_t)(A.span_b % RING) * TCTR_STRIDE : nullptr;
+    const int grp = (int)(blockIdx.x % TCTR_GROUPS);
+    uint32_t *ctr = ctrs ? ctrs + grp * 32 : nullptr;
     const int G = (int)gridDim.x;
-    int after = blockIdx.x + G;  // the tile after the current one (its metadata is loaded during this tile)
+    int after = min(total, (int)blockIdx.x + G);       // T(i+1): its metadata loads during tile T(i)
+    int after2 = min(total, (int)blockIdx.x + 2 * G);  // T(i+2)
+    // pending claim (lane 0) for T(i+3), issued one tile earlier.  Indices
+    // only grow along a CTA's sequence (static ones < 3G <= claimed ones, a
+    // counter only grows), so once one is >= total all later ones are: no
+    // claimed tile below total is ever dropped.
+    uint32_t pend = 0;
+    if (ctr && lane == 0) pend = atomicAdd(ctr, 1u);
     for (int tile = blockIdx.x; tile < total;) {
         const Meta m = nxt;
-        // claim the tile after `after` now; its index is needed only at the end of this tile
+        // claim T(i+4) now; its index is needed two tiles from here
         uint32_t claim = 0;
-        if (ctr && lane == 0 && after < total) claim = atomicAdd(ctr, 1u);
+        if (ctr && lane == 0 && after2 < total) claim = atomicAdd(ctr, 1u);
         auto advance = [&]() {
             tile = after;
-            if (after >= total) return;
-            after = ctr ? 2 * G + (int)__shfl_sync(0xffffffffu, claim, 0) : after + G;
-            if (after > total) after = total;
+            after = after2;
+            if (after2 < total)
+                after2 = ctr ? min(total, 3 * G + grp + TCTR_GROUPS * (int)__shfl_sync(0xffffffffu, pend, 0))
+                             : min(total, after2 + G);
+            pend = claim;
         };
         const int t = tile / NT, k = tile - t * NT;
         const int lo = k * TR;
@@ -907,10 +922,9 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         advance();
     }
     span_mark(spn, 1);
-    if (ctr && lane == 0) {  // every claim of every CTA precedes its exit: the last one out resets
-        if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
-            ctr[0] = 0u;
-            ctr[1] = 0u;
+    if (ctrs && lane == 0) {  // every claim of every CTA precedes its exit: the last one out resets
+        if (atomicAdd(ctrs + TCTR_GROUPS * 32, 1u) == gridDim.x - 1) {
+            for (int j = 0; j <= TCTR_GROUPS; j++) ctrs[j * 32] = 0u;
         }
     }
 }
@@ -962,13 +976,17 @@ __global__ void __launch_bounds__(256, 2) k_bwd_rows(TrainArgs A) {
                 const int lo = k * TR, nrows = min(TR, g.n - lo);
                 if (lo + nrows < g.n) {
                     const size_t tb = (size_t)t * g.n;
+                    // one wave: the tail row, the row after it and the tail row's
+                    // slot (every occurrence of a row has the same slot); then its
+                    // segment offsets
                     const uint32_t u = __ldg(A.bb.sorted_uid + tb + lo + nrows - 1);
                     const uint32_t un = __ldg(A.bb.sorted_uid + tb + lo + nrows);
+                    const uint32_t sl = __ldg(A.bb.sorted_slot + tb + lo + nrows - 1);
                     if (u != EMPTY && u == un) {
                         slo = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u);
+                        const uint32_t shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
                         if (slo >= (uint32_t)lo) {
-                            const uint32_t shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + u + 1);
-                            slot = __ldg(A.bb.sorted_slot + tb + slo);
+                            slot = sl;
                             it = make_uint4((uint32_t)t, u, (uint32_t)k, (shi - 1u) / (uint32_t)TR);
                         }
                     }

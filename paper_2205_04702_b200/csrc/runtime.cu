@@ -265,7 +265,7 @@ struct sp_ctx {
     double *d_tpart = nullptr;    // [T][ntiles][2][D]
     uint32_t *d_seg_cnt = nullptr, *d_grp_cnt = nullptr;  // [T][n], [T][ntiles][2]
     int bwd_tr = 0, bwd_ntiles = 0;
-    uint32_t *d_tctr = nullptr;   // [RING][2] k_bwd_tile tile claims / exits per batch slot
+    uint32_t *d_tctr = nullptr;   // [RING][TCTR_STRIDE] k_bwd_tile tile claims / exits per batch slot
     bool bwd_dyn = true;
     bool bwd_2p = true;           // two-phase backward (SP_BWD_2P=0: last-arriver counters in k_bwd_tile)          // k_bwd_tile claims tiles dynamically (SP_BWD_DYN=0: static round robin)
     int bwd_tma = 1;  // k_bwd_tile stages rows with TMA bulk copies; SP_BWD_TMA=0: LDGSTS (A/B, slower)
@@ -1354,8 +1354,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
         CKC(dalloc(c, &c->d_grp_cnt, tiles * 2));
         CKC(cudaMemset(c->d_seg_cnt, 0, Tn * sizeof(uint32_t)));
         CKC(cudaMemset(c->d_grp_cnt, 0, tiles * 2 * sizeof(uint32_t)));
-        CKC(dalloc(c, &c->d_tctr, (size_t)RING * 2));
-        CKC(cudaMemset(c->d_tctr, 0, (size_t)RING * 2 * sizeof(uint32_t)));
+        CKC(dalloc(c, &c->d_tctr, (size_t)RING * TCTR_STRIDE));
+        CKC(cudaMemset(c->d_tctr, 0, (size_t)RING * TCTR_STRIDE * sizeof(uint32_t)));
     }
     CKC(dalloc(c, &c->d_pprof, 18 * (size_t)c->T + 2 + 4096));
     CKC(cudaMemset(c->d_pprof, 0, (18 * (size_t)c->T + 2 + 4096) * sizeof(unsigned long long)));

@@ -185,6 +185,8 @@ struct PushArgs {
     unsigned long long *span;  // span timing (nullable): Plan(b) at slot b % RING
 };
 
+constexpr int TCTR_GROUPS = 8;
+constexpr int TCTR_STRIDE = (TCTR_GROUPS + 1) * 32;
 struct TrainArgs {
     Geometry g;
     BatchBufs bb;
@@ -206,7 +208,7 @@ struct TrainArgs {
     // (blockIdx.x, + gridDim.x), later ones claimed, so a CTA that becomes
     // resident late (its SM shared with the transfer / plan kernels) takes
     // fewer tiles; the last CTA to exit resets the pair
-    uint32_t *tctr;
+    uint32_t *tctr;      // [RING][TCTR_STRIDE]: TCTR_GROUPS claim counters + the exit counter, 128 B apart
     // two-phase backward (default; SP_BWD_2P=0: one phase with last-arriver
     // counters): k_bwd_tile only writes the fp64 pieces of rows spanning
     // tiles, k_bwd_rows then folds each such row's pieces and applies SGD

@@ -39,9 +39,9 @@ def line_map(cubin, func_regex):
         if ln.startswith(".text.") and ln.strip().endswith(":"):
             cur_fn = ln.strip()[:-1].replace(".text.", "")
             continue
-        lm = re.search(r'line (\d+)', ln)
+        lm = re.search(r'File "([^"]+)", line (\d+)', ln)
         if "//##" in ln and lm:
-            cur_line = int(lm.group(1))
+            cur_line = (lm.group(1).split("/")[-1], int(lm.group(2)))
             continue
         am = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if am and cur_fn and re.search(func_regex, cur_fn):
@@ -64,10 +64,19 @@ def main():
         by[lm.get(a - base)] += n
     tot = sum(by.values()) or 1
     print(f"{fn}: {tot} samples")
-    src = open(sys.argv[6]).read().splitlines() if len(sys.argv) > 6 else []
-    for line, n in by.most_common(40):
-        txt = src[line - 1].strip()[:90] if src and line and line <= len(src) else ""
-        print(f"{n:7d} {100 * n / tot:5.1f}%  line {line}  {txt}")
+    srcdir = sys.argv[6] if len(sys.argv) > 6 else None  # directory of the sources
+    cache = {}
+    for key, n in by.most_common(40):
+        txt = ""
+        if key and srcdir:
+            f, line = key
+            import os
+            fp = os.path.join(srcdir, f)
+            if f not in cache:
+                cache[f] = open(fp).read().splitlines() if os.path.exists(fp) else []
+            src = cache[f]
+            txt = src[line - 1].strip()[:90] if line <= len(src) else ""
+        print(f"{n:7d} {100 * n / tot:5.1f}%  {key}  {txt}")
 
 
 if __name__ == "__main__":
