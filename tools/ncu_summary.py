@@ -22,7 +22,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # kernel name prefix -> bench stage
-STAGE = {"k_fwd": "forward", "k_bwd_hot": "backward", "k_bwd": "backward", "k_bwd_tile": "backward", "k_push": "plan",
+STAGE = {"k_fwd": "forward", "k_bwd_hot": "backward", "k_bwd": "backward", "k_bwd_tile": "backward", "k_bwd_rows": "backward", "k_push": "plan",
          "k_xfer_warp": "transfer", "k_fwd_pad": "forward",
          "k_pullfill": "transfer", "k_surrogate": "surrogate"}
 
