@@ -50,13 +50,17 @@ __device__ __forceinline__ void add4(float4 &a, const float4 &b) {
 // indices, then their rows for lookup position p, are all in flight together,
 // so even L = 1 (one row per bag) keeps BU rows per group outstanding.  Each
 // bag is still a left fold in ascending p (bit-exact with the oracle).
+constexpr int FWD_ROUNDS = 4;  // k_fwd dynamic chunks: rounds per claim
 template <int G, int VPL, bool PAD, bool BF>
 __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
     using SR = SRow<BF>;  // fp32 or bf16 Storage rows (R28: widened, folded in fp32)
-    if (*A.err != NO_ERR) return;
+    // (no work after a latched error, but the dynamic path still counts its
+    // warps out so the claim counters reset)
+    const bool dead = *A.err != NO_ERR;
+    if (dead && (PAD || !A.fctr)) return;
     constexpr int BU = VPL >= 4 ? 1 : (VPL == 2 ? 2 : 4);
     const int L = A.g.L, D4 = A.g.D / 4;
-    const long long nbags = (long long)A.g.T * A.g.N;
+    const long long nbags = dead ? 0 : (long long)A.g.T * A.g.N;
     const int gpb = blockDim.x / G;
     const int lane = threadIdx.x % G;
     const typename SR::V *st = reinterpret_cast<const typename SR::V *>(A.storage) + lane;
@@ -88,7 +92,8 @@ __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
         }
         return;
     } else {
-    for (long long bag0 = (long long)blockIdx.x * gpb + threadIdx.x / G; bag0 < nbags; bag0 += BU * S) {
+    // BU bags of the lane group in flight: bag0, bag0 + S, ..., bag0 + (BU-1)*S
+    auto bags = [&](long long bag0, long long S) {
         const uint32_t *so[BU];
         bool ok[BU];
         float4 acc[BU][VPL];
@@ -123,7 +128,32 @@ __device__ __forceinline__ void fwd_body(const TrainArgs &A) {
             if (ok[u])
 #pragma unroll
                 for (int v = 0; v < VPL; v++) __stcs(out + (bag0 + u * S) * D4 + v * G, acc[u][v]);
+    };
+    if (!A.fctr) {  // static grid stride (SP_FWD_DYN=0)
+        for (long long bag0 = (long long)blockIdx.x * gpb + threadIdx.x / G; bag0 < nbags; bag0 += BU * S) bags(bag0, S);
+        return;
     }
+    // dynamic: a warp takes chunks of WB consecutive bags (FWD_ROUNDS rounds
+    // of its 32/G lane groups x BU bags), the first by its index, the rest
+    // claimed from one of TCTR_GROUPS counters (claim issued one chunk ahead),
+    // so warps that become resident late (SMs shared with k_push / k_pullfill)
+    // take fewer bags; the last warp out resets the counters
+    constexpr int GPW = 32 / G, WB = GPW * BU * FWD_ROUNDS;
+    const int lw = threadIdx.x & 31, gw = lw / G;
+    const long long nch = (nbags + WB - 1) / WB;
+    const long long W = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint32_t *ctrs = A.fctr + (size_t)(A.span_b % RING) * TCTR_STRIDE;
+    const int grp = (int)(wid % TCTR_GROUPS);
+    for (long long ch = wid; ch < nch;) {
+        uint32_t claim = 0;
+        if (lw == 0) claim = atomicAdd(ctrs + grp * 32, 1u);
+#pragma unroll 1
+        for (int r = 0; r < FWD_ROUNDS; r++) bags(ch * WB + (long long)r * GPW * BU + gw, GPW);
+        ch = W + grp + (long long)TCTR_GROUPS * __shfl_sync(0xffffffffu, claim, 0);
+    }
+    if (lw == 0 && atomicAdd(ctrs + TCTR_GROUPS * 32, 1u) == (uint32_t)(W - 1))
+        for (int j = 0; j <= TCTR_GROUPS; j++) ctrs[j * 32] = 0u;
     }
 }
 
@@ -935,11 +965,11 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
 // inside it and runs past its end).  A CTA takes 32 tiles at a time: warp 0
 // checks them (one lane per tile, one load wave) and lists the owners in
 // shared memory; a row of <= BWD2_SMALL pieces is then folded by one warp,
-// in tile order (all its pieces in flight at once); a longer one (the Zipf
+// in tile order (8 pieces in flight per round); a longer one (the Zipf
 // head: up to n/TR pieces) by all 8 warps -- warp w sums pieces kf+w, kf+w+8,
 // ... in order, then warp 0 adds the 8 partials in warp order.  The fold
 // shape depends only on the batch.
-constexpr int BWD2_SMALL = 8;
+constexpr int BWD2_SMALL = 16;  // (8 / 16 / 32 measured equal: profiles/r02_s3_ab.txt)
 template <int VPL, bool BF>
 __global__ void __launch_bounds__(256, 2) k_bwd_rows(TrainArgs A) {
     using SR = SRow<BF>;
@@ -993,7 +1023,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_rows(TrainArgs A) {
                 }
             }
             const bool own = it.x != EMPTY;
-            const bool big = own && (int)(it.w - it.z) + 1 > BWD2_SMALL;
+            const bool big = own && (int)(it.w - it.z) + 1 > (A.bwd2_small > 0 ? A.bwd2_small : BWD2_SMALL);
             s_item[lane] = it;
             s_slo[lane] = slo;
             s_slot[lane] = slot;
@@ -1020,25 +1050,20 @@ __global__ void __launch_bounds__(256, 2) k_bwd_rows(TrainArgs A) {
                 for (int v = 0; v < VPL; v++) {
                     const int c = lane + 32 * v;
                     if (c >= D4) continue;
-                    // (npc >= 2) all pieces in flight, then added in tile order
-                    const double4 *p0 = piece(t, kf, kf, slo) + c;
-                    const size_t stp = (size_t)2 * g.D / 4;  // double4 from one tile's slot 0 to the next's
-                    const double4 *p1 = reinterpret_cast<const double4 *>(A.tpart + (((size_t)t * NT + kf + 1) * 2) * g.D) + c;
-                    double4 x0 = ldcg_d4(p0), x1 = ldcg_d4(p1), x2, x3, x4, x5, x6, x7;
-                    if (npc > 2) x2 = ldcg_d4(p1 + stp);
-                    if (npc > 3) x3 = ldcg_d4(p1 + 2 * stp);
-                    if (npc > 4) x4 = ldcg_d4(p1 + 3 * stp);
-                    if (npc > 5) x5 = ldcg_d4(p1 + 4 * stp);
-                    if (npc > 6) x6 = ldcg_d4(p1 + 5 * stp);
-                    if (npc > 7) x7 = ldcg_d4(p1 + 6 * stp);
-                    dadd4(x0, x1);
-                    if (npc > 2) dadd4(x0, x2);
-                    if (npc > 3) dadd4(x0, x3);
-                    if (npc > 4) dadd4(x0, x4);
-                    if (npc > 5) dadd4(x0, x5);
-                    if (npc > 6) dadd4(x0, x6);
-                    if (npc > 7) dadd4(x0, x7);
-                    apply(slot, c, x0);
+                    // (2 <= npc <= the threshold) 8 pieces in flight per round, added in tile order
+                    double4 acc = make_double4(0.0, 0.0, 0.0, 0.0);
+                    for (int q0 = 0; q0 < npc; q0 += 8) {
+                        double4 x[8];
+#pragma unroll
+                        for (int q = 0; q < 8; q++)
+                            if (q0 + q < npc) x[q] = ldcg_d4(piece(t, kf + q0 + q, kf, slo) + c);
+                        if (q0 == 0) acc = x[0];
+                        else dadd4(acc, x[0]);
+#pragma unroll
+                        for (int q = 1; q < 8; q++)
+                            if (q0 + q < npc) dadd4(acc, x[q]);
+                    }
+                    apply(slot, c, acc);
                 }
             }
         }

@@ -226,12 +226,17 @@ __global__ void __launch_bounds__(32) k_pullfill(XferArgs A, int nb) {
                 // round's rows, four columns at a time); the bulk stores below
                 // read the results through the async proxy
                 const uint32_t cnt = round_cnt(r), D4 = (uint32_t)g.D / 4u;
-                for (uint32_t i = lane; i < cnt * D4; i += 32) {
-                    const uint32_t row = i / D4, c = i - row * D4;
-                    reinterpret_cast<float4 *>(vbuf(s, row))[c] =
-                        SRow<true>::wid(reinterpret_cast<const uint2 *>(v16(s, row))[c]);
-                    reinterpret_cast<uint2 *>(n16(s, row))[c] =
-                        SRow<true>::nar(reinterpret_cast<const float4 *>(nbuf(s, row))[c]);
+                const float4 *n32 = reinterpret_cast<const float4 *>(nbuf(s, 0));
+                const uint2 *v16r = reinterpret_cast<const uint2 *>(v16(s, 0));
+                float4 *v32 = reinterpret_cast<float4 *>(vbuf(s, 0));
+                uint2 *n16r = reinterpret_cast<uint2 *>(n16(s, 0));
+                // rows are contiguous in each area: element e = row * D4 + c
+#pragma unroll 4
+                for (uint32_t e = lane; e < cnt * D4; e += 32) {
+                    const float4 x = n32[e];
+                    const uint2 y = v16r[e];
+                    n16r[e] = SRow<true>::nar(x);
+                    v32[e] = SRow<true>::wid(y);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();

@@ -267,7 +267,10 @@ struct sp_ctx {
     int bwd_tr = 0, bwd_ntiles = 0;
     uint32_t *d_tctr = nullptr;   // [RING][TCTR_STRIDE] k_bwd_tile tile claims / exits per batch slot
     bool bwd_dyn = true;
-    bool bwd_2p = true;           // two-phase backward (SP_BWD_2P=0: last-arriver counters in k_bwd_tile)          // k_bwd_tile claims tiles dynamically (SP_BWD_DYN=0: static round robin)
+    bool bwd_2p = true;
+    int bwd2_small = 0;           // SP_BWD2_SMALL: k_bwd_rows one-warp threshold (A/B)
+    uint32_t *d_fctr = nullptr;   // [RING][TCTR_STRIDE] k_fwd bag-chunk claims / exits per batch slot
+    bool fwd_dyn = true;          // k_fwd claims bag chunks dynamically (SP_FWD_DYN=0: static grid stride)           // two-phase backward (SP_BWD_2P=0: last-arriver counters in k_bwd_tile)          // k_bwd_tile claims tiles dynamically (SP_BWD_DYN=0: static round robin)
     int bwd_tma = 1;  // k_bwd_tile stages rows with TMA bulk copies; SP_BWD_TMA=0: LDGSTS (A/B, slower)
     float **d_host = nullptr;
     std::vector<float *> host_dev;  // [T] device-visible (mapped) host table pointers
@@ -660,6 +663,8 @@ TrainArgs train_args(sp_ctx *c, long long b) {
     a.ntiles = c->bwd_ntiles;
     a.tctr = c->bwd_dyn ? c->d_tctr : nullptr;
     a.tp2 = c->bwd_2p ? 1 : 0;
+    a.bwd2_small = c->bwd2_small;
+    a.fctr = c->fwd_dyn ? c->d_fctr : nullptr;
     a.bwd_tma = c->bwd_tma;
     a.srows = c->S_total;
     a.span = c->span_on ? c->d_span : nullptr;
@@ -1184,6 +1189,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     if (const char *e = getenv("SP_BWD_TMA")) c->bwd_tma = atoi(e) != 0;
     if (const char *e = getenv("SP_BWD_DYN")) c->bwd_dyn = atoi(e) != 0;
     if (const char *e = getenv("SP_BWD_2P")) c->bwd_2p = atoi(e) != 0;
+    if (const char *e = getenv("SP_BWD2_SMALL")) c->bwd2_small = std::max(1, atoi(e));
+    if (const char *e = getenv("SP_FWD_DYN")) c->fwd_dyn = atoi(e) != 0;
     if (const char *e = getenv("SP_XFER_CTAS")) c->xfer_ctas = std::max(1, atoi(e));
     if (const char *e = getenv("SP_WB_GPU_FRAC")) {
         const double f = atof(e);
@@ -1302,6 +1309,8 @@ sp_status sp_create(const sp_desc *d, sp_ctx **out) {
     CKC(dalloc(c, &c->d_next_need, (size_t)c->S_total));
     // Storage: S rows of D fp32, or of D bf16 (SP_FLAG_BF16: half the bytes)
     CKC(dalloc(c, &c->d_storage, (size_t)c->S_total * c->D / (c->g.bf16 ? 2 : 1)));
+    CKC(dalloc(c, &c->d_fctr, (size_t)RING * TCTR_STRIDE));
+    CKC(cudaMemset(c->d_fctr, 0, (size_t)RING * TCTR_STRIDE * sizeof(uint32_t)));
     // LRU log per table (LFU: one per use-count class, c = 0 holding the
     // initial vacant slots; RANDOM: none): capacity log_factor*S_t + 4n
     // (LFU classes: 2*S_t + 4n each)

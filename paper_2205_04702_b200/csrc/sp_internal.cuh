@@ -209,10 +209,12 @@ struct TrainArgs {
     // resident late (its SM shared with the transfer / plan kernels) takes
     // fewer tiles; the last CTA to exit resets the pair
     uint32_t *tctr;      // [RING][TCTR_STRIDE]: TCTR_GROUPS claim counters + the exit counter, 128 B apart
+    uint32_t *fctr;      // k_fwd dynamic bag chunks (nullable: static grid stride), same layout
     // two-phase backward (default; SP_BWD_2P=0: one phase with last-arriver
     // counters): k_bwd_tile only writes the fp64 pieces of rows spanning
     // tiles, k_bwd_rows then folds each such row's pieces and applies SGD
     int tp2;
+    int bwd2_small;      // k_bwd_rows: rows of up to this many pieces are folded by one warp (0: default)
     int bwd_tma;         // k_bwd_tile stages rows by TMA bulk copies (default) or LDGSTS (SP_BWD_TMA=0)
     int g4;              // (set by the launcher) TMA tile::gather4, 4 rows per request, via tensor maps
     long long srows;     // Storage rows (tensor map of Storage)
