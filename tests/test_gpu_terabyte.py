@@ -117,3 +117,21 @@ def test_terabyte_graph_mode_2000_batches_log_wrap(tb_tables):
         worst = max(worst, cmp["max_rel"])
     assert worst <= TOL, worst
     sp.close()
+
+
+def test_terabyte_full_size_bf16_storage(tb_tables):
+    """bf16 Storage (SP_FLAG_BF16, reading R28) at the full Terabyte shape
+    against the oracle's bf16 mode: every Plan record and pooled output
+    bit-exact, sampled final rows within one bf16 unit (2^-7 relative)."""
+    c = CONFIGS["terabyte"]
+    nb = 24
+    tr = sample_trace(c.rows, c.batch, c.pooling, c.alpha, nb, c.trace_seed + 2, device="cuda").cpu()
+    slots = _tight_slots(c, tr.numpy(), 128)
+    _reinit(tb_tables, c)
+    g, d, e = c.surrogate()
+    rep = run_parity(c.rows, slots, c.dim, c.batch, c.pooling, nb, 3, 2, trace=tr,
+                     init_seed=c.init_seed, gde=(g, d, e), index_dtype="int32", index_on_device=True,
+                     check_slots=True, sample_rows=3000, tables=tb_tables, bf16=True)
+    assert rep["plans"] == nb and rep["pooled"] == nb
+    assert rep["evictions"] > 10000, rep["evictions"]
+    assert rep["tables"]["max_rel"] <= 2.0 ** -7, rep["tables"]
