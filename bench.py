@@ -597,6 +597,8 @@ def run_ours(args):
     from paper_2205_04702_b200._binding import KERNEL_ONLY
     launches = {k: st1["kernel_launches"][k] - st0["kernel_launches"][k] for k in st1["kernel_launches"]}
     gpu_launches = sum(v for k, v in launches.items() if k in KERNEL_ONLY)
+    # a backward launch is two kernels with the two-phase backward (k_bwd_tile + k_bwd_rows)
+    gpu_launches += launches.get("backward", 0) * (int(st1.get("backward_kernels", 1) or 1) - 1)
     # ---- profiling pass: per-kernel CUDA-event durations (separate from the timed region)
     sp.set_profiling(True)
     pp0 = sp.debug_plan_profile()

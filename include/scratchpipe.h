@@ -212,7 +212,9 @@ typedef struct {
                                     /* + row-copy helpers)                          */
     int32_t gpu_writeback;          /* 1: k_pullfill writes victims straight into  */
                                     /* their host rows (SP_WRITEBACK=gpu)           */
-    int32_t reserved_stats;
+    int32_t backward_kernels;       /* kernels per backward launch (kernel_launches */
+                                    /* counts launches of the stage): 2 = k_bwd_tile */
+                                    /* + k_bwd_rows (two-phase), else 1             */
     double gather_share;            /* share of the missed rows the CPU gathers    */
 } sp_stats;
 

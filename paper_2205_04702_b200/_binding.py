@@ -79,7 +79,7 @@ class SpStats(ctypes.Structure):
         ("wait_xfer_ms", ctypes.c_double), ("wait_list_ms", ctypes.c_double),
         ("graph_steps", ctypes.c_int64), ("graph_step_host_ms", ctypes.c_double),
         ("transfer_mode", ctypes.c_int32), ("engine_threads", ctypes.c_int32),
-        ("gpu_writeback", ctypes.c_int32), ("reserved_stats", ctypes.c_int32),
+        ("gpu_writeback", ctypes.c_int32), ("backward_kernels", ctypes.c_int32),
         ("gather_share", ctypes.c_double),
     ]
 
@@ -434,7 +434,7 @@ class ScratchPipe:
         out["kernel_timed"] = dict(zip(KERNEL_KINDS, list(s.kernel_timed)))
         for k in ("host_gather_ms", "host_scatter_ms", "host_rows_gathered", "host_rows_scattered",
                   "wait_xfer_ms", "wait_list_ms", "graph_steps", "graph_step_host_ms", "engine_threads",
-                  "gpu_writeback", "gather_share"):
+                  "gpu_writeback", "gather_share", "backward_kernels"):
             out[k] = getattr(s, k)
         out["transfer_mode"] = XFER_MODES.get(s.transfer_mode, str(s.transfer_mode))
         out["status"] = st

@@ -2056,6 +2056,7 @@ sp_status sp_get_stats(sp_ctx *c, sp_stats *o) {
     o->gather_share = c->cpu_gather ? c->gather_q16 / 65536.0 : 0.0;
     o->engine_threads = (c->gpu_wb ? 0 : 1 + c->scatter_helpers) + (c->cpu_gather ? 1 + c->gather_helpers : 0);
     o->gpu_writeback = c->gpu_wb ? 1 : 0;
+    o->backward_kernels = (c->d_tpart && c->bwd_2p && !getenv("SP_BWD_WS")) ? 2 : 1;
     if (!c->prof_pending.empty()) {
         cudaStreamSynchronize(c->xfer_s);
         cudaStreamSynchronize(c->xfer_s2);
