@@ -36,10 +36,11 @@ def _bf16_valued(x: np.ndarray) -> bool:
     return bool(np.all((x.view(np.uint32) & 0xFFFF) == 0))
 
 
-@pytest.mark.parametrize("D", [8, 24, 64, 128])
+@pytest.mark.parametrize("D", [8, 24, 64, 128, 256, 1024])
 def test_bf16_parity_dims(D):
     """D = 8 / 24: bulk-copy staging (no tile::gather4 for bf16 rows unless
-    D % 16 == 0), D = 24 the generic forward; D = 64 / 128 gather4."""
+    D % 16 == 0), D = 24 the generic forward; D = 64 / 128 / 256 gather4;
+    D = 1024: two rows per tile, 64 KB of k_bwd_rows partials."""
     rows, N, L, nb = [5000, 700, 90], 96, 3, 40
     tr = sample_trace(rows, N, L, 0.9, nb, 51)
     slots = [min(R, max_window_union(tr.numpy(), t, 3, 2) + 4) for t, R in enumerate(rows)]
