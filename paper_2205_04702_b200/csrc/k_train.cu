@@ -783,8 +783,11 @@ __device__ __forceinline__ void bwd_fold_tile(const TrainArgs &A, int t, int k, 
     }
 }
 
+#ifndef SP_META2
+#define SP_META2 1  // k_bwd_tile: metadata two tiles ahead (0: one tile ahead, A/B)
+#endif
 #ifndef SP_BWD_TILE_MINB
-#define SP_BWD_TILE_MINB 16  // resident warps per SM the registers are sized for (<= 128 regs)
+#define SP_BWD_TILE_MINB 12  // resident warps per SM the registers are sized for (<= 152 regs; 16 KB of staging per warp at D = 128 fits 13-14 per SM anyway)
 #endif
 template <int VPL, bool BF = false>
 __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_TILE_MINB)
@@ -830,8 +833,17 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             m.shi = __ldg(A.bb.seg_off + (size_t)t * g.n1 + m.uid + 1);
         }
     };
-    Meta nxt;
-    load_meta(blockIdx.x, nxt);  // (Plan's output: complete before the forward ran)
+    // metadata two tiles ahead: `cur` for this tile, `nxt` for T(i+1) (loaded
+    // during tile i-1), `nxt2` for T(i+2) (loaded during tile i), so both
+    // levels of the load chain (uid -> segment offsets) hide behind a tile
+    Meta cur, nxt, nxt2;
+    load_meta(blockIdx.x, cur);  // (Plan's output: complete before the forward ran)
+#if SP_META2
+    load_meta(blockIdx.x + (int)gridDim.x, nxt);
+#define SP_LOAD_NEXT_META() load_meta(after2, nxt2)
+#else  // (A/B) one tile ahead
+#define SP_LOAD_NEXT_META() load_meta(after, nxt)
+#endif
     griddep_wait();  // (PDL) the surrogate's gradients are complete from here on
     unsigned long long *spn = span_base(A.span, SPK_BWD, A.span_b);
     span_mark(spn, 0);
@@ -855,11 +867,15 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
     uint32_t pend = 0;
     if (ctr && lane == 0) pend = atomicAdd(ctr, 1u);
     for (int tile = blockIdx.x; tile < total;) {
-        const Meta m = nxt;
+        const Meta m = cur;
         // claim T(i+4) now; its index is needed two tiles from here
         uint32_t claim = 0;
         if (ctr && lane == 0 && after2 < total) claim = atomicAdd(ctr, 1u);
         auto advance = [&]() {
+            cur = nxt;
+#if SP_META2
+            nxt = nxt2;
+#endif
             tile = after;
             after = after2;
             if (after2 < total)
@@ -874,7 +890,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const bool act = uid != EMPTY;
         const unsigned amask = __ballot_sync(0xffffffffu, act);
         if (amask == 0u) {  // (warp-uniform) all padding
-            load_meta(after, nxt);
+            SP_LOAD_NEXT_META();
             advance();
             continue;
         }
@@ -890,7 +906,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         const unsigned wmask = __ballot_sync(0xffffffffu, whole);
         const unsigned lmask = __ballot_sync(0xffffffffu, lastr);
         if (A.diag & 128) {  // timing diagnostic: no staging (the fold reads stale shared memory)
-            load_meta(after, nxt);
+            SP_LOAD_NEXT_META();
         } else if (A.g4) {
             // TMA tile::gather4: lane q fetches tile rows 4q..4q+3 (the last
             // group padded with the last row) and lane q the Storage rows of
@@ -910,7 +926,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             }
             if (lane < ng) rows4_g2s(sg + (size_t)4 * lane * D4, &tmg, gr[0], gr[1], gr[2], gr[3], &bar);
             if (lane < nsg) rows4_g2s(sw + (size_t)4 * lane * D4, &tms, sr[0], sr[1], sr[2], sr[3], &bar);
-            load_meta(after, nxt);
+            SP_LOAD_NEXT_META();
             while (!bar_try(&bar, parity)) {
             }
             parity ^= 1u;
@@ -919,7 +935,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
             __syncwarp();
             if (act) row_g2s(sg + (size_t)lane * D4, grad + ((size_t)t * g.N + bagof(m.occ)) * D4, rowb, &bar);
             if (whole) row_g2s(sw + (size_t)lane * D4, st + (size_t)slot * D4, rowsb, &bar);
-            load_meta(after, nxt);  // the next tile's metadata, in flight with the copies
+            SP_LOAD_NEXT_META();  // the next tile's metadata, in flight with the copies
             while (!bar_try(&bar, parity)) {
             }
             parity ^= 1u;
@@ -940,7 +956,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
                 for (uint32_t c = lane; c < rowsb / 16u; c += 32) cp16(dst + 16 * c, src + 16 * c);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
-            load_meta(after, nxt);  // the next tile's metadata, in flight with the copies
+            SP_LOAD_NEXT_META();  // the next tile's metadata, in flight with the copies
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
         }
@@ -952,6 +968,7 @@ __global__ void __launch_bounds__(32, VPL >= 2 ? SP_BWD_TILE_MINB / 2 : SP_BWD_T
         advance();
     }
     span_mark(spn, 1);
+#undef SP_LOAD_NEXT_META
     if (ctrs && lane == 0) {  // every claim of every CTA precedes its exit: the last one out resets
         if (atomicAdd(ctrs + TCTR_GROUPS * 32, 1u) == gridDim.x - 1) {
             for (int j = 0; j <= TCTR_GROUPS; j++) ctrs[j * 32] = 0u;
