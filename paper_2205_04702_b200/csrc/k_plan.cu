@@ -112,24 +112,31 @@ struct PhaseClock {
 // (histogram and per-warp digit counts shared by both instantiations)
 __shared__ uint32_t s_hist[256];
 __shared__ uint32_t s_wcnt[NW][256];
+__shared__ uint32_t s_hist4[4][256];  // radix_sort_pairs: every pass's digit histogram, one read
 
 template <int IPT>
 __device__ bool radix_sort_pairs(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, int n, int bits) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int TILE = PUSH_THREADS * IPT;
     bool swapped = false;
-    for (int sh = 0; sh < bits; sh += 8) {
-        for (int d = threadIdx.x; d < 256; d += blockDim.x) s_hist[d] = 0;
-        __syncthreads();
-        for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-            const int i = i0 + threadIdx.x;
-            const unsigned d = i < n ? ((ka[i] >> sh) & 255u) : 256u;
+    // the digit histograms of every pass in ONE read of the keys (a stable
+    // pass permutes the keys, it does not change their multiset)
+    const int npass = (bits + 7) / 8;
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&s_hist4[0][0])[k] = 0;
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const uint32_t key = i < n ? ka[i] : 0u;
+        for (int p = 0; p < npass; p++) {
+            const unsigned d = i < n ? ((key >> (8 * p)) & 255u) : 256u;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (d < 256u && (peers & lanemask_lt()) == 0) atomicAdd(&s_hist[d], __popc(peers));
+            if (d < 256u && (peers & lanemask_lt()) == 0) atomicAdd(&s_hist4[p][d], __popc(peers));
         }
-        __syncthreads();
+    }
+    __syncthreads();
+    for (int sh = 0; sh < bits; sh += 8) {
         {
-            uint32_t v = threadIdx.x < 256 ? s_hist[threadIdx.x] : 0u, tot;
+            uint32_t v = threadIdx.x < 256 ? s_hist4[sh / 8][threadIdx.x] : 0u, tot;
             const uint32_t ex = block_scan(v, &tot);
             if (threadIdx.x < 256) s_hist[threadIdx.x] = ex;
         }
