@@ -24,4 +24,6 @@ run kg_d128 --config kaggle --dim 128
 run kg_d256 --config kaggle --dim 256
 run kg_l20 --config kaggle --pooling 20 --steps 50
 run kg_l50 --config kaggle --pooling 50 --steps 30 --preroll 300
+run serial --variant serial
+run bf16 --storage bf16
 cat $O/sweep.log
